@@ -1,0 +1,204 @@
+// ref_shim.cpp -- extern "C" shim over the UNMODIFIED reference headers
+// (/root/reference/proj/include/fracpint/*.hpp), compiled by oracle/Makefile into
+// oracle/_ref/libfracpint_ref.so.  TEST / BASELINE INFRASTRUCTURE ONLY: it pins the C oracle
+// (tests/test_oracle_pins.py), generates tests/golden fixtures (tests/golden/make_golden.py) and
+// is the CPU reference arm of bench.py (--impl reference, cpu_baseline kind "reference").
+// No reference source is copied: this file only calls the reference's public API
+// (driver.hpp:49-92 orchestration pattern).
+#include <fracpint/all_at_once.hpp>
+#include <fracpint/alpha_circulant.hpp>
+#include <fracpint/dst.hpp>
+#include <fracpint/jacobian.hpp>
+#include <fracpint/krylov.hpp>
+#include <fracpint/parallel.hpp>
+#include <fracpint/tau.hpp>
+#include <fracpint/time_stencil.hpp>
+#include <fracpint/toeplitz.hpp>
+#include <fracpint/weights.hpp>
+
+#include <algorithm>
+#include <chrono>
+#include <complex>
+#include <cstring>
+#include <memory>
+#include <optional>
+#include <stdexcept>
+#include <string>
+#include <variant>
+
+namespace {
+thread_local std::string g_err;
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return 0;
+  } catch (const std::invalid_argument& e) {
+    g_err = e.what();
+    return 1;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 2;
+  }
+}
+
+using fracpint::AllAtOnceOperator;
+using fracpint::RieszJacobian1D;
+using fracpint::RieszJacobian2D;
+
+struct RefProblem {
+  int nt = 0;
+  double dt = 0.0;
+  std::variant<AllAtOnceOperator<RieszJacobian1D>, AllAtOnceOperator<RieszJacobian2D>> op;
+  std::optional<fracpint::AlphaCirculantPlan> plan;
+
+  template <class J>
+  RefProblem(int nt_, double dt_, J jac)
+      : nt(nt_), dt(dt_), op(AllAtOnceOperator<J>(fracpint::TimeStencil(nt_), std::move(jac), dt_)) {}
+
+  std::size_t dim() const {
+    return std::visit([](const auto& o) { return o.dim(); }, op);
+  }
+};
+}  // namespace
+
+extern "C" {
+
+const char* ref_last_error() { return g_err.c_str(); }
+void ref_set_threads(int n) { fracpint::set_thread_count(n); }
+int ref_threads() { return fracpint::thread_count(); }
+
+void ref_fft_inplace(double* x, std::size_t n, int sign) {
+  fracpint::fft_inplace(reinterpret_cast<std::complex<double>*>(x), n, sign);
+}
+int ref_dst1_real(const double* x, double* y, std::size_t n) {
+  return guarded([&] { fracpint::dst1<double>({x, n}, {y, n}); });
+}
+int ref_dst1_complex(const double* x, double* y, std::size_t n) {
+  using C = std::complex<double>;
+  return guarded([&] {
+    std::vector<C> in(reinterpret_cast<const C*>(x), reinterpret_cast<const C*>(x) + n);
+    fracpint::dst1<C>(in, {reinterpret_cast<C*>(y), n});
+  });
+}
+int ref_centred_weights(double gamma, int count, double* out) {
+  return guarded([&] {
+    auto fw = fracpint::centred_weights(gamma, count);
+    std::copy(fw.weights.begin(), fw.weights.end(), out);
+  });
+}
+int ref_toeplitz_matvec(const double* col, std::size_t n, const double* v, double* out) {
+  return guarded([&] {
+    fracpint::SymToeplitz t(std::vector<double>(col, col + n));
+    t.matvec<double>({v, n}, {out, n});
+  });
+}
+int ref_tau_spectrum(const double* col, std::size_t n, double* sigma) {
+  return guarded([&] {
+    auto tau = fracpint::tau_spectrum(fracpint::SymToeplitz(std::vector<double>(col, col + n)));
+    std::copy(tau.sigma.begin(), tau.sigma.end(), sigma);
+  });
+}
+
+void* ref_problem_1d(double gamma, double kappa, double h, int n, int nt, double dt) {
+  RefProblem* p = nullptr;
+  if (guarded([&] { p = new RefProblem(nt, dt, RieszJacobian1D(gamma, kappa, h, n)); })) return nullptr;
+  return p;
+}
+void* ref_problem_2d(double gx, double gy, double kx, double ky, double h, int n, int nt,
+                     double dt) {
+  RefProblem* p = nullptr;
+  if (guarded([&] { p = new RefProblem(nt, dt, RieszJacobian2D(gx, gy, kx, ky, h, n)); }))
+    return nullptr;
+  return p;
+}
+void ref_problem_free(void* p) { delete static_cast<RefProblem*>(p); }
+
+int ref_matvec(void* hp, const double* v, double* out) {
+  auto* p = static_cast<RefProblem*>(hp);
+  const std::size_t n = p->dim();
+  return guarded([&] { std::visit([&](const auto& o) { o.apply({v, n}, {out, n}); }, p->op); });
+}
+
+int ref_assemble_rhs(int nt, int ns, double dt, const double* f, const double* u0, double* b) {
+  return guarded([&] {
+    const std::size_t N = static_cast<std::size_t>(nt) * ns;
+    auto r = fracpint::assemble_rhs(fracpint::TimeStencil(nt), dt, {f, N},
+                                    {u0, static_cast<std::size_t>(ns)});
+    std::copy(r.begin(), r.end(), b);
+  });
+}
+
+// alpha <= 0 selects PreconditionerKind::generalized().
+int ref_build_plan(void* hp, double alpha, double* min_margin, double* alpha_out) {
+  auto* p = static_cast<RefProblem*>(hp);
+  return guarded([&] {
+    const auto kind = alpha <= 0.0 ? fracpint::PreconditionerKind::generalized()
+                                   : fracpint::PreconditionerKind::with_alpha(alpha);
+    std::visit([&](const auto& o) { p->plan = fracpint::build_plan(kind, p->nt, p->dt, o.jacobian()); },
+               p->op);
+    if (min_margin) *min_margin = p->plan->min_shift_margin;
+    if (alpha_out) *alpha_out = p->plan->alpha;
+  });
+}
+
+int ref_tau_sigma(void* hp, double* sigma) {
+  auto* p = static_cast<RefProblem*>(hp);
+  if (!p->plan) return 1;
+  std::copy(p->plan->tau.sigma.begin(), p->plan->tau.sigma.end(), sigma);
+  return 0;
+}
+
+int ref_pc_apply(void* hp, const double* v, double* out, int full_sweep) {
+  auto* p = static_cast<RefProblem*>(hp);
+  const std::size_t n = p->dim();
+  return guarded([&] {
+    if (!p->plan) throw std::invalid_argument("no plan");
+    fracpint::apply_inverse(*p->plan, {v, n}, {out, n},
+                            full_sweep ? fracpint::InnerSweep::full : fracpint::InnerSweep::half);
+  });
+}
+int ref_pc_forward(void* hp, const double* v, double* out) {
+  auto* p = static_cast<RefProblem*>(hp);
+  const std::size_t n = p->dim();
+  return guarded([&] {
+    if (!p->plan) throw std::invalid_argument("no plan");
+    fracpint::apply_forward(*p->plan, {v, n}, {out, n});
+  });
+}
+
+// Unrestarted gmres_right exactly as driver.hpp:62-73 wires it.  Returns seconds =
+// report.seconds (the reference's own timed span krylov.hpp:87-190).
+int ref_gmres(void* hp, const double* b, double* x, double tol, int max_iter, int* converged,
+              int* iterations, double* final_rel, double* true_rel, double* seconds,
+              double* history, int history_cap, int* history_len) {
+  auto* p = static_cast<RefProblem*>(hp);
+  const std::size_t n = p->dim();
+  return guarded([&] {
+    if (!p->plan) throw std::invalid_argument("no plan");
+    fracpint::SolverConfig cfg;
+    cfg.tol = tol;
+    cfg.max_iter = max_iter;
+    auto apply_pinv = [p](std::span<const double> in, std::span<double> out) {
+      fracpint::apply_inverse(*p->plan, in, out);
+    };
+    fracpint::KrylovResult r = std::visit(
+        [&](const auto& o) {
+          auto apply_a = [&o](std::span<const double> in, std::span<double> out) { o.apply(in, out); };
+          return fracpint::gmres_right(n, apply_a, apply_pinv, {b, n}, cfg);
+        },
+        p->op);
+    std::copy(r.x.begin(), r.x.end(), x);
+    *converged = r.report.converged ? 1 : 0;
+    *iterations = static_cast<int>(r.report.iterations);
+    *final_rel = r.report.final_relative_residual;
+    *true_rel = r.report.true_relative_residual;
+    *seconds = r.report.seconds;
+    const int h = static_cast<int>(r.report.residual_history.size());
+    *history_len = h;
+    for (int i = 0; i < h && i < history_cap; ++i) history[i] = r.report.residual_history[i];
+  });
+}
+
+}  // extern "C"
