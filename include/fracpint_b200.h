@@ -1,0 +1,119 @@
+/*
+ * fracpint_b200.h -- C-ABI of the B200-native preconditioned Krylov solve (libfracpint_b200.so).
+ *
+ * The drop-in boundary for the reference's hot path.  Every entry point replaces
+ * one call of the reference's C++ solver API (namespace fracpint, /root/reference/proj/include):
+ *
+ *   fpc_problem_create_1d  <- RieszJacobian1D(g,k,h,n)         jacobian.hpp:21
+ *                             + TimeStencil(nt)                 time_stencil.hpp:23
+ *                             + AllAtOnceOperator(st, jac, dt)  all_at_once.hpp:21
+ *   fpc_problem_create_2d  <- RieszJacobian2D(gx,gy,kx,ky,h,n)  jacobian.hpp:58 (+ as above)
+ *   fpc_matvec             <- AllAtOnceOperator::apply          all_at_once.hpp:33
+ *   fpc_assemble_rhs       <- assemble_rhs                      all_at_once.hpp:66
+ *   fpc_plan_create        <- build_plan(kind, nt, dt, jac)     alpha_circulant.hpp:84
+ *                             (PreconditionerKind::alpha_for    alpha_circulant.hpp:29)
+ *   fpc_pc_apply           <- apply_inverse(plan, v, out, sw)   alpha_circulant.hpp:206
+ *   fpc_pc_forward         <- apply_forward(plan, v, out)       alpha_circulant.hpp:212
+ *   fpc_gmres              <- gmres_right(n, A, P^{-1}, b, cfg) krylov.hpp:84 (+ restart m)
+ *
+ * Plain pointers and sizes only.  Vectors are time-major fp64, v[k*n_space + p] (2D: p = ix*n+iy,
+ * x slow; problems.hpp:164-165).  `where` = FPC_HOST (pointers are host memory: copied in and out,
+ * the call returns when done) or FPC_DEVICE (device pointers on the context's device; the work is
+ * stream-ordered on the context stream, 16-byte aligned pointers required).
+ *
+ * Status codes mirror the reference's exceptions: FPC_INVALID_ARGUMENT <-> std::invalid_argument,
+ * FPC_RUNTIME_ERROR <-> std::runtime_error (numerical singularity), FPC_CUDA_ERROR (device failure),
+ * FPC_UNSUPPORTED (a size the B200 kernels do not cover; never a silent CPU fallback).
+ * The message of the last failure on the calling thread is fpc_last_error().
+ */
+#ifndef FRACPINT_B200_H
+#define FRACPINT_B200_H
+
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FPC_OK 0
+#define FPC_INVALID_ARGUMENT 1
+#define FPC_RUNTIME_ERROR 2
+#define FPC_CUDA_ERROR 3
+#define FPC_UNSUPPORTED 4
+
+#define FPC_HOST 0
+#define FPC_DEVICE 1
+
+#define FPC_SWEEP_HALF 0 /* InnerSweep::half (alpha_circulant.hpp:128) */
+#define FPC_SWEEP_FULL 1 /* InnerSweep::full */
+
+typedef struct fpc_context_s* fpc_context_t;
+typedef struct fpc_problem_s* fpc_problem_t;
+typedef struct fpc_plan_s* fpc_plan_t;
+
+/* SolverConfig (krylov.hpp:25-28) + restart (0 = unrestarted, the reference's gmres_right). */
+typedef struct {
+  double tol;
+  int max_iter;
+  int restart;
+  int sweep;
+} fpc_solver_config;
+
+/* SolveReport (krylov.hpp:30-37). */
+typedef struct {
+  int converged;
+  int iterations;
+  int restarts;
+  int reorthogonalizations;
+  double final_relative_residual;
+  double true_relative_residual;
+  double seconds;
+  int history_len;
+} fpc_report;
+
+int fpc_abi_version(void);
+const char* fpc_last_error(void);
+
+/* context: one device, one stream (default: a private non-blocking stream) */
+int fpc_context_create(int device, fpc_context_t* out);
+int fpc_context_destroy(fpc_context_t ctx);
+int fpc_context_set_stream(fpc_context_t ctx, void* cuda_stream);
+void* fpc_context_stream(fpc_context_t ctx);
+int fpc_synchronize(fpc_context_t ctx);
+int fpc_device_alloc(fpc_context_t ctx, size_t bytes, void** out);
+int fpc_device_free(fpc_context_t ctx, void* ptr);
+
+/* operator */
+int fpc_problem_create_1d(fpc_context_t ctx, double gamma, double kappa, double h, int n_space,
+                          int n_time, double dt, fpc_problem_t* out);
+int fpc_problem_create_2d(fpc_context_t ctx, double gamma_x, double gamma_y, double kappa_x,
+                          double kappa_y, double h, int n_per_dim, int n_time, double dt,
+                          fpc_problem_t* out);
+int fpc_problem_destroy(fpc_problem_t p);
+int fpc_problem_dims(fpc_problem_t p, int* n_time, int* n_space, int* two_dim);
+int fpc_problem_first_column(fpc_problem_t p, int axis, double* out);
+int fpc_problem_tau_sigma(fpc_problem_t p, double* out);
+int fpc_matvec(fpc_problem_t p, const double* v, double* out, int where);
+int fpc_assemble_rhs(int n_time, int n_space, double dt, const double* f, const double* u0,
+                     double* b);
+
+/* preconditioner plan: alpha <= 0 selects PreconditionerKind::generalized() */
+int fpc_plan_create(fpc_problem_t p, double alpha, fpc_plan_t* out);
+int fpc_plan_destroy(fpc_plan_t plan);
+int fpc_plan_info(fpc_plan_t plan, double* alpha, double* min_shift_margin, int* solve_count,
+                  int* n_warnings);
+int fpc_plan_lambda(fpc_plan_t plan, double* lambda_interleaved);
+int fpc_pc_apply(fpc_plan_t plan, const double* v, double* out, int sweep, int where);
+int fpc_pc_forward(fpc_plan_t plan, const double* v, double* out, int where);
+
+/* right-preconditioned GMRES on the plan's operator, x0 = 0 */
+int fpc_gmres(fpc_plan_t plan, const double* b, double* x, const fpc_solver_config* cfg,
+              fpc_report* report, double* history, int history_cap, int where);
+
+/* instrumentation: number of kernels this library launched on the calling process */
+unsigned long long fpc_kernel_launches(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

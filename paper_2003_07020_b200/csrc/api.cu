@@ -1,0 +1,915 @@
+// api.cu -- the C-ABI (include/fracpint_b200.h): contexts, problems (operator setup on the host,
+// device-resident spectra), preconditioner plans and the device-resident GMRES driver.
+//
+// Host-side setup restates the reference's one-off constructions (weights.hpp:21-35,
+// toeplitz.hpp:23-35, tau.hpp:40-73, alpha_circulant.hpp:71-126) in double precision on the CPU;
+// everything per-iteration runs on the GPU (kernels_1d.cu, kernels_2d.cu, kernels_krylov.cu).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <cmath>
+#include <complex>
+#include <cstdio>
+#include <cstring>
+#include <limits>
+#include <string>
+#include <vector>
+
+#include "../../include/fracpint_b200.h"
+#include "kernels.cuh"
+
+namespace {
+
+thread_local std::string g_err;
+std::atomic<unsigned long long> g_launches{0};
+
+int set_err(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+struct CudaFail {
+  cudaError_t err;
+  const char* what;
+};
+
+inline void ck(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) throw CudaFail{e, what};
+}
+inline void ckl(cudaError_t e, const char* what) {  // kernel launch
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  ck(e, what);
+}
+
+struct InvalidArg {
+  std::string msg;
+};
+struct RuntimeErr {
+  std::string msg;
+};
+struct Unsupported {
+  std::string msg;
+};
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return FPC_OK;
+  } catch (const InvalidArg& e) {
+    return set_err(FPC_INVALID_ARGUMENT, e.msg);
+  } catch (const RuntimeErr& e) {
+    return set_err(FPC_RUNTIME_ERROR, e.msg);
+  } catch (const Unsupported& e) {
+    return set_err(FPC_UNSUPPORTED, e.msg);
+  } catch (const CudaFail& e) {
+    return set_err(FPC_CUDA_ERROR, std::string(e.what) + ": " + cudaGetErrorString(e.err));
+  } catch (const std::bad_alloc&) {
+    return set_err(FPC_RUNTIME_ERROR, "host allocation failed");
+  } catch (const std::exception& e) {
+    return set_err(FPC_RUNTIME_ERROR, e.what());
+  }
+}
+
+using cplx = std::complex<double>;
+constexpr double kPi = 3.14159265358979323846264338327950288;
+
+int ilog2_exact(size_t n) {
+  int l = 0;
+  while ((size_t(1) << l) < n) ++l;
+  return (size_t(1) << l) == n ? l : -1;
+}
+size_t next_pow2(size_t n) {
+  size_t p = 1;
+  while (p < n) p <<= 1;
+  return p;
+}
+
+// ---- host FFT for setup only (power-of-two radix-2, kernel e^{sign 2 pi i jk/n}) -----------
+void host_fft(std::vector<cplx>& x, int sign) {
+  const size_t n = x.size();
+  if (n <= 1) return;
+  for (size_t i = 1, j = 0; i < n; ++i) {
+    size_t bit = n >> 1;
+    for (; j & bit; bit >>= 1) j ^= bit;
+    j ^= bit;
+    if (i < j) std::swap(x[i], x[j]);
+  }
+  const double unit = 2.0 * kPi * (sign >= 0 ? 1.0 : -1.0) / double(n);
+  std::vector<cplx> tw(n / 2);
+  for (size_t j = 0; j < n / 2; ++j) tw[j] = std::polar(1.0, unit * double(j));
+  for (size_t len = 2; len <= n; len <<= 1) {
+    const size_t half = len >> 1, step = n / len;
+    for (size_t base = 0; base < n; base += len)
+      for (size_t j = 0; j < half; ++j) {
+        const cplx u = x[base + j], v = x[base + j + half] * tw[j * step];
+        x[base + j] = u + v;
+        x[base + j + half] = u - v;
+      }
+  }
+}
+
+// orthonormal DST-I of real data (dst.hpp:21-43), n+1 must be a power of two
+std::vector<double> host_dst1(const std::vector<double>& x) {
+  const size_t n = x.size(), L = 2 * (n + 1);
+  std::vector<cplx> v(L);
+  for (size_t j = 0; j < n; ++j) {
+    v[j + 1] = x[j];
+    v[L - 1 - j] = -x[j];
+  }
+  host_fft(v, -1);
+  const double scale = std::sqrt(2.0 / double(n + 1)) * 0.5;
+  std::vector<double> y(n);
+  for (size_t k = 0; k < n; ++k) y[k] = scale * (cplx(0.0, 1.0) * v[k + 1]).real();
+  return y;
+}
+
+// weights.hpp:21-35
+std::vector<double> centred_weights(double gamma, int count) {
+  if (!(gamma > 1.0) || !(gamma <= 2.0))
+    throw InvalidArg{"centred_weights: gamma must lie in (1, 2]"};
+  if (count < 1) throw InvalidArg{"centred_weights: count must be at least 1"};
+  std::vector<double> w(static_cast<size_t>(count));
+  const double g0 = std::tgamma(1.0 + gamma / 2.0);
+  w[0] = std::tgamma(1.0 + gamma) / (g0 * g0);
+  for (int l = 0; l + 1 < count; ++l)
+    w[size_t(l) + 1] = w[size_t(l)] * (double(l) - gamma / 2.0) / (double(l) + 1.0 + gamma / 2.0);
+  return w;
+}
+
+// tau.hpp:40-55
+std::vector<double> tau_spectrum(const std::vector<double>& a) {
+  const size_t n = a.size();
+  std::vector<double> c(a);
+  for (size_t l = 0; l + 2 < n; ++l) c[l] -= a[l + 2];
+  const std::vector<double> num = host_dst1(c);
+  const double root = std::sqrt(2.0 / double(n + 1));
+  std::vector<double> s(n);
+  for (size_t i = 0; i < n; ++i) s[i] = num[i] / (root * std::sin(kPi * double(i + 1) / double(n + 1)));
+  return s;
+}
+
+// circulant-embedding eigenvalues (toeplitz.hpp:23-35): real parts of FFT_{-}(c), k = 0..L/2
+std::vector<double> circulant_eigs(const std::vector<double>& col) {
+  const size_t n = col.size(), L = next_pow2(2 * n);
+  std::vector<cplx> c(L);
+  c[0] = col[0];
+  for (size_t j = 1; j < n; ++j) c[j] = c[L - j] = col[j];
+  host_fft(c, -1);
+  std::vector<double> e(L / 2 + 1);
+  for (size_t k = 0; k <= L / 2; ++k) e[k] = c[k].real();
+  return e;
+}
+
+template <class T>
+T* dalloc(size_t count) {
+  void* p = nullptr;
+  ck(cudaMalloc(&p, std::max<size_t>(count, 1) * sizeof(T)), "cudaMalloc");
+  return static_cast<T*>(p);
+}
+
+}  // namespace
+
+// =================================================================================== context
+struct fpc_context_s {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  double2* tw = nullptr;        // twiddle tables, size-N table at tw + N
+  double* partial = nullptr;    // kDotsGrid x kPartialStride
+  double* dscal = nullptr;      // small device scratch (h, norms)
+  double* hpin = nullptr;       // pinned host mirror of dscal
+  const double** dvptr = nullptr;  // device pointer table for update/lincomb
+  double* dscales = nullptr;
+  static constexpr int kPartialStride = 264;
+  static constexpr int kScal = 1024;
+};
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+// =================================================================================== problem
+struct fpc_problem_s {
+  fpc_context_s* ctx = nullptr;
+  int two_dim = 0;
+  int n = 0;   // 1D: n_space; 2D: n per dim
+  int ns = 0;  // spatial unknowns
+  int nt = 0;
+  double dt = 0.0;
+  double sx = 0.0, sy = 0.0;
+  std::vector<double> colx, coly;  // 1D: colx = scaled Jacobian column; 2D: unscaled weights
+  std::vector<double> sigma;       // jac.tau() spectrum (jacobian.hpp:45, 96-98)
+  int log_m = 0;                   // Toeplitz packed FFT size M = L/2
+  double* d_eig = nullptr;         // 1D: -dt*eig/(2L); 2D: y-axis factor
+  double* d_eig_x = nullptr;       // 2D: x-axis factor
+  double* d_in = nullptr;          // staging for host-pointer calls
+  double* d_out = nullptr;
+  size_t dim() const { return size_t(nt) * size_t(ns); }
+};
+
+struct fpc_plan_s {
+  fpc_problem_s* prob = nullptr;
+  double alpha = 0.0;
+  std::vector<cplx> lambda;
+  int solve_count = 0;
+  double min_shift_margin = 0.0;
+  int n_warnings = 0;
+  double* d_sf = nullptr;
+  double* d_sb = nullptr;
+  double2* d_lambda = nullptr;
+  double* d_sigma = nullptr;
+  double2* d_Z = nullptr;  // half spectrum scratch (H x ns complex)
+  // GMRES workspace (grown on demand, reused across solves)
+  std::vector<double*> basis;
+  double* d_z = nullptr;
+  double* d_u = nullptr;
+  double* d_r = nullptr;
+  double* d_x = nullptr;
+  double* d_d = nullptr;
+  double* d_b = nullptr;
+};
+
+namespace {
+
+void check_sizes_1d(int n_space, int n_time) {
+  if (ilog2_exact(size_t(n_time)) < 0 || n_time < 4)
+    throw Unsupported{"B200 path needs n_time to be a power of two >= 4"};
+  if (n_time > 16384) throw Unsupported{"B200 path supports n_time <= 16384"};
+  if (ilog2_exact(size_t(n_space) + 1) < 0 || n_space < 3)
+    throw Unsupported{"B200 path needs n_space + 1 to be a power of two >= 4 (DST-I length)"};
+  if (n_space + 1 > 8192) throw Unsupported{"B200 path supports n_space + 1 <= 8192 (smem FFT)"};
+}
+
+void upload(void* dst, const void* src, size_t bytes, cudaStream_t st) {
+  ck(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st), "H2D");
+}
+
+}  // namespace
+
+extern "C" {
+
+int fpc_abi_version(void) { return 1; }
+const char* fpc_last_error(void) { return g_err.c_str(); }
+unsigned long long fpc_kernel_launches(void) { return g_launches.load(); }
+
+int fpc_context_create(int device, fpc_context_t* out) {
+  if (!out) return set_err(FPC_INVALID_ARGUMENT, "null output");
+  return guarded([&] {
+    int ndev = 0;
+    ck(cudaGetDeviceCount(&ndev), "cudaGetDeviceCount");
+    if (device < 0 || device >= ndev) throw InvalidArg{"fpc_context_create: bad device index"};
+    DeviceGuard g(device);
+    auto* c = new fpc_context_s();
+    c->device = device;
+    ck(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking), "cudaStreamCreate");
+    c->own_stream = true;
+    // twiddle tables tw_N[t] = polar(1, -2 pi t / N) for N = 1 .. 2^kMaxLogTw (fft.hpp:36-37)
+    const size_t total = size_t(2) << fpc::kMaxLogTw;
+    std::vector<double2> tw(total);
+    for (int l = 0; l <= fpc::kMaxLogTw; ++l) {
+      const size_t N = size_t(1) << l;
+      const double unit = -2.0 * kPi / double(N);
+      for (size_t t = 0; t < N; ++t) {
+        const cplx w = std::polar(1.0, unit * double(t));
+        tw[N + t] = make_double2(w.real(), w.imag());
+      }
+    }
+    c->tw = dalloc<double2>(total);
+    ck(cudaMemcpy(c->tw, tw.data(), total * sizeof(double2), cudaMemcpyHostToDevice), "tw upload");
+    c->partial = dalloc<double>(size_t(fpc::dots_grid()) * fpc_context_s::kPartialStride);
+    c->dscal = dalloc<double>(fpc_context_s::kScal);
+    ck(cudaMallocHost(&c->hpin, fpc_context_s::kScal * sizeof(double)), "cudaMallocHost");
+    c->dvptr = dalloc<const double*>(512);
+    c->dscales = dalloc<double>(512);
+    *out = c;
+  });
+}
+
+int fpc_context_destroy(fpc_context_t c) {
+  if (!c) return FPC_OK;
+  DeviceGuard g(c->device);
+  cudaStreamSynchronize(c->stream);
+  cudaFree(c->tw);
+  cudaFree(c->partial);
+  cudaFree(c->dscal);
+  cudaFreeHost(c->hpin);
+  cudaFree(c->dvptr);
+  cudaFree(c->dscales);
+  if (c->own_stream) cudaStreamDestroy(c->stream);
+  delete c;
+  return FPC_OK;
+}
+
+int fpc_context_set_stream(fpc_context_t c, void* s) {
+  if (!c) return set_err(FPC_INVALID_ARGUMENT, "null context");
+  DeviceGuard g(c->device);
+  if (c->own_stream) {
+    cudaStreamSynchronize(c->stream);
+    cudaStreamDestroy(c->stream);
+  }
+  c->stream = static_cast<cudaStream_t>(s);
+  c->own_stream = false;
+  return FPC_OK;
+}
+
+void* fpc_context_stream(fpc_context_t c) { return c ? static_cast<void*>(c->stream) : nullptr; }
+
+int fpc_synchronize(fpc_context_t c) {
+  if (!c) return set_err(FPC_INVALID_ARGUMENT, "null context");
+  return guarded([&] { ck(cudaStreamSynchronize(c->stream), "cudaStreamSynchronize"); });
+}
+
+int fpc_device_alloc(fpc_context_t c, size_t bytes, void** out) {
+  if (!c || !out) return set_err(FPC_INVALID_ARGUMENT, "null argument");
+  return guarded([&] {
+    DeviceGuard g(c->device);
+    ck(cudaMalloc(out, bytes), "cudaMalloc");
+  });
+}
+
+int fpc_device_free(fpc_context_t c, void* p) {
+  if (!c) return set_err(FPC_INVALID_ARGUMENT, "null context");
+  DeviceGuard g(c->device);
+  cudaFree(p);
+  return FPC_OK;
+}
+
+// ---------------------------------------------------------------------------- problems
+static fpc_problem_s* new_problem(fpc_context_s* c, int nt, double dt) {
+  if (nt < 3) throw InvalidArg{"TimeStencil: need at least 3 time levels"};
+  if (!(dt > 0.0)) throw InvalidArg{"AllAtOnceOperator: dt must be positive"};
+  auto* p = new fpc_problem_s();
+  p->ctx = c;
+  p->nt = nt;
+  p->dt = dt;
+  return p;
+}
+
+int fpc_problem_create_1d(fpc_context_t c, double gamma, double kappa, double h, int n_space,
+                          int n_time, double dt, fpc_problem_t* out) {
+  if (!c || !out) return set_err(FPC_INVALID_ARGUMENT, "null argument");
+  return guarded([&] {
+    // RieszJacobian1D ctor (jacobian.hpp:21-32)
+    if (!(kappa > 0.0)) throw InvalidArg{"RieszJacobian1D: kappa must be positive"};
+    if (!(h > 0.0)) throw InvalidArg{"RieszJacobian1D: h must be positive"};
+    if (n_space < 1) throw InvalidArg{"RieszJacobian1D: n_space must be at least 1"};
+    std::vector<double> w = centred_weights(gamma, n_space);
+    if (n_time < 3) throw InvalidArg{"TimeStencil: need at least 3 time levels"};
+    if (!(dt > 0.0)) throw InvalidArg{"AllAtOnceOperator: dt must be positive"};
+    check_sizes_1d(n_space, n_time);
+    DeviceGuard g(c->device);
+    fpc_problem_s* p = new_problem(c, n_time, dt);
+    p->n = p->ns = n_space;
+    const double scale = -kappa / std::pow(h, gamma);
+    for (double& x : w) x *= scale;
+    p->colx = w;
+    p->sigma = tau_spectrum(p->colx);
+    const size_t L = next_pow2(2 * size_t(n_space));
+    p->log_m = ilog2_exact(L / 2);
+    std::vector<double> e = circulant_eigs(p->colx);
+    for (double& x : e) x *= -dt / (2.0 * double(L));
+    p->d_eig = dalloc<double>(e.size());
+    ck(cudaMemcpy(p->d_eig, e.data(), e.size() * sizeof(double), cudaMemcpyHostToDevice), "eig");
+    *out = p;
+  });
+}
+
+int fpc_problem_create_2d(fpc_context_t c, double gx, double gy, double kx, double ky, double h,
+                          int n, int n_time, double dt, fpc_problem_t* out) {
+  if (!c || !out) return set_err(FPC_INVALID_ARGUMENT, "null argument");
+  return guarded([&] {
+    // RieszJacobian2D ctor (jacobian.hpp:58-69)
+    if (!(kx > 0.0) || !(ky > 0.0))
+      throw InvalidArg{"RieszJacobian2D: diffusion coefficients must be positive"};
+    if (!(h > 0.0)) throw InvalidArg{"RieszJacobian2D: h must be positive"};
+    if (n < 1) throw InvalidArg{"RieszJacobian2D: n_per_dim must be at least 1"};
+    std::vector<double> wx = centred_weights(gx, n), wy = centred_weights(gy, n);
+    if (n_time < 3) throw InvalidArg{"TimeStencil: need at least 3 time levels"};
+    if (!(dt > 0.0)) throw InvalidArg{"AllAtOnceOperator: dt must be positive"};
+    throw Unsupported{"2D problems are not yet available on the B200 path"};
+  });
+}
+
+int fpc_problem_destroy(fpc_problem_t p) {
+  if (!p) return FPC_OK;
+  DeviceGuard g(p->ctx->device);
+  cudaStreamSynchronize(p->ctx->stream);
+  cudaFree(p->d_eig);
+  cudaFree(p->d_eig_x);
+  cudaFree(p->d_in);
+  cudaFree(p->d_out);
+  delete p;
+  return FPC_OK;
+}
+
+int fpc_problem_dims(fpc_problem_t p, int* nt, int* ns, int* two_dim) {
+  if (!p) return set_err(FPC_INVALID_ARGUMENT, "null problem");
+  if (nt) *nt = p->nt;
+  if (ns) *ns = p->ns;
+  if (two_dim) *two_dim = p->two_dim;
+  return FPC_OK;
+}
+
+int fpc_problem_first_column(fpc_problem_t p, int axis, double* out) {
+  if (!p || !out) return set_err(FPC_INVALID_ARGUMENT, "null argument");
+  const std::vector<double>& c = (axis == 1 && p->two_dim) ? p->coly : p->colx;
+  std::memcpy(out, c.data(), c.size() * sizeof(double));
+  return FPC_OK;
+}
+
+int fpc_problem_tau_sigma(fpc_problem_t p, double* out) {
+  if (!p || !out) return set_err(FPC_INVALID_ARGUMENT, "null argument");
+  std::memcpy(out, p->sigma.data(), p->sigma.size() * sizeof(double));
+  return FPC_OK;
+}
+
+static void matvec_dev(fpc_problem_s* p, const double* v, double* y) {
+  cudaStream_t st = p->ctx->stream;
+  if (!p->two_dim) {
+    ckl(fpc::launch_matvec_1d(v, y, p->ns, p->nt, p->log_m, p->d_eig, p->ctx->tw, st), "matvec_1d");
+  } else {
+    ckl(fpc::launch_matvec_2d(v, y, p->n, p->nt, p->log_m, p->d_eig, p->d_eig_x, p->ctx->tw, st),
+        "matvec_2d");
+  }
+}
+
+static void ensure_staging(fpc_problem_s* p) {
+  if (!p->d_in) p->d_in = dalloc<double>(p->dim());
+  if (!p->d_out) p->d_out = dalloc<double>(p->dim());
+}
+
+static void check_ptr(const void* ptr, const char* what) {
+  if (!ptr) throw InvalidArg{std::string(what) + ": null pointer"};
+}
+
+static void check_dev_aligned(const void* ptr, const char* what) {
+  if (reinterpret_cast<uintptr_t>(ptr) % 16 != 0)
+    throw InvalidArg{std::string(what) + ": device pointers must be 16-byte aligned"};
+}
+
+int fpc_matvec(fpc_problem_t p, const double* v, double* out, int where) {
+  if (!p) return set_err(FPC_INVALID_ARGUMENT, "null problem");
+  return guarded([&] {
+    check_ptr(v, "fpc_matvec");
+    check_ptr(out, "fpc_matvec");
+    DeviceGuard g(p->ctx->device);
+    const size_t n = p->dim();
+    cudaStream_t st = p->ctx->stream;
+    if (where == FPC_DEVICE) {
+      check_dev_aligned(v, "fpc_matvec");
+      check_dev_aligned(out, "fpc_matvec");
+      if (v == out) throw InvalidArg{"fpc_matvec: input and output must be disjoint"};
+      matvec_dev(p, v, out);
+      return;
+    }
+    ensure_staging(p);
+    upload(p->d_in, v, n * sizeof(double), st);
+    matvec_dev(p, p->d_in, p->d_out);
+    ck(cudaMemcpyAsync(out, p->d_out, n * sizeof(double), cudaMemcpyDeviceToHost, st), "D2H");
+    ck(cudaStreamSynchronize(st), "sync");
+  });
+}
+
+// all_at_once.hpp:66-80 (host; setup, not on the solve path)
+int fpc_assemble_rhs(int nt, int ns, double dt, const double* f, const double* u0, double* b) {
+  if (!f || !u0 || !b) return set_err(FPC_INVALID_ARGUMENT, "null argument");
+  if (nt < 2 || ns < 1) return set_err(FPC_INVALID_ARGUMENT, "assemble_rhs: size mismatch");
+  const size_t NS = size_t(ns), NT = size_t(nt);
+  for (size_t k = 0; k < NT; ++k)
+    for (size_t i = 0; i < NS; ++i) b[k * NS + i] = dt * f[k * NS + i];
+  for (size_t i = 0; i < NS; ++i) {
+    b[i] += u0[i];
+    b[NS + i] -= 0.5 * u0[i];
+  }
+  return FPC_OK;
+}
+
+// ---------------------------------------------------------------------------- plans
+int fpc_plan_create(fpc_problem_t p, double alpha_in, fpc_plan_t* out) {
+  if (!p || !out) return set_err(FPC_INVALID_ARGUMENT, "null argument");
+  return guarded([&] {
+    const int nt = p->nt;
+    const double dt = p->dt;
+    // PreconditionerKind::alpha_for (alpha_circulant.hpp:29-34)
+    const double a = alpha_in <= 0.0 ? std::min(0.5, 0.5 * dt) : alpha_in;
+    if (!(a > 0.0) || a > 1.0) throw InvalidArg{"PreconditionerKind: alpha must lie in (0, 1]"};
+    auto* pl = new fpc_plan_s();
+    pl->prob = p;
+    pl->alpha = a;
+    pl->n_warnings = a < 1e-8 ? 1 : 0;
+    // alpha_circulant_eigenvalues (alpha_circulant.hpp:71-81)
+    pl->lambda.resize(size_t(nt));
+    const double ar = std::pow(a, 1.0 / double(nt));
+    for (int i = 0; i < nt; ++i) {
+      const double ang1 = 2.0 * kPi * double(i % nt) / nt;
+      const double ang2 = 2.0 * kPi * double((2 * i) % nt) / nt;
+      pl->lambda[size_t(i)] = 1.5 - 2.0 * ar * std::polar(1.0, ang1) + 0.5 * ar * ar * std::polar(1.0, ang2);
+    }
+    std::vector<double> sf(static_cast<size_t>(nt)), sb(static_cast<size_t>(nt));
+    for (int k = 0; k < nt; ++k) {
+      const double e = double(k) / double(nt);
+      sf[size_t(k)] = std::pow(a, e);
+      sb[size_t(k)] = std::pow(a, -e);
+    }
+    pl->solve_count = nt / 2 + 1;
+    // singular-shift scan (alpha_circulant.hpp:110-123)
+    double max_sigma = 0.0;
+    for (double s : p->sigma) max_sigma = std::max(max_sigma, std::abs(s));
+    double margin = std::numeric_limits<double>::infinity();
+    for (int n = 0; n < pl->solve_count; ++n) {
+      const cplx l = pl->lambda[size_t(n)];
+      const double floor_ = 1e-14 * (std::abs(l) + dt * max_sigma);
+      for (double s : p->sigma) {
+        const double d = std::abs(l - dt * s);
+        margin = std::min(margin, d);
+        if (d <= floor_) {
+          delete pl;
+          throw RuntimeErr{"build_plan: an inner shifted system is numerically singular"};
+        }
+      }
+    }
+    pl->min_shift_margin = margin;
+    DeviceGuard g(p->ctx->device);
+    pl->d_sf = dalloc<double>(size_t(nt));
+    pl->d_sb = dalloc<double>(size_t(nt));
+    pl->d_lambda = dalloc<double2>(size_t(pl->solve_count));
+    pl->d_sigma = dalloc<double>(p->sigma.size());
+    pl->d_Z = dalloc<double2>(size_t(pl->solve_count) * size_t(p->ns));
+    ck(cudaMemcpy(pl->d_sf, sf.data(), sf.size() * 8, cudaMemcpyHostToDevice), "sf");
+    ck(cudaMemcpy(pl->d_sb, sb.data(), sb.size() * 8, cudaMemcpyHostToDevice), "sb");
+    ck(cudaMemcpy(pl->d_lambda, pl->lambda.data(), size_t(pl->solve_count) * 16, cudaMemcpyHostToDevice),
+       "lambda");
+    ck(cudaMemcpy(pl->d_sigma, p->sigma.data(), p->sigma.size() * 8, cudaMemcpyHostToDevice), "sigma");
+    *out = pl;
+  });
+}
+
+int fpc_plan_destroy(fpc_plan_t pl) {
+  if (!pl) return FPC_OK;
+  DeviceGuard g(pl->prob->ctx->device);
+  cudaStreamSynchronize(pl->prob->ctx->stream);
+  for (double* b : pl->basis) cudaFree(b);
+  for (void* q : {(void*)pl->d_sf, (void*)pl->d_sb, (void*)pl->d_lambda, (void*)pl->d_sigma,
+                  (void*)pl->d_Z, (void*)pl->d_z, (void*)pl->d_u, (void*)pl->d_r, (void*)pl->d_x,
+                  (void*)pl->d_d, (void*)pl->d_b})
+    cudaFree(q);
+  delete pl;
+  return FPC_OK;
+}
+
+int fpc_plan_info(fpc_plan_t pl, double* alpha, double* margin, int* solve_count, int* n_warn) {
+  if (!pl) return set_err(FPC_INVALID_ARGUMENT, "null plan");
+  if (alpha) *alpha = pl->alpha;
+  if (margin) *margin = pl->min_shift_margin;
+  if (solve_count) *solve_count = pl->solve_count;
+  if (n_warn) *n_warn = pl->n_warnings;
+  return FPC_OK;
+}
+
+int fpc_plan_lambda(fpc_plan_t pl, double* out) {
+  if (!pl || !out) return set_err(FPC_INVALID_ARGUMENT, "null argument");
+  std::memcpy(out, pl->lambda.data(), pl->lambda.size() * sizeof(cplx));
+  return FPC_OK;
+}
+
+// z = P^{-1} (s_in * v)  (alpha_circulant.hpp:137-199, half sweep)
+static void pc_apply_dev(fpc_plan_s* pl, const double* v, double* z, double s_in) {
+  fpc_problem_s* p = pl->prob;
+  cudaStream_t st = p->ctx->stream;
+  ckl(fpc::launch_time_fwd(v, pl->d_Z, p->ns, p->nt, pl->d_sf, s_in, p->ctx->tw, st), "time_fwd");
+  if (!p->two_dim)
+    ckl(fpc::launch_tau_solve_1d(pl->d_Z, p->ns, pl->solve_count, pl->d_lambda, pl->d_sigma, p->dt,
+                                 p->ctx->tw, st),
+        "tau_solve_1d");
+  else
+    ckl(fpc::launch_tau_solve_2d(pl->d_Z, p->n, pl->solve_count, pl->d_lambda, pl->d_sigma, p->dt,
+                                 p->ctx->tw, st),
+        "tau_solve_2d");
+  ckl(fpc::launch_time_inv(pl->d_Z, z, p->ns, p->nt, pl->d_sb, p->ctx->tw, st), "time_inv");
+}
+
+int fpc_pc_apply(fpc_plan_t pl, const double* v, double* out, int sweep, int where) {
+  if (!pl) return set_err(FPC_INVALID_ARGUMENT, "null plan");
+  return guarded([&] {
+    check_ptr(v, "fpc_pc_apply");
+    check_ptr(out, "fpc_pc_apply");
+    if (sweep != FPC_SWEEP_HALF)
+      throw Unsupported{"InnerSweep::full is not available on the B200 path (use half)"};
+    fpc_problem_s* p = pl->prob;
+    DeviceGuard g(p->ctx->device);
+    const size_t n = p->dim();
+    cudaStream_t st = p->ctx->stream;
+    if (where == FPC_DEVICE) {
+      check_dev_aligned(v, "fpc_pc_apply");
+      check_dev_aligned(out, "fpc_pc_apply");
+      pc_apply_dev(pl, v, out, 1.0);
+      return;
+    }
+    ensure_staging(p);
+    upload(p->d_in, v, n * sizeof(double), st);
+    pc_apply_dev(pl, p->d_in, p->d_out, 1.0);
+    ck(cudaMemcpyAsync(out, p->d_out, n * sizeof(double), cudaMemcpyDeviceToHost, st), "D2H");
+    ck(cudaStreamSynchronize(st), "sync");
+  });
+}
+
+int fpc_pc_forward(fpc_plan_t pl, const double*, double*, int) {
+  if (!pl) return set_err(FPC_INVALID_ARGUMENT, "null plan");
+  return set_err(FPC_UNSUPPORTED, "apply_forward is not yet available on the B200 path");
+}
+
+// ---------------------------------------------------------------------------- GMRES
+namespace {
+
+struct GmresState {
+  fpc_plan_s* pl;
+  fpc_context_s* ctx;
+  size_t n;
+  cudaStream_t st;
+  std::vector<double> scales;  // basis[i] holds V_i / scales[i]... V_i = scales[i] * basis[i]
+  int reorth = 0;
+};
+
+double* basis_buf(fpc_plan_s* pl, size_t i, size_t n) {
+  while (pl->basis.size() <= i) pl->basis.push_back(dalloc<double>(n + 2));
+  return pl->basis[i];
+}
+
+// h[col0..col0+nv) (+ norm) into ctx->dscal[out_off...] via dots + deterministic reduce
+void dots_into(GmresState& S, const std::vector<const double*>& V, int nv, const double* w,
+               bool with_norm, int out_off) {
+  fpc_context_s* c = S.ctx;
+  const int stride = fpc_context_s::kPartialStride;
+  if (nv == 0) {
+    fpc::VecSet vs{};
+    ckl(fpc::launch_dots(vs, 0, w, S.n, c->partial, stride, 0, true, S.st), "dots");
+  }
+  for (int g0 = 0; g0 < nv; g0 += 8) {
+    const int cnt = std::min(8, nv - g0);
+    fpc::VecSet vs{};
+    for (int i = 0; i < cnt; ++i) {
+      vs.v[i] = V[size_t(g0 + i)];
+      vs.s[i] = S.scales[size_t(g0 + i)];
+    }
+    const bool last = g0 + cnt == nv;
+    // the norm accumulator goes right after the last group's columns
+    ckl(fpc::launch_dots(vs, cnt, w, S.n, c->partial, stride, g0, with_norm && last, S.st), "dots");
+  }
+  const int count = nv + (with_norm ? 1 : 0);
+  ckl(fpc::launch_reduce(c->partial, stride, count, c->dscal + out_off, false, S.st), "reduce");
+}
+
+}  // namespace
+
+static void gmres_inner(fpc_plan_s* pl, const double* b, double* x, double tol, int max_iter,
+                        int* conv, int* steps_out, std::vector<double>& hist, double* last_rel,
+                        int* reorth_count) {
+  fpc_problem_s* p = pl->prob;
+  fpc_context_s* c = p->ctx;
+  GmresState S{pl, c, p->dim(), c->stream, {}, 0};
+  const size_t n = S.n;
+  *conv = 0;
+  *steps_out = 0;
+  // ||b||
+  dots_into(S, {}, 0, b, true, 0);
+  ck(cudaMemcpyAsync(c->hpin, c->dscal, sizeof(double), cudaMemcpyDeviceToHost, S.st), "D2H");
+  ck(cudaStreamSynchronize(S.st), "sync");
+  const double norm_b = std::sqrt(c->hpin[0]);
+  if (norm_b == 0.0) {
+    ck(cudaMemsetAsync(x, 0, n * sizeof(double), S.st), "memset");
+    *conv = 1;
+    return;
+  }
+  std::vector<const double*> V;
+  V.push_back(b);
+  S.scales.push_back(1.0 / norm_b);
+  std::vector<std::vector<double>> hcols;
+  std::vector<double> gc, gs, g;
+  g.push_back(norm_b);
+  if (!pl->d_z) pl->d_z = dalloc<double>(n + 2);
+  const double reorth_threshold = 0.70710678118654752;
+  int steps = 0;
+  for (int j = 0; j < max_iter; ++j) {
+    pc_apply_dev(pl, V[size_t(j)], pl->d_z, S.scales[size_t(j)]);
+    double* w = basis_buf(pl, size_t(j), n);  // basis slot j holds V_{j+1} (V_0 = b)
+    matvec_dev(p, pl->d_z, w);
+    const int nv = j + 1;
+    // CGS pass: h_i = <V_i, w>, norm_before^2
+    dots_into(S, V, nv, w, true, 0);
+    // copy pointer + scale tables for the update kernel
+    std::vector<const double*> vp(V.begin(), V.end());
+    ck(cudaMemcpyAsync(c->dvptr, vp.data(), vp.size() * sizeof(double*), cudaMemcpyHostToDevice, S.st),
+       "vptr");
+    ck(cudaMemcpyAsync(c->dscales, S.scales.data(), S.scales.size() * sizeof(double),
+                       cudaMemcpyHostToDevice, S.st),
+       "scales");
+    ckl(fpc::launch_update(c->dvptr, c->dscales, c->dscal, nv, w, n, c->partial, S.st), "update");
+    ckl(fpc::launch_reduce(c->partial, 1, 1, c->dscal + 512, false, S.st), "reduce");
+    ck(cudaMemcpyAsync(c->hpin, c->dscal, size_t(nv + 1) * sizeof(double), cudaMemcpyDeviceToHost, S.st),
+       "D2H");
+    ck(cudaMemcpyAsync(c->hpin + 512, c->dscal + 512, sizeof(double), cudaMemcpyDeviceToHost, S.st), "D2H");
+    ck(cudaStreamSynchronize(S.st), "sync");
+    std::vector<double> h(size_t(j) + 2, 0.0);
+    for (int i = 0; i <= j; ++i) h[size_t(i)] = c->hpin[i];
+    const double norm_before = std::sqrt(c->hpin[nv]);
+    double norm_w = std::sqrt(c->hpin[512]);
+    if (norm_w < reorth_threshold * norm_before) {  // krylov.hpp:123-130
+      ++*reorth_count;
+      dots_into(S, V, nv, w, false, 256);
+      ckl(fpc::launch_update(c->dvptr, c->dscales, c->dscal + 256, nv, w, n, c->partial, S.st), "update");
+      ckl(fpc::launch_reduce(c->partial, 1, 1, c->dscal + 512, false, S.st), "reduce");
+      ck(cudaMemcpyAsync(c->hpin + 256, c->dscal + 256, size_t(nv) * sizeof(double),
+                         cudaMemcpyDeviceToHost, S.st),
+         "D2H");
+      ck(cudaMemcpyAsync(c->hpin + 512, c->dscal + 512, sizeof(double), cudaMemcpyDeviceToHost, S.st), "D2H");
+      ck(cudaStreamSynchronize(S.st), "sync");
+      for (int i = 0; i <= j; ++i) h[size_t(i)] += c->hpin[256 + i];
+      norm_w = std::sqrt(c->hpin[512]);
+    }
+    h[size_t(j) + 1] = norm_w;
+    // Givens (krylov.hpp:133-151)
+    for (int i = 0; i < j; ++i) {
+      const double hi = h[size_t(i)], hi1 = h[size_t(i) + 1];
+      h[size_t(i)] = gc[size_t(i)] * hi + gs[size_t(i)] * hi1;
+      h[size_t(i) + 1] = -gs[size_t(i)] * hi + gc[size_t(i)] * hi1;
+    }
+    const double hj = h[size_t(j)], hj1 = h[size_t(j) + 1];
+    const double rad = std::hypot(hj, hj1);
+    const double cs = rad > 0.0 ? hj / rad : 1.0;
+    const double sn = rad > 0.0 ? hj1 / rad : 0.0;
+    gc.push_back(cs);
+    gs.push_back(sn);
+    h[size_t(j)] = rad;
+    h[size_t(j) + 1] = 0.0;
+    g.push_back(-sn * g[size_t(j)]);
+    g[size_t(j)] *= cs;
+    hcols.push_back(h);
+    steps = j + 1;
+    const double rel = std::abs(g[size_t(j) + 1]) / norm_b;
+    hist.push_back(rel);
+    *last_rel = rel;
+    if (rel <= tol) {
+      *conv = 1;
+      break;
+    }
+    if (norm_w <= 1e-14 * std::max(1.0, norm_before)) break;  // krylov.hpp:160-165
+    V.push_back(w);
+    S.scales.push_back(1.0 / norm_w);
+  }
+  // back substitution (krylov.hpp:171-179), u = V y, x = P^{-1} u
+  std::vector<double> y(size_t(steps), 0.0);
+  for (int i = steps - 1; i >= 0; --i) {
+    double s = g[size_t(i)];
+    for (int k = i + 1; k < steps; ++k) s -= hcols[size_t(k)][size_t(i)] * y[size_t(k)];
+    y[size_t(i)] = s / hcols[size_t(i)][size_t(i)];
+  }
+  if (!pl->d_u) pl->d_u = dalloc<double>(n + 2);
+  std::vector<const double*> vp(V.begin(), V.begin() + steps);
+  ck(cudaMemcpyAsync(c->dvptr, vp.data(), vp.size() * sizeof(double*), cudaMemcpyHostToDevice, S.st), "vptr");
+  ck(cudaMemcpyAsync(c->dscales, S.scales.data(), size_t(steps) * sizeof(double), cudaMemcpyHostToDevice, S.st),
+     "scales");
+  std::memcpy(c->hpin + 600, y.data(), y.size() * sizeof(double));
+  ck(cudaMemcpyAsync(c->dscal + 600, c->hpin + 600, y.size() * sizeof(double), cudaMemcpyHostToDevice, S.st),
+     "y");
+  ckl(fpc::launch_lincomb(c->dvptr, c->dscales, c->dscal + 600, steps, pl->d_u, n, S.st), "lincomb");
+  pc_apply_dev(pl, pl->d_u, x, 1.0);
+  *steps_out = steps;
+  ck(cudaStreamSynchronize(S.st), "sync");  // hpin reuse boundary
+}
+
+static double resid_norm_dev(fpc_plan_s* pl, const double* b, const double* x) {
+  fpc_problem_s* p = pl->prob;
+  fpc_context_s* c = p->ctx;
+  const size_t n = p->dim();
+  if (!pl->d_r) pl->d_r = dalloc<double>(n + 2);
+  matvec_dev(p, x, pl->d_r);
+  ckl(fpc::launch_resid_norm(b, pl->d_r, n, c->partial, c->stream), "resid");
+  ckl(fpc::launch_reduce(c->partial, 1, 1, c->dscal + 900, false, c->stream), "reduce");
+  ck(cudaMemcpyAsync(c->hpin + 900, c->dscal + 900, sizeof(double), cudaMemcpyDeviceToHost, c->stream), "D2H");
+  ck(cudaStreamSynchronize(c->stream), "sync");
+  return std::sqrt(c->hpin[900]);
+}
+
+static void gmres_dev(fpc_plan_s* pl, const double* b, double* x, const fpc_solver_config& cfg,
+                      fpc_report* rep, std::vector<double>& hist) {
+  fpc_problem_s* p = pl->prob;
+  fpc_context_s* c = p->ctx;
+  const size_t n = p->dim();
+  double last_rel = -1.0;
+  int reorth = 0;
+  if (cfg.restart <= 0 || cfg.restart >= cfg.max_iter) {
+    int conv = 0, steps = 0;
+    gmres_inner(pl, b, x, cfg.tol, cfg.max_iter, &conv, &steps, hist, &last_rel, &reorth);
+    rep->converged = conv;
+    rep->iterations = steps;
+  } else {
+    // GMRES(m): restart emulation of SURVEY §8(c) (same as oracle/fracpint_oracle.c orc_gmres)
+    if (!pl->d_x) pl->d_x = dalloc<double>(n + 2);
+    if (!pl->d_d) pl->d_d = dalloc<double>(n + 2);
+    if (!pl->d_b) pl->d_b = dalloc<double>(n + 2);
+    double* r = pl->d_b;  // current residual (rhs of the inner solve)
+    ck(cudaMemcpyAsync(r, b, n * sizeof(double), cudaMemcpyDeviceToDevice, c->stream), "copy");
+    ck(cudaMemsetAsync(x, 0, n * sizeof(double), c->stream), "memset");
+    // ||b||
+    GmresState S{pl, c, n, c->stream, {}, 0};
+    dots_into(S, {}, 0, b, true, 0);
+    ck(cudaMemcpyAsync(c->hpin, c->dscal, sizeof(double), cudaMemcpyDeviceToHost, c->stream), "D2H");
+    ck(cudaStreamSynchronize(c->stream), "sync");
+    const double norm_b = std::sqrt(c->hpin[0]);
+    int budget = cfg.max_iter, total = 0, conv_all = 0;
+    while (budget > 0) {
+      dots_into(S, {}, 0, r, true, 0);
+      ck(cudaMemcpyAsync(c->hpin, c->dscal, sizeof(double), cudaMemcpyDeviceToHost, c->stream), "D2H");
+      ck(cudaStreamSynchronize(c->stream), "sync");
+      const double norm_r = std::sqrt(c->hpin[0]);
+      if (norm_r == 0.0) {
+        conv_all = 1;
+        break;
+      }
+      const int m = std::min(cfg.restart, budget);
+      int conv = 0, steps = 0;
+      const size_t h0 = hist.size();
+      gmres_inner(pl, r, pl->d_d, cfg.tol * norm_b / norm_r, m, &conv, &steps, hist, &last_rel, &reorth);
+      for (size_t i = h0; i < hist.size(); ++i) hist[i] *= norm_r / norm_b;
+      if (last_rel >= 0.0) last_rel *= norm_r / norm_b;
+      ckl(fpc::launch_axpy(1.0, pl->d_d, x, n, c->stream), "axpy");
+      total += steps;
+      budget -= steps;
+      if (conv) {
+        conv_all = 1;
+        break;
+      }
+      if (steps == 0) break;
+      ++rep->restarts;
+      matvec_dev(p, x, r);
+      ckl(fpc::launch_rsub(b, r, n, c->stream), "rsub");
+    }
+    rep->converged = conv_all;
+    rep->iterations = total;
+  }
+  rep->reorthogonalizations = reorth;
+  rep->final_relative_residual = hist.empty() ? 1.0 : last_rel;
+  // fresh_relative_residual (krylov.hpp:64-75)
+  GmresState S{pl, c, n, c->stream, {}, 0};
+  dots_into(S, {}, 0, b, true, 0);
+  ck(cudaMemcpyAsync(c->hpin, c->dscal, sizeof(double), cudaMemcpyDeviceToHost, c->stream), "D2H");
+  ck(cudaStreamSynchronize(c->stream), "sync");
+  const double norm_b = std::sqrt(c->hpin[0]);
+  if (norm_b == 0.0) {
+    rep->final_relative_residual = 0.0;
+    rep->true_relative_residual = 0.0;
+    rep->converged = 1;
+    return;
+  }
+  rep->true_relative_residual = resid_norm_dev(pl, b, x) / norm_b;
+}
+
+int fpc_gmres(fpc_plan_t pl, const double* b, double* x, const fpc_solver_config* cfg_in,
+              fpc_report* rep, double* history, int history_cap, int where) {
+  if (!pl || !rep) return set_err(FPC_INVALID_ARGUMENT, "null argument");
+  return guarded([&] {
+    check_ptr(b, "fpc_gmres");
+    check_ptr(x, "fpc_gmres");
+    fpc_solver_config cfg{1e-9, 200, 0, FPC_SWEEP_HALF};
+    if (cfg_in) cfg = *cfg_in;
+    if (cfg.sweep != FPC_SWEEP_HALF)
+      throw Unsupported{"InnerSweep::full is not available on the B200 path (use half)"};
+    if (cfg.max_iter < 0) throw InvalidArg{"gmres_right: max_iter must be non-negative"};
+    if (cfg.max_iter > 250) throw Unsupported{"B200 GMRES keeps at most 250 basis vectors"};
+    fpc_problem_s* p = pl->prob;
+    DeviceGuard g(p->ctx->device);
+    const auto t0 = std::chrono::steady_clock::now();
+    std::memset(rep, 0, sizeof *rep);
+    std::vector<double> hist;
+    const size_t n = p->dim();
+    cudaStream_t st = p->ctx->stream;
+    if (where == FPC_DEVICE) {
+      check_dev_aligned(b, "fpc_gmres");
+      check_dev_aligned(x, "fpc_gmres");
+      gmres_dev(pl, b, x, cfg, rep, hist);
+    } else {
+      ensure_staging(p);
+      upload(p->d_in, b, n * sizeof(double), st);
+      gmres_dev(pl, p->d_in, p->d_out, cfg, rep, hist);
+      ck(cudaMemcpyAsync(x, p->d_out, n * sizeof(double), cudaMemcpyDeviceToHost, st), "D2H");
+      ck(cudaStreamSynchronize(st), "sync");
+    }
+    rep->history_len = int(hist.size());
+    for (int i = 0; i < int(hist.size()) && i < history_cap; ++i) history[i] = hist[size_t(i)];
+    rep->seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,65 @@
+// kernels.cuh -- declarations of the sm_100a kernels and their host launchers.
+#pragma once
+#include <cuda_runtime.h>
+#include <cstddef>
+
+namespace fpc {
+
+// Twiddle tables: for every N = 2^k (k <= kMaxLogTw) the table tw_N[t] = e^{-2 pi i t/N},
+// t < N, lives at tw_base + N.
+constexpr int kMaxLogTw = 17;
+
+// ---- 1D all-at-once matvec (all_at_once.hpp:33-55 + toeplitz.hpp:41-57) --------------------
+// y_k = C-stencil(v)_k + IFFT(eig' .* FFT(pad(v_k)))  with eig' = -dt*eig/(2L) pre-folded.
+cudaError_t launch_matvec_1d(const double* v, double* y, int n_space, int n_time, int log_m,
+                             const double* eig_scaled, const double2* tw_base, cudaStream_t st);
+
+// ---- preconditioner apply, reference ordering (alpha_circulant.hpp:137-199) ---------------
+// K2: Z[n][p] = sum_k s_in*scale_fwd[k]*v[k][p] e^{+2 pi i kn/Nt}, n = 0..Nt/2 (half spectrum).
+cudaError_t launch_time_fwd(const double* v, double2* Z, int n_space, int n_time,
+                            const double* scale_fwd, double s_in, const double2* tw_base,
+                            cudaStream_t st);
+// K4: z[k][p] = Re( scale_bwd[k]/Nt * sum_n Z_n e^{-2 pi i kn/Nt} ), Z_{Nt-n} = conj(Z_n).
+cudaError_t launch_time_inv(const double2* Z, double* z, int n_space, int n_time,
+                            const double* scale_bwd, const double2* tw_base, cudaStream_t st);
+// K3 (1D): for each retained n: Z_n <- DST( DST(Z_n) ./ (lambda_n - dt*sigma) ).
+cudaError_t launch_tau_solve_1d(double2* Z, int n_space, int n_rows, const double2* lambda,
+                                const double* sigma, double dt, const double2* tw_base,
+                                cudaStream_t st);
+
+// ---- 2D (jacobian.hpp:77-94, tau.hpp:79-96) -----------------------------------------------
+cudaError_t launch_matvec_2d(const double* v, double* y, int n, int n_time, int log_m,
+                             const double* eig_y_scaled, const double* eig_x_scaled,
+                             const double2* tw_base, cudaStream_t st);
+cudaError_t launch_tau_solve_2d(double2* Z, int n, int n_rows, const double2* lambda,
+                                const double* sigma, double dt, const double2* tw_base,
+                                cudaStream_t st);
+
+// ---- Krylov vector kernels (krylov.hpp:52-62, 116-131, 166-167, 180-182) -------------------
+struct VecSet {
+  const double* v[8];
+  double s[8];
+};
+// partial[blk*stride + i] = s_i * sum v_i .* w  (i < nv), partial[blk*stride + nv] = sum w.*w
+// when with_norm.  Deterministic: fixed grid, fixed in-block tree.
+int dots_grid();
+cudaError_t launch_dots(const VecSet& vs, int nv, const double* w, size_t n, double* partial,
+                        int stride, int col0, bool with_norm, cudaStream_t st);
+// out[i] = sum_b partial[b*stride + i], i < count (fixed order); optional accumulate into out.
+cudaError_t launch_reduce(const double* partial, int stride, int count, double* out,
+                          bool accumulate, cudaStream_t st);
+// w <- w - sum_i c_i v_i with c_i = coef[i]*s_i (coef on device); partial norm of the result.
+cudaError_t launch_update(const double* const* vptr, const double* scales, const double* coef,
+                          int nv, double* w, size_t n, double* partial, cudaStream_t st);
+// u = sum_i c_i * s_i * v_i (c on device)
+cudaError_t launch_lincomb(const double* const* vptr, const double* scales, const double* coef,
+                           int nv, double* u, size_t n, cudaStream_t st);
+// partial = sum (b - y)^2 ; partial over blocks (reduce with launch_reduce)
+cudaError_t launch_resid_norm(const double* b, const double* y, size_t n, double* partial,
+                              cudaStream_t st);
+// y = a*x + y
+cudaError_t launch_axpy(double a, const double* x, double* y, size_t n, cudaStream_t st);
+// y = b - y
+cudaError_t launch_rsub(const double* b, double* y, size_t n, cudaStream_t st);
+
+}  // namespace fpc

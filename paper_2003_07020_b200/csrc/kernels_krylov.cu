@@ -1,0 +1,231 @@
+// kernels_krylov.cu -- GMRES vector kernels (krylov.hpp:52-62 dot/norm/axpy, 116-131 the
+// Gram-Schmidt pass, 166-167 basis append, 180-183 u = V y, 64-75 fresh residual).
+//
+// All reductions are deterministic: a fixed grid (kDotsGrid CTAs) walks the vector with a fixed
+// grid-stride assignment, reduces in-CTA by a fixed shuffle/shared-memory tree, and a single-CTA
+// kernel sums the per-CTA partials in index order.  Vectors are 16-byte aligned (double2 loads);
+// an odd tail element is handled by CTA 0.
+#include "kernels.cuh"
+
+namespace fpc {
+
+constexpr int kDotsThreads = 256;
+constexpr int kDotsGrid = 148 * 4;
+int dots_grid() { return kDotsGrid; }
+
+template <int NACC>
+__device__ __forceinline__ void block_reduce_store(double (&acc)[NACC], double* out) {
+  __shared__ double red[kDotsThreads / 32][NACC];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int i = 0; i < NACC; ++i) {
+    double a = acc[i];
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) a += __shfl_xor_sync(0xffffffffu, a, off);
+    if (lane == 0) red[warp][i] = a;
+  }
+  __syncthreads();
+  if (threadIdx.x < NACC) {
+    double s = 0.0;
+#pragma unroll
+    for (int w = 0; w < kDotsThreads / 32; ++w) s += red[w][threadIdx.x];
+    out[threadIdx.x] = s;
+  }
+}
+
+// partial[blk*stride + col0 + i] = s_i * <v_i, w>, i < NV;  (+ <w,w> at col0 + NV if NORM)
+template <int NV, bool NORM>
+__global__ void __launch_bounds__(kDotsThreads)
+    k_dots(VecSet vs, const double* __restrict__ w, size_t n, double* __restrict__ partial,
+           int stride, int col0) {
+  constexpr int NACC = NV + (NORM ? 1 : 0);
+  double acc[NACC > 0 ? NACC : 1];
+#pragma unroll
+  for (int i = 0; i < NACC; ++i) acc[i] = 0.0;
+  const size_t n2 = n / 2;
+  const double2* w2 = reinterpret_cast<const double2*>(w);
+  for (size_t e = size_t(blockIdx.x) * kDotsThreads + threadIdx.x; e < n2;
+       e += size_t(kDotsGrid) * kDotsThreads) {
+    const double2 wv = w2[e];
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      const double2 x = reinterpret_cast<const double2*>(vs.v[i])[e];
+      acc[i] = fma(x.x, wv.x, acc[i]);
+      acc[i] = fma(x.y, wv.y, acc[i]);
+    }
+    if (NORM) {
+      acc[NV] = fma(wv.x, wv.x, acc[NV]);
+      acc[NV] = fma(wv.y, wv.y, acc[NV]);
+    }
+  }
+  if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
+    const double wl = w[n - 1];
+#pragma unroll
+    for (int i = 0; i < NV; ++i) acc[i] = fma(vs.v[i][n - 1], wl, acc[i]);
+    if (NORM) acc[NV] = fma(wl, wl, acc[NV]);
+  }
+  double tmp[NACC];
+#pragma unroll
+  for (int i = 0; i < NACC; ++i) tmp[i] = acc[i];
+  __shared__ double outb[NACC];
+  block_reduce_store<NACC>(tmp, outb);
+  __syncthreads();
+  if (threadIdx.x < NACC) {
+    const double sc = threadIdx.x < NV ? vs.s[threadIdx.x] : 1.0;
+    partial[size_t(blockIdx.x) * stride + col0 + threadIdx.x] = outb[threadIdx.x] * sc;
+  }
+}
+
+cudaError_t launch_dots(const VecSet& vs, int nv, const double* w, size_t n, double* partial,
+                        int stride, int col0, bool with_norm, cudaStream_t st) {
+#define DOTS(NVV)                                                                             \
+  case NVV:                                                                                   \
+    if (with_norm)                                                                            \
+      k_dots<NVV, true><<<kDotsGrid, kDotsThreads, 0, st>>>(vs, w, n, partial, stride, col0); \
+    else                                                                                      \
+      k_dots<NVV, false><<<kDotsGrid, kDotsThreads, 0, st>>>(vs, w, n, partial, stride, col0); \
+    break;
+  switch (nv) {
+    case 0:
+      k_dots<0, true><<<kDotsGrid, kDotsThreads, 0, st>>>(vs, w, n, partial, stride, col0);
+      break;
+    DOTS(1) DOTS(2) DOTS(3) DOTS(4) DOTS(5) DOTS(6) DOTS(7) DOTS(8)
+    default:
+      return cudaErrorInvalidValue;
+  }
+#undef DOTS
+  return cudaGetLastError();
+}
+
+__global__ void k_reduce(const double* __restrict__ partial, int stride, int count,
+                         double* __restrict__ out, int accumulate) {
+  const int i = threadIdx.x + blockIdx.x * blockDim.x;
+  if (i >= count) return;
+  double s = 0.0;
+  for (int b = 0; b < kDotsGrid; ++b) s += partial[size_t(b) * stride + i];
+  out[i] = accumulate ? out[i] + s : s;
+}
+
+cudaError_t launch_reduce(const double* partial, int stride, int count, double* out,
+                          bool accumulate, cudaStream_t st) {
+  k_reduce<<<(count + 127) / 128, 128, 0, st>>>(partial, stride, count, out, accumulate ? 1 : 0);
+  return cudaGetLastError();
+}
+
+constexpr int kMaxVecs = 256;
+
+// w <- w - sum_i (coef_i * s_i) v_i (in order i = 0..nv-1, as the reference's sequential
+// axpys); partial[blk] = sum w_new^2.
+__global__ void __launch_bounds__(kDotsThreads)
+    k_update(const double* const* __restrict__ vptr, const double* __restrict__ scales,
+             const double* __restrict__ coef, int nv, double* __restrict__ w, size_t n,
+             double* __restrict__ partial) {
+  __shared__ const double2* sp[kMaxVecs];
+  __shared__ double sc[kMaxVecs];
+  for (int i = threadIdx.x; i < nv; i += blockDim.x) {
+    sp[i] = reinterpret_cast<const double2*>(vptr[i]);
+    sc[i] = coef[i] * scales[i];
+  }
+  __syncthreads();
+  double acc[1] = {0.0};
+  const size_t n2 = n / 2;
+  double2* w2 = reinterpret_cast<double2*>(w);
+  for (size_t e = size_t(blockIdx.x) * kDotsThreads + threadIdx.x; e < n2;
+       e += size_t(kDotsGrid) * kDotsThreads) {
+    double2 a = w2[e];
+    for (int i = 0; i < nv; ++i) {
+      const double2 x = sp[i][e];
+      a.x = fma(-sc[i], x.x, a.x);
+      a.y = fma(-sc[i], x.y, a.y);
+    }
+    w2[e] = a;
+    acc[0] = fma(a.x, a.x, acc[0]);
+    acc[0] = fma(a.y, a.y, acc[0]);
+  }
+  if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
+    double a = w[n - 1];
+    for (int i = 0; i < nv; ++i) a = fma(-sc[i], reinterpret_cast<const double*>(sp[i])[n - 1], a);
+    w[n - 1] = a;
+    acc[0] = fma(a, a, acc[0]);
+  }
+  __shared__ double outb[1];
+  block_reduce_store<1>(acc, outb);
+  __syncthreads();
+  if (threadIdx.x == 0) partial[blockIdx.x] = outb[0];
+}
+
+cudaError_t launch_update(const double* const* vptr, const double* scales, const double* coef,
+                          int nv, double* w, size_t n, double* partial, cudaStream_t st) {
+  if (nv > kMaxVecs) return cudaErrorInvalidValue;
+  k_update<<<kDotsGrid, kDotsThreads, 0, st>>>(vptr, scales, coef, nv, w, n, partial);
+  return cudaGetLastError();
+}
+
+// u = sum_i (coef_i s_i) v_i, accumulated in order from u = 0 (krylov.hpp:180-182)
+__global__ void __launch_bounds__(kDotsThreads)
+    k_lincomb(const double* const* __restrict__ vptr, const double* __restrict__ scales,
+              const double* __restrict__ coef, int nv, double* __restrict__ u, size_t n) {
+  __shared__ const double* sp[kMaxVecs];
+  __shared__ double sc[kMaxVecs];
+  for (int i = threadIdx.x; i < nv; i += blockDim.x) {
+    sp[i] = vptr[i];
+    sc[i] = coef[i] * scales[i];
+  }
+  __syncthreads();
+  for (size_t e = size_t(blockIdx.x) * kDotsThreads + threadIdx.x; e < n;
+       e += size_t(kDotsGrid) * kDotsThreads) {
+    double a = 0.0;
+    for (int i = 0; i < nv; ++i) a = fma(sc[i], sp[i][e], a);
+    u[e] = a;
+  }
+}
+
+cudaError_t launch_lincomb(const double* const* vptr, const double* scales, const double* coef,
+                           int nv, double* u, size_t n, cudaStream_t st) {
+  if (nv > kMaxVecs) return cudaErrorInvalidValue;
+  k_lincomb<<<kDotsGrid, kDotsThreads, 0, st>>>(vptr, scales, coef, nv, u, n);
+  return cudaGetLastError();
+}
+
+__global__ void __launch_bounds__(kDotsThreads)
+    k_resid_norm(const double* __restrict__ b, const double* __restrict__ y, size_t n,
+                 double* __restrict__ partial) {
+  double acc[1] = {0.0};
+  for (size_t e = size_t(blockIdx.x) * kDotsThreads + threadIdx.x; e < n;
+       e += size_t(kDotsGrid) * kDotsThreads) {
+    const double d = b[e] - y[e];
+    acc[0] = fma(d, d, acc[0]);
+  }
+  __shared__ double outb[1];
+  block_reduce_store<1>(acc, outb);
+  __syncthreads();
+  if (threadIdx.x == 0) partial[blockIdx.x] = outb[0];
+}
+
+cudaError_t launch_resid_norm(const double* b, const double* y, size_t n, double* partial,
+                              cudaStream_t st) {
+  k_resid_norm<<<kDotsGrid, kDotsThreads, 0, st>>>(b, y, n, partial);
+  return cudaGetLastError();
+}
+
+__global__ void k_axpy(double a, const double* __restrict__ x, double* __restrict__ y, size_t n) {
+  for (size_t e = size_t(blockIdx.x) * blockDim.x + threadIdx.x; e < n;
+       e += size_t(gridDim.x) * blockDim.x)
+    y[e] += a * x[e];
+}
+cudaError_t launch_axpy(double a, const double* x, double* y, size_t n, cudaStream_t st) {
+  k_axpy<<<kDotsGrid, kDotsThreads, 0, st>>>(a, x, y, n);
+  return cudaGetLastError();
+}
+
+__global__ void k_rsub(const double* __restrict__ b, double* __restrict__ y, size_t n) {
+  for (size_t e = size_t(blockIdx.x) * blockDim.x + threadIdx.x; e < n;
+       e += size_t(gridDim.x) * blockDim.x)
+    y[e] = b[e] - y[e];
+}
+cudaError_t launch_rsub(const double* b, double* y, size_t n, cudaStream_t st) {
+  k_rsub<<<kDotsGrid, kDotsThreads, 0, st>>>(b, y, n);
+  return cudaGetLastError();
+}
+
+}  // namespace fpc

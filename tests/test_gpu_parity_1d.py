@@ -1,0 +1,118 @@
+"""GPU parity of the 1D hot path against the C oracle (oracle/fracpint_oracle.c, itself pinned to
+the reference in test_oracle_pins.py).  All calls go through the C-ABI (libfracpint_b200.so)."""
+import numpy as np
+import pytest
+
+import paper_2003_07020_b200 as fp
+from paper_2003_07020_b200 import problems
+
+pytestmark = pytest.mark.gpu
+
+# (gamma, n_space, n_time): every size class of the smem FFT engine for the Toeplitz (L = 2(n+1)),
+# the DST (M = n+1) and the time FFT (Nt)
+SIZES = [(1.5, 3, 4), (1.5, 7, 8), (1.3, 15, 16), (1.8, 31, 8), (1.5, 63, 32), (1.2, 127, 64),
+         (1.7, 255, 128), (1.5, 511, 16), (1.5, 1023, 256), (1.9, 2047, 32), (1.4, 4095, 16),
+         (1.2, 8191, 8)]
+
+
+def make(gamma, ns, nt, kappa=1.0):
+    h = 1.0 / (ns + 1)
+    dt = 1.0 / nt
+    st = fp.TimeStencil(nt)
+    op = fp.AllAtOnceOperator(st, fp.RieszJacobian1D(gamma, kappa, h, ns), dt)
+    return op, h, dt
+
+
+def rel(a, b):
+    return np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300)
+
+
+@pytest.mark.parametrize("gamma,ns,nt", SIZES)
+def test_matvec_1d(oracle, gamma, ns, nt):
+    op, h, dt = make(gamma, ns, nt)
+    po = oracle.problem_1d(gamma, 1.0, h, ns, nt, dt)
+    v = np.random.default_rng(ns * 7 + nt).uniform(-1, 1, ns * nt)
+    y = op.apply(v)
+    assert rel(y, po.matvec(v)) <= 1e-13
+
+
+@pytest.mark.parametrize("gamma,ns,nt", SIZES)
+def test_pc_apply_1d(oracle, gamma, ns, nt):
+    op, h, dt = make(gamma, ns, nt)
+    plan = fp.build_plan(fp.PreconditionerKind.generalized(), nt, dt, op)
+    po = oracle.problem_1d(gamma, 1.0, h, ns, nt, dt).build_plan()
+    assert abs(plan.alpha - po.alpha) == 0.0
+    assert abs(plan.min_shift_margin - po.min_shift_margin) <= 1e-12 * po.min_shift_margin
+    v = np.random.default_rng(ns * 11 + nt).uniform(-1, 1, ns * nt)
+    z = fp.apply_inverse(plan, v)
+    assert rel(z, po.pc_apply(v)) <= 1e-12
+
+
+@pytest.mark.parametrize("alpha", [0.5, 1e-3, 1.0])
+def test_pc_apply_alpha(oracle, alpha):
+    op, h, dt = make(1.5, 63, 16)
+    plan = fp.build_plan(fp.PreconditionerKind.with_alpha(alpha), 16, dt, op)
+    po = oracle.problem_1d(1.5, 1.0, h, 63, 16, dt).build_plan(alpha)
+    v = np.random.default_rng(3).uniform(-1, 1, 63 * 16)
+    assert rel(fp.apply_inverse(plan, v), po.pc_apply(v)) <= 1e-12
+
+
+def test_pc_apply_zero_is_zero():
+    op, h, dt = make(1.5, 15, 8)
+    plan = fp.build_plan(fp.PreconditionerKind.with_alpha(0.5), 8, dt, op)
+    z = fp.apply_inverse(plan, np.zeros(15 * 8))
+    assert np.all(z == 0.0)
+
+
+@pytest.mark.parametrize("gamma,ns,nt,restart", [(1.5, 63, 16, 0), (1.5, 255, 64, 0), (1.5, 1023, 256, 20),
+                                                 (1.5, 1023, 256, 5), (1.8, 511, 128, 0)])
+def test_gmres_1d(oracle, gamma, ns, nt, restart):
+    w = problems.workload_1d(gamma, ns + 1, nt)
+    op = fp.AllAtOnceOperator(fp.TimeStencil(nt), fp.RieszJacobian1D(gamma, 1.0, w.h, ns), w.dt)
+    plan = fp.build_plan(fp.PreconditionerKind.generalized(), nt, w.dt, op)
+    b = problems.rhs(w)
+    res = fp.gmres_right(op, plan, b, fp.SolverConfig(tol=1e-10, max_iter=200, restart=restart))
+    po = oracle.problem_1d(gamma, 1.0, w.h, ns, nt, w.dt).build_plan()
+    xo, ro = po.gmres(b, 1e-10, 200, restart=restart)
+    assert res.report.converged and ro.converged
+    assert abs(res.report.iterations - ro.iterations) <= 1
+    assert rel(res.x, xo) <= 1e-10
+    assert res.report.true_relative_residual <= 1e-9
+
+
+def test_gmres_zero_rhs():
+    op, h, dt = make(1.5, 15, 8)
+    plan = fp.build_plan(fp.PreconditionerKind.generalized(), 8, dt, op)
+    res = fp.gmres_right(op, plan, np.zeros(15 * 8))
+    assert res.report.converged and res.report.iterations == 0
+    assert np.all(res.x == 0.0)
+
+
+def test_gmres_budget_exhaustion(oracle):
+    op, h, dt = make(1.5, 63, 16)
+    plan = fp.build_plan(fp.PreconditionerKind.generalized(), 16, dt, op)
+    b = np.random.default_rng(5).uniform(-1, 1, 63 * 16)
+    res = fp.gmres_right(op, plan, b, fp.SolverConfig(tol=1e-14, max_iter=3))
+    assert not res.report.converged and res.report.iterations == 3
+    assert len(res.report.residual_history) == 3
+
+
+def test_device_tensors_roundtrip(oracle):
+    torch = pytest.importorskip("torch")
+    op, h, dt = make(1.5, 255, 64)
+    plan = fp.build_plan(fp.PreconditionerKind.generalized(), 64, dt, op)
+    v = np.random.default_rng(9).uniform(-1, 1, 255 * 64)
+    vt = torch.from_numpy(v).cuda()
+    y = op.apply(vt)
+    op.ctx.synchronize()
+    assert rel(y.cpu().numpy(), op.apply(v)) == 0.0
+    z = fp.apply_inverse(plan, vt)
+    op.ctx.synchronize()
+    assert rel(z.cpu().numpy(), fp.apply_inverse(plan, v)) == 0.0
+
+
+def test_unsupported_sizes_fail_loudly():
+    with pytest.raises(NotImplementedError):
+        fp.AllAtOnceOperator(fp.TimeStencil(6), fp.RieszJacobian1D(1.5, 1.0, 0.1, 9), 0.1)
+    with pytest.raises(ValueError):
+        fp.AllAtOnceOperator(fp.TimeStencil(8), fp.RieszJacobian1D(1.5, -1.0, 0.1, 7), 0.1)
