@@ -12,6 +12,7 @@
 #include <cmath>
 #include <complex>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <string>
@@ -38,9 +39,17 @@ struct CudaFail {
 inline void ck(cudaError_t e, const char* what) {
   if (e != cudaSuccess) throw CudaFail{e, what};
 }
+bool debug_sync() {
+  static const bool on = [] {
+    const char* e = std::getenv("FPC_DEBUG_SYNC");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
 inline void ckl(cudaError_t e, const char* what) {  // kernel launch
   g_launches.fetch_add(1, std::memory_order_relaxed);
   ck(e, what);
+  if (debug_sync()) ck(cudaDeviceSynchronize(), what);
 }
 
 struct InvalidArg {

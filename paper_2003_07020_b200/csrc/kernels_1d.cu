@@ -170,9 +170,9 @@ __global__ void __launch_bounds__(Geo<LOGM, kTotT>::NT)
     const int c = t % B, n = t / B;
     const int p = p0 + c;
     double2* s = smem + c * padded(M);
-    if (p >= ns) {
+    if (p >= ns) {  // padding column: keep its buffer finite
       s[pad16(n)] = make_double2(0.0, 0.0);
-      s[pad16(M - n)] = make_double2(0.0, 0.0);
+      if (n != 0) s[pad16(M - n)] = make_double2(0.0, 0.0);
       continue;
     }
     if (n == 0) {
