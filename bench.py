@@ -1,0 +1,313 @@
+"""bench.py -- BC-preconditioned GMRES time-to-tol on B200 (BASELINE.json metric, configs[1]).
+
+A "step" = one full right-preconditioned GMRES(20) solve to tol 1e-10 of the all-at-once BDF2
+system of config 1 (1D Riesz FDE, gamma=1.2, Nx=8191, Nt=2048, fp64, seeded uniform source),
+with b resident in HBM: the reference's timed span krylov.hpp:87-190 (k+1 PC applies, k+1
+matvecs, the Gram-Schmidt work, x = P^{-1} V y and the fresh TRR).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--gamma 1.2]
+
+N > 1 (torchrun): every rank solves its own replica (the solve is not sharded yet -- "replicas
+only"); value = N * solves / max-over-ranks time.  --impl reference times the
+reference's own CPU solver (oracle/_ref, the unmodified reference headers) on this host's cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "BC-preconditioned GMRES time-to-tol (solves/s)"
+UNIT = "solves/s"
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device, self.rows, self.proc = device, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 7:
+                self.rows.append(parts)
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+        return False
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[3 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# ------------------------------------------------------------------------------------ reference arm
+def cpu_reference_sample(w, threads: int, sample_iters: int):
+    """Time the unmodified reference (oracle/_ref) gmres_right on this workload, bounded to
+    `sample_iters` iterations; returns (seconds, sample_iters_done, true iteration count k)."""
+    from oracle import oracle as O
+    ref = O.Reference()
+    ref.set_threads(threads)
+    p = ref.problem_1d(w.gamma[0], 1.0, w.h, w.n, w.n_time, w.dt).build_plan()
+    from paper_2003_07020_b200 import problems
+    b = problems.rhs(w)
+    _, rep = p.gmres(b, w.tol, sample_iters)
+    return rep.seconds, rep.iterations
+
+
+def run_reference(args, w, k_full: int):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    times = []
+    for i in range(args.warmup_ref + args.steps_ref):
+        sec, done = cpu_reference_sample(w, threads, args.ref_iters)
+        if i >= args.warmup_ref:
+            times.append(sec * (k_full + 1) / (done + 1))
+    t = statistics.mean(times)
+    val = 1.0 / t
+    sample = (f"reference gmres_right (oracle/_ref, unmodified headers) on {w.name}, max_iter={args.ref_iters} of the "
+              f"{k_full}-iteration solve, time x ({k_full}+1)/({args.ref_iters}+1)")
+    line = {"impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps_ref, "warmup": args.warmup_ref, "ms_per_step": t * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded uniform source)",
+            "config": {"workload": w.name, "n_space": w.n, "n_time": w.n_time, "gamma": w.gamma[0], "tol": w.tol,
+                       "restart": w.restart},
+            "cpu_baseline": {"value": val, "unit": UNIT, "cores": threads, "kind": "reference", "sample": sample},
+            "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+
+
+# ------------------------------------------------------------------------------------ our arm
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=1)
+    ap.add_argument("--gamma", type=float, default=1.2)
+    ap.add_argument("--ref-iters", type=int, default=2, help="reference sample: GMRES iterations per step")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.steps_ref = max(1, min(args.steps, 3))
+    args.warmup_ref = 0
+
+    from paper_2003_07020_b200 import problems
+    w = problems.config(args.config, args.gamma if args.config == 1 else None)
+    k_full_known = {1: 13}.get(args.config, 12)
+
+    if args.impl == "reference":
+        run_reference(args, w, k_full_known)
+        return
+
+    import torch
+    import torch.distributed as dist
+    rank, world, local = dist_env()
+    if world > 1:
+        dist.init_process_group("nccl" if torch.cuda.is_available() else "gloo")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+
+    import paper_2003_07020_b200 as fp
+    stream = torch.cuda.Stream(device=dev)
+    ctx = fp.Context(local, stream)
+    if w.two_dim:
+        jac = fp.RieszJacobian2D(w.gamma[0], w.gamma[1], 1.0, 1.0, w.h, w.n)
+    else:
+        jac = fp.RieszJacobian1D(w.gamma[0], 1.0, w.h, w.n)
+    op = fp.AllAtOnceOperator(fp.TimeStencil(w.n_time), jac, w.dt, ctx)
+    plan = fp.build_plan(fp.PreconditionerKind.generalized(), w.n_time, w.dt, op)
+    cfg = fp.SolverConfig(tol=w.tol, max_iter=200, restart=w.restart)
+    b_host = problems.rhs(w)
+    N = w.dim
+    with torch.cuda.stream(stream):
+        b = torch.from_numpy(b_host).to(dev)
+        x = torch.empty_like(b)
+    stream.synchronize()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    # warm-up (untimed)
+    for _ in range(args.warmup):
+        res = fp.gmres_right(op, plan, b, cfg, out=x)
+    torch.cuda.synchronize()
+    k = int(res.report.iterations)
+
+    # timed region: K device-resident solves; inputs (134 MB vectors) exceed the 126 MB L2
+    launches0 = fp.kernel_launches()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        barrier()
+        torch.cuda.synchronize()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            res = fp.gmres_right(op, plan, b, cfg, out=x)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+    launches = fp.kernel_launches() - launches0
+    t_step = ev0.elapsed_time(ev1) * 1e-3 / args.steps
+    if world > 1:
+        tt = torch.tensor([t_step], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_step = float(tt.item())
+    value = world / t_step
+
+    # e2e: the public API with HOST buffers (H2D of b and D2H of x inside the timed region)
+    x_host = np.empty(N)
+    fp.gmres_right(op, plan, b_host, cfg, out=x_host)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        r_e2e = fp.gmres_right(op, plan, b_host, cfg, out=x_host)
+    t_e2e = (time.perf_counter() - t0) / args.steps
+    if world > 1:
+        tt = torch.tensor([t_e2e], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_e2e = float(tt.item())
+
+    # live per-kernel device time inside one solve (events around every launch)
+    with fp.KernelProfile() as prof:
+        fp.gmres_right(op, plan, b, cfg, out=x)
+    table = prof.table
+    # standalone operator rates (device-resident, events on the launching stream)
+    def rate(fn, reps=20):
+        for _ in range(3):
+            fn()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(reps):
+            fn()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        return ev_s(e0, e1) / reps
+
+    def ev_s(e0, e1):
+        return e0.elapsed_time(e1) * 1e-3
+
+    y = torch.empty_like(b)
+    t_mv = rate(lambda: op.apply(b, y))
+    t_pc = rate(lambda: fp.apply_inverse(plan, b, y))
+    H = w.n_time // 2 + 1
+    B_mv = 16.0 * N
+    B_pc = 16.0 * N + 64.0 * H * w.n_space
+    peak, peak_kind = load_peaks()
+
+    # dominant kernel by live device time inside the solve
+    dom = max(table.items(), key=lambda kv: kv[1][0])
+    dom_name, (dom_ms, dom_cnt) = dom
+    per_launch_bytes = {"matvec_1d": B_mv, "matvec_2d": B_mv, "time_fwd": 8.0 * N + 16.0 * H * w.n_space,
+                        "time_inv": 8.0 * N + 16.0 * H * w.n_space, "tau_solve_1d": 32.0 * H * w.n_space,
+                        "tau_solve_2d": 32.0 * H * w.n_space}
+    dom_bytes = per_launch_bytes.get(dom_name)
+    dom_t = dom_ms * 1e-3 / dom_cnt
+    achieved = dom_bytes / dom_t / 1e9 if dom_bytes else None
+    traffic = None
+    tfile = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tfile):
+        try:
+            traffic = json.load(open(tfile)).get(dom_name)
+        except Exception:
+            traffic = None
+
+    # CPU baseline: the reference on this host, bounded sample (rank 0, N = 1 only)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            threads = os.cpu_count() or 1
+            sec, done = cpu_reference_sample(w, threads, args.ref_iters)
+            t_cpu = sec * (k + 1) / (done + 1)
+            cpu = {"value": 1.0 / t_cpu, "unit": UNIT, "cores": threads, "kind": "reference",
+                   "sample": f"reference gmres_right (oracle/_ref) on {w.name}, max_iter={args.ref_iters} of {k} "
+                             f"iterations, {sec:.1f} s, extrapolated x({k}+1)/({done}+1)"}
+        except Exception as e:  # noqa: BLE001
+            cpu = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "reference",
+                   "sample": f"unavailable: {e}"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": t_step * 1e3, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded uniform[-1,1] source, u0=x^2(1-x)^2)",
+            "config": {"workload": w.name, "n_space": w.n, "n_time": w.n_time, "gamma": w.gamma[0], "kappa": 1.0,
+                       "tol": w.tol, "restart": w.restart, "solver": "GMRES(20) right-preconditioned, BC alpha=dt/2",
+                       "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
+                       "l2": "inputs larger than L2 (134 MB per Krylov vector vs 126 MB L2)"},
+            "time_to_tol_s": t_step, "iterations": k, "true_relative_residual": res.report.true_relative_residual,
+            "pc_applies_per_s": 1.0 / t_pc, "matvecs_per_s": 1.0 / t_mv,
+            "pc_apply_gbs": B_pc / t_pc / 1e9, "matvec_gbs": B_mv / t_mv / 1e9,
+            "e2e": {"value": world / t_e2e, "unit": UNIT, "h2d_bytes_per_step": 8 * N, "d2h_bytes_per_step": 8 * N,
+                    "iterations": int(r_e2e.report.iterations)},
+            "gpu_launches": launches,
+            "roofline": {"bound": "hbm", "kernel": dom_name, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": (achieved / peak) if achieved else None, "traffic": traffic,
+                         "algorithmic_bytes_per_launch": dom_bytes, "avg_launch_us": dom_t * 1e6,
+                         "peak_source": peak_kind},
+            "kernel_time_ms_per_solve": {k_: v[0] for k_, v in table.items()},
+            "kernel_launches_per_solve": {k_: v[1] for k_, v in table.items()},
+            "clocks": clk.summary(),
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -110,8 +110,13 @@ int fpc_pc_forward(fpc_plan_t plan, const double* v, double* out, int where);
 int fpc_gmres(fpc_plan_t plan, const double* b, double* x, const fpc_solver_config* cfg,
               fpc_report* report, double* history, int history_cap, int where);
 
-/* instrumentation: number of kernels this library launched on the calling process */
+/* instrumentation: number of kernels this library launched in this process */
 unsigned long long fpc_kernel_launches(void);
+/* live per-kernel device time: CUDA events on the launching stream around every launch while
+ * enabled.  stop() synchronizes the device and returns the number of kernel categories. */
+int fpc_profile_start(void);
+int fpc_profile_stop(void);
+int fpc_profile_entry(int index, char* name, int name_cap, double* total_ms, long long* launches);
 
 #ifdef __cplusplus
 }

@@ -22,7 +22,8 @@ EXPORTS = [
     "fpc_device_free", "fpc_problem_create_1d", "fpc_problem_create_2d", "fpc_problem_destroy",
     "fpc_problem_dims", "fpc_problem_first_column", "fpc_problem_tau_sigma", "fpc_matvec",
     "fpc_assemble_rhs", "fpc_plan_create", "fpc_plan_destroy", "fpc_plan_info", "fpc_plan_lambda",
-    "fpc_pc_apply", "fpc_pc_forward", "fpc_gmres", "fpc_kernel_launches",
+    "fpc_pc_apply", "fpc_pc_forward", "fpc_gmres", "fpc_kernel_launches", "fpc_profile_start",
+    "fpc_profile_stop", "fpc_profile_entry",
 ]
 
 
@@ -76,6 +77,7 @@ def load():
     lib.fpc_pc_forward.argtypes = [vp, dp, dp, C.c_int]
     lib.fpc_gmres.argtypes = [vp, dp, dp, C.POINTER(SolverConfigC), C.POINTER(ReportC), dp, C.c_int, C.c_int]
     lib.fpc_kernel_launches.restype = C.c_ulonglong
+    lib.fpc_profile_entry.argtypes = [C.c_int, C.c_char_p, C.c_int, C.POINTER(d), C.POINTER(C.c_longlong)]
     _lib = lib
     return lib
 

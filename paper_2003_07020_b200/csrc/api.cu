@@ -52,6 +52,75 @@ inline void ckl(cudaError_t e, const char* what) {  // kernel launch
   if (debug_sync()) ck(cudaDeviceSynchronize(), what);
 }
 
+// Live per-kernel timing (fpc_profile_*): CUDA events recorded on the launching stream around
+// every launch while enabled; resolved after the caller synchronizes.
+struct Profiler {
+  bool on = false;
+  struct Pending {
+    cudaEvent_t a, b;
+    int cat;
+  };
+  std::vector<Pending> pending;
+  std::vector<cudaEvent_t> pool;
+  std::vector<std::string> names;
+  std::vector<double> ms;
+  std::vector<long long> count;
+  cudaEvent_t get() {
+    if (pool.empty()) {
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      return e;
+    }
+    cudaEvent_t e = pool.back();
+    pool.pop_back();
+    return e;
+  }
+  int cat(const char* name) {
+    for (size_t i = 0; i < names.size(); ++i)
+      if (names[i] == name) return int(i);
+    names.emplace_back(name);
+    ms.push_back(0.0);
+    count.push_back(0);
+    return int(names.size()) - 1;
+  }
+  void resolve() {
+    for (auto& p : pending) {
+      float t = 0.f;
+      if (cudaEventElapsedTime(&t, p.a, p.b) == cudaSuccess) {
+        ms[size_t(p.cat)] += t;
+        count[size_t(p.cat)] += 1;
+      }
+      pool.push_back(p.a);
+      pool.push_back(p.b);
+    }
+    pending.clear();
+  }
+};
+Profiler g_prof;
+
+struct ProfScope {
+  cudaStream_t st;
+  int cat = -1;
+  cudaEvent_t a{};
+  ProfScope(const char* name, cudaStream_t s) : st(s) {
+    if (!g_prof.on) return;
+    cat = g_prof.cat(name);
+    a = g_prof.get();
+    cudaEventRecord(a, st);
+  }
+  ~ProfScope() {
+    if (cat < 0) return;
+    cudaEvent_t b = g_prof.get();
+    cudaEventRecord(b, st);
+    g_prof.pending.push_back({a, b, cat});
+  }
+};
+#define LAUNCH(name, stream, call)   \
+  do {                               \
+    ProfScope ps_(name, stream);     \
+    ckl((call), name);               \
+  } while (0)
+
 struct InvalidArg {
   std::string msg;
 };
@@ -273,6 +342,32 @@ int fpc_abi_version(void) { return 1; }
 const char* fpc_last_error(void) { return g_err.c_str(); }
 unsigned long long fpc_kernel_launches(void) { return g_launches.load(); }
 
+int fpc_profile_start(void) {
+  g_prof.resolve();
+  for (auto& m : g_prof.ms) m = 0.0;
+  for (auto& c : g_prof.count) c = 0;
+  g_prof.on = true;
+  return FPC_OK;
+}
+
+int fpc_profile_stop(void) {
+  cudaDeviceSynchronize();
+  g_prof.resolve();
+  g_prof.on = false;
+  return int(g_prof.names.size());
+}
+
+int fpc_profile_entry(int i, char* name, int name_cap, double* total_ms, long long* launches) {
+  if (i < 0 || size_t(i) >= g_prof.names.size()) return set_err(FPC_INVALID_ARGUMENT, "bad index");
+  if (name && name_cap > 0) {
+    std::strncpy(name, g_prof.names[size_t(i)].c_str(), size_t(name_cap) - 1);
+    name[name_cap - 1] = 0;
+  }
+  if (total_ms) *total_ms = g_prof.ms[size_t(i)];
+  if (launches) *launches = g_prof.count[size_t(i)];
+  return FPC_OK;
+}
+
 int fpc_context_create(int device, fpc_context_t* out) {
   if (!out) return set_err(FPC_INVALID_ARGUMENT, "null output");
   return guarded([&] {
@@ -447,10 +542,9 @@ int fpc_problem_tau_sigma(fpc_problem_t p, double* out) {
 static void matvec_dev(fpc_problem_s* p, const double* v, double* y) {
   cudaStream_t st = p->ctx->stream;
   if (!p->two_dim) {
-    ckl(fpc::launch_matvec_1d(v, y, p->ns, p->nt, p->log_m, p->d_eig, p->ctx->tw, st), "matvec_1d");
+    LAUNCH("matvec_1d", st, fpc::launch_matvec_1d(v, y, p->ns, p->nt, p->log_m, p->d_eig, p->ctx->tw, st));
   } else {
-    ckl(fpc::launch_matvec_2d(v, y, p->n, p->nt, p->log_m, p->d_eig, p->d_eig_x, p->ctx->tw, st),
-        "matvec_2d");
+    LAUNCH("matvec_2d", st, fpc::launch_matvec_2d(v, y, p->n, p->nt, p->log_m, p->d_eig, p->d_eig_x, p->ctx->tw, st));
   }
 }
 
@@ -597,16 +691,14 @@ int fpc_plan_lambda(fpc_plan_t pl, double* out) {
 static void pc_apply_dev(fpc_plan_s* pl, const double* v, double* z, double s_in) {
   fpc_problem_s* p = pl->prob;
   cudaStream_t st = p->ctx->stream;
-  ckl(fpc::launch_time_fwd(v, pl->d_Z, p->ns, p->nt, pl->d_sf, s_in, p->ctx->tw, st), "time_fwd");
+  LAUNCH("time_fwd", st, fpc::launch_time_fwd(v, pl->d_Z, p->ns, p->nt, pl->d_sf, s_in, p->ctx->tw, st));
   if (!p->two_dim)
-    ckl(fpc::launch_tau_solve_1d(pl->d_Z, p->ns, pl->solve_count, pl->d_lambda, pl->d_sigma, p->dt,
-                                 p->ctx->tw, st),
-        "tau_solve_1d");
+    LAUNCH("tau_solve_1d", st, fpc::launch_tau_solve_1d(pl->d_Z, p->ns, pl->solve_count, pl->d_lambda, pl->d_sigma, p->dt,
+                                 p->ctx->tw, st));
   else
-    ckl(fpc::launch_tau_solve_2d(pl->d_Z, p->n, pl->solve_count, pl->d_lambda, pl->d_sigma, p->dt,
-                                 p->ctx->tw, st),
-        "tau_solve_2d");
-  ckl(fpc::launch_time_inv(pl->d_Z, z, p->ns, p->nt, pl->d_sb, p->ctx->tw, st), "time_inv");
+    LAUNCH("tau_solve_2d", st, fpc::launch_tau_solve_2d(pl->d_Z, p->n, pl->solve_count, pl->d_lambda, pl->d_sigma, p->dt,
+                                 p->ctx->tw, st));
+  LAUNCH("time_inv", st, fpc::launch_time_inv(pl->d_Z, z, p->ns, p->nt, pl->d_sb, p->ctx->tw, st));
 }
 
 int fpc_pc_apply(fpc_plan_t pl, const double* v, double* out, int sweep, int where) {
@@ -663,7 +755,7 @@ void dots_into(GmresState& S, const std::vector<const double*>& V, int nv, const
   const int stride = fpc_context_s::kPartialStride;
   if (nv == 0) {
     fpc::VecSet vs{};
-    ckl(fpc::launch_dots(vs, 0, w, S.n, c->partial, stride, 0, true, S.st), "dots");
+    LAUNCH("dots", S.st, fpc::launch_dots(vs, 0, w, S.n, c->partial, stride, 0, true, S.st));
   }
   for (int g0 = 0; g0 < nv; g0 += 8) {
     const int cnt = std::min(8, nv - g0);
@@ -674,10 +766,10 @@ void dots_into(GmresState& S, const std::vector<const double*>& V, int nv, const
     }
     const bool last = g0 + cnt == nv;
     // the norm accumulator goes right after the last group's columns
-    ckl(fpc::launch_dots(vs, cnt, w, S.n, c->partial, stride, g0, with_norm && last, S.st), "dots");
+    LAUNCH("dots", S.st, fpc::launch_dots(vs, cnt, w, S.n, c->partial, stride, g0, with_norm && last, S.st));
   }
   const int count = nv + (with_norm ? 1 : 0);
-  ckl(fpc::launch_reduce(c->partial, stride, count, c->dscal + out_off, false, S.st), "reduce");
+  LAUNCH("reduce", S.st, fpc::launch_reduce(c->partial, stride, count, c->dscal + out_off, false, S.st));
 }
 
 }  // namespace
@@ -724,28 +816,59 @@ static void gmres_inner(fpc_plan_s* pl, const double* b, double* x, double tol, 
     ck(cudaMemcpyAsync(c->dscales, S.scales.data(), S.scales.size() * sizeof(double),
                        cudaMemcpyHostToDevice, S.st),
        "scales");
-    ckl(fpc::launch_update(c->dvptr, c->dscales, c->dscal, nv, w, n, c->partial, S.st), "update");
-    ckl(fpc::launch_reduce(c->partial, 1, 1, c->dscal + 512, false, S.st), "reduce");
-    ck(cudaMemcpyAsync(c->hpin, c->dscal, size_t(nv + 1) * sizeof(double), cudaMemcpyDeviceToHost, S.st),
-       "D2H");
-    ck(cudaMemcpyAsync(c->hpin + 512, c->dscal + 512, sizeof(double), cudaMemcpyDeviceToHost, S.st), "D2H");
-    ck(cudaStreamSynchronize(S.st), "sync");
     std::vector<double> h(size_t(j) + 2, 0.0);
-    for (int i = 0; i <= j; ++i) h[size_t(i)] = c->hpin[i];
-    const double norm_before = std::sqrt(c->hpin[nv]);
-    double norm_w = std::sqrt(c->hpin[512]);
-    if (norm_w < reorth_threshold * norm_before) {  // krylov.hpp:123-130
-      ++*reorth_count;
-      dots_into(S, V, nv, w, false, 256);
-      ckl(fpc::launch_update(c->dvptr, c->dscales, c->dscal + 256, nv, w, n, c->partial, S.st), "update");
-      ckl(fpc::launch_reduce(c->partial, 1, 1, c->dscal + 512, false, S.st), "reduce");
-      ck(cudaMemcpyAsync(c->hpin + 256, c->dscal + 256, size_t(nv) * sizeof(double),
+    double norm_before = 0.0, norm_w = 0.0;
+    const int stride = fpc_context_s::kPartialStride;
+    if (nv <= fpc::kMaxFused) {
+      // fused: w' = w - V h and, in the same pass, c = V^T w' and ||w'||^2
+      fpc::VecSetN vs{};
+      for (int i = 0; i < nv; ++i) {
+        vs.v[i] = V[size_t(i)];
+        vs.s[i] = S.scales[size_t(i)];
+      }
+      LAUNCH("update_dots", S.st, fpc::launch_update_dots(vs, nv, c->dscal, w, n, c->partial, stride, S.st));
+      LAUNCH("reduce", S.st, fpc::launch_reduce(c->partial, stride, nv + 1, c->dscal + 256, false, S.st));
+      ck(cudaMemcpyAsync(c->hpin, c->dscal, size_t(nv + 1) * sizeof(double), cudaMemcpyDeviceToHost, S.st),
+         "D2H");
+      ck(cudaMemcpyAsync(c->hpin + 256, c->dscal + 256, size_t(nv + 1) * sizeof(double),
                          cudaMemcpyDeviceToHost, S.st),
+         "D2H");
+      ck(cudaStreamSynchronize(S.st), "sync");
+      for (int i = 0; i <= j; ++i) h[size_t(i)] = c->hpin[i];
+      norm_before = std::sqrt(c->hpin[nv]);
+      norm_w = std::sqrt(c->hpin[256 + nv]);
+      if (norm_w < reorth_threshold * norm_before) {  // krylov.hpp:123-130 (dots already done)
+        ++*reorth_count;
+        LAUNCH("update", S.st, fpc::launch_update(c->dvptr, c->dscales, c->dscal + 256, nv, w, n, c->partial, S.st));
+        LAUNCH("reduce", S.st, fpc::launch_reduce(c->partial, 1, 1, c->dscal + 512, false, S.st));
+        ck(cudaMemcpyAsync(c->hpin + 512, c->dscal + 512, sizeof(double), cudaMemcpyDeviceToHost, S.st), "D2H");
+        ck(cudaStreamSynchronize(S.st), "sync");
+        for (int i = 0; i <= j; ++i) h[size_t(i)] += c->hpin[256 + i];
+        norm_w = std::sqrt(c->hpin[512]);
+      }
+    } else {
+      LAUNCH("update", S.st, fpc::launch_update(c->dvptr, c->dscales, c->dscal, nv, w, n, c->partial, S.st));
+      LAUNCH("reduce", S.st, fpc::launch_reduce(c->partial, 1, 1, c->dscal + 512, false, S.st));
+      ck(cudaMemcpyAsync(c->hpin, c->dscal, size_t(nv + 1) * sizeof(double), cudaMemcpyDeviceToHost, S.st),
          "D2H");
       ck(cudaMemcpyAsync(c->hpin + 512, c->dscal + 512, sizeof(double), cudaMemcpyDeviceToHost, S.st), "D2H");
       ck(cudaStreamSynchronize(S.st), "sync");
-      for (int i = 0; i <= j; ++i) h[size_t(i)] += c->hpin[256 + i];
+      for (int i = 0; i <= j; ++i) h[size_t(i)] = c->hpin[i];
+      norm_before = std::sqrt(c->hpin[nv]);
       norm_w = std::sqrt(c->hpin[512]);
+      if (norm_w < reorth_threshold * norm_before) {  // krylov.hpp:123-130
+        ++*reorth_count;
+        dots_into(S, V, nv, w, false, 256);
+        LAUNCH("update", S.st, fpc::launch_update(c->dvptr, c->dscales, c->dscal + 256, nv, w, n, c->partial, S.st));
+        LAUNCH("reduce", S.st, fpc::launch_reduce(c->partial, 1, 1, c->dscal + 512, false, S.st));
+        ck(cudaMemcpyAsync(c->hpin + 256, c->dscal + 256, size_t(nv) * sizeof(double),
+                           cudaMemcpyDeviceToHost, S.st),
+           "D2H");
+        ck(cudaMemcpyAsync(c->hpin + 512, c->dscal + 512, sizeof(double), cudaMemcpyDeviceToHost, S.st), "D2H");
+        ck(cudaStreamSynchronize(S.st), "sync");
+        for (int i = 0; i <= j; ++i) h[size_t(i)] += c->hpin[256 + i];
+        norm_w = std::sqrt(c->hpin[512]);
+      }
     }
     h[size_t(j) + 1] = norm_w;
     // Givens (krylov.hpp:133-151)
@@ -792,7 +915,7 @@ static void gmres_inner(fpc_plan_s* pl, const double* b, double* x, double tol, 
   std::memcpy(c->hpin + 600, y.data(), y.size() * sizeof(double));
   ck(cudaMemcpyAsync(c->dscal + 600, c->hpin + 600, y.size() * sizeof(double), cudaMemcpyHostToDevice, S.st),
      "y");
-  ckl(fpc::launch_lincomb(c->dvptr, c->dscales, c->dscal + 600, steps, pl->d_u, n, S.st), "lincomb");
+  LAUNCH("lincomb", S.st, fpc::launch_lincomb(c->dvptr, c->dscales, c->dscal + 600, steps, pl->d_u, n, S.st));
   pc_apply_dev(pl, pl->d_u, x, 1.0);
   *steps_out = steps;
   ck(cudaStreamSynchronize(S.st), "sync");  // hpin reuse boundary
@@ -804,8 +927,8 @@ static double resid_norm_dev(fpc_plan_s* pl, const double* b, const double* x) {
   const size_t n = p->dim();
   if (!pl->d_r) pl->d_r = dalloc<double>(n + 2);
   matvec_dev(p, x, pl->d_r);
-  ckl(fpc::launch_resid_norm(b, pl->d_r, n, c->partial, c->stream), "resid");
-  ckl(fpc::launch_reduce(c->partial, 1, 1, c->dscal + 900, false, c->stream), "reduce");
+  LAUNCH("resid", c->stream, fpc::launch_resid_norm(b, pl->d_r, n, c->partial, c->stream));
+  LAUNCH("reduce", c->stream, fpc::launch_reduce(c->partial, 1, 1, c->dscal + 900, false, c->stream));
   ck(cudaMemcpyAsync(c->hpin + 900, c->dscal + 900, sizeof(double), cudaMemcpyDeviceToHost, c->stream), "D2H");
   ck(cudaStreamSynchronize(c->stream), "sync");
   return std::sqrt(c->hpin[900]);
@@ -853,7 +976,7 @@ static void gmres_dev(fpc_plan_s* pl, const double* b, double* x, const fpc_solv
       gmres_inner(pl, r, pl->d_d, cfg.tol * norm_b / norm_r, m, &conv, &steps, hist, &last_rel, &reorth);
       for (size_t i = h0; i < hist.size(); ++i) hist[i] *= norm_r / norm_b;
       if (last_rel >= 0.0) last_rel *= norm_r / norm_b;
-      ckl(fpc::launch_axpy(1.0, pl->d_d, x, n, c->stream), "axpy");
+      LAUNCH("axpy", c->stream, fpc::launch_axpy(1.0, pl->d_d, x, n, c->stream));
       total += steps;
       budget -= steps;
       if (conv) {
@@ -863,7 +986,7 @@ static void gmres_dev(fpc_plan_s* pl, const double* b, double* x, const fpc_solv
       if (steps == 0) break;
       ++rep->restarts;
       matvec_dev(p, x, r);
-      ckl(fpc::launch_rsub(b, r, n, c->stream), "rsub");
+      LAUNCH("rsub", c->stream, fpc::launch_rsub(b, r, n, c->stream));
     }
     rep->converged = conv_all;
     rep->iterations = total;

@@ -106,10 +106,10 @@ __device__ __forceinline__ double2 twid(const double2* __restrict__ tw, int t) {
   return S > 0 ? cconj(w) : w;
 }
 
-// Multiply v[r] (r = 1..R-1) by w^r, w = tw[t1] (w4 = tw[4 t1] when R > 4).
+// Multiply v[r] (r = 1..R-1) by w^r, w = tw[t1] (w4 = tw[4 t1] when R > 4).  t1 = 0 gives the
+// identity through the table (tw[0] = 1), so there is no divergent early exit.
 template <int R, int S>
 __device__ __forceinline__ void apply_twiddles(double2* v, const double2* __restrict__ tw, int t1) {
-  if (t1 == 0) return;
   const double2 w1 = twid<S>(tw, t1);
   if constexpr (R == 2) {
     v[1] = cmul(v[1], w1);
@@ -142,66 +142,63 @@ __device__ __forceinline__ void apply_twiddles(double2* v, const double2* __rest
   }
 }
 
-// One Stockham pass of radix R over B buffers of size N held in smem (padded, stride padded(N)).
-// Each thread processes 16/R butterflies (16 complex values).  Ns = current sub-transform length.
-template <int LOGN, int R, int S>
-__device__ __forceinline__ void stockham_pass(double2* s, const double2* __restrict__ tw, int Ns,
-                                              int nbuf) {
+// One Stockham pass of radix R over B buffers of size N = 2^LOGN held in smem (buffer stride BS,
+// pad16 inside a buffer).  NS = current sub-transform length (compile time, so all index
+// arithmetic folds to shifts/masks).  Each thread processes E/R butterflies (E complex values).
+template <int LOGN, int R, int S, int BS, int E, int NS>
+__device__ __forceinline__ void stockham_pass(double2* s, const double2* __restrict__ tw) {
   constexpr int N = 1 << LOGN;
-  constexpr int NB = N / R;          // butterflies per buffer
-  constexpr int PER = 16 / R;        // butterflies per thread
+  constexpr int NB = N / R;   // butterflies per buffer
+  constexpr int PER = E / R;  // butterflies per thread
   double2 v[PER][R];
-  int dst_b[PER], dst_off[PER];
+  int dst[PER];
   const int nthr = blockDim.x;
 #pragma unroll
   for (int q = 0; q < PER; ++q) {
-    const int g = threadIdx.x + q * nthr;  // global butterfly index across buffers
+    const int g = threadIdx.x + q * nthr;  // butterfly index across buffers
     const int b = g / NB;
-    const int j = g - b * NB;
-    dst_b[q] = -1;
-    if (b < nbuf) {
-      const double2* base = s + b * padded(N);
+    const int j = g & (NB - 1);
+    const double2* base = s + b * BS;
 #pragma unroll
-      for (int r = 0; r < R; ++r) v[q][r] = base[pad16(j + r * NB)];
-      const int jm = j & (Ns - 1);
-      apply_twiddles<R, S>(v[q], tw, jm * (N / (Ns * R)));
-      Dft<R, S>::run(v[q]);
-      dst_b[q] = b;
-      dst_off[q] = (j - jm) * R + jm;
-    }
+    for (int r = 0; r < R; ++r) v[q][r] = base[pad16(j + r * NB)];
+    const int jm = j & (NS - 1);
+    if constexpr (NS > 1) apply_twiddles<R, S>(v[q], tw, jm * (N / (NS * R)));
+    Dft<R, S>::run(v[q]);
+    dst[q] = b * BS + (j - jm) * R + jm;  // buffer base + logical offset (pad applied below)
   }
   __syncthreads();
 #pragma unroll
   for (int q = 0; q < PER; ++q) {
-    if (dst_b[q] >= 0) {
-      double2* base = s + dst_b[q] * padded(N);
+    const int b = dst[q] / BS;
+    const int off = dst[q] - b * BS;
+    double2* base = s + b * BS;
 #pragma unroll
-      for (int r = 0; r < R; ++r) base[pad16(dst_off[q] + r * Ns)] = v[q][r];
-    }
+    for (int r = 0; r < R; ++r) base[pad16(off + r * NS)] = v[q][r];
   }
   __syncthreads();
 }
 
-// Full transform of B = nbuf buffers; requires blockDim.x * 16 == nbuf * N (or more threads
-// than needed: extra butterflies are masked).  The caller must __syncthreads() before the call
-// (data written to smem) and may read the result after it returns.
-template <int LOGN, int S>
-__device__ __forceinline__ void block_fft(double2* s, const double2* __restrict__ tw, int nbuf) {
+template <int LOGN, int S, int BS, int E, int NS>
+__device__ __forceinline__ void fft_passes(double2* s, const double2* __restrict__ tw) {
   constexpr int N = 1 << LOGN;
-  int Ns = 1;
-  // radix-16 passes first, then the remainder (8, 4 or 2)
-  if constexpr (LOGN >= 4) {
-#pragma unroll
-    for (int p = 0; p < LOGN / 4; ++p) {
-      stockham_pass<LOGN, 16, S>(s, tw, Ns, nbuf);
-      Ns *= 16;
-    }
+  if constexpr (NS < N) {
+    constexpr int LE = E == 16 ? 4 : E == 8 ? 3 : E == 4 ? 2 : 1;
+    // the remainder radix goes first (NS = 1 needs no twiddles), full radix-E passes after it,
+    // so the twiddle sets the later passes touch stay small and L1 resident
+    constexpr int rem = (NS == 1) ? (LOGN % LE) : 0;
+    constexpr int R = rem == 3 ? 8 : rem == 2 ? 4 : rem == 1 ? 2 : E;
+    stockham_pass<LOGN, R, S, BS, E, NS>(s, tw);
+    fft_passes<LOGN, S, BS, E, NS * R>(s, tw);
   }
-  constexpr int rem = LOGN % 4;
-  if constexpr (rem == 3) stockham_pass<LOGN, 8, S>(s, tw, Ns, nbuf);
-  if constexpr (rem == 2) stockham_pass<LOGN, 4, S>(s, tw, Ns, nbuf);
-  if constexpr (rem == 1) stockham_pass<LOGN, 2, S>(s, tw, Ns, nbuf);
-  (void)N;
+}
+
+// Full transform of B buffers: requires blockDim.x * E == B * N (every buffer is transformed;
+// unused buffers must hold finite data).  E = complex values per thread per pass (16: radix-16
+// passes; 8: radix-8 passes at twice the threads).  The caller must __syncthreads() before the
+// call and may read the result after it returns.
+template <int LOGN, int S, int BS = padded(1 << LOGN), int E = 16>
+__device__ __forceinline__ void block_fft(double2* s, const double2* __restrict__ tw, int /*nbuf*/) {
+  fft_passes<LOGN, S, BS, E, 1>(s, tw);
 }
 
 }  // namespace fpc

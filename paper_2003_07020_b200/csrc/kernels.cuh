@@ -51,6 +51,15 @@ cudaError_t launch_reduce(const double* partial, int stride, int count, double* 
 // w <- w - sum_i c_i v_i with c_i = coef[i]*s_i (coef on device); partial norm of the result.
 cudaError_t launch_update(const double* const* vptr, const double* scales, const double* coef,
                           int nv, double* w, size_t n, double* partial, cudaStream_t st);
+// fused: w <- w - sum_i coef_i s_i v_i; partial[blk*stride + i] = s_i <v_i, w_new> (i < nv) and
+// partial[blk*stride + nv] = ||w_new||^2.  nv <= kMaxFused.
+constexpr int kMaxFused = 24;
+struct VecSetN {
+  const double* v[kMaxFused];
+  double s[kMaxFused];
+};
+cudaError_t launch_update_dots(const VecSetN& vs, int nv, const double* coef, double* w, size_t n,
+                               double* partial, int stride, cudaStream_t st);
 // u = sum_i c_i * s_i * v_i (c on device)
 cudaError_t launch_lincomb(const double* const* vptr, const double* scales, const double* coef,
                            int nv, double* u, size_t n, cudaStream_t st);

@@ -97,18 +97,24 @@ cudaError_t launch_dots(const VecSet& vs, int nv, const double* w, size_t n, dou
   return cudaGetLastError();
 }
 
-__global__ void k_reduce(const double* __restrict__ partial, int stride, int count,
-                         double* __restrict__ out, int accumulate) {
-  const int i = threadIdx.x + blockIdx.x * blockDim.x;
-  if (i >= count) return;
-  double s = 0.0;
-  for (int b = 0; b < kDotsGrid; ++b) s += partial[size_t(b) * stride + i];
-  out[i] = accumulate ? out[i] + s : s;
+// One CTA per output: thread t sums partials b = t, t+256, ... in order, then a fixed
+// shuffle/smem tree -> the result is independent of scheduling (deterministic).
+__global__ void __launch_bounds__(kDotsThreads)
+    k_reduce(const double* __restrict__ partial, int stride, int count, double* __restrict__ out,
+             int accumulate) {
+  const int i = blockIdx.x;
+  double acc[1] = {0.0};
+  for (int b = threadIdx.x; b < kDotsGrid; b += kDotsThreads) acc[0] += partial[size_t(b) * stride + i];
+  __shared__ double outb[1];
+  block_reduce_store<1>(acc, outb);
+  __syncthreads();
+  if (threadIdx.x == 0) out[i] = accumulate ? out[i] + outb[0] : outb[0];
 }
 
 cudaError_t launch_reduce(const double* partial, int stride, int count, double* out,
                           bool accumulate, cudaStream_t st) {
-  k_reduce<<<(count + 127) / 128, 128, 0, st>>>(partial, stride, count, out, accumulate ? 1 : 0);
+  if (count <= 0) return cudaSuccess;
+  k_reduce<<<count, kDotsThreads, 0, st>>>(partial, stride, count, out, accumulate ? 1 : 0);
   return cudaGetLastError();
 }
 
@@ -225,6 +231,82 @@ __global__ void k_rsub(const double* __restrict__ b, double* __restrict__ y, siz
 }
 cudaError_t launch_rsub(const double* b, double* y, size_t n, cudaStream_t st) {
   k_rsub<<<kDotsGrid, kDotsThreads, 0, st>>>(b, y, n);
+  return cudaGetLastError();
+}
+
+}  // namespace fpc
+
+namespace fpc {
+
+// Fused Gram-Schmidt step: w' = w - sum_i (coef_i s_i) v_i (sequential order, as the reference's
+// axpys, krylov.hpp:116-121), and in the same pass the re-orthogonalisation dots
+// partial[i] = s_i <v_i, w'> plus ||w'||^2 (krylov.hpp:122-130).  One read of the basis instead of
+// two when the reference's reorthogonalisation test fires.
+template <int NV>
+__global__ void __launch_bounds__(kDotsThreads)
+    k_update_dots(VecSetN vs, const double* __restrict__ coef, double* __restrict__ w, size_t n,
+                  double* __restrict__ partial, int stride) {
+  double c[NV];
+#pragma unroll
+  for (int i = 0; i < NV; ++i) c[i] = coef[i] * vs.s[i];
+  double acc[NV + 1];
+#pragma unroll
+  for (int i = 0; i <= NV; ++i) acc[i] = 0.0;
+  const size_t n2 = n / 2;
+  double2* w2 = reinterpret_cast<double2*>(w);
+  for (size_t e = size_t(blockIdx.x) * kDotsThreads + threadIdx.x; e < n2;
+       e += size_t(kDotsGrid) * kDotsThreads) {
+    double2 x[NV];
+#pragma unroll
+    for (int i = 0; i < NV; ++i) x[i] = reinterpret_cast<const double2*>(vs.v[i])[e];
+    double2 a = w2[e];
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      a.x = fma(-c[i], x[i].x, a.x);
+      a.y = fma(-c[i], x[i].y, a.y);
+    }
+    w2[e] = a;
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      acc[i] = fma(x[i].x, a.x, acc[i]);
+      acc[i] = fma(x[i].y, a.y, acc[i]);
+    }
+    acc[NV] = fma(a.x, a.x, acc[NV]);
+    acc[NV] = fma(a.y, a.y, acc[NV]);
+  }
+  if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
+    double a = w[n - 1];
+    double xl[NV];
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      xl[i] = vs.v[i][n - 1];
+      a = fma(-c[i], xl[i], a);
+    }
+    w[n - 1] = a;
+#pragma unroll
+    for (int i = 0; i < NV; ++i) acc[i] = fma(xl[i], a, acc[i]);
+    acc[NV] = fma(a, a, acc[NV]);
+  }
+  __shared__ double outb[NV + 1];
+  block_reduce_store<NV + 1>(acc, outb);
+  __syncthreads();
+  if (threadIdx.x <= NV) {
+    const double sc = threadIdx.x < NV ? vs.s[threadIdx.x] : 1.0;
+    partial[size_t(blockIdx.x) * stride + threadIdx.x] = outb[threadIdx.x] * sc;
+  }
+}
+
+cudaError_t launch_update_dots(const VecSetN& vs, int nv, const double* coef, double* w, size_t n,
+                               double* partial, int stride, cudaStream_t st) {
+  switch (nv) {
+#define UD(NVV) \
+  case NVV: k_update_dots<NVV><<<kDotsGrid, kDotsThreads, 0, st>>>(vs, coef, w, n, partial, stride); break;
+    UD(1) UD(2) UD(3) UD(4) UD(5) UD(6) UD(7) UD(8) UD(9) UD(10) UD(11) UD(12)
+    UD(13) UD(14) UD(15) UD(16) UD(17) UD(18) UD(19) UD(20) UD(21) UD(22) UD(23) UD(24)
+#undef UD
+    default:
+      return cudaErrorInvalidValue;
+  }
   return cudaGetLastError();
 }
 

@@ -73,6 +73,26 @@ def kernel_launches() -> int:
     return int(N.load().fpc_kernel_launches())
 
 
+class KernelProfile:
+    """Live per-kernel device time (CUDA events around every launch of this library)."""
+
+    def __enter__(self):
+        self.lib = N.load()
+        self.lib.fpc_profile_start()
+        return self
+
+    def __exit__(self, *exc):
+        n = self.lib.fpc_profile_stop()
+        self.table = {}
+        for i in range(n):
+            name = C.create_string_buffer(64)
+            ms, cnt = C.c_double(), C.c_longlong()
+            N.check(self.lib.fpc_profile_entry(i, name, 64, C.byref(ms), C.byref(cnt)))
+            if cnt.value:
+                self.table[name.value.decode()] = (ms.value, cnt.value)
+        return False
+
+
 # ---------------------------------------------------------------------------------- arrays
 def _is_torch(x) -> bool:
     return type(x).__module__.startswith("torch")
