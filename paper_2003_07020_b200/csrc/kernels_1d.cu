@@ -36,6 +36,10 @@ struct Geo {
   static constexpr size_t SMEM = size_t(B) * BS * sizeof(double2);
 };
 
+// CTAs per SM the register budget is sized for: radix-16 passes need ~128 registers per thread,
+// so 256-thread CTAs run two per SM (16 warps) and 512-thread CTAs one.
+__host__ __device__ constexpr int minb(int nt) { return nt <= 256 ? 2 : 1; }
+
 __device__ __forceinline__ double& comp(double2* s, int slot_padded, int c) {
   return reinterpret_cast<double*>(s + slot_padded)[c];
 }
@@ -56,7 +60,7 @@ struct MvGeo {
 };
 
 template <int LOGM>
-__global__ void __launch_bounds__(Geo<LOGM, kTotMv, 16>::NT)
+__global__ void __launch_bounds__(Geo<LOGM, kTotMv, 16>::NT, minb(Geo<LOGM, kTotMv, 16>::NT))
     k_matvec_1d(const double* __restrict__ v, double* __restrict__ y, int ns, int nt,
                 const double* __restrict__ eig, const double2* __restrict__ twb) {
   using G = Geo<LOGM, kTotMv, 16>;
@@ -143,18 +147,125 @@ __global__ void __launch_bounds__(Geo<LOGM, kTotMv, 16>::NT)
 }
 
 // =====================================================================================
+// K1 (large M): the same matvec on a 2-CTA cluster, one half-length (H = M/2) FFT per CTA.
+// The packed input z has z_m = 0 for m >= H (Ns < M), so the first decimation-in-frequency
+// stage of the M-point forward FFT is free: rank 0 transforms z (even bins), rank 1 transforms
+// z_m e^{-2 pi i m/M} (odd bins).  Spectral pairs (k, M-k) share parity, so the eigenvalue
+// product is CTA-local.  The inverse is split the same way (E = even bins, O = odd bins,
+// y_m = E_m + e^{+2 pi i m/M} O_m) and only y_m, m < H, is needed; each rank assembles half of
+// those outputs reading the partner's half through distributed shared memory.  Two CTAs of
+// ~100 KB per SM instead of one of ~200 KB (the radix-16 register budget allows two).
+// =====================================================================================
+template <int LOGM>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((1 << (LOGM - 1)) / 16, 2)
+    k_matvec_1d_split(const double* __restrict__ v, double* __restrict__ y, int ns,
+                      const double* __restrict__ eig, const double2* __restrict__ twb) {
+  constexpr int M = 1 << LOGM, H = M / 2, L = 2 * M, NT = H / 16, BS = padded(H);
+  constexpr int U = 4;
+  extern __shared__ double2 smem[];
+  double* cst = reinterpret_cast<double*>(smem + BS);  // stencil part for my H outputs
+  cg::cluster_group cluster = cg::this_cluster();
+  const int q = int(cluster.block_rank());
+  const size_t k = blockIdx.x >> 1;
+  const double* vk = v + k * ns;
+  const double2* twM = twb + M;
+
+  // load: packed input (rank 1 pre-twiddled) and the BDF2 stencil part of my outputs
+  for (int m0 = threadIdx.x; m0 < H; m0 += U * NT) {
+    double xe[U], xo[U], s0[U], s1[U], s2[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int m = m0 + u * NT;
+      const int i0 = 2 * m, i1 = 2 * m + 1;
+      xe[u] = i0 < ns ? vk[i0] : 0.0;
+      xo[u] = i1 < ns ? vk[i1] : 0.0;
+      const int j = q * H + m;  // my output index
+      const bool ok = j < ns;
+      s0[u] = ok ? vk[j] : 0.0;
+      s1[u] = (ok && k >= 1) ? vk[j - ns] : 0.0;
+      s2[u] = (ok && k >= 2) ? vk[j - 2 * size_t(ns)] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int m = m0 + u * NT;
+      double2 z = make_double2(xe[u], xo[u]);
+      if (q == 1) z = cmul(z, __ldg(twM + m));
+      smem[pad16(m)] = z;
+      double c;
+      if (k == 0)
+        c = s0[u];
+      else if (k == 1)
+        c = 1.5 * s0[u] + -2.0 * s1[u];
+      else
+        c = 1.5 * s0[u] + -2.0 * s1[u] + 0.5 * s2[u];
+      cst[m] = c;
+    }
+  }
+  __syncthreads();
+  block_fft<LOGM - 1, -1, BS, 16>(smem, twb + H, 1);
+
+  // eigenvalue product on (kappa, M - kappa) pairs; slot j of rank q holds bin 2j + q
+  const double2* twL = twb + L;
+  auto pair = [&](int s1, int s2, int kap) {
+    const double2 w = __ldg(twL + kap);  // e^{-2 pi i kappa/L}
+    const double ek = __ldg(eig + kap), em = __ldg(eig + M - kap);
+    const double2 a = smem[pad16(s1)], bq = smem[pad16(s2)];
+    const double2 P = cadd(a, cconj(bq)), Q = csub(a, cconj(bq));
+    const double2 iwQ = mul_si<1>(cmul(w, Q));
+    const double2 Yk = cscale(csub(P, iwQ), ek);
+    const double2 Ym = cscale(cconj(cadd(P, iwQ)), em);
+    const double2 A = cadd(Yk, cconj(Ym));
+    const double2 D = csub(Yk, cconj(Ym));
+    smem[pad16(s1)] = cadd(A, mul_si<1>(cmul(D, cconj(w))));
+    if (s1 != s2) smem[pad16(s2)] = cadd(cconj(A), mul_si<1>(cmul(cconj(D), w)));
+  };
+  if (q == 0) {
+    for (int j = threadIdx.x; j <= H / 2; j += NT) {
+      if (j == 0) {
+        const double2 z = smem[0];
+        const double y0 = eig[0] * (2.0 * (z.x + z.y));
+        const double ym = eig[M] * (2.0 * (z.x - z.y));
+        smem[0] = make_double2(y0 + ym, y0 - ym);
+      } else {
+        pair(j, H - j, 2 * j);
+      }
+    }
+  } else {
+    for (int j = threadIdx.x; j < H / 2; j += NT) pair(j, H - 1 - j, 2 * j + 1);
+  }
+  __syncthreads();
+  block_fft<LOGM - 1, 1, BS, 16>(smem, twb + H, 1);
+  if (q == 1) {
+    for (int m = threadIdx.x; m < H; m += NT) smem[pad16(m)] = cmul(smem[pad16(m)], cconj(__ldg(twM + m)));
+  }
+  cluster.sync();
+  // y_m = E_m + O'_m for my half of m; outputs 2m, 2m+1
+  const double2* Eb = cluster.map_shared_rank(smem, 0);
+  const double2* Ob = cluster.map_shared_rank(smem, 1);
+  double* yk = y + k * ns;
+  for (int mm = threadIdx.x; mm < H / 2; mm += NT) {
+    const int m = q * (H / 2) + mm;
+    const double2 e = Eb[pad16(m)], o = Ob[pad16(m)];
+    const int j0 = 2 * m, jl = 2 * mm;  // output index, local stencil slot
+    if (j0 < ns) yk[j0] = cst[jl] + (e.x + o.x);
+    if (j0 + 1 < ns) yk[j0 + 1] = cst[jl + 1] + (e.y + o.y);
+  }
+  cluster.sync();  // keep both buffers alive until the partner has read them
+}
+
+// =====================================================================================
 // K2: time FFT forward over spatial columns (alpha_circulant.hpp:146-156), Hermitian half.
 // CTA = B columns; M = Nt/2.
 // =====================================================================================
 constexpr int kTotT = 4096;
 
 template <int LOGM>
-__global__ void __launch_bounds__(Geo<LOGM, kTotT>::NT)
+__global__ void __launch_bounds__(Geo<LOGM, kTotT>::NT, minb(Geo<LOGM, kTotT>::NT))
     k_time_fwd(const double* __restrict__ v, double2* __restrict__ Z, int ns,
                const double* __restrict__ sf, double s_in, const double2* __restrict__ twb) {
   using G = Geo<LOGM, kTotT>;
   constexpr int M = G::M, B = G::B, NTIME = 2 * M, BS = G::BS, NT = G::NT;
-  constexpr int U = 8;
+  constexpr int U = 16;
   extern __shared__ double2 smem[];
   const int p0 = blockIdx.x * B;
 
@@ -205,12 +316,12 @@ __global__ void __launch_bounds__(Geo<LOGM, kTotT>::NT)
 // Z_{Nt-n} = conj(Z_n) (alpha_circulant.hpp:167-175) is folded into the real-output packing.
 // =====================================================================================
 template <int LOGM>
-__global__ void __launch_bounds__(Geo<LOGM, kTotT>::NT)
+__global__ void __launch_bounds__(Geo<LOGM, kTotT>::NT, minb(Geo<LOGM, kTotT>::NT))
     k_time_inv(const double2* __restrict__ Z, double* __restrict__ z, int ns,
                const double* __restrict__ sb, const double2* __restrict__ twb) {
   using G = Geo<LOGM, kTotT>;
   constexpr int M = G::M, B = G::B, NTIME = 2 * M, BS = G::BS, NT = G::NT;
-  constexpr int U = 4;
+  constexpr int U = 8;
   constexpr int TASKS = B * (M / 2 + 1);
   extern __shared__ double2 smem[];
   const int p0 = blockIdx.x * B;
@@ -275,7 +386,7 @@ struct TauGeo {
 };
 
 template <int LOGM>
-__global__ void __launch_bounds__(TauGeo<LOGM>::G::NT)
+__global__ void __launch_bounds__(TauGeo<LOGM>::G::NT, minb(TauGeo<LOGM>::G::NT))
     k_tau_solve_1d(double2* __restrict__ Z, int n_rows, const double2* __restrict__ lam,
                    const double* __restrict__ sigma, double dt, const double2* __restrict__ twb) {
   using G = typename TauGeo<LOGM>::G;
@@ -345,6 +456,8 @@ __global__ void __launch_bounds__(TauGeo<LOGM>::G::NT)
 // =====================================================================================
 template <class K>
 static cudaError_t prep(K kernel, size_t smem) {
+  cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+  if (e != cudaSuccess) return e;
   if (smem > 48 * 1024)
     return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   return cudaSuccess;
@@ -371,6 +484,12 @@ static cudaError_t prep(K kernel, size_t smem) {
 cudaError_t launch_matvec_1d(const double* v, double* y, int n_space, int n_time, int log_m,
                              const double* eig_scaled, const double2* tw_base, cudaStream_t st) {
   cudaError_t err = cudaSuccess;
+  if (log_m == 13) {
+    constexpr size_t smem = size_t(padded(4096)) * sizeof(double2) + 4096 * sizeof(double);
+    if ((err = prep(k_matvec_1d_split<13>, smem)) != cudaSuccess) return err;
+    k_matvec_1d_split<13><<<2 * n_time, 256, smem, st>>>(v, y, n_space, eig_scaled, tw_base);
+    return cudaGetLastError();
+  }
 #define CALL(LM)                                                                          \
   {                                                                                       \
     using G = Geo<LM, kTotMv, 16>;                                       \
