@@ -502,7 +502,36 @@ int fpc_problem_create_2d(fpc_context_t c, double gx, double gy, double kx, doub
     std::vector<double> wx = centred_weights(gx, n), wy = centred_weights(gy, n);
     if (n_time < 3) throw InvalidArg{"TimeStencil: need at least 3 time levels"};
     if (!(dt > 0.0)) throw InvalidArg{"AllAtOnceOperator: dt must be positive"};
-    throw Unsupported{"2D problems are not yet available on the B200 path"};
+    if (ilog2_exact(size_t(n_time)) < 0 || n_time < 4 || n_time > 16384)
+      throw Unsupported{"B200 path needs n_time to be a power of two in [4, 16384]"};
+    if (ilog2_exact(size_t(n) + 1) < 0 || n < 3 || n + 1 > 4096)
+      throw Unsupported{"B200 2D path needs n_per_dim + 1 to be a power of two in [4, 4096]"};
+    DeviceGuard g(c->device);
+    fpc_problem_s* p = new_problem(c, n_time, dt);
+    p->two_dim = 1;
+    p->n = n;
+    p->ns = n * n;
+    p->colx = wx;
+    p->coly = wy;
+    p->sx = kx / std::pow(h, gx);  // jacobian.hpp:67-68
+    p->sy = ky / std::pow(h, gy);
+    // tau_spectrum_2d(tau(Tx), tau(Ty), -sx, -sy) (jacobian.hpp:96-98, tau.hpp:59-73)
+    const std::vector<double> sgx = tau_spectrum(wx), sgy = tau_spectrum(wy);
+    p->sigma.resize(size_t(n) * n);
+    for (int ix = 0; ix < n; ++ix)
+      for (int iy = 0; iy < n; ++iy)
+        p->sigma[size_t(ix) * n + iy] = (-p->sx) * sgx[size_t(ix)] + (-p->sy) * sgy[size_t(iy)];
+    const size_t L = next_pow2(2 * size_t(n));
+    p->log_m = ilog2_exact(L / 2);
+    // y = c - dt*A v with A = -sx Tx(x)I - sy I(x)Ty: the device factors are +dt*s*eig/(2L)
+    std::vector<double> ey = circulant_eigs(wy), ex = circulant_eigs(wx);
+    for (double& x : ey) x *= dt * p->sy / (2.0 * double(L));
+    for (double& x : ex) x *= dt * p->sx / (2.0 * double(L));
+    p->d_eig = dalloc<double>(ey.size());
+    p->d_eig_x = dalloc<double>(ex.size());
+    ck(cudaMemcpy(p->d_eig, ey.data(), ey.size() * sizeof(double), cudaMemcpyHostToDevice), "eig_y");
+    ck(cudaMemcpy(p->d_eig_x, ex.data(), ex.size() * sizeof(double), cudaMemcpyHostToDevice), "eig_x");
+    *out = p;
   });
 }
 

@@ -35,6 +35,17 @@ __device__ __forceinline__ double2 mul_si(double2 a) {
   return S > 0 ? make_double2(-a.y, a.x) : make_double2(a.y, -a.x);
 }
 
+// a / (cr + i ci) by Smith's algorithm (the robust complex division std::complex uses, up to
+// rounding; tau.hpp:114)
+__device__ __forceinline__ double2 cdiv_smith(double2 a, double cr, double ci) {
+  if (fabs(cr) >= fabs(ci)) {
+    const double rr = ci / cr, den = cr + ci * rr;
+    return make_double2((a.x + a.y * rr) / den, (a.y - a.x * rr) / den);
+  }
+  const double rr = cr / ci, den = cr * rr + ci;
+  return make_double2((a.x * rr + a.y) / den, (a.y * rr - a.x) / den);
+}
+
 // cos/sin(2 pi k / 16), k = 0..15
 __device__ __constant__ double kC16[16] = {
     1.0, 0.92387953251128674, 0.70710678118654752, 0.38268343236508977,

@@ -27,6 +27,14 @@ cudaError_t launch_tau_solve_1d(double2* Z, int n_space, int n_rows, const doubl
                                 const double* sigma, double dt, const double2* tw_base,
                                 cudaStream_t st);
 
+// Toeplitz along nrows contiguous rows of length len (row r at v + r*len, time level r / rpt) +
+// BDF2 stencil with stride sstride: 1D (rpt=1, sstride=len) and the 2D y-direction pass.
+cudaError_t launch_matvec_rows(const double* v, double* y, int len, int nrows, int rpt,
+                               int sstride, int log_m, const double* eig_scaled,
+                               const double2* tw_base, cudaStream_t st);
+// in-place orthonormal DST-I of n_rows contiguous complex rows of length n (n + 1 = 2^k)
+cudaError_t launch_dst_rows(double2* Z, int n, int n_rows, const double2* tw_base, cudaStream_t st);
+
 // ---- 2D (jacobian.hpp:77-94, tau.hpp:79-96) -----------------------------------------------
 cudaError_t launch_matvec_2d(const double* v, double* y, int n, int n_time, int log_m,
                              const double* eig_y_scaled, const double* eig_x_scaled,

@@ -61,15 +61,20 @@ struct MvGeo {
 
 template <int LOGM>
 __global__ void __launch_bounds__(Geo<LOGM, kTotMv, 16>::NT, minb(Geo<LOGM, kTotMv, 16>::NT))
-    k_matvec_1d(const double* __restrict__ v, double* __restrict__ y, int ns, int nt,
-                const double* __restrict__ eig, const double2* __restrict__ twb) {
+    k_matvec_1d(const double* __restrict__ v, double* __restrict__ y, int ns, int nrows, int rpt,
+                int sstride, const double* __restrict__ eig, const double2* __restrict__ twb) {
+  // Generic "Toeplitz along contiguous rows + BDF2 stencil" pass: row r (length ns) sits at
+  // v + r*ns and belongs to time level k = r / rpt; the stencil reads the same position
+  // sstride and 2*sstride earlier.  1D: rows = time blocks (rpt = 1, sstride = ns);
+  // 2D: rows = lattice rows ix of every time block (rpt = n, sstride = n^2), the y-direction
+  // half of jacobian.hpp:84-87.
   using G = Geo<LOGM, kTotMv, 16>;
   constexpr int M = G::M, B = G::B, L = 2 * M, BS = G::BS, NT = G::NT;
   constexpr int U = 4;
   extern __shared__ double2 smem[];
   double* cst = reinterpret_cast<double*>(smem + B * BS);  // stencil part, B x M
   const int k0 = blockIdx.x * B;
-  const int nb = min(B, nt - k0);
+  const int nb = min(B, nrows - k0);
 
   for (int e0 = threadIdx.x; e0 < B * L; e0 += U * NT) {
     double x0[U], x1[U], x2[U];
@@ -77,19 +82,19 @@ __global__ void __launch_bounds__(Geo<LOGM, kTotMv, 16>::NT, minb(Geo<LOGM, kTot
     for (int u = 0; u < U; ++u) {
       const int e = e0 + u * NT;
       const int b = e / L, idx = e - b * L;
-      const int k = k0 + b;
+      const int k = (k0 + b) / rpt;
       const bool ok = e < B * L && b < nb && idx < ns;
-      const size_t o = size_t(k) * ns + idx;
+      const size_t o = size_t(k0 + b) * ns + idx;
       x0[u] = ok ? v[o] : 0.0;
-      x1[u] = (ok && k >= 1) ? v[o - ns] : 0.0;
-      x2[u] = (ok && k >= 2) ? v[o - 2 * size_t(ns)] : 0.0;
+      x1[u] = (ok && k >= 1) ? v[o - sstride] : 0.0;
+      x2[u] = (ok && k >= 2) ? v[o - 2 * size_t(sstride)] : 0.0;
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int e = e0 + u * NT;
       if (e < B * L) {
         const int b = e / L, idx = e - b * L;
-        const int k = k0 + b;
+        const int k = (k0 + b) / rpt;
         comp(smem, b * BS + pad16(idx >> 1), idx & 1) = x0[u];
         if (idx < ns) {
           double c;
@@ -385,7 +390,7 @@ struct TauGeo {
   static constexpr size_t SMEM = G::SMEM + size_t(G::NT / 32 + 1) * sizeof(double2);
 };
 
-template <int LOGM>
+template <int LOGM, bool DIVIDE>
 __global__ void __launch_bounds__(TauGeo<LOGM>::G::NT, minb(TauGeo<LOGM>::G::NT))
     k_tau_solve_1d(double2* __restrict__ Z, int n_rows, const double2* __restrict__ lam,
                    const double* __restrict__ sigma, double dt, const double2* __restrict__ twb) {
@@ -418,29 +423,17 @@ __global__ void __launch_bounds__(TauGeo<LOGM>::G::NT, minb(TauGeo<LOGM>::G::NT)
     }
   }
   __syncthreads();
-  block_dst<LOGM, BS, E, 1>(smem, twb, scale, scratch);
-
-  // divide by the shifted tau eigenvalues (slot i + 1 <-> index i)
-  for (int b = 0; b < B; ++b) {
-    double2* s = smem + b * BS;
-    const double2 l = (b < nb) ? __ldg(lam + r0 + b) : make_double2(1.0, 0.0);
-    for (int i = threadIdx.x; i < NSR; i += NT) {
-      const double cr = l.x - dt * __ldg(sigma + i), ci = l.y;
-      const double2 a = s[pad16(i + 1)];
-      double qr, qi;  // Smith's division a / (cr + i ci)
-      if (fabs(cr) >= fabs(ci)) {
-        const double rr = ci / cr, den = cr + ci * rr;
-        qr = (a.x + a.y * rr) / den;
-        qi = (a.y - a.x * rr) / den;
-      } else {
-        const double rr = cr / ci, den = cr * rr + ci;
-        qr = (a.x * rr + a.y) / den;
-        qi = (a.y * rr - a.x) / den;
-      }
-      s[pad16(i + 1)] = make_double2(qr, qi);
+  if constexpr (DIVIDE) {
+    block_dst<LOGM, BS, E, 1>(smem, twb, scale, scratch);
+    // divide by the shifted tau eigenvalues (slot i + 1 <-> index i)
+    for (int b = 0; b < B; ++b) {
+      double2* s = smem + b * BS;
+      const double2 l = (b < nb) ? __ldg(lam + r0 + b) : make_double2(1.0, 0.0);
+      for (int i = threadIdx.x; i < NSR; i += NT)
+        s[pad16(i + 1)] = cdiv_smith(s[pad16(i + 1)], l.x - dt * __ldg(sigma + i), l.y);
     }
+    __syncthreads();
   }
-  __syncthreads();
   block_dst<LOGM, BS, E, 0>(smem, twb, scale, scratch);
 
   // store rows (slot i <-> index i), coalesced
@@ -481,6 +474,22 @@ static cudaError_t prep(K kernel, size_t smem) {
     default: return cudaErrorInvalidValue; \
   }
 
+cudaError_t launch_matvec_rows(const double* v, double* y, int len, int nrows, int rpt,
+                               int sstride, int log_m, const double* eig_scaled,
+                               const double2* tw_base, cudaStream_t st) {
+  cudaError_t err = cudaSuccess;
+#define CALL(LM)                                                                          \
+  {                                                                                       \
+    using G = Geo<LM, kTotMv, 16>;                                                        \
+    if ((err = prep(k_matvec_1d<LM>, MvGeo<LM>::SMEM)) != cudaSuccess) return err;        \
+    k_matvec_1d<LM><<<(nrows + G::B - 1) / G::B, G::NT, MvGeo<LM>::SMEM, st>>>(           \
+        v, y, len, nrows, rpt, sstride, eig_scaled, tw_base);                             \
+  }
+  FPC_DISPATCH_LOGM(log_m, CALL)
+#undef CALL
+  return cudaGetLastError();
+}
+
 cudaError_t launch_matvec_1d(const double* v, double* y, int n_space, int n_time, int log_m,
                              const double* eig_scaled, const double2* tw_base, cudaStream_t st) {
   cudaError_t err = cudaSuccess;
@@ -490,16 +499,7 @@ cudaError_t launch_matvec_1d(const double* v, double* y, int n_space, int n_time
     k_matvec_1d_split<13><<<2 * n_time, 256, smem, st>>>(v, y, n_space, eig_scaled, tw_base);
     return cudaGetLastError();
   }
-#define CALL(LM)                                                                          \
-  {                                                                                       \
-    using G = Geo<LM, kTotMv, 16>;                                       \
-    if ((err = prep(k_matvec_1d<LM>, MvGeo<LM>::SMEM)) != cudaSuccess) return err;        \
-    k_matvec_1d<LM><<<(n_time + G::B - 1) / G::B, G::NT, MvGeo<LM>::SMEM, st>>>(          \
-        v, y, n_space, n_time, eig_scaled, tw_base);                                      \
-  }
-  FPC_DISPATCH_LOGM(log_m, CALL)
-#undef CALL
-  return cudaGetLastError();
+  return launch_matvec_rows(v, y, n_space, n_time, 1, n_space, log_m, eig_scaled, tw_base, st);
 }
 
 static int ilog2(int n) {
@@ -541,6 +541,23 @@ cudaError_t launch_time_inv(const double2* Z, double* z, int n_space, int n_time
   return cudaGetLastError();
 }
 
+// in-place orthonormal DST-I of n_rows contiguous complex rows of length n (n + 1 = 2^k)
+cudaError_t launch_dst_rows(double2* Z, int n, int n_rows, const double2* tw_base, cudaStream_t st) {
+  cudaError_t err = cudaSuccess;
+  const int lm = ilog2(n + 1);
+#define CALL(LM)                                                                          \
+  {                                                                                       \
+    using TG = TauGeo<LM>;                                                                \
+    if ((err = prep(k_tau_solve_1d<LM, false>, TG::SMEM)) != cudaSuccess) return err;     \
+    const int grid = (n_rows + TG::G::B - 1) / TG::G::B;                                  \
+    k_tau_solve_1d<LM, false><<<grid, TG::G::NT, TG::SMEM, st>>>(Z, n_rows, nullptr, nullptr, \
+                                                                 0.0, tw_base);           \
+  }
+  FPC_DISPATCH_LOGM(lm, CALL)
+#undef CALL
+  return cudaGetLastError();
+}
+
 cudaError_t launch_tau_solve_1d(double2* Z, int n_space, int n_rows, const double2* lambda,
                                 const double* sigma, double dt, const double2* tw_base,
                                 cudaStream_t st) {
@@ -549,9 +566,9 @@ cudaError_t launch_tau_solve_1d(double2* Z, int n_space, int n_rows, const doubl
 #define CALL(LM)                                                                          \
   {                                                                                       \
     using TG = TauGeo<LM>;                                                                \
-    if ((err = prep(k_tau_solve_1d<LM>, TG::SMEM)) != cudaSuccess) return err;            \
+    if ((err = prep(k_tau_solve_1d<LM, true>, TG::SMEM)) != cudaSuccess) return err;            \
     const int grid = (n_rows + TG::G::B - 1) / TG::G::B;                                  \
-    k_tau_solve_1d<LM><<<grid, TG::G::NT, TG::SMEM, st>>>(Z, n_rows, lambda, sigma, dt,   \
+    k_tau_solve_1d<LM, true><<<grid, TG::G::NT, TG::SMEM, st>>>(Z, n_rows, lambda, sigma, dt, \
                                                           tw_base);                       \
   }
   FPC_DISPATCH_LOGM(lm, CALL)

@@ -1,16 +1,241 @@
-// kernels_2d.cu -- 2D lattice kernels (RieszJacobian2D::apply jacobian.hpp:77-94 and the 2D tau
-// solves tau.hpp:79-96).  Filled in by the 2D milestone.
+// kernels_2d.cu -- 2D lattice kernels: the x-direction half of RieszJacobian2D::apply
+// (jacobian.hpp:88-93, strided columns) and the column passes of the 2D tau solves
+// (tau.hpp:79-96 dst_lattice_inplace, columns after rows).  The contiguous-row halves reuse the
+// 1D kernels (launch_matvec_rows / launch_dst_rows in kernels_1d.cu).
+//
+// Lattice p = ix*n + iy (x slow, problems.hpp:164-165).  A CTA owns C consecutive iy columns of one
+// time block (matvec) or one frequency row (tau): each lattice row ix contributes C contiguous
+// values (coalesced), and each column becomes one smem FFT buffer.
+#include "dst_block.cuh"
+#include "fft_block.cuh"
 #include "kernels.cuh"
 
 namespace fpc {
 
-cudaError_t launch_matvec_2d(const double*, double*, int, int, int, const double*, const double*,
-                             const double2*, cudaStream_t) {
-  return cudaErrorNotSupported;
+namespace {
+
+__host__ __device__ constexpr int skew2(int m) {
+  return m < 16 ? padded(m) : padded(m) + ((9 - padded(m) % 8) % 8);
 }
-cudaError_t launch_tau_solve_2d(double2*, int, int, const double2*, const double*, double,
-                                const double2*, cudaStream_t) {
-  return cudaErrorNotSupported;
+__device__ __forceinline__ double& comp2(double2* s, int slot_padded, int c) {
+  return reinterpret_cast<double*>(s + slot_padded)[c];
+}
+
+template <class K>
+cudaError_t prep2(K kernel, size_t smem) {
+  cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+  if (e != cudaSuccess) return e;
+  if (smem > 48 * 1024)
+    return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  return cudaSuccess;
+}
+
+int ilog2i(int n) {
+  int l = 0;
+  while ((1 << l) < n) ++l;
+  return l;
+}
+
+constexpr int kTot2 = 4096;
+
+template <int LOGM>
+struct ColGeo {
+  static constexpr int M = 1 << LOGM;
+  static constexpr int E = M < 16 ? M : 16;
+  static constexpr int C = kTot2 / M > 0 ? kTot2 / M : 1;  // columns per CTA
+  static constexpr int NT = C * M / E;
+  static constexpr int BS = C > 1 ? skew2(M) : padded(M);
+  static constexpr size_t SMEM = size_t(C) * BS * sizeof(double2) + size_t(NT / 32 + 1) * sizeof(double2);
+};
+
+}  // namespace
+
+// ------------------------------------------------------------------------------------------
+// y[k][ix][iy] += (dt sx / (2L)) * (T_x v[k][.][iy])[ix]  for C columns iy of time block k.
+// eig = dt*sx*eig(Tx)/(2L) pre-folded (the sign: y = c - dt*A v, A = -sx Tx (x) I - ...).
+// ------------------------------------------------------------------------------------------
+template <int LOGM>
+__global__ void __launch_bounds__(ColGeo<LOGM>::NT, (ColGeo<LOGM>::NT <= 256 ? 2 : 1))
+    k_matvec_2d_cols(const double* __restrict__ v, double* __restrict__ y, int n,
+                     const double* __restrict__ eig, const double2* __restrict__ twb) {
+  using G = ColGeo<LOGM>;
+  constexpr int M = G::M, C = G::C, NT = G::NT, BS = G::BS, L = 2 * M, E = G::E;
+  constexpr int U = 8;
+  extern __shared__ double2 smem[];
+  const int tiles = (n + C - 1) / C;
+  const int k = blockIdx.x / tiles;
+  const int iy0 = (blockIdx.x - k * tiles) * C;
+  const size_t base = size_t(k) * n * n;
+
+  // load columns: element (ix, c) -> buffer c, packed slot ix/2 (real packing of length L)
+  for (int e0 = threadIdx.x; e0 < C * L; e0 += U * NT) {
+    double x[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int e = e0 + u * NT;
+      const int c = e % C, ix = e / C;
+      const int iy = iy0 + c;
+      x[u] = (e < C * L && ix < n && iy < n) ? v[base + size_t(ix) * n + iy] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int e = e0 + u * NT;
+      if (e < C * L) {
+        const int c = e % C, ix = e / C;
+        comp2(smem, c * BS + pad16(ix >> 1), ix & 1) = x[u];
+      }
+    }
+  }
+  __syncthreads();
+  block_fft<LOGM, -1, BS, E>(smem, twb + M, C);
+  const double2* twL = twb + L;
+  for (int t = threadIdx.x; t < C * (M / 2 + 1); t += NT) {
+    const int c = t % C, kk = t / C;
+    double2* s = smem + c * BS;
+    if (kk == 0) {
+      const double2 z = s[0];
+      const double y0 = eig[0] * (2.0 * (z.x + z.y));
+      const double ym = eig[M] * (2.0 * (z.x - z.y));
+      s[0] = make_double2(y0 + ym, y0 - ym);
+    } else {
+      const int i1 = pad16(kk), i2 = pad16(M - kk);
+      const double2 w = __ldg(twL + kk);
+      const double ek = __ldg(eig + kk), em = __ldg(eig + M - kk);
+      const double2 a = s[i1], bq = s[i2];
+      const double2 P = cadd(a, cconj(bq)), Q = csub(a, cconj(bq));
+      const double2 iwQ = mul_si<1>(cmul(w, Q));
+      const double2 Yk = cscale(csub(P, iwQ), ek);
+      const double2 Ym = cscale(cconj(cadd(P, iwQ)), em);
+      const double2 A = cadd(Yk, cconj(Ym));
+      const double2 D = csub(Yk, cconj(Ym));
+      s[i1] = cadd(A, mul_si<1>(cmul(D, cconj(w))));
+      if (kk != M - kk) s[i2] = cadd(cconj(A), mul_si<1>(cmul(cconj(D), w)));
+    }
+  }
+  __syncthreads();
+  block_fft<LOGM, 1, BS, E>(smem, twb + M, C);
+  for (int e = threadIdx.x; e < C * n; e += NT) {
+    const int c = e % C, ix = e / C;
+    const int iy = iy0 + c;
+    if (iy >= n) continue;
+    const size_t o = base + size_t(ix) * n + iy;
+    y[o] += comp2(smem, c * BS + pad16(ix >> 1), ix & 1);
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// Column pass of the 2D tau solve for frequency row r: DST over ix of C columns, divide by
+// (lambda_r - dt sigma[ix*n + iy]), DST over ix again.  Rows (iy) are done before and after by
+// launch_dst_rows.
+// ------------------------------------------------------------------------------------------
+template <int LOGM>
+__global__ void __launch_bounds__(ColGeo<LOGM>::NT, (ColGeo<LOGM>::NT <= 256 ? 2 : 1))
+    k_tau_2d_cols(double2* __restrict__ Z, int n, const double2* __restrict__ lam,
+                  const double* __restrict__ sigma, double dt, const double2* __restrict__ twb) {
+  using G = ColGeo<LOGM>;
+  constexpr int M = G::M, C = G::C, NT = G::NT, BS = G::BS, E = G::E;
+  constexpr int NSR = M - 1;  // column length n
+  constexpr int U = 4;
+  extern __shared__ double2 smem[];
+  double2* scratch = smem + C * BS;
+  const int tiles = (NSR + C - 1) / C;
+  const int r = blockIdx.x / tiles;
+  const int iy0 = (blockIdx.x - r * tiles) * C;
+  double2* Zr = Z + size_t(r) * NSR * NSR;
+  const double scale = sqrt(2.0 / double(M));
+  (void)n;
+
+  for (int e0 = threadIdx.x; e0 < C * NSR; e0 += U * NT) {
+    double2 x[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int e = e0 + u * NT;
+      const int c = e % C, ix = e / C;
+      const int iy = iy0 + c;
+      x[u] = (e < C * NSR && iy < NSR) ? Zr[size_t(ix) * NSR + iy] : make_double2(0.0, 0.0);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int e = e0 + u * NT;
+      if (e < C * NSR) {
+        const int c = e % C, ix = e / C;
+        smem[c * BS + pad16(ix + 1)] = x[u];
+      }
+    }
+  }
+  __syncthreads();
+  block_dst<LOGM, BS, E, 1>(smem, twb, scale, scratch);
+  const double2 l = __ldg(lam + r);
+  for (int e = threadIdx.x; e < C * NSR; e += NT) {
+    const int c = e % C, ix = e / C;
+    const int iy = iy0 + c;
+    if (iy >= NSR) continue;
+    double2* s = smem + c * BS + pad16(ix + 1);
+    *s = cdiv_smith(*s, l.x - dt * __ldg(sigma + size_t(ix) * NSR + iy), l.y);
+  }
+  __syncthreads();
+  block_dst<LOGM, BS, E, 0>(smem, twb, scale, scratch);
+  for (int e = threadIdx.x; e < C * NSR; e += NT) {
+    const int c = e % C, ix = e / C;
+    const int iy = iy0 + c;
+    if (iy >= NSR) continue;
+    Zr[size_t(ix) * NSR + iy] = smem[c * BS + pad16(ix)];
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+#define FPC_DISPATCH_2D(logm, CALL)        \
+  switch (logm) {                          \
+    case 2: CALL(2); break;                \
+    case 3: CALL(3); break;                \
+    case 4: CALL(4); break;                \
+    case 5: CALL(5); break;                \
+    case 6: CALL(6); break;                \
+    case 7: CALL(7); break;                \
+    case 8: CALL(8); break;                \
+    case 9: CALL(9); break;                \
+    case 10: CALL(10); break;              \
+    case 11: CALL(11); break;              \
+    case 12: CALL(12); break;              \
+    default: return cudaErrorInvalidValue; \
+  }
+
+cudaError_t launch_matvec_2d(const double* v, double* y, int n, int n_time, int log_m,
+                             const double* eig_y_scaled, const double* eig_x_scaled,
+                             const double2* tw_base, cudaStream_t st) {
+  // y-direction on contiguous rows + BDF2 stencil (writes y), then x-direction columns (adds)
+  cudaError_t err = launch_matvec_rows(v, y, n, n_time * n, n, n * n, log_m, eig_y_scaled, tw_base, st);
+  if (err != cudaSuccess) return err;
+#define CALL(LM)                                                                          \
+  {                                                                                       \
+    using G = ColGeo<LM>;                                                                 \
+    if ((err = prep2(k_matvec_2d_cols<LM>, G::SMEM)) != cudaSuccess) return err;          \
+    const int tiles = (n + G::C - 1) / G::C;                                              \
+    k_matvec_2d_cols<LM><<<n_time * tiles, G::NT, G::SMEM, st>>>(v, y, n, eig_x_scaled, tw_base); \
+  }
+  FPC_DISPATCH_2D(log_m, CALL)
+#undef CALL
+  return cudaGetLastError();
+}
+
+cudaError_t launch_tau_solve_2d(double2* Z, int n, int n_rows, const double2* lambda,
+                                const double* sigma, double dt, const double2* tw_base,
+                                cudaStream_t st) {
+  // rows (iy) DST, columns (ix) DST-divide-DST, rows DST again (tau.hpp:79-96, 98-119)
+  cudaError_t err = launch_dst_rows(Z, n, n_rows * n, tw_base, st);
+  if (err != cudaSuccess) return err;
+  const int lm = ilog2i(n + 1);
+#define CALL(LM)                                                                          \
+  {                                                                                       \
+    using G = ColGeo<LM>;                                                                 \
+    if ((err = prep2(k_tau_2d_cols<LM>, G::SMEM)) != cudaSuccess) return err;             \
+    const int tiles = (n + G::C - 1) / G::C;                                              \
+    k_tau_2d_cols<LM><<<n_rows * tiles, G::NT, G::SMEM, st>>>(Z, n, lambda, sigma, dt, tw_base); \
+  }
+  FPC_DISPATCH_2D(lm, CALL)
+#undef CALL
+  if ((err = cudaGetLastError()) != cudaSuccess) return err;
+  return launch_dst_rows(Z, n, n_rows * n, tw_base, st);
 }
 
 }  // namespace fpc
