@@ -101,7 +101,10 @@ def cpu_reference_sample(w, threads: int, sample_iters: int):
     from oracle import oracle as O
     ref = O.Reference()
     ref.set_threads(threads)
-    p = ref.problem_1d(w.gamma[0], 1.0, w.h, w.n, w.n_time, w.dt).build_plan()
+    if w.two_dim:
+        p = ref.problem_2d(w.gamma[0], w.gamma[1], 1.0, 1.0, w.h, w.n, w.n_time, w.dt).build_plan()
+    else:
+        p = ref.problem_1d(w.gamma[0], 1.0, w.h, w.n, w.n_time, w.dt).build_plan()
     from paper_2003_07020_b200 import problems
     b = problems.rhs(w)
     _, rep = p.gmres(b, w.tol, sample_iters)

@@ -252,6 +252,7 @@ T* dalloc(size_t count) {
 
 // =================================================================================== context
 struct fpc_context_s {
+  int refs = 1;
   int device = 0;
   cudaStream_t stream = nullptr;
   bool own_stream = false;
@@ -280,6 +281,7 @@ struct DeviceGuard {
 
 // =================================================================================== problem
 struct fpc_problem_s {
+  int refs = 1;
   fpc_context_s* ctx = nullptr;
   int two_dim = 0;
   int n = 0;   // 1D: n_space; 2D: n per dim
@@ -401,8 +403,10 @@ int fpc_context_create(int device, fpc_context_t* out) {
   });
 }
 
-int fpc_context_destroy(fpc_context_t c) {
-  if (!c) return FPC_OK;
+// Handles are reference counted: a problem holds its context and a plan its problem, so the
+// owner may destroy them in any order (e.g. Python finalizers at interpreter exit).
+static void release_ctx(fpc_context_s* c) {
+  if (--c->refs > 0) return;
   DeviceGuard g(c->device);
   cudaStreamSynchronize(c->stream);
   cudaFree(c->tw);
@@ -413,6 +417,11 @@ int fpc_context_destroy(fpc_context_t c) {
   cudaFree(c->dscales);
   if (c->own_stream) cudaStreamDestroy(c->stream);
   delete c;
+}
+
+int fpc_context_destroy(fpc_context_t c) {
+  if (!c) return FPC_OK;
+  release_ctx(c);
   return FPC_OK;
 }
 
@@ -456,6 +465,7 @@ static fpc_problem_s* new_problem(fpc_context_s* c, int nt, double dt) {
   if (!(dt > 0.0)) throw InvalidArg{"AllAtOnceOperator: dt must be positive"};
   auto* p = new fpc_problem_s();
   p->ctx = c;
+  ++c->refs;
   p->nt = nt;
   p->dt = dt;
   return p;
@@ -535,15 +545,24 @@ int fpc_problem_create_2d(fpc_context_t c, double gx, double gy, double kx, doub
   });
 }
 
+static void release_problem(fpc_problem_s* p) {
+  if (--p->refs > 0) return;
+  fpc_context_s* c = p->ctx;
+  {
+    DeviceGuard g(c->device);
+    cudaStreamSynchronize(c->stream);
+    cudaFree(p->d_eig);
+    cudaFree(p->d_eig_x);
+    cudaFree(p->d_in);
+    cudaFree(p->d_out);
+  }
+  delete p;
+  release_ctx(c);
+}
+
 int fpc_problem_destroy(fpc_problem_t p) {
   if (!p) return FPC_OK;
-  DeviceGuard g(p->ctx->device);
-  cudaStreamSynchronize(p->ctx->stream);
-  cudaFree(p->d_eig);
-  cudaFree(p->d_eig_x);
-  cudaFree(p->d_in);
-  cudaFree(p->d_out);
-  delete p;
+  release_problem(p);
   return FPC_OK;
 }
 
@@ -684,20 +703,25 @@ int fpc_plan_create(fpc_problem_t p, double alpha_in, fpc_plan_t* out) {
     ck(cudaMemcpy(pl->d_lambda, pl->lambda.data(), size_t(pl->solve_count) * 16, cudaMemcpyHostToDevice),
        "lambda");
     ck(cudaMemcpy(pl->d_sigma, p->sigma.data(), p->sigma.size() * 8, cudaMemcpyHostToDevice), "sigma");
+    ++p->refs;
     *out = pl;
   });
 }
 
 int fpc_plan_destroy(fpc_plan_t pl) {
   if (!pl) return FPC_OK;
-  DeviceGuard g(pl->prob->ctx->device);
-  cudaStreamSynchronize(pl->prob->ctx->stream);
-  for (double* b : pl->basis) cudaFree(b);
-  for (void* q : {(void*)pl->d_sf, (void*)pl->d_sb, (void*)pl->d_lambda, (void*)pl->d_sigma,
-                  (void*)pl->d_Z, (void*)pl->d_z, (void*)pl->d_u, (void*)pl->d_r, (void*)pl->d_x,
-                  (void*)pl->d_d, (void*)pl->d_b})
-    cudaFree(q);
+  fpc_problem_s* p = pl->prob;
+  {
+    DeviceGuard g(p->ctx->device);
+    cudaStreamSynchronize(p->ctx->stream);
+    for (double* b : pl->basis) cudaFree(b);
+    for (void* q : {(void*)pl->d_sf, (void*)pl->d_sb, (void*)pl->d_lambda, (void*)pl->d_sigma,
+                    (void*)pl->d_Z, (void*)pl->d_z, (void*)pl->d_u, (void*)pl->d_r, (void*)pl->d_x,
+                    (void*)pl->d_d, (void*)pl->d_b})
+      cudaFree(q);
+  }
   delete pl;
+  release_problem(p);
   return FPC_OK;
 }
 

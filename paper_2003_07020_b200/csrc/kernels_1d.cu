@@ -387,7 +387,8 @@ template <int LOGM>
 struct TauGeo {
   static constexpr int EE = (1 << LOGM) < 16 ? (1 << LOGM) : 16;
   using G = Geo<LOGM, (LOGM >= 13 ? (1 << LOGM) : kTotTau), EE>;
-  static constexpr size_t SMEM = G::SMEM + size_t(G::NT / 32 + 1) * sizeof(double2);
+  static constexpr int BH = G::B > 1 ? skewed(G::M / 2) : padded(G::M / 2);
+  static constexpr size_t SMEM = G::SMEM + size_t(G::B) * BH * sizeof(double2);
 };
 
 template <int LOGM, bool DIVIDE>
@@ -399,7 +400,8 @@ __global__ void __launch_bounds__(TauGeo<LOGM>::G::NT, minb(TauGeo<LOGM>::G::NT)
   constexpr int NSR = M - 1;  // row length (n_space)
   constexpr int U = 4;
   extern __shared__ double2 smem[];
-  double2* scratch = smem + B * BS;
+  double2* hbuf = smem + B * BS;  // DCT-III scratch rows (dst_block.cuh)
+  constexpr int BH = TauGeo<LOGM>::BH;
   const int r0 = blockIdx.x * B;
   const int nb = min(B, n_rows - r0);
   const double scale = sqrt(2.0 / double(M));
@@ -424,7 +426,7 @@ __global__ void __launch_bounds__(TauGeo<LOGM>::G::NT, minb(TauGeo<LOGM>::G::NT)
   }
   __syncthreads();
   if constexpr (DIVIDE) {
-    block_dst<LOGM, BS, E, 1>(smem, twb, scale, scratch);
+    block_dst<LOGM, BS, BH, 1>(smem, hbuf, twb, scale);
     // divide by the shifted tau eigenvalues (slot i + 1 <-> index i)
     for (int b = 0; b < B; ++b) {
       double2* s = smem + b * BS;
@@ -434,7 +436,7 @@ __global__ void __launch_bounds__(TauGeo<LOGM>::G::NT, minb(TauGeo<LOGM>::G::NT)
     }
     __syncthreads();
   }
-  block_dst<LOGM, BS, E, 0>(smem, twb, scale, scratch);
+  block_dst<LOGM, BS, BH, 0>(smem, hbuf, twb, scale);
 
   // store rows (slot i <-> index i), coalesced
   for (int b = 0; b < nb; ++b) {

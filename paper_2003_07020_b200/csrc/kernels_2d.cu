@@ -45,7 +45,8 @@ struct ColGeo {
   static constexpr int C = kTot2 / M > 0 ? kTot2 / M : 1;  // columns per CTA
   static constexpr int NT = C * M / E;
   static constexpr int BS = C > 1 ? skew2(M) : padded(M);
-  static constexpr size_t SMEM = size_t(C) * BS * sizeof(double2) + size_t(NT / 32 + 1) * sizeof(double2);
+  static constexpr int BH = C > 1 ? skew2(M / 2) : padded(M / 2);  // DCT-III scratch (tau)
+  static constexpr size_t SMEM = size_t(C) * (BS + BH) * sizeof(double2);
 };
 
 }  // namespace
@@ -137,7 +138,8 @@ __global__ void __launch_bounds__(ColGeo<LOGM>::NT, (ColGeo<LOGM>::NT <= 256 ? 2
   constexpr int NSR = M - 1;  // column length n
   constexpr int U = 4;
   extern __shared__ double2 smem[];
-  double2* scratch = smem + C * BS;
+  double2* hbuf = smem + C * BS;  // DCT-III scratch columns (dst_block.cuh)
+  constexpr int BH = G::BH;
   const int tiles = (NSR + C - 1) / C;
   const int r = blockIdx.x / tiles;
   const int iy0 = (blockIdx.x - r * tiles) * C;
@@ -164,7 +166,7 @@ __global__ void __launch_bounds__(ColGeo<LOGM>::NT, (ColGeo<LOGM>::NT <= 256 ? 2
     }
   }
   __syncthreads();
-  block_dst<LOGM, BS, E, 1>(smem, twb, scale, scratch);
+  block_dst<LOGM, BS, BH, 1>(smem, hbuf, twb, scale);
   const double2 l = __ldg(lam + r);
   for (int e = threadIdx.x; e < C * NSR; e += NT) {
     const int c = e % C, ix = e / C;
@@ -174,7 +176,7 @@ __global__ void __launch_bounds__(ColGeo<LOGM>::NT, (ColGeo<LOGM>::NT <= 256 ? 2
     *s = cdiv_smith(*s, l.x - dt * __ldg(sigma + size_t(ix) * NSR + iy), l.y);
   }
   __syncthreads();
-  block_dst<LOGM, BS, E, 0>(smem, twb, scale, scratch);
+  block_dst<LOGM, BS, BH, 0>(smem, hbuf, twb, scale);
   for (int e = threadIdx.x; e < C * NSR; e += NT) {
     const int c = e % C, ix = e / C;
     const int iy = iy0 + c;
