@@ -1,0 +1,83 @@
+"""The drop-in boundary on CPU: libfracpint_b200.so loads, exports every entry point the header
+declares, and fails loudly (no CPU fallback) when no GPU is present.  Host-side API validation
+(argument checks that the reference performs before any compute) is exercised too."""
+import ctypes as C
+import os
+import re
+
+import numpy as np
+import pytest
+
+import paper_2003_07020_b200 as fp
+from paper_2003_07020_b200 import _native as N
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "fracpint_b200.h")
+
+
+def declared():
+    src = open(HEADER).read()
+    return sorted(set(re.findall(r"\b(fpc_[a-z0-9_]+)\s*\(", src)))
+
+
+def test_library_loads_and_exports_every_declared_symbol():
+    lib = C.CDLL(N.LIB_PATH)
+    names = declared()
+    assert len(names) >= 25
+    for name in names:
+        assert hasattr(lib, name), f"{name} declared in include/fracpint_b200.h but not exported"
+    assert sorted(N.EXPORTS) == names
+
+
+def test_abi_version_and_error_string():
+    lib = N.load()
+    assert lib.fpc_abi_version() == 1
+    assert isinstance(lib.fpc_last_error(), bytes)
+
+
+def test_no_cpu_fallback_without_gpu():
+    try:
+        import torch
+        if torch.cuda.is_available():
+            pytest.skip("GPU present")
+    except ImportError:
+        pass
+    h = C.c_void_p()
+    rc = N.load().fpc_context_create(0, C.byref(h))
+    assert rc in (N.FPC_CUDA_ERROR, N.FPC_INVALID_ARGUMENT)
+    with pytest.raises((RuntimeError, ValueError)):
+        fp.AllAtOnceOperator(fp.TimeStencil(8), fp.RieszJacobian1D(1.5, 1.0, 1 / 8, 7), 1 / 8)
+
+
+def test_host_assemble_rhs_matches_reference_rule():
+    nt, ns, dt = 4, 3, 0.25
+    f = np.arange(nt * ns, dtype=float)
+    u0 = np.array([1.0, 2.0, 3.0])
+    b = fp.assemble_rhs(fp.TimeStencil(nt), dt, f, u0)
+    ref = dt * f
+    ref[:ns] += u0
+    ref[ns:2 * ns] -= 0.5 * u0
+    assert np.array_equal(b, ref)
+    with pytest.raises(ValueError):
+        fp.assemble_rhs(fp.TimeStencil(nt), dt, f[:-1], u0)
+
+
+def test_argument_validation_matches_reference():
+    with pytest.raises(ValueError):
+        fp.TimeStencil(2)                                # time_stencil.hpp:24
+    with pytest.raises(ValueError):
+        fp.RieszJacobian1D(1.5, 0.0, 0.1, 4)             # jacobian.hpp:23
+    with pytest.raises(ValueError):
+        fp.RieszJacobian1D(0.9, 1.0, 0.1, 4)             # weights.hpp:24
+    with pytest.raises(ValueError):
+        fp.RieszJacobian2D(1.5, 1.5, 1.0, -1.0, 0.1, 4)  # jacobian.hpp:61
+    with pytest.raises(ValueError):
+        fp.PreconditionerKind.with_alpha(1.5).alpha_for(0.1)  # alpha_circulant.hpp:31
+    assert fp.PreconditionerKind.generalized().alpha_for(0.004) == pytest.approx(0.002)
+    assert fp.PreconditionerKind.generalized().alpha_for(3.0) == pytest.approx(0.5)
+    assert fp.PreconditionerKind.strang().alpha_for(0.1) == 1.0
+
+
+def test_weights_host_match_oracle(oracle):
+    for g in (1.2, 1.5, 1.99, 2.0):
+        assert np.allclose(fp.centred_weights(g, 33), oracle.centred_weights(g, 33), rtol=1e-14, atol=0)
