@@ -741,16 +741,21 @@ int fpc_plan_lambda(fpc_plan_t pl, double* out) {
 }
 
 // z = P^{-1} (s_in * v)  (alpha_circulant.hpp:137-199, half sweep)
-static void pc_apply_dev(fpc_plan_s* pl, const double* v, double* z, double s_in) {
+// forward = true: z = P (s_in v) from the same factors (apply_forward, alpha_circulant.hpp:212-215;
+// the reference runs it as a full sweep, which for real v equals the Hermitian half sweep).
+static void pc_apply_dev(fpc_plan_s* pl, const double* v, double* z, double s_in,
+                         bool forward = false) {
   fpc_problem_s* p = pl->prob;
   cudaStream_t st = p->ctx->stream;
   LAUNCH("time_fwd", st, fpc::launch_time_fwd(v, pl->d_Z, p->ns, p->nt, pl->d_sf, s_in, p->ctx->tw, st));
   if (!p->two_dim)
-    LAUNCH("tau_solve_1d", st, fpc::launch_tau_solve_1d(pl->d_Z, p->ns, pl->solve_count, pl->d_lambda, pl->d_sigma, p->dt,
-                                 p->ctx->tw, st));
+    LAUNCH("tau_solve_1d", st,
+           fpc::launch_tau_solve_1d(pl->d_Z, p->ns, pl->solve_count, pl->d_lambda, pl->d_sigma, p->dt,
+                                    p->ctx->tw, st, forward));
   else
-    LAUNCH("tau_solve_2d", st, fpc::launch_tau_solve_2d(pl->d_Z, p->n, pl->solve_count, pl->d_lambda, pl->d_sigma, p->dt,
-                                 p->ctx->tw, st));
+    LAUNCH("tau_solve_2d", st,
+           fpc::launch_tau_solve_2d(pl->d_Z, p->n, pl->solve_count, pl->d_lambda, pl->d_sigma, p->dt,
+                                    p->ctx->tw, st, forward));
   LAUNCH("time_inv", st, fpc::launch_time_inv(pl->d_Z, z, p->ns, p->nt, pl->d_sb, p->ctx->tw, st));
 }
 
@@ -779,9 +784,27 @@ int fpc_pc_apply(fpc_plan_t pl, const double* v, double* out, int sweep, int whe
   });
 }
 
-int fpc_pc_forward(fpc_plan_t pl, const double*, double*, int) {
+int fpc_pc_forward(fpc_plan_t pl, const double* v, double* out, int where) {
   if (!pl) return set_err(FPC_INVALID_ARGUMENT, "null plan");
-  return set_err(FPC_UNSUPPORTED, "apply_forward is not yet available on the B200 path");
+  return guarded([&] {
+    check_ptr(v, "fpc_pc_forward");
+    check_ptr(out, "fpc_pc_forward");
+    fpc_problem_s* p = pl->prob;
+    DeviceGuard g(p->ctx->device);
+    const size_t n = p->dim();
+    cudaStream_t st = p->ctx->stream;
+    if (where == FPC_DEVICE) {
+      check_dev_aligned(v, "fpc_pc_forward");
+      check_dev_aligned(out, "fpc_pc_forward");
+      pc_apply_dev(pl, v, out, 1.0, true);
+      return;
+    }
+    ensure_staging(p);
+    upload(p->d_in, v, n * sizeof(double), st);
+    pc_apply_dev(pl, p->d_in, p->d_out, 1.0, true);
+    ck(cudaMemcpyAsync(out, p->d_out, n * sizeof(double), cudaMemcpyDeviceToHost, st), "D2H");
+    ck(cudaStreamSynchronize(st), "sync");
+  });
 }
 
 // ---------------------------------------------------------------------------- GMRES

@@ -46,6 +46,14 @@ __device__ __forceinline__ double2 cdiv_smith(double2 a, double cr, double ci) {
   return make_double2((a.x * rr + a.y) / den, (a.y * rr - a.x) / den);
 }
 
+// the per-mode step of the shifted tau action (tau.hpp:109-118): MODE 1 = solve (divide by the
+// shifted eigenvalue), MODE 2 = forward action (multiply)
+template <int MODE>
+__device__ __forceinline__ double2 shift_apply(double2 a, double cr, double ci) {
+  if constexpr (MODE == 2) return cmul(a, make_double2(cr, ci));
+  return cdiv_smith(a, cr, ci);
+}
+
 // cos/sin(2 pi k / 16), k = 0..15
 __device__ __constant__ double kC16[16] = {
     1.0, 0.92387953251128674, 0.70710678118654752, 0.38268343236508977,

@@ -22,10 +22,11 @@ cudaError_t launch_time_fwd(const double* v, double2* Z, int n_space, int n_time
 // K4: z[k][p] = Re( scale_bwd[k]/Nt * sum_n Z_n e^{-2 pi i kn/Nt} ), Z_{Nt-n} = conj(Z_n).
 cudaError_t launch_time_inv(const double2* Z, double* z, int n_space, int n_time,
                             const double* scale_bwd, const double2* tw_base, cudaStream_t st);
-// K3 (1D): for each retained n: Z_n <- DST( DST(Z_n) ./ (lambda_n - dt*sigma) ).
+// K3 (1D): for each retained n: Z_n <- DST( DST(Z_n) ./ (lambda_n - dt*sigma) )
+// (forward = true: .* instead of ./, the apply_forward action tau.hpp:132-136).
 cudaError_t launch_tau_solve_1d(double2* Z, int n_space, int n_rows, const double2* lambda,
                                 const double* sigma, double dt, const double2* tw_base,
-                                cudaStream_t st);
+                                cudaStream_t st, bool forward = false);
 
 // Toeplitz along nrows contiguous rows of length len (row r at v + r*len, time level r / rpt) +
 // BDF2 stencil with stride sstride: 1D (rpt=1, sstride=len) and the 2D y-direction pass.
@@ -41,7 +42,7 @@ cudaError_t launch_matvec_2d(const double* v, double* y, int n, int n_time, int 
                              const double2* tw_base, cudaStream_t st);
 cudaError_t launch_tau_solve_2d(double2* Z, int n, int n_rows, const double2* lambda,
                                 const double* sigma, double dt, const double2* tw_base,
-                                cudaStream_t st);
+                                cudaStream_t st, bool forward = false);
 
 // ---- Krylov vector kernels (krylov.hpp:52-62, 116-131, 166-167, 180-182) -------------------
 struct VecSet {

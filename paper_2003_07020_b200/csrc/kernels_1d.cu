@@ -391,7 +391,7 @@ struct TauGeo {
   static constexpr size_t SMEM = G::SMEM + size_t(G::B) * BH * sizeof(double2);
 };
 
-template <int LOGM, bool DIVIDE>
+template <int LOGM, int MODE>  // 0: DST rows only; 1: DST-divide-DST (solve); 2: DST-multiply-DST
 __global__ void __launch_bounds__(TauGeo<LOGM>::G::NT, minb(TauGeo<LOGM>::G::NT))
     k_tau_solve_1d(double2* __restrict__ Z, int n_rows, const double2* __restrict__ lam,
                    const double* __restrict__ sigma, double dt, const double2* __restrict__ twb) {
@@ -425,14 +425,14 @@ __global__ void __launch_bounds__(TauGeo<LOGM>::G::NT, minb(TauGeo<LOGM>::G::NT)
     }
   }
   __syncthreads();
-  if constexpr (DIVIDE) {
+  if constexpr (MODE != 0) {
     block_dst<LOGM, BS, BH, 1>(smem, hbuf, twb, scale);
     // divide by the shifted tau eigenvalues (slot i + 1 <-> index i)
     for (int b = 0; b < B; ++b) {
       double2* s = smem + b * BS;
       const double2 l = (b < nb) ? __ldg(lam + r0 + b) : make_double2(1.0, 0.0);
       for (int i = threadIdx.x; i < NSR; i += NT)
-        s[pad16(i + 1)] = cdiv_smith(s[pad16(i + 1)], l.x - dt * __ldg(sigma + i), l.y);
+        s[pad16(i + 1)] = shift_apply<MODE>(s[pad16(i + 1)], l.x - dt * __ldg(sigma + i), l.y);
     }
     __syncthreads();
   }
@@ -550,9 +550,9 @@ cudaError_t launch_dst_rows(double2* Z, int n, int n_rows, const double2* tw_bas
 #define CALL(LM)                                                                          \
   {                                                                                       \
     using TG = TauGeo<LM>;                                                                \
-    if ((err = prep(k_tau_solve_1d<LM, false>, TG::SMEM)) != cudaSuccess) return err;     \
+    if ((err = prep(k_tau_solve_1d<LM, 0>, TG::SMEM)) != cudaSuccess) return err;     \
     const int grid = (n_rows + TG::G::B - 1) / TG::G::B;                                  \
-    k_tau_solve_1d<LM, false><<<grid, TG::G::NT, TG::SMEM, st>>>(Z, n_rows, nullptr, nullptr, \
+    k_tau_solve_1d<LM, 0><<<grid, TG::G::NT, TG::SMEM, st>>>(Z, n_rows, nullptr, nullptr, \
                                                                  0.0, tw_base);           \
   }
   FPC_DISPATCH_LOGM(lm, CALL)
@@ -560,22 +560,28 @@ cudaError_t launch_dst_rows(double2* Z, int n, int n_rows, const double2* tw_bas
   return cudaGetLastError();
 }
 
+template <int LM, int MODE>
+static cudaError_t tau1d(double2* Z, int n_rows, const double2* lambda, const double* sigma,
+                         double dt, const double2* tw_base, cudaStream_t st) {
+  using TG = TauGeo<LM>;
+  cudaError_t err = prep(k_tau_solve_1d<LM, MODE>, TG::SMEM);
+  if (err != cudaSuccess) return err;
+  const int grid = (n_rows + TG::G::B - 1) / TG::G::B;
+  k_tau_solve_1d<LM, MODE><<<grid, TG::G::NT, TG::SMEM, st>>>(Z, n_rows, lambda, sigma, dt, tw_base);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_tau_solve_1d(double2* Z, int n_space, int n_rows, const double2* lambda,
                                 const double* sigma, double dt, const double2* tw_base,
-                                cudaStream_t st) {
+                                cudaStream_t st, bool forward) {
   cudaError_t err = cudaSuccess;
   const int lm = ilog2(n_space + 1);
-#define CALL(LM)                                                                          \
-  {                                                                                       \
-    using TG = TauGeo<LM>;                                                                \
-    if ((err = prep(k_tau_solve_1d<LM, true>, TG::SMEM)) != cudaSuccess) return err;            \
-    const int grid = (n_rows + TG::G::B - 1) / TG::G::B;                                  \
-    k_tau_solve_1d<LM, true><<<grid, TG::G::NT, TG::SMEM, st>>>(Z, n_rows, lambda, sigma, dt, \
-                                                          tw_base);                       \
-  }
+#define CALL(LM)                                                                  \
+  err = forward ? tau1d<LM, 2>(Z, n_rows, lambda, sigma, dt, tw_base, st)         \
+                : tau1d<LM, 1>(Z, n_rows, lambda, sigma, dt, tw_base, st);
   FPC_DISPATCH_LOGM(lm, CALL)
 #undef CALL
-  return cudaGetLastError();
+  return err;
 }
 
 }  // namespace fpc

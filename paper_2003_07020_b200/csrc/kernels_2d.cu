@@ -129,7 +129,7 @@ __global__ void __launch_bounds__(ColGeo<LOGM>::NT, (ColGeo<LOGM>::NT <= 256 ? 2
 // (lambda_r - dt sigma[ix*n + iy]), DST over ix again.  Rows (iy) are done before and after by
 // launch_dst_rows.
 // ------------------------------------------------------------------------------------------
-template <int LOGM>
+template <int LOGM, int MODE>  // MODE 1: solve (divide), 2: forward action (multiply)
 __global__ void __launch_bounds__(ColGeo<LOGM>::NT, (ColGeo<LOGM>::NT <= 256 ? 2 : 1))
     k_tau_2d_cols(double2* __restrict__ Z, int n, const double2* __restrict__ lam,
                   const double* __restrict__ sigma, double dt, const double2* __restrict__ twb) {
@@ -173,7 +173,7 @@ __global__ void __launch_bounds__(ColGeo<LOGM>::NT, (ColGeo<LOGM>::NT <= 256 ? 2
     const int iy = iy0 + c;
     if (iy >= NSR) continue;
     double2* s = smem + c * BS + pad16(ix + 1);
-    *s = cdiv_smith(*s, l.x - dt * __ldg(sigma + size_t(ix) * NSR + iy), l.y);
+    *s = shift_apply<MODE>(*s, l.x - dt * __ldg(sigma + size_t(ix) * NSR + iy), l.y);
   }
   __syncthreads();
   block_dst<LOGM, BS, BH, 0>(smem, hbuf, twb, scale);
@@ -220,20 +220,29 @@ cudaError_t launch_matvec_2d(const double* v, double* y, int n, int n_time, int 
   return cudaGetLastError();
 }
 
+template <int LM, int MODE>
+static cudaError_t tau2d_cols(double2* Z, int n, int n_rows, const double2* lambda,
+                              const double* sigma, double dt, const double2* tw_base,
+                              cudaStream_t st) {
+  using G = ColGeo<LM>;
+  cudaError_t err = prep2(k_tau_2d_cols<LM, MODE>, G::SMEM);
+  if (err != cudaSuccess) return err;
+  const int tiles = (n + G::C - 1) / G::C;
+  k_tau_2d_cols<LM, MODE><<<n_rows * tiles, G::NT, G::SMEM, st>>>(Z, n, lambda, sigma, dt, tw_base);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_tau_solve_2d(double2* Z, int n, int n_rows, const double2* lambda,
                                 const double* sigma, double dt, const double2* tw_base,
-                                cudaStream_t st) {
+                                cudaStream_t st, bool forward) {
   // rows (iy) DST, columns (ix) DST-divide-DST, rows DST again (tau.hpp:79-96, 98-119)
   cudaError_t err = launch_dst_rows(Z, n, n_rows * n, tw_base, st);
   if (err != cudaSuccess) return err;
   const int lm = ilog2i(n + 1);
-#define CALL(LM)                                                                          \
-  {                                                                                       \
-    using G = ColGeo<LM>;                                                                 \
-    if ((err = prep2(k_tau_2d_cols<LM>, G::SMEM)) != cudaSuccess) return err;             \
-    const int tiles = (n + G::C - 1) / G::C;                                              \
-    k_tau_2d_cols<LM><<<n_rows * tiles, G::NT, G::SMEM, st>>>(Z, n, lambda, sigma, dt, tw_base); \
-  }
+#define CALL(LM)                                                                            \
+  err = forward ? tau2d_cols<LM, 2>(Z, n, n_rows, lambda, sigma, dt, tw_base, st)           \
+                : tau2d_cols<LM, 1>(Z, n, n_rows, lambda, sigma, dt, tw_base, st);          \
+  if (err != cudaSuccess) return err;
   FPC_DISPATCH_2D(lm, CALL)
 #undef CALL
   if ((err = cudaGetLastError()) != cudaSuccess) return err;

@@ -116,3 +116,15 @@ def test_unsupported_sizes_fail_loudly():
         fp.AllAtOnceOperator(fp.TimeStencil(6), fp.RieszJacobian1D(1.5, 1.0, 0.1, 9), 0.1)
     with pytest.raises(ValueError):
         fp.AllAtOnceOperator(fp.TimeStencil(8), fp.RieszJacobian1D(1.5, -1.0, 0.1, 7), 0.1)
+
+
+@pytest.mark.parametrize("gamma,ns,nt", [(1.9, 7, 8), (1.5, 63, 16), (1.5, 1023, 64), (1.2, 8191, 8)])
+def test_pc_forward_1d(oracle, gamma, ns, nt):
+    # apply_forward (alpha_circulant.hpp:212-215) vs the oracle, and the round trip P^{-1} P v = v
+    op, h, dt = make(gamma, ns, nt)
+    plan = fp.build_plan(fp.PreconditionerKind.with_alpha(0.35), nt, dt, op)
+    po = oracle.problem_1d(gamma, 1.0, h, ns, nt, dt).build_plan(0.35)
+    v = np.random.default_rng(ns).uniform(-1, 1, ns * nt)
+    pv = fp.apply_forward(plan, v)
+    assert rel(pv, po.pc_forward(v)) <= 1e-12
+    assert rel(fp.apply_inverse(plan, pv), v) <= 1e-10

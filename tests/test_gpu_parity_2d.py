@@ -65,3 +65,14 @@ def test_gmres_2d(oracle, gx, gy, n, nt, restart):
     assert res.report.converged and ro.converged
     assert abs(res.report.iterations - ro.iterations) <= 1
     assert rel(res.x, xo) <= 1e-10
+
+
+def test_pc_forward_2d(oracle):
+    n, nt, dt = 15, 8, 0.2
+    op = fp.AllAtOnceOperator(fp.TimeStencil(nt), fp.RieszJacobian2D(1.4, 1.8, 0.03, 0.05, 0.25, n), dt)
+    plan = fp.build_plan(fp.PreconditionerKind.with_alpha(0.6), nt, dt, op)
+    po = oracle.problem_2d(1.4, 1.8, 0.03, 0.05, 0.25, n, nt, dt).build_plan(0.6)
+    v = np.random.default_rng(2).uniform(-1, 1, n * n * nt)
+    pv = fp.apply_forward(plan, v)
+    assert rel(pv, po.pc_forward(v)) <= 1e-12
+    assert rel(fp.apply_inverse(plan, pv), v) <= 1e-10
