@@ -110,6 +110,25 @@ int fpc_pc_forward(fpc_plan_t plan, const double* v, double* out, int where);
 int fpc_gmres(fpc_plan_t plan, const double* b, double* x, const fpc_solver_config* cfg,
               fpc_report* report, double* history, int history_cap, int where);
 
+/* shard level: the per-rank pieces of the frequency-sharded multi-GPU solve
+ * (paper_2003_07020_b200/distributed.py).  Device pointers, stream-ordered; sizes are local.
+ *   matvec on nt_local time blocks starting at global level k_offset (the two previous blocks must
+ *     sit right before v when k_offset > 0)                           all_at_once.hpp:33-55
+ *   time_fwd / time_inv on ns_local spatial columns (row stride ns_local), Z half spectrum
+ *     [Nt/2+1][ns_local] complex                                      alpha_circulant.hpp:146-198
+ *   tau on frequency rows [row0, row0+nrows) of a [nrows][n_space] complex block  tau.hpp:98-136
+ *   dots / update / lincomb: the Gram-Schmidt vector kernels on local shards   krylov.hpp:116-183 */
+int fpc_shard_matvec(fpc_problem_t p, const double* v, double* y, int nt_local, int k_offset);
+int fpc_shard_time_fwd(fpc_plan_t plan, const double* v, double* Z, int ns_local, double s_in);
+int fpc_shard_tau(fpc_plan_t plan, double* Z, int row0, int nrows, int forward);
+int fpc_shard_time_inv(fpc_plan_t plan, const double* Z, double* z, int ns_local);
+int fpc_shard_dots(fpc_context_t ctx, const double* const* V, const double* scales, int nv,
+                   const double* w, size_t n, int with_norm, double* out_host);
+int fpc_shard_update(fpc_context_t ctx, const double* const* V, const double* coef, int nv,
+                     double* w, size_t n, double* norm2_host);
+int fpc_shard_lincomb(fpc_context_t ctx, const double* const* V, const double* coef, int nv,
+                      double* u, size_t n);
+
 /* instrumentation: number of kernels this library launched in this process */
 unsigned long long fpc_kernel_launches(void);
 /* live per-kernel device time: CUDA events on the launching stream around every launch while

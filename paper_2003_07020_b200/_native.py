@@ -23,7 +23,8 @@ EXPORTS = [
     "fpc_problem_dims", "fpc_problem_first_column", "fpc_problem_tau_sigma", "fpc_matvec",
     "fpc_assemble_rhs", "fpc_plan_create", "fpc_plan_destroy", "fpc_plan_info", "fpc_plan_lambda",
     "fpc_pc_apply", "fpc_pc_forward", "fpc_gmres", "fpc_kernel_launches", "fpc_profile_start",
-    "fpc_profile_stop", "fpc_profile_entry",
+    "fpc_profile_stop", "fpc_profile_entry", "fpc_shard_matvec", "fpc_shard_time_fwd", "fpc_shard_tau",
+    "fpc_shard_time_inv", "fpc_shard_dots", "fpc_shard_update", "fpc_shard_lincomb",
 ]
 
 
@@ -78,6 +79,13 @@ def load():
     lib.fpc_gmres.argtypes = [vp, dp, dp, C.POINTER(SolverConfigC), C.POINTER(ReportC), dp, C.c_int, C.c_int]
     lib.fpc_kernel_launches.restype = C.c_ulonglong
     lib.fpc_profile_entry.argtypes = [C.c_int, C.c_char_p, C.c_int, C.POINTER(d), C.POINTER(C.c_longlong)]
+    lib.fpc_shard_matvec.argtypes = [vp, vp, vp, C.c_int, C.c_int]
+    lib.fpc_shard_time_fwd.argtypes = [vp, vp, vp, C.c_int, d]
+    lib.fpc_shard_tau.argtypes = [vp, vp, C.c_int, C.c_int, C.c_int]
+    lib.fpc_shard_time_inv.argtypes = [vp, vp, vp, C.c_int]
+    lib.fpc_shard_dots.argtypes = [vp, vp, vp, C.c_int, vp, C.c_size_t, C.c_int, vp]
+    lib.fpc_shard_update.argtypes = [vp, vp, vp, C.c_int, vp, C.c_size_t, vp]
+    lib.fpc_shard_lincomb.argtypes = [vp, vp, vp, C.c_int, vp, C.c_size_t]
     _lib = lib
     return lib
 

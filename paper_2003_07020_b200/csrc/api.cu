@@ -1120,4 +1120,117 @@ int fpc_gmres(fpc_plan_t pl, const double* b, double* x, const fpc_solver_config
   });
 }
 
+// ---------------------------------------------------------------------------- shard level
+// The per-rank pieces of the frequency-sharded multi-GPU solve (paper_2003_07020_b200/
+// distributed.py): device pointers on the context device, stream-ordered on its stream.
+
+int fpc_shard_matvec(fpc_problem_t p, const double* v, double* y, int nt_local, int k_offset) {
+  if (!p) return set_err(FPC_INVALID_ARGUMENT, "null problem");
+  return guarded([&] {
+    check_ptr(v, "fpc_shard_matvec");
+    check_ptr(y, "fpc_shard_matvec");
+    if (nt_local < 1 || k_offset < 0 || k_offset + nt_local > p->nt)
+      throw InvalidArg{"fpc_shard_matvec: bad time range"};
+    DeviceGuard g(p->ctx->device);
+    cudaStream_t st = p->ctx->stream;
+    if (!p->two_dim)
+      LAUNCH("matvec_1d", st, fpc::launch_matvec_1d(v, y, p->ns, nt_local, p->log_m, p->d_eig, p->ctx->tw, st, k_offset));
+    else
+      LAUNCH("matvec_2d", st, fpc::launch_matvec_2d(v, y, p->n, nt_local, p->log_m, p->d_eig, p->d_eig_x, p->ctx->tw, st, k_offset));
+  });
+}
+
+int fpc_shard_time_fwd(fpc_plan_t pl, const double* v, double* Z, int ns_local, double s_in) {
+  if (!pl) return set_err(FPC_INVALID_ARGUMENT, "null plan");
+  return guarded([&] {
+    fpc_problem_s* p = pl->prob;
+    if (ns_local < 1 || ns_local > p->ns) throw InvalidArg{"fpc_shard_time_fwd: bad column count"};
+    DeviceGuard g(p->ctx->device);
+    cudaStream_t st = p->ctx->stream;
+    LAUNCH("time_fwd", st, fpc::launch_time_fwd(v, reinterpret_cast<double2*>(Z), ns_local, p->nt, pl->d_sf, s_in, p->ctx->tw, st));
+  });
+}
+
+int fpc_shard_tau(fpc_plan_t pl, double* Z, int row0, int nrows, int forward) {
+  if (!pl) return set_err(FPC_INVALID_ARGUMENT, "null plan");
+  return guarded([&] {
+    fpc_problem_s* p = pl->prob;
+    if (row0 < 0 || nrows < 0 || row0 + nrows > pl->solve_count)
+      throw InvalidArg{"fpc_shard_tau: bad frequency range"};
+    if (nrows == 0) return;
+    DeviceGuard g(p->ctx->device);
+    cudaStream_t st = p->ctx->stream;
+    double2* z = reinterpret_cast<double2*>(Z);
+    if (!p->two_dim)
+      LAUNCH("tau_solve_1d", st, fpc::launch_tau_solve_1d(z, p->ns, nrows, pl->d_lambda + row0, pl->d_sigma, p->dt, p->ctx->tw, st, forward != 0));
+    else
+      LAUNCH("tau_solve_2d", st, fpc::launch_tau_solve_2d(z, p->n, nrows, pl->d_lambda + row0, pl->d_sigma, p->dt, p->ctx->tw, st, forward != 0));
+  });
+}
+
+int fpc_shard_time_inv(fpc_plan_t pl, const double* Z, double* z, int ns_local) {
+  if (!pl) return set_err(FPC_INVALID_ARGUMENT, "null plan");
+  return guarded([&] {
+    fpc_problem_s* p = pl->prob;
+    if (ns_local < 1 || ns_local > p->ns) throw InvalidArg{"fpc_shard_time_inv: bad column count"};
+    DeviceGuard g(p->ctx->device);
+    cudaStream_t st = p->ctx->stream;
+    LAUNCH("time_inv", st, fpc::launch_time_inv(reinterpret_cast<const double2*>(Z), z, ns_local, p->nt, pl->d_sb, p->ctx->tw, st));
+  });
+}
+
+// out_host[i] = s_i <V_i, w> (i < nv), out_host[nv] = <w, w> when with_norm; synchronous.
+int fpc_shard_dots(fpc_context_t c, const double* const* V, const double* scales, int nv,
+                   const double* w, size_t n, int with_norm, double* out_host) {
+  if (!c || !out_host) return set_err(FPC_INVALID_ARGUMENT, "null argument");
+  return guarded([&] {
+    if (nv < 0 || nv > 250) throw InvalidArg{"fpc_shard_dots: 0 <= nv <= 250"};
+    DeviceGuard g(c->device);
+    GmresState S{nullptr, c, n, c->stream, std::vector<double>(scales, scales + nv), 0};
+    std::vector<const double*> vv(V, V + nv);
+    dots_into(S, vv, nv, w, nv == 0 ? true : with_norm != 0, 0);
+    const int cnt = nv + ((with_norm || nv == 0) ? 1 : 0);
+    ck(cudaMemcpyAsync(c->hpin, c->dscal, size_t(cnt) * sizeof(double), cudaMemcpyDeviceToHost, c->stream), "D2H");
+    ck(cudaStreamSynchronize(c->stream), "sync");
+    std::memcpy(out_host, c->hpin, size_t(cnt) * sizeof(double));
+  });
+}
+
+// w <- w - sum_i coef_i * V_i (coef on the host, scales already folded in); returns ||w||^2.
+int fpc_shard_update(fpc_context_t c, const double* const* V, const double* coef, int nv, double* w,
+                     size_t n, double* norm2_host) {
+  if (!c || !norm2_host) return set_err(FPC_INVALID_ARGUMENT, "null argument");
+  return guarded([&] {
+    if (nv < 0 || nv > 250) throw InvalidArg{"fpc_shard_update: 0 <= nv <= 250"};
+    DeviceGuard g(c->device);
+    std::vector<double> ones(size_t(nv), 1.0);
+    ck(cudaMemcpyAsync(c->dvptr, V, size_t(nv) * sizeof(double*), cudaMemcpyHostToDevice, c->stream), "vptr");
+    ck(cudaMemcpyAsync(c->dscales, ones.data(), size_t(nv) * sizeof(double), cudaMemcpyHostToDevice, c->stream), "scales");
+    std::memcpy(c->hpin + 700, coef, size_t(nv) * sizeof(double));
+    ck(cudaMemcpyAsync(c->dscal + 700, c->hpin + 700, size_t(nv) * sizeof(double), cudaMemcpyHostToDevice, c->stream), "coef");
+    LAUNCH("update", c->stream, fpc::launch_update(c->dvptr, c->dscales, c->dscal + 700, nv, w, n, c->partial, c->stream));
+    LAUNCH("reduce", c->stream, fpc::launch_reduce(c->partial, 1, 1, c->dscal + 512, false, c->stream));
+    ck(cudaMemcpyAsync(c->hpin + 512, c->dscal + 512, sizeof(double), cudaMemcpyDeviceToHost, c->stream), "D2H");
+    ck(cudaStreamSynchronize(c->stream), "sync");
+    *norm2_host = c->hpin[512];
+  });
+}
+
+// u = sum_i coef_i V_i (coef on the host)
+int fpc_shard_lincomb(fpc_context_t c, const double* const* V, const double* coef, int nv, double* u,
+                      size_t n) {
+  if (!c) return set_err(FPC_INVALID_ARGUMENT, "null context");
+  return guarded([&] {
+    if (nv < 1 || nv > 250) throw InvalidArg{"fpc_shard_lincomb: 1 <= nv <= 250"};
+    DeviceGuard g(c->device);
+    std::vector<double> ones(size_t(nv), 1.0);
+    ck(cudaMemcpyAsync(c->dvptr, V, size_t(nv) * sizeof(double*), cudaMemcpyHostToDevice, c->stream), "vptr");
+    ck(cudaMemcpyAsync(c->dscales, ones.data(), size_t(nv) * sizeof(double), cudaMemcpyHostToDevice, c->stream), "scales");
+    std::memcpy(c->hpin + 700, coef, size_t(nv) * sizeof(double));
+    ck(cudaMemcpyAsync(c->dscal + 700, c->hpin + 700, size_t(nv) * sizeof(double), cudaMemcpyHostToDevice, c->stream), "coef");
+    LAUNCH("lincomb", c->stream, fpc::launch_lincomb(c->dvptr, c->dscales, c->dscal + 700, nv, u, n, c->stream));
+    ck(cudaStreamSynchronize(c->stream), "sync");
+  });
+}
+
 }  // extern "C"

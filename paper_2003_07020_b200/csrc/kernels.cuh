@@ -11,8 +11,11 @@ constexpr int kMaxLogTw = 17;
 
 // ---- 1D all-at-once matvec (all_at_once.hpp:33-55 + toeplitz.hpp:41-57) --------------------
 // y_k = C-stencil(v)_k + IFFT(eig' .* FFT(pad(v_k)))  with eig' = -dt*eig/(2L) pre-folded.
+// koff = global time level of v's first block (time-sharded callers: the two previous blocks
+// must sit right before v in memory when koff > 0).
 cudaError_t launch_matvec_1d(const double* v, double* y, int n_space, int n_time, int log_m,
-                             const double* eig_scaled, const double2* tw_base, cudaStream_t st);
+                             const double* eig_scaled, const double2* tw_base, cudaStream_t st,
+                             int koff = 0);
 
 // ---- preconditioner apply, reference ordering (alpha_circulant.hpp:137-199) ---------------
 // K2: Z[n][p] = sum_k s_in*scale_fwd[k]*v[k][p] e^{+2 pi i kn/Nt}, n = 0..Nt/2 (half spectrum).
@@ -32,14 +35,14 @@ cudaError_t launch_tau_solve_1d(double2* Z, int n_space, int n_rows, const doubl
 // BDF2 stencil with stride sstride: 1D (rpt=1, sstride=len) and the 2D y-direction pass.
 cudaError_t launch_matvec_rows(const double* v, double* y, int len, int nrows, int rpt,
                                int sstride, int log_m, const double* eig_scaled,
-                               const double2* tw_base, cudaStream_t st);
+                               const double2* tw_base, cudaStream_t st, int koff = 0);
 // in-place orthonormal DST-I of n_rows contiguous complex rows of length n (n + 1 = 2^k)
 cudaError_t launch_dst_rows(double2* Z, int n, int n_rows, const double2* tw_base, cudaStream_t st);
 
 // ---- 2D (jacobian.hpp:77-94, tau.hpp:79-96) -----------------------------------------------
 cudaError_t launch_matvec_2d(const double* v, double* y, int n, int n_time, int log_m,
                              const double* eig_y_scaled, const double* eig_x_scaled,
-                             const double2* tw_base, cudaStream_t st);
+                             const double2* tw_base, cudaStream_t st, int koff = 0);
 cudaError_t launch_tau_solve_2d(double2* Z, int n, int n_rows, const double2* lambda,
                                 const double* sigma, double dt, const double2* tw_base,
                                 cudaStream_t st, bool forward = false);

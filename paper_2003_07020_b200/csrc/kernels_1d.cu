@@ -62,7 +62,8 @@ struct MvGeo {
 template <int LOGM>
 __global__ void __launch_bounds__(Geo<LOGM, kTotMv, 16>::NT, minb(Geo<LOGM, kTotMv, 16>::NT))
     k_matvec_1d(const double* __restrict__ v, double* __restrict__ y, int ns, int nrows, int rpt,
-                int sstride, const double* __restrict__ eig, const double2* __restrict__ twb) {
+                int sstride, int koff, const double* __restrict__ eig,
+                const double2* __restrict__ twb) {
   // Generic "Toeplitz along contiguous rows + BDF2 stencil" pass: row r (length ns) sits at
   // v + r*ns and belongs to time level k = r / rpt; the stencil reads the same position
   // sstride and 2*sstride earlier.  1D: rows = time blocks (rpt = 1, sstride = ns);
@@ -82,7 +83,7 @@ __global__ void __launch_bounds__(Geo<LOGM, kTotMv, 16>::NT, minb(Geo<LOGM, kTot
     for (int u = 0; u < U; ++u) {
       const int e = e0 + u * NT;
       const int b = e / L, idx = e - b * L;
-      const int k = (k0 + b) / rpt;
+      const int k = (k0 + b) / rpt + koff;
       const bool ok = e < B * L && b < nb && idx < ns;
       const size_t o = size_t(k0 + b) * ns + idx;
       x0[u] = ok ? v[o] : 0.0;
@@ -94,7 +95,7 @@ __global__ void __launch_bounds__(Geo<LOGM, kTotMv, 16>::NT, minb(Geo<LOGM, kTot
       const int e = e0 + u * NT;
       if (e < B * L) {
         const int b = e / L, idx = e - b * L;
-        const int k = (k0 + b) / rpt;
+        const int k = (k0 + b) / rpt + koff;
         comp(smem, b * BS + pad16(idx >> 1), idx & 1) = x0[u];
         if (idx < ns) {
           double c;
@@ -163,7 +164,7 @@ __global__ void __launch_bounds__(Geo<LOGM, kTotMv, 16>::NT, minb(Geo<LOGM, kTot
 // =====================================================================================
 template <int LOGM>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((1 << (LOGM - 1)) / 16, 2)
-    k_matvec_1d_split(const double* __restrict__ v, double* __restrict__ y, int ns,
+    k_matvec_1d_split(const double* __restrict__ v, double* __restrict__ y, int ns, int koff,
                       const double* __restrict__ eig, const double2* __restrict__ twb) {
   constexpr int M = 1 << LOGM, H = M / 2, L = 2 * M, NT = H / 16, BS = padded(H);
   constexpr int U = 4;
@@ -172,6 +173,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((1 << (LOGM - 1)) / 
   cg::cluster_group cluster = cg::this_cluster();
   const int q = int(cluster.block_rank());
   const size_t k = blockIdx.x >> 1;
+  const long kg = long(k) + koff;  // global time level (time-sharded callers pass a halo + offset)
   const double* vk = v + k * ns;
   const double2* twM = twb + M;
 
@@ -187,8 +189,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((1 << (LOGM - 1)) / 
       const int j = q * H + m;  // my output index
       const bool ok = j < ns;
       s0[u] = ok ? vk[j] : 0.0;
-      s1[u] = (ok && k >= 1) ? vk[j - ns] : 0.0;
-      s2[u] = (ok && k >= 2) ? vk[j - 2 * size_t(ns)] : 0.0;
+      s1[u] = (ok && kg >= 1) ? vk[long(j) - ns] : 0.0;
+      s2[u] = (ok && kg >= 2) ? vk[long(j) - 2 * long(ns)] : 0.0;
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
@@ -197,9 +199,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((1 << (LOGM - 1)) / 
       if (q == 1) z = cmul(z, __ldg(twM + m));
       smem[pad16(m)] = z;
       double c;
-      if (k == 0)
+      if (kg == 0)
         c = s0[u];
-      else if (k == 1)
+      else if (kg == 1)
         c = 1.5 * s0[u] + -2.0 * s1[u];
       else
         c = 1.5 * s0[u] + -2.0 * s1[u] + 0.5 * s2[u];
@@ -478,14 +480,14 @@ static cudaError_t prep(K kernel, size_t smem) {
 
 cudaError_t launch_matvec_rows(const double* v, double* y, int len, int nrows, int rpt,
                                int sstride, int log_m, const double* eig_scaled,
-                               const double2* tw_base, cudaStream_t st) {
+                               const double2* tw_base, cudaStream_t st, int koff) {
   cudaError_t err = cudaSuccess;
 #define CALL(LM)                                                                          \
   {                                                                                       \
     using G = Geo<LM, kTotMv, 16>;                                                        \
     if ((err = prep(k_matvec_1d<LM>, MvGeo<LM>::SMEM)) != cudaSuccess) return err;        \
     k_matvec_1d<LM><<<(nrows + G::B - 1) / G::B, G::NT, MvGeo<LM>::SMEM, st>>>(           \
-        v, y, len, nrows, rpt, sstride, eig_scaled, tw_base);                             \
+        v, y, len, nrows, rpt, sstride, koff, eig_scaled, tw_base);                       \
   }
   FPC_DISPATCH_LOGM(log_m, CALL)
 #undef CALL
@@ -493,15 +495,16 @@ cudaError_t launch_matvec_rows(const double* v, double* y, int len, int nrows, i
 }
 
 cudaError_t launch_matvec_1d(const double* v, double* y, int n_space, int n_time, int log_m,
-                             const double* eig_scaled, const double2* tw_base, cudaStream_t st) {
+                             const double* eig_scaled, const double2* tw_base, cudaStream_t st,
+                             int koff) {
   cudaError_t err = cudaSuccess;
   if (log_m == 13) {
     constexpr size_t smem = size_t(padded(4096)) * sizeof(double2) + 4096 * sizeof(double);
     if ((err = prep(k_matvec_1d_split<13>, smem)) != cudaSuccess) return err;
-    k_matvec_1d_split<13><<<2 * n_time, 256, smem, st>>>(v, y, n_space, eig_scaled, tw_base);
+    k_matvec_1d_split<13><<<2 * n_time, 256, smem, st>>>(v, y, n_space, koff, eig_scaled, tw_base);
     return cudaGetLastError();
   }
-  return launch_matvec_rows(v, y, n_space, n_time, 1, n_space, log_m, eig_scaled, tw_base, st);
+  return launch_matvec_rows(v, y, n_space, n_time, 1, n_space, log_m, eig_scaled, tw_base, st, koff);
 }
 
 static int ilog2(int n) {

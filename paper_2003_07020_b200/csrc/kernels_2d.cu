@@ -204,9 +204,10 @@ __global__ void __launch_bounds__(ColGeo<LOGM>::NT, (ColGeo<LOGM>::NT <= 256 ? 2
 
 cudaError_t launch_matvec_2d(const double* v, double* y, int n, int n_time, int log_m,
                              const double* eig_y_scaled, const double* eig_x_scaled,
-                             const double2* tw_base, cudaStream_t st) {
+                             const double2* tw_base, cudaStream_t st, int koff) {
   // y-direction on contiguous rows + BDF2 stencil (writes y), then x-direction columns (adds)
-  cudaError_t err = launch_matvec_rows(v, y, n, n_time * n, n, n * n, log_m, eig_y_scaled, tw_base, st);
+  cudaError_t err =
+      launch_matvec_rows(v, y, n, n_time * n, n, n * n, log_m, eig_y_scaled, tw_base, st, koff);
   if (err != cudaSuccess) return err;
 #define CALL(LM)                                                                          \
   {                                                                                       \

@@ -1,0 +1,304 @@
+"""Frequency-sharded multi-GPU solve: one process per GPU, torch.distributed
+(NCCL over NVLink on B200; gloo for the CPU tests) for the plumbing, the per-rank kernels through
+the shard-level C-ABI (`fpc_shard_*`).
+
+Layouts (G ranks, N = Nt*Ns, H = Nt/2 + 1):
+  * Krylov vectors: time-sharded, rank g owns time blocks [g*Nt/G, (g+1)*Nt/G) (contiguous).
+  * matvec (all_at_once.hpp:33-55): local, after an all-gather of every rank's last two blocks
+    (the BDF2 halo of the next rank).
+  * PC apply (alpha_circulant.hpp:137-199), the reference ordering:
+      all-to-all time -> space columns; time FFT (local columns); all-to-all space -> frequency rows;
+      tau solves (local rows, alpha_circulant.hpp:160 -- the independent PinT work);
+      all-to-all back to space; inverse time FFT; all-to-all back to time.
+  * Gram-Schmidt dots / norms: local partials + all_reduce (krylov.hpp:116-131).
+Every rank runs the same host-side Hessenberg/Givens recurrence on the reduced values.
+
+The local kernels are an object with the methods of `CudaShardKernels`; tests/dist_cpu_kernels.py
+provides a numpy implementation so the communication logic runs under gloo on CPU.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+from . import _native as N
+
+
+def split_counts(total: int, parts: int) -> list[int]:
+    return [total // parts + (1 if g < total % parts else 0) for g in range(parts)]
+
+
+def offsets(counts: list[int]) -> list[int]:
+    out, acc = [], 0
+    for c in counts:
+        out.append(acc)
+        acc += c
+    return out
+
+
+@dataclass
+class ShardReport:
+    converged: bool = False
+    iterations: int = 0
+    restarts: int = 0
+    residual_history: list = field(default_factory=list)
+    final_relative_residual: float = 0.0
+    true_relative_residual: float = 0.0
+    reorthogonalizations: int = 0
+
+
+class CudaShardKernels:
+    """Per-rank kernels on CUDA tensors through the shard-level C-ABI."""
+
+    def __init__(self, op, plan):
+        self.op, self.plan, self.lib = op, plan, op.lib
+        self.ctx = op.ctx
+        self.device = torch.device("cuda", op.ctx.device)
+
+    @staticmethod
+    def _p(t):
+        return C.c_void_p(t.data_ptr())
+
+    def empty(self, n, complex_=False):
+        return torch.empty(n, dtype=torch.complex128 if complex_ else torch.float64, device=self.device)
+
+    def matvec(self, buf, nt_local, koff, halo):
+        ns = self.op.n_space()
+        y = self.empty(nt_local * ns)
+        vptr = buf.data_ptr() + (2 * ns * 8 if halo else 0)
+        N.check(self.lib.fpc_shard_matvec(self.op.h, C.c_void_p(vptr), self._p(y), nt_local, koff))
+        return y
+
+    def time_fwd(self, cols, ns_local, s_in):
+        Z = self.empty((self.plan.n_time // 2 + 1) * ns_local, True)
+        N.check(self.lib.fpc_shard_time_fwd(self.plan.h, self._p(cols), self._p(Z), ns_local, float(s_in)))
+        return Z
+
+    def tau(self, Zrows, row0, nrows, forward=False):
+        N.check(self.lib.fpc_shard_tau(self.plan.h, self._p(Zrows), row0, nrows, int(forward)))
+
+    def time_inv(self, Z, ns_local):
+        z = self.empty(self.plan.n_time * ns_local)
+        N.check(self.lib.fpc_shard_time_inv(self.plan.h, self._p(Z), self._p(z), ns_local))
+        return z
+
+    def _ptrs(self, V):
+        arr = (C.c_void_p * max(len(V), 1))(*[v.data_ptr() for v in V])
+        return arr
+
+    def dots(self, V, scales, w, with_norm):
+        out = np.zeros(len(V) + 1)
+        sc = np.ascontiguousarray(scales, dtype=np.float64)
+        N.check(self.lib.fpc_shard_dots(self.ctx.h, self._ptrs(V), C.c_void_p(sc.ctypes.data), len(V),
+                                        self._p(w), w.numel(), int(with_norm), C.c_void_p(out.ctypes.data)))
+        return out[:len(V) + (1 if with_norm or not V else 0)]
+
+    def update(self, V, coef, w):
+        c = np.ascontiguousarray(coef, dtype=np.float64)
+        out = np.zeros(1)
+        N.check(self.lib.fpc_shard_update(self.ctx.h, self._ptrs(V), C.c_void_p(c.ctypes.data), len(V),
+                                          self._p(w), w.numel(), C.c_void_p(out.ctypes.data)))
+        return float(out[0])
+
+    def lincomb(self, V, coef):
+        u = self.empty(V[0].numel())
+        c = np.ascontiguousarray(coef, dtype=np.float64)
+        N.check(self.lib.fpc_shard_lincomb(self.ctx.h, self._ptrs(V), C.c_void_p(c.ctypes.data), len(V),
+                                           self._p(u), u.numel()))
+        return u
+
+    def synchronize(self):
+        self.ctx.synchronize()
+
+
+class ShardedSolver:
+    """Right-preconditioned GMRES (krylov.hpp:83-192, + GMRES(m) restarts) over G ranks."""
+
+    def __init__(self, n_time: int, n_space: int, kernels, group=None):
+        self.k = kernels
+        self.group = group
+        self.G = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        if n_time % self.G:
+            raise ValueError("ShardedSolver: n_time must be divisible by the number of ranks")
+        self.nt, self.ns = n_time, n_space
+        self.H = n_time // 2 + 1
+        self.nt_loc = n_time // self.G
+        self.cs = split_counts(n_space, self.G)
+        self.co = offsets(self.cs)
+        self.hs = split_counts(self.H, self.G)
+        self.ho = offsets(self.hs)
+        self.koff = self.rank * self.nt_loc
+
+    # ------------------------------------------------------------------ collectives
+    def _a2a(self, send_chunks, recv_sizes, like):
+        """all_to_all of flat float64 views; send_chunks[d] goes to rank d."""
+        if self.G == 1:
+            return [send_chunks[0]]
+        real = lambda t: torch.view_as_real(t).reshape(-1) if t.is_complex() else t.reshape(-1)
+        f = 2 if like.is_complex() else 1
+        inp = torch.cat([real(c.contiguous()) for c in send_chunks])
+        out = torch.empty(sum(recv_sizes) * f, dtype=torch.float64, device=inp.device)
+        dist.all_to_all_single(out, inp, output_split_sizes=[s * f for s in recv_sizes],
+                               input_split_sizes=[c.numel() * f for c in send_chunks], group=self.group)
+        parts, o = [], 0
+        for s in recv_sizes:
+            p = out[o:o + s * f]
+            parts.append(torch.view_as_complex(p.view(-1, 2)) if f == 2 else p)
+            o += s * f
+        return parts
+
+    def _allreduce(self, arr: np.ndarray) -> np.ndarray:
+        if self.G == 1:
+            return arr
+        dev = self.k.device if hasattr(self.k, "device") else torch.device("cpu")
+        t = torch.from_numpy(np.ascontiguousarray(arr)).to(dev)
+        dist.all_reduce(t, group=self.group)
+        return t.cpu().numpy()
+
+    # ------------------------------------------------------------------ operators
+    def matvec(self, v_loc):
+        ns, G, r = self.ns, self.G, self.rank
+        halo = None
+        if G > 1:
+            tail = v_loc[(self.nt_loc - 2) * ns:].contiguous() if self.nt_loc >= 2 else None
+            if tail is None:
+                raise ValueError("ShardedSolver: need at least two time blocks per rank")
+            gathered = [torch.empty_like(tail) for _ in range(G)]
+            dist.all_gather(gathered, tail, group=self.group)
+            if r > 0:
+                halo = gathered[r - 1]
+        if halo is not None:
+            buf = torch.cat([halo, v_loc])
+            return self.k.matvec(buf, self.nt_loc, self.koff, True)
+        return self.k.matvec(v_loc, self.nt_loc, self.koff, False)
+
+    def pc_apply(self, v_loc, s_in=1.0, forward=False):
+        G, r, ns, nt_loc = self.G, self.rank, self.ns, self.nt_loc
+        V = v_loc.view(nt_loc, ns)
+        # 1. time -> space columns
+        parts = self._a2a([V[:, self.co[d]:self.co[d] + self.cs[d]] for d in range(G)],
+                          [nt_loc * self.cs[r]] * G, v_loc)
+        cols = torch.cat([p.view(nt_loc, self.cs[r]) for p in parts]).reshape(-1)
+        # 2. time FFT on my columns -> half spectrum [H][cs]
+        Z = self.k.time_fwd(cols, self.cs[r], s_in).view(self.H, self.cs[r])
+        # 3. space -> frequency rows
+        parts = self._a2a([Z[self.ho[d]:self.ho[d] + self.hs[d]] for d in range(G)],
+                          [self.hs[r] * self.cs[s] for s in range(G)], Z)
+        rows = torch.cat([p.view(self.hs[r], self.cs[s]) for s, p in enumerate(parts)], dim=1).contiguous()
+        # 4. tau solves on my frequency rows
+        self.k.tau(rows.view(-1), self.ho[r], self.hs[r], forward)
+        # 5. frequency -> space
+        parts = self._a2a([rows[:, self.co[d]:self.co[d] + self.cs[d]] for d in range(G)],
+                          [self.hs[s] * self.cs[r] for s in range(G)], rows)
+        Z = torch.cat([p.view(self.hs[s], self.cs[r]) for s, p in enumerate(parts)]).contiguous()
+        # 6. inverse time FFT -> [Nt][cs]
+        z = self.k.time_inv(Z.view(-1), self.cs[r]).view(self.nt, self.cs[r])
+        # 7. space -> time
+        parts = self._a2a([z[d * nt_loc:(d + 1) * nt_loc] for d in range(G)],
+                          [nt_loc * self.cs[s] for s in range(G)], z)
+        return torch.cat([p.view(nt_loc, self.cs[s]) for s, p in enumerate(parts)], dim=1).reshape(-1).contiguous()
+
+    # ------------------------------------------------------------------ GMRES
+    def _norm(self, w):
+        return math.sqrt(float(self._allreduce(self.k.dots([], [], w, True))[0]))
+
+    def _inner(self, b, tol, max_iter, rep):
+        """One unrestarted gmres_right (x0 = 0) on rhs b; returns x, steps, converged."""
+        norm_b = self._norm(b)
+        if norm_b == 0.0:
+            return torch.zeros_like(b), 0, True
+        V, sc = [b], [1.0 / norm_b]
+        hcols, gc, gs, g = [], [], [], [norm_b]
+        steps, conv = 0, False
+        for j in range(max_iter):
+            z = self.pc_apply(V[j], sc[j])
+            w = self.matvec(z)
+            nv = j + 1
+            d = self._allreduce(self.k.dots(V, sc, w, True))
+            h = list(d[:nv]) + [0.0]
+            norm_before = math.sqrt(d[nv])
+            nw2 = self._allreduce(np.array([self.k.update(V, [h[i] * sc[i] for i in range(nv)], w)]))[0]
+            norm_w = math.sqrt(nw2)
+            if norm_w < 0.70710678118654752 * norm_before:  # krylov.hpp:123-130
+                rep.reorthogonalizations += 1
+                c2 = self._allreduce(self.k.dots(V, sc, w, False))
+                nw2 = self._allreduce(np.array([self.k.update(V, [c2[i] * sc[i] for i in range(nv)], w)]))[0]
+                for i in range(nv):
+                    h[i] += c2[i]
+                norm_w = math.sqrt(nw2)
+            h[j + 1] = norm_w
+            for i in range(j):  # krylov.hpp:133-151
+                hi, hi1 = h[i], h[i + 1]
+                h[i] = gc[i] * hi + gs[i] * hi1
+                h[i + 1] = -gs[i] * hi + gc[i] * hi1
+            rad = math.hypot(h[j], h[j + 1])
+            cs_ = h[j] / rad if rad > 0 else 1.0
+            sn_ = h[j + 1] / rad if rad > 0 else 0.0
+            gc.append(cs_)
+            gs.append(sn_)
+            h[j], h[j + 1] = rad, 0.0
+            g.append(-sn_ * g[j])
+            g[j] *= cs_
+            hcols.append(h)
+            steps = j + 1
+            rel = abs(g[j + 1]) / norm_b
+            rep.residual_history.append(rel)
+            if rel <= tol:
+                conv = True
+                break
+            if norm_w <= 1e-14 * max(1.0, norm_before):
+                break
+            V.append(w)
+            sc.append(1.0 / norm_w)
+        y = [0.0] * steps
+        for i in range(steps - 1, -1, -1):
+            s = g[i]
+            for kk in range(i + 1, steps):
+                s -= hcols[kk][i] * y[kk]
+            y[i] = s / hcols[i][i]
+        u = self.k.lincomb(V[:steps], [y[i] * sc[i] for i in range(steps)]) if steps else torch.zeros_like(b)
+        return self.pc_apply(u), steps, conv
+
+    def gmres(self, b_loc, tol=1e-9, max_iter=200, restart=0):
+        rep = ShardReport()
+        norm_b = self._norm(b_loc)
+        if restart <= 0 or restart >= max_iter:
+            x, steps, conv = self._inner(b_loc, tol, max_iter, rep)
+            rep.iterations, rep.converged = steps, conv
+        else:  # restart emulation, SURVEY §8(c) (same as oracle/fracpint_oracle.c)
+            x = torch.zeros_like(b_loc)
+            r = b_loc.clone()
+            budget, total, conv = max_iter, 0, False
+            while budget > 0:
+                norm_r = self._norm(r)
+                if norm_r == 0.0:
+                    conv = True
+                    break
+                h0 = len(rep.residual_history)
+                d, steps, c = self._inner(r, tol * norm_b / norm_r, min(restart, budget), rep)
+                for i in range(h0, len(rep.residual_history)):
+                    rep.residual_history[i] *= norm_r / norm_b
+                x = x + d
+                total += steps
+                budget -= steps
+                if c:
+                    conv = True
+                    break
+                if steps == 0:
+                    break
+                rep.restarts += 1
+                r = b_loc - self.matvec(x)
+            rep.iterations, rep.converged = total, conv
+        rep.final_relative_residual = rep.residual_history[-1] if rep.residual_history else 1.0
+        if norm_b == 0.0:
+            rep.true_relative_residual = 0.0
+        else:
+            res = b_loc - self.matvec(x)
+            rep.true_relative_residual = self._norm(res) / norm_b
+        return x, rep
