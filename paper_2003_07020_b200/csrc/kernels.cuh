@@ -25,6 +25,12 @@ cudaError_t launch_time_fwd(const double* v, double2* Z, int n_space, int n_time
 // K4: z[k][p] = Re( scale_bwd[k]/Nt * sum_n Z_n e^{-2 pi i kn/Nt} ), Z_{Nt-n} = conj(Z_n).
 cudaError_t launch_time_inv(const double2* Z, double* z, int n_space, int n_time,
                             const double* scale_bwd, const double2* tw_base, cudaStream_t st);
+// persistent double-buffered variants (kernels_time.cu), n_time <= 8192
+cudaError_t launch_time_fwd_pipe(const double* v, double2* Z, int n_space, int n_time,
+                                 const double* scale_fwd, double s_in, const double2* tw_base,
+                                 cudaStream_t st);
+cudaError_t launch_time_inv_pipe(const double2* Z, double* z, int n_space, int n_time,
+                                 const double* scale_bwd, const double2* tw_base, cudaStream_t st);
 // K3 (1D): for each retained n: Z_n <- DST( DST(Z_n) ./ (lambda_n - dt*sigma) )
 // (forward = true: .* instead of ./, the apply_forward action tau.hpp:132-136).
 cudaError_t launch_tau_solve_1d(double2* Z, int n_space, int n_rows, const double2* lambda,

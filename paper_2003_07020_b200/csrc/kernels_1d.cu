@@ -11,6 +11,8 @@
 // latency of HBM is overlapped; buffers of multi-buffer CTAs are skewed by one bank group.
 #include <cooperative_groups.h>
 
+#include <cstdlib>
+
 #include "dst_block.cuh"
 #include "fft_block.cuh"
 #include "kernels.cuh"
@@ -38,7 +40,7 @@ struct Geo {
 
 // CTAs per SM the register budget is sized for: radix-16 passes need ~128 registers per thread,
 // so 256-thread CTAs run two per SM (16 warps) and 512-thread CTAs one.
-__host__ __device__ constexpr int minb(int nt) { return nt <= 256 ? 2 : 1; }
+__host__ __device__ constexpr int minb(int nt) { return nt <= 128 ? 4 : nt <= 256 ? 2 : 1; }
 
 __device__ __forceinline__ double& comp(double2* s, int slot_padded, int c) {
   return reinterpret_cast<double*>(s + slot_padded)[c];
@@ -513,9 +515,22 @@ static int ilog2(int n) {
   return l;
 }
 
+// The persistent cp.async double-buffered variants (kernels_time.cu) are opt-in (FPC_TIME_PIPE=1):
+// at 190+ registers they run one 8-warp CTA per SM and measured slower (186 vs 157 us at
+// config 1) than the plain kernels at two CTAs per SM.
+static bool time_pipe_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("FPC_TIME_PIPE");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+
 cudaError_t launch_time_fwd(const double* v, double2* Z, int n_space, int n_time,
                             const double* scale_fwd, double s_in, const double2* tw_base,
                             cudaStream_t st) {
+  if (n_time <= 8192 && time_pipe_enabled())  // kernels_time.cu (double-buffered, persistent)
+    return launch_time_fwd_pipe(v, Z, n_space, n_time, scale_fwd, s_in, tw_base, st);
   cudaError_t err = cudaSuccess;
   const int lm = ilog2(n_time) - 1;
 #define CALL(LM)                                                                          \
@@ -532,6 +547,8 @@ cudaError_t launch_time_fwd(const double* v, double2* Z, int n_space, int n_time
 
 cudaError_t launch_time_inv(const double2* Z, double* z, int n_space, int n_time,
                             const double* scale_bwd, const double2* tw_base, cudaStream_t st) {
+  if (n_time <= 8192 && time_pipe_enabled())
+    return launch_time_inv_pipe(Z, z, n_space, n_time, scale_bwd, tw_base, st);
   cudaError_t err = cudaSuccess;
   const int lm = ilog2(n_time) - 1;
 #define CALL(LM)                                                                            \
