@@ -311,6 +311,8 @@ struct fpc_plan_s {
   double2* d_lambda = nullptr;
   double* d_sigma = nullptr;
   double2* d_Z = nullptr;  // half spectrum scratch (H x ns complex)
+  double2* d_Zf = nullptr; // full spectrum (Nt x ns complex), InnerSweep::full only
+  int sweep_mode = FPC_SWEEP_HALF;
   // GMRES workspace (grown on demand, reused across solves)
   std::vector<double*> basis;
   double* d_z = nullptr;
@@ -695,13 +697,12 @@ int fpc_plan_create(fpc_problem_t p, double alpha_in, fpc_plan_t* out) {
     DeviceGuard g(p->ctx->device);
     pl->d_sf = dalloc<double>(size_t(nt));
     pl->d_sb = dalloc<double>(size_t(nt));
-    pl->d_lambda = dalloc<double2>(size_t(pl->solve_count));
+    pl->d_lambda = dalloc<double2>(size_t(nt));  // all Nt: the full sweep solves every frequency
     pl->d_sigma = dalloc<double>(p->sigma.size());
     pl->d_Z = dalloc<double2>(size_t(pl->solve_count) * size_t(p->ns));
     ck(cudaMemcpy(pl->d_sf, sf.data(), sf.size() * 8, cudaMemcpyHostToDevice), "sf");
     ck(cudaMemcpy(pl->d_sb, sb.data(), sb.size() * 8, cudaMemcpyHostToDevice), "sb");
-    ck(cudaMemcpy(pl->d_lambda, pl->lambda.data(), size_t(pl->solve_count) * 16, cudaMemcpyHostToDevice),
-       "lambda");
+    ck(cudaMemcpy(pl->d_lambda, pl->lambda.data(), size_t(nt) * 16, cudaMemcpyHostToDevice), "lambda");
     ck(cudaMemcpy(pl->d_sigma, p->sigma.data(), p->sigma.size() * 8, cudaMemcpyHostToDevice), "sigma");
     ++p->refs;
     *out = pl;
@@ -717,7 +718,7 @@ int fpc_plan_destroy(fpc_plan_t pl) {
     for (double* b : pl->basis) cudaFree(b);
     for (void* q : {(void*)pl->d_sf, (void*)pl->d_sb, (void*)pl->d_lambda, (void*)pl->d_sigma,
                     (void*)pl->d_Z, (void*)pl->d_z, (void*)pl->d_u, (void*)pl->d_r, (void*)pl->d_x,
-                    (void*)pl->d_d, (void*)pl->d_b})
+                    (void*)pl->d_d, (void*)pl->d_b, (void*)pl->d_Zf})
       cudaFree(q);
   }
   delete pl;
@@ -743,8 +744,14 @@ int fpc_plan_lambda(fpc_plan_t pl, double* out) {
 // z = P^{-1} (s_in * v)  (alpha_circulant.hpp:137-199, half sweep)
 // forward = true: z = P (s_in v) from the same factors (apply_forward, alpha_circulant.hpp:212-215;
 // the reference runs it as a full sweep, which for real v equals the Hermitian half sweep).
+static void pc_apply_full_dev(fpc_plan_s* pl, const double* v, double* z, double s_in, bool forward);
+
 static void pc_apply_dev(fpc_plan_s* pl, const double* v, double* z, double s_in,
                          bool forward = false) {
+  if (pl->sweep_mode == FPC_SWEEP_FULL) {
+    pc_apply_full_dev(pl, v, z, s_in, forward);
+    return;
+  }
   fpc_problem_s* p = pl->prob;
   cudaStream_t st = p->ctx->stream;
   LAUNCH("time_fwd", st, fpc::launch_time_fwd(v, pl->d_Z, p->ns, p->nt, pl->d_sf, s_in, p->ctx->tw, st));
@@ -759,13 +766,38 @@ static void pc_apply_dev(fpc_plan_s* pl, const double* v, double* z, double s_in
   LAUNCH("time_inv", st, fpc::launch_time_inv(pl->d_Z, z, p->ns, p->nt, pl->d_sb, p->ctx->tw, st));
 }
 
+// InnerSweep::full (alpha_circulant.hpp:158-159): all Nt frequency rows solved, complex inverse
+// time FFT, and the imaginary-residue guard of alpha_circulant.hpp:196-198 (synchronous).
+static void pc_apply_full_dev(fpc_plan_s* pl, const double* v, double* z, double s_in, bool forward) {
+  fpc_problem_s* p = pl->prob;
+  fpc_context_s* c = p->ctx;
+  cudaStream_t st = c->stream;
+  if (p->nt > 8192) throw Unsupported{"InnerSweep::full supports n_time <= 8192"};
+  if (!pl->d_Zf) pl->d_Zf = dalloc<double2>(size_t(p->nt) * size_t(p->ns));
+  LAUNCH("time_fwd", st, fpc::launch_time_fwd(v, pl->d_Zf, p->ns, p->nt, pl->d_sf, s_in, c->tw, st));
+  LAUNCH("mirror_fill", st, fpc::launch_mirror_fill(pl->d_Zf, p->ns, p->nt, st));
+  if (!p->two_dim)
+    LAUNCH("tau_solve_1d", st,
+           fpc::launch_tau_solve_1d(pl->d_Zf, p->ns, p->nt, pl->d_lambda, pl->d_sigma, p->dt, c->tw, st, forward));
+  else
+    LAUNCH("tau_solve_2d", st,
+           fpc::launch_tau_solve_2d(pl->d_Zf, p->n, p->nt, pl->d_lambda, pl->d_sigma, p->dt, c->tw, st, forward));
+  LAUNCH("time_inv_full", st, fpc::launch_time_inv_full(pl->d_Zf, z, p->ns, p->nt, pl->d_sb, c->tw, c->partial, st));
+  LAUNCH("reduce", st, fpc::launch_reduce(c->partial, 2, 2, c->dscal + 960, false, st));
+  ck(cudaMemcpyAsync(c->hpin + 960, c->dscal + 960, 2 * sizeof(double), cudaMemcpyDeviceToHost, st), "D2H");
+  ck(cudaStreamSynchronize(st), "sync");
+  const double im2 = c->hpin[960], tot2 = c->hpin[961];
+  if (tot2 > 0.0 && std::sqrt(im2) > 1e-10 * std::sqrt(tot2))
+    throw RuntimeErr{"alpha-circulant action: imaginary residue exceeds 1e-10 of the output norm"};
+}
+
 int fpc_pc_apply(fpc_plan_t pl, const double* v, double* out, int sweep, int where) {
   if (!pl) return set_err(FPC_INVALID_ARGUMENT, "null plan");
   return guarded([&] {
     check_ptr(v, "fpc_pc_apply");
     check_ptr(out, "fpc_pc_apply");
-    if (sweep != FPC_SWEEP_HALF)
-      throw Unsupported{"InnerSweep::full is not available on the B200 path (use half)"};
+    if (sweep != FPC_SWEEP_HALF && sweep != FPC_SWEEP_FULL) throw InvalidArg{"fpc_pc_apply: bad sweep"};
+    pl->sweep_mode = sweep;
     fpc_problem_s* p = pl->prob;
     DeviceGuard g(p->ctx->device);
     const size_t n = p->dim();
@@ -789,6 +821,8 @@ int fpc_pc_forward(fpc_plan_t pl, const double* v, double* out, int where) {
   return guarded([&] {
     check_ptr(v, "fpc_pc_forward");
     check_ptr(out, "fpc_pc_forward");
+    // apply_forward is the full sweep in the reference (alpha_circulant.hpp:212-215)
+    pl->sweep_mode = pl->prob->nt <= 8192 ? FPC_SWEEP_FULL : FPC_SWEEP_HALF;
     fpc_problem_s* p = pl->prob;
     DeviceGuard g(p->ctx->device);
     const size_t n = p->dim();
@@ -1092,8 +1126,8 @@ int fpc_gmres(fpc_plan_t pl, const double* b, double* x, const fpc_solver_config
     check_ptr(x, "fpc_gmres");
     fpc_solver_config cfg{1e-9, 200, 0, FPC_SWEEP_HALF};
     if (cfg_in) cfg = *cfg_in;
-    if (cfg.sweep != FPC_SWEEP_HALF)
-      throw Unsupported{"InnerSweep::full is not available on the B200 path (use half)"};
+    if (cfg.sweep != FPC_SWEEP_HALF && cfg.sweep != FPC_SWEEP_FULL) throw InvalidArg{"fpc_gmres: bad sweep"};
+    pl->sweep_mode = cfg.sweep;
     if (cfg.max_iter < 0) throw InvalidArg{"gmres_right: max_iter must be non-negative"};
     if (cfg.max_iter > 250) throw Unsupported{"B200 GMRES keeps at most 250 basis vectors"};
     fpc_problem_s* p = pl->prob;

@@ -31,6 +31,13 @@ cudaError_t launch_time_fwd_pipe(const double* v, double2* Z, int n_space, int n
                                  cudaStream_t st);
 cudaError_t launch_time_inv_pipe(const double2* Z, double* z, int n_space, int n_time,
                                  const double* scale_bwd, const double2* tw_base, cudaStream_t st);
+// InnerSweep::full (kernels_full.cu): mirror-fill rows Nt/2+1..Nt-1 of a full [Nt][ns] spectrum,
+// and the complex inverse time FFT with the imaginary-residue partials (partial[blk*2 + {0,1}] =
+// {sum Im^2, sum |.|^2}, dots_grid() CTAs).
+cudaError_t launch_mirror_fill(double2* Z, int n_space, int n_time, cudaStream_t st);
+cudaError_t launch_time_inv_full(const double2* Z, double* z, int n_space, int n_time,
+                                 const double* scale_bwd, const double2* tw_base, double* partial,
+                                 cudaStream_t st);
 // K3 (1D): for each retained n: Z_n <- DST( DST(Z_n) ./ (lambda_n - dt*sigma) )
 // (forward = true: .* instead of ./, the apply_forward action tau.hpp:132-136).
 cudaError_t launch_tau_solve_1d(double2* Z, int n_space, int n_rows, const double2* lambda,

@@ -128,3 +128,20 @@ def test_pc_forward_1d(oracle, gamma, ns, nt):
     pv = fp.apply_forward(plan, v)
     assert rel(pv, po.pc_forward(v)) <= 1e-12
     assert rel(fp.apply_inverse(plan, pv), v) <= 1e-10
+
+
+@pytest.mark.parametrize("gamma,ns,nt", [(1.5, 15, 8), (1.7, 63, 16), (1.5, 1023, 64)])
+def test_full_sweep_1d(oracle, gamma, ns, nt):
+    # InnerSweep::full (alpha_circulant.hpp:158-159) vs the oracle's full sweep, and the reference's
+    # half == full property (test_pint.cpp:203-216)
+    op, h, dt = make(gamma, ns, nt)
+    plan = fp.build_plan(fp.PreconditionerKind.generalized(), nt, dt, op)
+    po = oracle.problem_1d(gamma, 1.0, h, ns, nt, dt).build_plan()
+    v = np.random.default_rng(ns).uniform(-1, 1, ns * nt)
+    full = fp.apply_inverse(plan, v, sweep=fp.InnerSweep.full)
+    assert rel(full, po.pc_apply(v, True)) <= 1e-12
+    assert rel(fp.apply_inverse(plan, v), full) <= 1e-12
+    b = np.random.default_rng(1).uniform(-1, 1, ns * nt)
+    r = fp.gmres_right(op, plan, b, fp.SolverConfig(tol=1e-10, sweep=fp.InnerSweep.full))
+    xo, ro = po.gmres(b, 1e-10, 200, full_sweep=True)
+    assert abs(r.report.iterations - ro.iterations) <= 1 and rel(r.x, xo) <= 1e-10

@@ -76,3 +76,12 @@ def test_pc_forward_2d(oracle):
     pv = fp.apply_forward(plan, v)
     assert rel(pv, po.pc_forward(v)) <= 1e-12
     assert rel(fp.apply_inverse(plan, pv), v) <= 1e-10
+
+
+def test_full_sweep_2d(oracle):
+    n, nt, dt = 15, 8, 0.125
+    op = fp.AllAtOnceOperator(fp.TimeStencil(nt), fp.RieszJacobian2D(1.3, 1.7, 1.0, 1.0, 1 / 16, n), dt)
+    plan = fp.build_plan(fp.PreconditionerKind.generalized(), nt, dt, op)
+    po = oracle.problem_2d(1.3, 1.7, 1.0, 1.0, 1 / 16, n, nt, dt).build_plan()
+    v = np.random.default_rng(4).uniform(-1, 1, n * n * nt)
+    assert rel(fp.apply_inverse(plan, v, sweep=fp.InnerSweep.full), po.pc_apply(v, True)) <= 1e-12
