@@ -1017,7 +1017,8 @@ static void gmres_inner(fpc_plan_s* pl, const double* b, double* x, double tol, 
     for (int k = i + 1; k < steps; ++k) s -= hcols[size_t(k)][size_t(i)] * y[size_t(k)];
     y[size_t(i)] = s / hcols[size_t(i)][size_t(i)];
   }
-  if (!pl->d_u) pl->d_u = dalloc<double>(n + 2);
+  // u = V y lives in the z buffer (z is dead after the loop): one 8N buffer less at config 3
+  double* u = pl->d_z;
   std::vector<const double*> vp(V.begin(), V.begin() + steps);
   ck(cudaMemcpyAsync(c->dvptr, vp.data(), vp.size() * sizeof(double*), cudaMemcpyHostToDevice, S.st), "vptr");
   ck(cudaMemcpyAsync(c->dscales, S.scales.data(), size_t(steps) * sizeof(double), cudaMemcpyHostToDevice, S.st),
@@ -1025,8 +1026,8 @@ static void gmres_inner(fpc_plan_s* pl, const double* b, double* x, double tol, 
   std::memcpy(c->hpin + 600, y.data(), y.size() * sizeof(double));
   ck(cudaMemcpyAsync(c->dscal + 600, c->hpin + 600, y.size() * sizeof(double), cudaMemcpyHostToDevice, S.st),
      "y");
-  LAUNCH("lincomb", S.st, fpc::launch_lincomb(c->dvptr, c->dscales, c->dscal + 600, steps, pl->d_u, n, S.st));
-  pc_apply_dev(pl, pl->d_u, x, 1.0);
+  LAUNCH("lincomb", S.st, fpc::launch_lincomb(c->dvptr, c->dscales, c->dscal + 600, steps, u, n, S.st));
+  pc_apply_dev(pl, u, x, 1.0);
   *steps_out = steps;
   ck(cudaStreamSynchronize(S.st), "sync");  // hpin reuse boundary
 }
@@ -1035,9 +1036,10 @@ static double resid_norm_dev(fpc_plan_s* pl, const double* b, const double* x) {
   fpc_problem_s* p = pl->prob;
   fpc_context_s* c = p->ctx;
   const size_t n = p->dim();
-  if (!pl->d_r) pl->d_r = dalloc<double>(n + 2);
-  matvec_dev(p, x, pl->d_r);
-  LAUNCH("resid", c->stream, fpc::launch_resid_norm(b, pl->d_r, n, c->partial, c->stream));
+  if (!pl->d_z) pl->d_z = dalloc<double>(n + 2);
+  double* r = pl->d_z;  // scratch; z is not live here
+  matvec_dev(p, x, r);
+  LAUNCH("resid", c->stream, fpc::launch_resid_norm(b, r, n, c->partial, c->stream));
   LAUNCH("reduce", c->stream, fpc::launch_reduce(c->partial, 1, 1, c->dscal + 900, false, c->stream));
   ck(cudaMemcpyAsync(c->hpin + 900, c->dscal + 900, sizeof(double), cudaMemcpyDeviceToHost, c->stream), "D2H");
   ck(cudaStreamSynchronize(c->stream), "sync");
@@ -1058,7 +1060,6 @@ static void gmres_dev(fpc_plan_s* pl, const double* b, double* x, const fpc_solv
     rep->iterations = steps;
   } else {
     // GMRES(m): restart emulation of SURVEY §8(c) (same as oracle/fracpint_oracle.c orc_gmres)
-    if (!pl->d_x) pl->d_x = dalloc<double>(n + 2);
     if (!pl->d_d) pl->d_d = dalloc<double>(n + 2);
     if (!pl->d_b) pl->d_b = dalloc<double>(n + 2);
     double* r = pl->d_b;  // current residual (rhs of the inner solve)
