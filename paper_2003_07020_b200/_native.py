@@ -9,7 +9,8 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libfracpint_b200.so")
+# FPC_LIB overrides the library path (development builds, e.g. the phase-timing build)
+LIB_PATH = os.environ.get("FPC_LIB") or os.path.join(HERE, "libfracpint_b200.so")
 
 FPC_OK, FPC_INVALID_ARGUMENT, FPC_RUNTIME_ERROR, FPC_CUDA_ERROR, FPC_UNSUPPORTED = 0, 1, 2, 3, 4
 FPC_HOST, FPC_DEVICE = 0, 1

@@ -139,25 +139,30 @@ __device__ __forceinline__ void apply_twiddles(double2* v, const double2* __rest
     v[2] = cmul(v[2], w2);
     v[3] = cmul(v[3], w3);
   } else {
+    // powers built and applied on the fly (few live twiddles -> fewer registers):
+    // w^{4a+b} = (w^4)^a w^b, at most three products deep
     const double2 w4 = twid<S>(tw, 4 * t1);
     const double2 w2 = cmul(w1, w1);
     const double2 w3 = cmul(w2, w1);
-    double2 w[R];
-    w[1] = w1;
-    w[2] = w2;
-    w[3] = w3;
-    w[4] = w4;
-    w[5] = cmul(w4, w1);
-    w[6] = cmul(w4, w2);
-    w[7] = cmul(w4, w3);
+    v[1] = cmul(v[1], w1);
+    v[2] = cmul(v[2], w2);
+    v[3] = cmul(v[3], w3);
+    v[4] = cmul(v[4], w4);
+    v[5] = cmul(v[5], cmul(w4, w1));
+    v[6] = cmul(v[6], cmul(w4, w2));
+    v[7] = cmul(v[7], cmul(w4, w3));
     if constexpr (R == 16) {
       const double2 w8 = cmul(w4, w4);
-      w[8] = w8;
-#pragma unroll
-      for (int r = 1; r < 8; ++r) w[8 + r] = cmul(w8, w[r]);
+      const double2 w12 = cmul(w8, w4);
+      v[8] = cmul(v[8], w8);
+      v[9] = cmul(v[9], cmul(w8, w1));
+      v[10] = cmul(v[10], cmul(w8, w2));
+      v[11] = cmul(v[11], cmul(w8, w3));
+      v[12] = cmul(v[12], w12);
+      v[13] = cmul(v[13], cmul(w12, w1));
+      v[14] = cmul(v[14], cmul(w12, w2));
+      v[15] = cmul(v[15], cmul(w12, w3));
     }
-#pragma unroll
-    for (int r = 1; r < R; ++r) v[r] = cmul(v[r], w[r]);
   }
 }
 

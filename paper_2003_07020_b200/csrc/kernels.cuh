@@ -17,6 +17,10 @@ cudaError_t launch_matvec_1d(const double* v, double* y, int n_space, int n_time
                              const double* eig_scaled, const double2* tw_base, cudaStream_t st,
                              int koff = 0);
 
+// M = 8192 (Ns up to 8191) on a 2-CTA cluster (kernels_mv.cu)
+cudaError_t launch_matvec_split13(const double* v, double* y, int n_space, int n_time, int koff,
+                                  const double* eig_scaled, const double2* tw_base, cudaStream_t st);
+
 // ---- preconditioner apply, reference ordering (alpha_circulant.hpp:137-199) ---------------
 // K2: Z[n][p] = sum_k s_in*scale_fwd[k]*v[k][p] e^{+2 pi i kn/Nt}, n = 0..Nt/2 (half spectrum).
 cudaError_t launch_time_fwd(const double* v, double2* Z, int n_space, int n_time,

@@ -21,6 +21,20 @@ namespace cg = cooperative_groups;
 
 namespace fpc {
 
+#ifdef FPC_PHASE_TIMING
+// development instrumentation: per-CTA clock64 stamps at phase boundaries (one thread per CTA)
+__device__ long long g_phase[1 << 16][8];
+#define FPC_PH(i) \
+  do { if (threadIdx.x == 0 && blockIdx.x < (1 << 16)) g_phase[blockIdx.x][i] = clock64(); } while (0)
+extern "C" int fpc_debug_phases(long long* out, int nblocks) {
+  return int(cudaMemcpyFromSymbol(out, g_phase, size_t(nblocks) * 8 * sizeof(long long)));
+}
+#else
+#define FPC_PH(i) \
+  do {            \
+  } while (0)
+#endif
+
 // buffer stride with stride % 8 == 1 (in 16-byte units): consecutive buffers start in
 // consecutive bank groups, so "same slot, next buffer" accesses are conflict free
 __host__ __device__ constexpr int skewed(int m) {
@@ -152,114 +166,6 @@ __global__ void __launch_bounds__(Geo<LOGM, kTotMv, 16>::NT, minb(Geo<LOGM, kTot
       yb[idx] = cst[b * M + idx] + tv;
     }
   }
-}
-
-// =====================================================================================
-// K1 (large M): the same matvec on a 2-CTA cluster, one half-length (H = M/2) FFT per CTA.
-// The packed input z has z_m = 0 for m >= H (Ns < M), so the first decimation-in-frequency
-// stage of the M-point forward FFT is free: rank 0 transforms z (even bins), rank 1 transforms
-// z_m e^{-2 pi i m/M} (odd bins).  Spectral pairs (k, M-k) share parity, so the eigenvalue
-// product is CTA-local.  The inverse is split the same way (E = even bins, O = odd bins,
-// y_m = E_m + e^{+2 pi i m/M} O_m) and only y_m, m < H, is needed; each rank assembles half of
-// those outputs reading the partner's half through distributed shared memory.  Two CTAs of
-// ~100 KB per SM instead of one of ~200 KB (the radix-16 register budget allows two).
-// =====================================================================================
-template <int LOGM>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((1 << (LOGM - 1)) / 16, 2)
-    k_matvec_1d_split(const double* __restrict__ v, double* __restrict__ y, int ns, int koff,
-                      const double* __restrict__ eig, const double2* __restrict__ twb) {
-  constexpr int M = 1 << LOGM, H = M / 2, L = 2 * M, NT = H / 16, BS = padded(H);
-  constexpr int U = 4;
-  extern __shared__ double2 smem[];
-  double* cst = reinterpret_cast<double*>(smem + BS);  // stencil part for my H outputs
-  cg::cluster_group cluster = cg::this_cluster();
-  const int q = int(cluster.block_rank());
-  const size_t k = blockIdx.x >> 1;
-  const long kg = long(k) + koff;  // global time level (time-sharded callers pass a halo + offset)
-  const double* vk = v + k * ns;
-  const double2* twM = twb + M;
-
-  // load: packed input (rank 1 pre-twiddled) and the BDF2 stencil part of my outputs
-  for (int m0 = threadIdx.x; m0 < H; m0 += U * NT) {
-    double xe[U], xo[U], s0[U], s1[U], s2[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int m = m0 + u * NT;
-      const int i0 = 2 * m, i1 = 2 * m + 1;
-      xe[u] = i0 < ns ? vk[i0] : 0.0;
-      xo[u] = i1 < ns ? vk[i1] : 0.0;
-      const int j = q * H + m;  // my output index
-      const bool ok = j < ns;
-      s0[u] = ok ? vk[j] : 0.0;
-      s1[u] = (ok && kg >= 1) ? vk[long(j) - ns] : 0.0;
-      s2[u] = (ok && kg >= 2) ? vk[long(j) - 2 * long(ns)] : 0.0;
-    }
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int m = m0 + u * NT;
-      double2 z = make_double2(xe[u], xo[u]);
-      if (q == 1) z = cmul(z, __ldg(twM + m));
-      smem[pad16(m)] = z;
-      double c;
-      if (kg == 0)
-        c = s0[u];
-      else if (kg == 1)
-        c = 1.5 * s0[u] + -2.0 * s1[u];
-      else
-        c = 1.5 * s0[u] + -2.0 * s1[u] + 0.5 * s2[u];
-      cst[m] = c;
-    }
-  }
-  __syncthreads();
-  block_fft<LOGM - 1, -1, BS, 16>(smem, twb + H, 1);
-
-  // eigenvalue product on (kappa, M - kappa) pairs; slot j of rank q holds bin 2j + q
-  const double2* twL = twb + L;
-  auto pair = [&](int s1, int s2, int kap) {
-    const double2 w = __ldg(twL + kap);  // e^{-2 pi i kappa/L}
-    const double ek = __ldg(eig + kap), em = __ldg(eig + M - kap);
-    const double2 a = smem[pad16(s1)], bq = smem[pad16(s2)];
-    const double2 P = cadd(a, cconj(bq)), Q = csub(a, cconj(bq));
-    const double2 iwQ = mul_si<1>(cmul(w, Q));
-    const double2 Yk = cscale(csub(P, iwQ), ek);
-    const double2 Ym = cscale(cconj(cadd(P, iwQ)), em);
-    const double2 A = cadd(Yk, cconj(Ym));
-    const double2 D = csub(Yk, cconj(Ym));
-    smem[pad16(s1)] = cadd(A, mul_si<1>(cmul(D, cconj(w))));
-    if (s1 != s2) smem[pad16(s2)] = cadd(cconj(A), mul_si<1>(cmul(cconj(D), w)));
-  };
-  if (q == 0) {
-    for (int j = threadIdx.x; j <= H / 2; j += NT) {
-      if (j == 0) {
-        const double2 z = smem[0];
-        const double y0 = eig[0] * (2.0 * (z.x + z.y));
-        const double ym = eig[M] * (2.0 * (z.x - z.y));
-        smem[0] = make_double2(y0 + ym, y0 - ym);
-      } else {
-        pair(j, H - j, 2 * j);
-      }
-    }
-  } else {
-    for (int j = threadIdx.x; j < H / 2; j += NT) pair(j, H - 1 - j, 2 * j + 1);
-  }
-  __syncthreads();
-  block_fft<LOGM - 1, 1, BS, 16>(smem, twb + H, 1);
-  if (q == 1) {
-    for (int m = threadIdx.x; m < H; m += NT) smem[pad16(m)] = cmul(smem[pad16(m)], cconj(__ldg(twM + m)));
-  }
-  cluster.sync();
-  // y_m = E_m + O'_m for my half of m; outputs 2m, 2m+1
-  const double2* Eb = cluster.map_shared_rank(smem, 0);
-  const double2* Ob = cluster.map_shared_rank(smem, 1);
-  double* yk = y + k * ns;
-  for (int mm = threadIdx.x; mm < H / 2; mm += NT) {
-    const int m = q * (H / 2) + mm;
-    const double2 e = Eb[pad16(m)], o = Ob[pad16(m)];
-    const int j0 = 2 * m, jl = 2 * mm;  // output index, local stencil slot
-    if (j0 < ns) yk[j0] = cst[jl] + (e.x + o.x);
-    if (j0 + 1 < ns) yk[j0 + 1] = cst[jl + 1] + (e.y + o.y);
-  }
-  cluster.sync();  // keep both buffers alive until the partner has read them
 }
 
 // =====================================================================================
@@ -500,12 +406,9 @@ cudaError_t launch_matvec_1d(const double* v, double* y, int n_space, int n_time
                              const double* eig_scaled, const double2* tw_base, cudaStream_t st,
                              int koff) {
   cudaError_t err = cudaSuccess;
-  if (log_m == 13) {
-    constexpr size_t smem = size_t(padded(4096)) * sizeof(double2) + 4096 * sizeof(double);
-    if ((err = prep(k_matvec_1d_split<13>, smem)) != cudaSuccess) return err;
-    k_matvec_1d_split<13><<<2 * n_time, 256, smem, st>>>(v, y, n_space, koff, eig_scaled, tw_base);
-    return cudaGetLastError();
-  }
+  if (log_m == 13)  // kernels_mv.cu: 2-CTA cluster, half-length FFTs
+    return launch_matvec_split13(v, y, n_space, n_time, koff, eig_scaled, tw_base, st);
+  (void)err;
   return launch_matvec_rows(v, y, n_space, n_time, 1, n_space, log_m, eig_scaled, tw_base, st, koff);
 }
 

@@ -1,0 +1,159 @@
+// kernels_mv.cu -- K1 for the large 1D case (M = 8192 packed points, Ns up to 8191): the
+// all-at-once matvec (all_at_once.hpp:33-55 + toeplitz.hpp:41-57) on a 2-CTA cluster.
+//
+// The packed input z (real length-L embedding, L = 2M) has z_m = 0 for m >= H = M/2, so the first
+// decimation-in-frequency stage of the M-point forward FFT is free: rank 0 transforms z (even
+// bins), rank 1 transforms z_m e^{-2 pi i m/M} (odd bins), one H-point FFT each.  Spectral pairs
+// (k, M-k) share parity, so the eigenvalue product stays CTA-local.  The inverse is split the same
+// way (E = even bins, O = odd bins, y_m = E_m + e^{+2 pi i m/M} O_m); only y_m for m < H is needed
+// and each rank assembles half of those, reading the partner's buffer through DSMEM.
+//
+// Memory phases are asynchronous or batched so their latency is paid once per CTA (measured with
+// clock64 phase stamps: the first version spent ~60% of its cycles waiting on loads and the
+// cluster barrier):
+//   * the packed FFT input lands by cp.async (8-byte granules, zero-filled past Ns);
+//   * the post-twiddle of the odd half is applied by whichever rank assembles the output, so the
+//     two ranks reach the cluster barrier with equal work;
+//   * the BDF2 stencil inputs, both spectral halves and the twiddles of a thread's outputs are all
+//     requested before any of them is used.
+#include <cooperative_groups.h>
+
+#include "fft_block.cuh"
+#include "kernels.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace fpc {
+
+namespace {
+__device__ __forceinline__ void cpa8(void* smem, const void* gmem, bool valid) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(valid ? 8 : 0));
+}
+}  // namespace
+
+template <int LOGM>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((1 << (LOGM - 1)) / 16, 2)
+    k_matvec_split(const double* __restrict__ v, double* __restrict__ y, int ns, int koff,
+                   const double* __restrict__ eig, const double2* __restrict__ twb) {
+  constexpr int M = 1 << LOGM, H = M / 2, L = 2 * M, NT = H / 16, BS = padded(H);
+  extern __shared__ double2 smem[];
+  cg::cluster_group cluster = cg::this_cluster();
+  const int q = int(cluster.block_rank());
+  const size_t k = blockIdx.x >> 1;
+  const long kg = long(k) + koff;  // global time level (time-sharded callers pass halo + offset)
+  const double* vk = v + k * ns;
+  const double2* twM = twb + M;
+
+  // 1. packed input by cp.async: real index i -> slot i/2, component i%2
+  for (int i = threadIdx.x; i < 2 * H; i += NT) {
+    double* dst = reinterpret_cast<double*>(smem + pad16(i >> 1)) + (i & 1);
+    cpa8(dst, i < ns ? vk + i : vk, i < ns);
+  }
+  asm volatile("cp.async.commit_group;\n" ::);
+  asm volatile("cp.async.wait_group 0;\n" ::);
+  __syncthreads();
+  if (q == 1)  // odd bins: b_m = z_m e^{-2 pi i m/M}
+    for (int m = threadIdx.x; m < H; m += NT) smem[pad16(m)] = cmul(smem[pad16(m)], __ldg(twM + m));
+  __syncthreads();
+  block_fft<LOGM - 1, -1, BS, 16>(smem, twb + H, 1);
+
+  // 2. eigenvalue product on (kappa, M - kappa) pairs; slot j of rank q holds bin 2j + q.
+  //    task t: rank 0 -> (slot t+1, slot H-t-1, kappa 2t+2); rank 1 -> (t, H-1-t, 2t+1)
+  const double2* twL = twb + L;
+  constexpr int UP = 4;
+  constexpr int ntask = H / 2;
+  if (q == 0 && threadIdx.x == 0) {
+    const double2 z = smem[0];
+    const double y0 = eig[0] * (2.0 * (z.x + z.y));
+    const double ym = eig[M] * (2.0 * (z.x - z.y));
+    smem[0] = make_double2(y0 + ym, y0 - ym);
+  }
+  for (int t0 = threadIdx.x; t0 < ntask; t0 += UP * NT) {
+    double2 wv[UP];
+    double ek[UP], em[UP];
+#pragma unroll
+    for (int u = 0; u < UP; ++u) {
+      const int t = t0 + u * NT;
+      const int kap = q == 0 ? 2 * (t + 1) : 2 * t + 1;
+      const bool ok = t < ntask;
+      wv[u] = ok ? __ldg(twL + kap) : make_double2(1.0, 0.0);  // e^{-2 pi i kappa/L}
+      ek[u] = ok ? __ldg(eig + kap) : 0.0;
+      em[u] = ok ? __ldg(eig + M - kap) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < UP; ++u) {
+      const int t = t0 + u * NT;
+      if (t >= ntask) continue;
+      const int s1 = q == 0 ? t + 1 : t, s2 = q == 0 ? H - (t + 1) : H - 1 - t;
+      const double2 w = wv[u];
+      const double2 a = smem[pad16(s1)], bq = smem[pad16(s2)];
+      const double2 P = cadd(a, cconj(bq)), Q = csub(a, cconj(bq));
+      const double2 iwQ = mul_si<1>(cmul(w, Q));
+      const double2 Yk = cscale(csub(P, iwQ), ek[u]);
+      const double2 Ym = cscale(cconj(cadd(P, iwQ)), em[u]);
+      const double2 A = cadd(Yk, cconj(Ym));
+      const double2 D = csub(Yk, cconj(Ym));
+      smem[pad16(s1)] = cadd(A, mul_si<1>(cmul(D, cconj(w))));
+      if (s1 != s2) smem[pad16(s2)] = cadd(cconj(A), mul_si<1>(cmul(cconj(D), w)));
+    }
+  }
+  __syncthreads();
+  block_fft<LOGM - 1, 1, BS, 16>(smem, twb + H, 1);
+  cluster.sync();
+
+  // 3. outputs 2m, 2m+1 for my half of m: y_m = E_m + e^{+2 pi i m/M} O_m, + the BDF2 stencil
+  const double2* Eb = cluster.map_shared_rank(smem, 0);
+  const double2* Ob = cluster.map_shared_rank(smem, 1);
+  double* yk = y + k * ns;
+  constexpr int PER = (H / 2) / NT;  // m values per thread
+  static_assert(PER * NT == H / 2, "H/2 must be a multiple of the thread count");
+  constexpr int UB = 2;              // m values whose loads are in flight together
+#pragma unroll 1
+  for (int u0 = 0; u0 < PER; u0 += UB) {
+    double2 e[UB], o[UB], w[UB], c0[UB], c1[UB], c2[UB];
+#pragma unroll
+    for (int u = 0; u < UB; ++u) {
+      const int m = q * (H / 2) + threadIdx.x + (u0 + u) * NT;
+      const int j0 = 2 * m;
+      e[u] = Eb[pad16(m)];
+      o[u] = Ob[pad16(m)];
+      w[u] = __ldg(twM + m);
+      const bool ok0 = j0 < ns, ok1 = j0 + 1 < ns;
+      c0[u] = make_double2(ok0 ? vk[j0] : 0.0, ok1 ? vk[j0 + 1] : 0.0);
+      c1[u] = make_double2(ok0 && kg >= 1 ? vk[long(j0) - ns] : 0.0, ok1 && kg >= 1 ? vk[long(j0) + 1 - ns] : 0.0);
+      c2[u] = make_double2(ok0 && kg >= 2 ? vk[long(j0) - 2 * long(ns)] : 0.0,
+                           ok1 && kg >= 2 ? vk[long(j0) + 1 - 2 * long(ns)] : 0.0);
+    }
+#pragma unroll
+    for (int u = 0; u < UB; ++u) {
+      const int m = q * (H / 2) + threadIdx.x + (u0 + u) * NT;
+      const int j0 = 2 * m;
+      const double2 t = cadd(e[u], cmul(o[u], cconj(w[u])));
+      double2 c;  // time_stencil.hpp:16-26 (same association as all_at_once.hpp:44-53)
+      if (kg == 0)
+        c = c0[u];
+      else if (kg == 1)
+        c = make_double2(1.5 * c0[u].x + -2.0 * c1[u].x, 1.5 * c0[u].y + -2.0 * c1[u].y);
+      else
+        c = make_double2(1.5 * c0[u].x + -2.0 * c1[u].x + 0.5 * c2[u].x,
+                         1.5 * c0[u].y + -2.0 * c1[u].y + 0.5 * c2[u].y);
+      if (j0 < ns) yk[j0] = c.x + t.x;
+      if (j0 + 1 < ns) yk[j0 + 1] = c.y + t.y;
+    }
+  }
+  cluster.sync();  // keep both buffers alive until the partner has read them
+}
+
+cudaError_t launch_matvec_split13(const double* v, double* y, int n_space, int n_time, int koff,
+                                  const double* eig_scaled, const double2* tw_base, cudaStream_t st) {
+  constexpr size_t smem = size_t(padded(4096)) * sizeof(double2);
+  cudaError_t err = cudaFuncSetAttribute(k_matvec_split<13>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+  if (err != cudaSuccess) return err;
+  err = cudaFuncSetAttribute(k_matvec_split<13>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  if (err != cudaSuccess) return err;
+  k_matvec_split<13><<<2 * n_time, 256, smem, st>>>(v, y, n_space, koff, eig_scaled, tw_base);
+  return cudaGetLastError();
+}
+
+}  // namespace fpc

@@ -56,6 +56,7 @@ int main() {
   for (int l = 0; l <= 17; ++l) { size_t N = size_t(1) << l; for (size_t t = 0; t < N; ++t) { double th = -2 * M_PI * t / N; h[N + t] = make_double2(cos(th), sin(th)); } }
   cudaMalloc(&tw, h.size() * 16); cudaMemcpy(tw, h.data(), h.size() * 16, cudaMemcpyHostToDevice);
   run<13, 1, 16, 1>(in, out, tw, total >> 13);
+  run<12, 1, 16, 3>(in, out, tw, total >> 12);
   run<12, 1, 16, 2>(in, out, tw, total >> 12);
   run<12, 1, 16, 3>(in, out, tw, total >> 12);
   run<12, 2, 16, 1>(in, out, tw, total >> 12);
