@@ -25,6 +25,19 @@ namespace cg = cooperative_groups;
 
 namespace fpc {
 
+#ifdef FPC_PHASE_TIMING
+__device__ long long g_phase_mv[1 << 16][8];
+#define FPC_PHM(i) \
+  do { if (threadIdx.x == 0 && blockIdx.x < (1 << 16)) g_phase_mv[blockIdx.x][i] = clock64(); } while (0)
+extern "C" int fpc_debug_phases_mv(long long* out, int nblocks) {
+  return int(cudaMemcpyFromSymbol(out, g_phase_mv, size_t(nblocks) * 8 * sizeof(long long)));
+}
+#else
+#define FPC_PHM(i) \
+  do {             \
+  } while (0)
+#endif
+
 namespace {
 __device__ __forceinline__ void cpa8(void* smem, const void* gmem, bool valid) {
   const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
@@ -44,6 +57,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((1 << (LOGM - 1)) / 
   const long kg = long(k) + koff;  // global time level (time-sharded callers pass halo + offset)
   const double* vk = v + k * ns;
   const double2* twM = twb + M;
+  FPC_PHM(0);
 
   // 1. packed input by cp.async: real index i -> slot i/2, component i%2
   for (int i = threadIdx.x; i < 2 * H; i += NT) {
@@ -56,7 +70,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((1 << (LOGM - 1)) / 
   if (q == 1)  // odd bins: b_m = z_m e^{-2 pi i m/M}
     for (int m = threadIdx.x; m < H; m += NT) smem[pad16(m)] = cmul(smem[pad16(m)], __ldg(twM + m));
   __syncthreads();
+  FPC_PHM(1);
   block_fft<LOGM - 1, -1, BS, 16>(smem, twb + H, 1);
+  FPC_PHM(2);
 
   // 2. eigenvalue product on (kappa, M - kappa) pairs; slot j of rank q holds bin 2j + q.
   //    task t: rank 0 -> (slot t+1, slot H-t-1, kappa 2t+2); rank 1 -> (t, H-1-t, 2t+1)
@@ -99,8 +115,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((1 << (LOGM - 1)) / 
     }
   }
   __syncthreads();
+  FPC_PHM(3);
   block_fft<LOGM - 1, 1, BS, 16>(smem, twb + H, 1);
+  FPC_PHM(4);
   cluster.sync();
+  FPC_PHM(5);
 
   // 3. outputs 2m, 2m+1 for my half of m: y_m = E_m + e^{+2 pi i m/M} O_m, + the BDF2 stencil
   const double2* Eb = cluster.map_shared_rank(smem, 0);
@@ -142,6 +161,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((1 << (LOGM - 1)) / 
       if (j0 + 1 < ns) yk[j0 + 1] = c.y + t.y;
     }
   }
+  FPC_PHM(6);
   cluster.sync();  // keep both buffers alive until the partner has read them
 }
 

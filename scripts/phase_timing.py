@@ -17,9 +17,9 @@ print("kernel ms", e0.elapsed_time(e1))
 nb = 2 * w.n_time
 buf = np.zeros((nb, 8), dtype=np.int64)
 lib = N.load()
-lib.fpc_debug_phases.argtypes = [C.c_void_p, C.c_int]
-assert lib.fpc_debug_phases(buf.ctypes.data, nb) == 0
-names = ["load", "fft_fwd", "pointwise", "fft_inv", "twiddle+cluster_sync", "combine+store"]
+lib.fpc_debug_phases_mv.argtypes = [C.c_void_p, C.c_int]
+assert lib.fpc_debug_phases_mv(buf.ctypes.data, nb) == 0
+names = ["load(cp.async)+pretw", "fft_fwd", "pointwise", "fft_inv", "cluster_sync", "combine+stencil+store"]
 d = np.diff(buf[:, :7], axis=1)
 for i, n in enumerate(names):
     print(f"{n:22s} mean {d[:, i].mean():9.0f} cyc  median {np.median(d[:, i]):9.0f}")
