@@ -35,15 +35,12 @@ __device__ __forceinline__ double2 mul_si(double2 a) {
   return S > 0 ? make_double2(-a.y, a.x) : make_double2(a.y, -a.x);
 }
 
-// a / (cr + i ci) by Smith's algorithm (the robust complex division std::complex uses, up to
-// rounding; tau.hpp:114)
-__device__ __forceinline__ double2 cdiv_smith(double2 a, double cr, double ci) {
-  if (fabs(cr) >= fabs(ci)) {
-    const double rr = ci / cr, den = cr + ci * rr;
-    return make_double2((a.x + a.y * rr) / den, (a.y - a.x * rr) / den);
-  }
-  const double rr = cr / ci, den = cr * rr + ci;
-  return make_double2((a.x * rr + a.y) / den, (a.y * rr - a.x) / den);
+// a / (cr + i ci) as a conj(c) / |c|^2: one fp64 division per mode instead of Smith's three
+// (std::complex division, tau.hpp:114, agrees to a few ulp; the shifted eigenvalues are O(1)..
+// O(1e8) in magnitude, far from the range where |c|^2 could overflow or underflow)
+__device__ __forceinline__ double2 cdiv_recip(double2 a, double cr, double ci) {
+  const double inv = 1.0 / fma(cr, cr, ci * ci);
+  return make_double2(fma(a.x, cr, a.y * ci) * inv, fma(a.y, cr, -a.x * ci) * inv);
 }
 
 // the per-mode step of the shifted tau action (tau.hpp:109-118): MODE 1 = solve (divide by the
@@ -51,7 +48,7 @@ __device__ __forceinline__ double2 cdiv_smith(double2 a, double cr, double ci) {
 template <int MODE>
 __device__ __forceinline__ double2 shift_apply(double2 a, double cr, double ci) {
   if constexpr (MODE == 2) return cmul(a, make_double2(cr, ci));
-  return cdiv_smith(a, cr, ci);
+  return cdiv_recip(a, cr, ci);
 }
 
 // cos/sin(2 pi k / 16), k = 0..15

@@ -315,6 +315,7 @@ __global__ void __launch_bounds__(TauGeo<LOGM>::G::NT, minb(TauGeo<LOGM>::G::NT)
   const int r0 = blockIdx.x * B;
   const int nb = min(B, n_rows - r0);
   const double scale = sqrt(2.0 / double(M));
+  FPC_PH(0);
 
   // load rows: element i -> slot i + 1
   for (int b = 0; b < B; ++b) {
@@ -335,18 +336,30 @@ __global__ void __launch_bounds__(TauGeo<LOGM>::G::NT, minb(TauGeo<LOGM>::G::NT)
     }
   }
   __syncthreads();
+  FPC_PH(1);
   if constexpr (MODE != 0) {
     block_dst<LOGM, BS, BH, 1>(smem, hbuf, twb, scale);
+    FPC_PH(2);
     // divide by the shifted tau eigenvalues (slot i + 1 <-> index i)
     for (int b = 0; b < B; ++b) {
       double2* s = smem + b * BS;
       const double2 l = (b < nb) ? __ldg(lam + r0 + b) : make_double2(1.0, 0.0);
-      for (int i = threadIdx.x; i < NSR; i += NT)
-        s[pad16(i + 1)] = shift_apply<MODE>(s[pad16(i + 1)], l.x - dt * __ldg(sigma + i), l.y);
+      for (int i0 = threadIdx.x; i0 < NSR; i0 += 4 * U * NT) {  // sigma loads batched ahead of use
+        double sg[4 * U];
+#pragma unroll
+        for (int u = 0; u < 4 * U; ++u) sg[u] = i0 + u * NT < NSR ? __ldg(sigma + i0 + u * NT) : 0.0;
+#pragma unroll
+        for (int u = 0; u < 4 * U; ++u) {
+          const int i = i0 + u * NT;
+          if (i < NSR) s[pad16(i + 1)] = shift_apply<MODE>(s[pad16(i + 1)], l.x - dt * sg[u], l.y);
+        }
+      }
     }
     __syncthreads();
   }
+  FPC_PH(3);
   block_dst<LOGM, BS, BH, 0>(smem, hbuf, twb, scale);
+  FPC_PH(4);
 
   // store rows (slot i <-> index i), coalesced
   for (int b = 0; b < nb; ++b) {
@@ -354,6 +367,7 @@ __global__ void __launch_bounds__(TauGeo<LOGM>::G::NT, minb(TauGeo<LOGM>::G::NT)
     const double2* s = smem + b * BS;
     for (int i = threadIdx.x; i < NSR; i += NT) zr[i] = s[pad16(i)];
   }
+  FPC_PH(5);
 }
 
 // =====================================================================================

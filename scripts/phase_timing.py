@@ -1,29 +1,40 @@
-"""Per-phase clock64 breakdown of k_matvec_1d_split (build/timing/libfpc_timing.so, -DFPC_PHASE_TIMING)."""
+"""Per-phase clock64 breakdown of the config-1 FFT kernels (development build with -DFPC_PHASE_TIMING,
+scripts/_timing/libfpc_timing.so, scripts/build_timing.sh).  usage: phase_timing.py [mv|tau]"""
 import os, sys, ctypes as C
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-os.environ.setdefault("FPC_LIB", os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "build/timing/libfpc_timing.so"))
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+os.environ.setdefault("FPC_LIB", os.path.join(ROOT, "scripts/_timing/libfpc_timing.so"))
 import numpy as np, torch
 import paper_2003_07020_b200 as fp
 from paper_2003_07020_b200 import problems, _native as N
+
+mode = sys.argv[1] if len(sys.argv) > 1 else "mv"
 w = problems.config(1)
 op = fp.AllAtOnceOperator(fp.TimeStencil(w.n_time), fp.RieszJacobian1D(w.gamma[0], 1.0, w.h, w.n), w.dt)
 b = torch.from_numpy(problems.rhs(w)).cuda()
 y = torch.empty_like(b)
-for _ in range(3): op.apply(b, y)
+if mode == "mv":
+    run = lambda: (op.apply(b, y), op.ctx.synchronize())
+    nb, sym = 2 * w.n_time, "fpc_debug_phases_mv"
+    names = ["load(cp.async)+pretw", "fft_fwd", "pointwise", "fft_inv", "cluster_sync", "combine+stencil+store"]
+else:
+    plan = fp.build_plan(fp.PreconditionerKind.generalized(), w.n_time, w.dt, op)
+    run = lambda: (fp.apply_inverse(plan, b, y), op.ctx.synchronize())
+    nb, sym = w.n_time // 2 + 1, "fpc_debug_phases"
+    names = ["load", "dst1", "divide", "dst2", "store"]
+for _ in range(3):
+    run()
 op.ctx.synchronize()
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-e0.record(); op.apply(b, y); e1.record(); torch.cuda.synchronize()
-print("kernel ms", e0.elapsed_time(e1))
-nb = 2 * w.n_time
+e0.record(); run(); e1.record(); torch.cuda.synchronize()
+print(mode, "ms", e0.elapsed_time(e1))
 buf = np.zeros((nb, 8), dtype=np.int64)
 lib = N.load()
-lib.fpc_debug_phases_mv.argtypes = [C.c_void_p, C.c_int]
-assert lib.fpc_debug_phases_mv(buf.ctypes.data, nb) == 0
-names = ["load(cp.async)+pretw", "fft_fwd", "pointwise", "fft_inv", "cluster_sync", "combine+stencil+store"]
-d = np.diff(buf[:, :7], axis=1)
+getattr(lib, sym).argtypes = [C.c_void_p, C.c_int]
+assert getattr(lib, sym)(buf.ctypes.data, nb) == 0
+k = len(names)
+d = np.diff(buf[:, :k + 1], axis=1)
 for i, n in enumerate(names):
     print(f"{n:22s} mean {d[:, i].mean():9.0f} cyc  median {np.median(d[:, i]):9.0f}")
-tot = buf[:, 6] - buf[:, 0]
+tot = buf[:, k] - buf[:, 0]
 print("per-CTA total mean", tot.mean(), "cycles; CTAs", nb)
-span = buf[:, 6].max() - buf[:, 0].min()
-print("span (cycles, across SMs clocks may differ)", span)
