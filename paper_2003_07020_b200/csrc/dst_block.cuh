@@ -17,6 +17,12 @@
 #pragma once
 #include "fft_block.cuh"
 
+#ifndef FPC_DST_PH
+#define FPC_DST_PH(i) \
+  do {                \
+  } while (0)
+#endif
+
 namespace fpc {
 
 // Buffers: B = blockDim.x * 16 / N rows; row b has an N-slot buffer at s + b*BS (input f_j at
@@ -70,8 +76,11 @@ __device__ __forceinline__ void block_dst(double2* s, double2* h, const double2*
     if (j != M / 2) hv[pad16(M - j)] = cscale(cmul(cconj(wm), csub(sj, mul_si<1>(sm))), 0.5);
   }
   __syncthreads();
+  FPC_DST_PH(0);
   block_fft<LOGN, 1, BS, E>(s, twb + N, 0);
+  FPC_DST_PH(1);
   block_fft<LOGN - 1, 1, BH, E / 2>(h, twb + M, 0);
+  FPC_DST_PH(2);
 
   // 2. post: thread handles k = tb*KP .. tb*KP + KP-1 of its row
   const int b = threadIdx.x / TPB, tb = threadIdx.x - b * TPB;
@@ -96,6 +105,7 @@ __device__ __forceinline__ void block_dst(double2* s, double2* h, const double2*
   }
   if (OUT_SHIFT == 1 && tb == 0) rw[0] = make_double2(0.0, 0.0);
   __syncthreads();
+  FPC_DST_PH(3);
 }
 
 }  // namespace fpc

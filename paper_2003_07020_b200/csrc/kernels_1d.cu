@@ -13,6 +13,14 @@
 
 #include <cstdlib>
 
+#ifdef FPC_PHASE_TIMING
+namespace fpc {
+__device__ long long g_phase[1 << 16][16];
+}
+// stamps 8.. inside block_dst (first call per CTA wins the slot: later calls overwrite)
+#define FPC_DST_PH(i) \
+  do { if (threadIdx.x == 0 && blockIdx.x < (1 << 16)) fpc::g_phase[blockIdx.x][8 + (i)] = clock64(); } while (0)
+#endif
 #include "dst_block.cuh"
 #include "fft_block.cuh"
 #include "kernels.cuh"
@@ -23,11 +31,10 @@ namespace fpc {
 
 #ifdef FPC_PHASE_TIMING
 // development instrumentation: per-CTA clock64 stamps at phase boundaries (one thread per CTA)
-__device__ long long g_phase[1 << 16][8];
 #define FPC_PH(i) \
   do { if (threadIdx.x == 0 && blockIdx.x < (1 << 16)) g_phase[blockIdx.x][i] = clock64(); } while (0)
 extern "C" int fpc_debug_phases(long long* out, int nblocks) {
-  return int(cudaMemcpyFromSymbol(out, g_phase, size_t(nblocks) * 8 * sizeof(long long)));
+  return int(cudaMemcpyFromSymbol(out, g_phase, size_t(nblocks) * 16 * sizeof(long long)));
 }
 #else
 #define FPC_PH(i) \

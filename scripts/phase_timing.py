@@ -28,7 +28,7 @@ op.ctx.synchronize()
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 e0.record(); run(); e1.record(); torch.cuda.synchronize()
 print(mode, "ms", e0.elapsed_time(e1))
-buf = np.zeros((nb, 8), dtype=np.int64)
+buf = np.zeros((nb, 16 if mode == "tau" else 8), dtype=np.int64)
 lib = N.load()
 getattr(lib, sym).argtypes = [C.c_void_p, C.c_int]
 assert getattr(lib, sym)(buf.ctypes.data, nb) == 0
@@ -38,3 +38,9 @@ for i, n in enumerate(names):
     print(f"{n:22s} mean {d[:, i].mean():9.0f} cyc  median {np.median(d[:, i]):9.0f}")
 tot = buf[:, k] - buf[:, 0]
 print("per-CTA total mean", tot.mean(), "cycles; CTAs", nb)
+if mode == "tau":  # inside the second block_dst (stamps 8..11 are overwritten by the last call)
+    dd = np.diff(buf[:, 8:12], axis=1)
+    pre = buf[:, 8] - buf[:, 3]
+    print(f"  dst2 pre            mean {pre.mean():9.0f}")
+    for i, n in enumerate(["fft N", "fft N/2", "post"]):
+        print(f"  dst2 {n:14s} mean {dd[:, i].mean():9.0f}")
