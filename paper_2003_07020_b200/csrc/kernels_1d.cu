@@ -36,9 +36,20 @@ namespace fpc {
 extern "C" int fpc_debug_phases(long long* out, int nblocks) {
   return int(cudaMemcpyFromSymbol(out, g_phase, size_t(nblocks) * 16 * sizeof(long long)));
 }
+// time kernels: kid 0 = k_time_fwd, 1 = k_time_inv
+__device__ long long g_phase_t[2][1 << 14][4];
+#define FPC_PT(kid, i) \
+  do { if (threadIdx.x == 0 && blockIdx.x < (1 << 14)) g_phase_t[kid][blockIdx.x][i] = clock64(); } while (0)
+extern "C" int fpc_debug_phases_t(long long* out, int kid, int nblocks) {
+  return int(cudaMemcpyFromSymbol(out, g_phase_t, size_t(nblocks) * 4 * sizeof(long long),
+                                  size_t(kid) * (1 << 14) * 4 * sizeof(long long)));
+}
 #else
 #define FPC_PH(i) \
   do {            \
+  } while (0)
+#define FPC_PT(kid, i) \
+  do {                 \
   } while (0)
 #endif
 
@@ -179,17 +190,23 @@ __global__ void __launch_bounds__(Geo<LOGM, kTotMv, 16>::NT, minb(Geo<LOGM, kTot
 // K2: time FFT forward over spatial columns (alpha_circulant.hpp:146-156), Hermitian half.
 // CTA = B columns; M = Nt/2.
 // =====================================================================================
-constexpr int kTotT = 4096;
+// Complex slots per CTA.  A CTA reads B = TOT/M columns of every time row, i.e. B*8-byte segments
+// at a stride of Ns*8 bytes; for long series (M >= 1024) 8 columns per CTA (64-byte segments, one
+// 512-thread CTA per SM) beat 4 columns at two CTAs per SM (B200, config 1: 155 -> 145 us),
+// because the load/store phases are bound by DRAM efficiency on these strided segments.
+template <int LOGM>
+constexpr int tot_t() { return LOGM >= 10 ? 8192 : 4096; }
 
 template <int LOGM>
-__global__ void __launch_bounds__(Geo<LOGM, kTotT>::NT, minb(Geo<LOGM, kTotT>::NT))
+__global__ void __launch_bounds__(Geo<LOGM, tot_t<LOGM>()>::NT, minb(Geo<LOGM, tot_t<LOGM>()>::NT))
     k_time_fwd(const double* __restrict__ v, double2* __restrict__ Z, int ns,
                const double* __restrict__ sf, double s_in, const double2* __restrict__ twb) {
-  using G = Geo<LOGM, kTotT>;
+  using G = Geo<LOGM, tot_t<LOGM>()>;
   constexpr int M = G::M, B = G::B, NTIME = 2 * M, BS = G::BS, NT = G::NT;
   constexpr int U = 16;
   extern __shared__ double2 smem[];
   const int p0 = blockIdx.x * B;
+  FPC_PT(0, 0);
 
   for (int e0 = threadIdx.x; e0 < B * NTIME; e0 += U * NT) {
     double x[U];
@@ -210,7 +227,9 @@ __global__ void __launch_bounds__(Geo<LOGM, kTotT>::NT, minb(Geo<LOGM, kTotT>::N
     }
   }
   __syncthreads();
+  FPC_PT(0, 1);
   block_fft<LOGM, 1, BS, G::E>(smem, twb + M, B);
+  FPC_PT(0, 2);
 
   const double2* twT = twb + NTIME;  // e^{-2 pi i n/Nt}; the forward kernel here is e^{+...}
   for (int t = threadIdx.x; t < B * (M / 2 + 1); t += NT) {
@@ -231,6 +250,7 @@ __global__ void __launch_bounds__(Geo<LOGM, kTotT>::NT, minb(Geo<LOGM, kTotT>::N
       if (n != M - n) Z[size_t(M - n) * ns + p] = cscale(cconj(cadd(P, iwQ)), 0.5);
     }
   }
+  FPC_PT(0, 3);
 }
 
 // =====================================================================================
@@ -238,16 +258,17 @@ __global__ void __launch_bounds__(Geo<LOGM, kTotT>::NT, minb(Geo<LOGM, kTotT>::N
 // Z_{Nt-n} = conj(Z_n) (alpha_circulant.hpp:167-175) is folded into the real-output packing.
 // =====================================================================================
 template <int LOGM>
-__global__ void __launch_bounds__(Geo<LOGM, kTotT>::NT, minb(Geo<LOGM, kTotT>::NT))
+__global__ void __launch_bounds__(Geo<LOGM, tot_t<LOGM>()>::NT, minb(Geo<LOGM, tot_t<LOGM>()>::NT))
     k_time_inv(const double2* __restrict__ Z, double* __restrict__ z, int ns,
                const double* __restrict__ sb, const double2* __restrict__ twb) {
-  using G = Geo<LOGM, kTotT>;
+  using G = Geo<LOGM, tot_t<LOGM>()>;
   constexpr int M = G::M, B = G::B, NTIME = 2 * M, BS = G::BS, NT = G::NT;
   constexpr int U = 8;
   constexpr int TASKS = B * (M / 2 + 1);
   extern __shared__ double2 smem[];
   const int p0 = blockIdx.x * B;
   const double2* twT = twb + NTIME;
+  FPC_PT(1, 0);
 
   for (int t0 = threadIdx.x; t0 < TASKS; t0 += U * NT) {
     double2 ya[U], yb[U];
@@ -279,7 +300,9 @@ __global__ void __launch_bounds__(Geo<LOGM, kTotT>::NT, minb(Geo<LOGM, kTotT>::N
     }
   }
   __syncthreads();
+  FPC_PT(1, 1);
   block_fft<LOGM, -1, BS, G::E>(smem, twb + M, B);
+  FPC_PT(1, 2);
 
   const double inv_nt = 1.0 / double(NTIME);
   for (int e = threadIdx.x; e < B * NTIME; e += NT) {
@@ -289,6 +312,7 @@ __global__ void __launch_bounds__(Geo<LOGM, kTotT>::NT, minb(Geo<LOGM, kTotT>::N
     const double val = comp(smem, c * BS + pad16(kk >> 1), kk & 1);
     z[size_t(kk) * ns + p] = (__ldg(sb + kk) * inv_nt) * val;
   }
+  FPC_PT(1, 3);
 }
 
 // =====================================================================================
@@ -459,7 +483,7 @@ cudaError_t launch_time_fwd(const double* v, double2* Z, int n_space, int n_time
   const int lm = ilog2(n_time) - 1;
 #define CALL(LM)                                                                          \
   {                                                                                       \
-    using G = Geo<LM, kTotT>;                                                             \
+    using G = Geo<LM, tot_t<LM>()>;                                                             \
     if ((err = prep(k_time_fwd<LM>, G::SMEM)) != cudaSuccess) return err;                 \
     k_time_fwd<LM><<<(n_space + G::B - 1) / G::B, G::NT, G::SMEM, st>>>(                  \
         v, Z, n_space, scale_fwd, s_in, tw_base);                                         \
@@ -477,7 +501,7 @@ cudaError_t launch_time_inv(const double2* Z, double* z, int n_space, int n_time
   const int lm = ilog2(n_time) - 1;
 #define CALL(LM)                                                                            \
   {                                                                                         \
-    using G = Geo<LM, kTotT>;                                                               \
+    using G = Geo<LM, tot_t<LM>()>;                                                               \
     if ((err = prep(k_time_inv<LM>, G::SMEM)) != cudaSuccess) return err;                   \
     k_time_inv<LM><<<(n_space + G::B - 1) / G::B, G::NT, G::SMEM, st>>>(Z, z, n_space,       \
                                                                         scale_bwd, tw_base); \

@@ -1,5 +1,5 @@
 """Per-phase clock64 breakdown of the config-1 FFT kernels (development build with -DFPC_PHASE_TIMING,
-scripts/_timing/libfpc_timing.so, scripts/build_timing.sh).  usage: phase_timing.py [mv|tau]"""
+scripts/_timing/libfpc_timing.so, scripts/build_timing.sh).  usage: phase_timing.py [mv|tau|time]"""
 import os, sys, ctypes as C
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
@@ -17,6 +17,22 @@ if mode == "mv":
     run = lambda: (op.apply(b, y), op.ctx.synchronize())
     nb, sym = 2 * w.n_time, "fpc_debug_phases_mv"
     names = ["load(cp.async)+pretw", "fft_fwd", "pointwise", "fft_inv", "cluster_sync", "combine+stencil+store"]
+elif mode == "time":
+    plan = fp.build_plan(fp.PreconditionerKind.generalized(), w.n_time, w.dt, op)
+    run = lambda: (fp.apply_inverse(plan, b, y), op.ctx.synchronize())
+    for _ in range(3):
+        run()
+    lib = N.load()
+    lib.fpc_debug_phases_t.argtypes = [C.c_void_p, C.c_int, C.c_int]
+    nb = (w.n_space + 3) // 4
+    for kid, nm in [(0, "time_fwd"), (1, "time_inv")]:
+        buf = np.zeros((nb, 4), dtype=np.int64)
+        assert lib.fpc_debug_phases_t(buf.ctypes.data, kid, nb) == 0
+        d = np.diff(buf, axis=1)
+        for i, n in enumerate(["load/pack", "fft", "unpack/store"]):
+            print(f"{nm} {n:14s} mean {d[:, i].mean():9.0f} cyc  median {np.median(d[:, i]):9.0f}")
+        print(f"{nm} per-CTA total mean {(buf[:, 3] - buf[:, 0]).mean():.0f}; CTAs {nb}")
+    sys.exit(0)
 else:
     plan = fp.build_plan(fp.PreconditionerKind.generalized(), w.n_time, w.dt, op)
     run = lambda: (fp.apply_inverse(plan, b, y), op.ctx.synchronize())

@@ -130,7 +130,7 @@ def test_pc_forward_1d(oracle, gamma, ns, nt):
     assert rel(fp.apply_inverse(plan, pv), v) <= 1e-10
 
 
-@pytest.mark.parametrize("gamma,ns,nt", [(1.5, 15, 8), (1.7, 63, 16), (1.5, 1023, 64)])
+@pytest.mark.parametrize("gamma,ns,nt", [(1.5, 15, 8), (1.7, 63, 16), (1.5, 1023, 64), (1.2, 8191, 8)])
 def test_full_sweep_1d(oracle, gamma, ns, nt):
     # InnerSweep::full (alpha_circulant.hpp:158-159) vs the oracle's full sweep, and the reference's
     # half == full property (test_pint.cpp:203-216)
