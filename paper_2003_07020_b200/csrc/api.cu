@@ -331,7 +331,7 @@ void check_sizes_1d(int n_space, int n_time) {
   if (n_time > 16384) throw Unsupported{"B200 path supports n_time <= 16384"};
   if (ilog2_exact(size_t(n_space) + 1) < 0 || n_space < 3)
     throw Unsupported{"B200 path needs n_space + 1 to be a power of two >= 4 (DST-I length)"};
-  if (n_space + 1 > 8192) throw Unsupported{"B200 path supports n_space + 1 <= 8192 (smem FFT)"};
+  if (n_space + 1 > 65536) throw Unsupported{"B200 path supports n_space + 1 <= 65536"};
 }
 
 void upload(void* dst, const void* src, size_t bytes, cudaStream_t st) {

@@ -21,6 +21,10 @@ cudaError_t launch_matvec_1d(const double* v, double* y, int n_space, int n_time
 cudaError_t launch_matvec_split13(const double* v, double* y, int n_space, int n_time, int koff,
                                   const double* eig_scaled, const double2* tw_base, cudaStream_t st);
 
+// Ns + 1 = 16384 .. 65536 (kernels_large.cu): clusters of C = L/8192 CTAs (4, 8, 16)
+cudaError_t launch_matvec_large(const double* v, double* y, int n_space, int n_time, int log_m, int koff,
+                                const double* eig_scaled, const double2* tw_base, cudaStream_t st);
+
 // ---- preconditioner apply, reference ordering (alpha_circulant.hpp:137-199) ---------------
 // K2: Z[n][p] = sum_k s_in*scale_fwd[k]*v[k][p] e^{+2 pi i kn/Nt}, n = 0..Nt/2 (half spectrum).
 cudaError_t launch_time_fwd(const double* v, double2* Z, int n_space, int n_time,
@@ -47,6 +51,10 @@ cudaError_t launch_time_inv_full(const double2* Z, double* z, int n_space, int n
 cudaError_t launch_tau_solve_1d(double2* Z, int n_space, int n_rows, const double2* lambda,
                                 const double* sigma, double dt, const double2* tw_base,
                                 cudaStream_t st, bool forward = false);
+
+// Ns + 1 = 16384 .. 65536 (kernels_large.cu): DST-I via the odd extension on clusters of 2N/8192 CTAs
+cudaError_t launch_tau_large(double2* Z, int n_space, int n_rows, const double2* lambda, const double* sigma,
+                             double dt, const double2* tw_base, cudaStream_t st, bool forward);
 
 // Toeplitz along nrows contiguous rows of length len (row r at v + r*len, time level r / rpt) +
 // BDF2 stencil with stride sstride: 1D (rpt=1, sstride=len) and the 2D y-direction pass.

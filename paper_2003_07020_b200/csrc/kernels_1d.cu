@@ -203,7 +203,10 @@ __global__ void __launch_bounds__(Geo<LOGM, tot_t<LOGM>()>::NT, minb(Geo<LOGM, t
                const double* __restrict__ sf, double s_in, const double2* __restrict__ twb) {
   using G = Geo<LOGM, tot_t<LOGM>()>;
   constexpr int M = G::M, B = G::B, NTIME = 2 * M, BS = G::BS, NT = G::NT;
-  constexpr int U = 16;
+#ifndef FPC_TF_U
+#define FPC_TF_U 16
+#endif
+  constexpr int U = FPC_TF_U;
   extern __shared__ double2 smem[];
   const int p0 = blockIdx.x * B;
   FPC_PT(0, 0);
@@ -453,6 +456,8 @@ cudaError_t launch_matvec_1d(const double* v, double* y, int n_space, int n_time
   cudaError_t err = cudaSuccess;
   if (log_m == 13)  // kernels_mv.cu: 2-CTA cluster, half-length FFTs
     return launch_matvec_split13(v, y, n_space, n_time, koff, eig_scaled, tw_base, st);
+  if (log_m >= 14)  // kernels_large.cu: 4..16-CTA clusters
+    return launch_matvec_large(v, y, n_space, n_time, log_m, koff, eig_scaled, tw_base, st);
   (void)err;
   return launch_matvec_rows(v, y, n_space, n_time, 1, n_space, log_m, eig_scaled, tw_base, st, koff);
 }
@@ -544,6 +549,7 @@ cudaError_t launch_tau_solve_1d(double2* Z, int n_space, int n_rows, const doubl
                                 cudaStream_t st, bool forward) {
   cudaError_t err = cudaSuccess;
   const int lm = ilog2(n_space + 1);
+  if (lm >= 14) return launch_tau_large(Z, n_space, n_rows, lambda, sigma, dt, tw_base, st, forward);
 #define CALL(LM)                                                                  \
   err = forward ? tau1d<LM, 2>(Z, n_rows, lambda, sigma, dt, tw_base, st)         \
                 : tau1d<LM, 1>(Z, n_rows, lambda, sigma, dt, tw_base, st);

@@ -24,7 +24,7 @@ elif mode == "time":
         run()
     lib = N.load()
     lib.fpc_debug_phases_t.argtypes = [C.c_void_p, C.c_int, C.c_int]
-    nb = (w.n_space + 3) // 4
+    nb = (w.n_space + 7) // 8
     for kid, nm in [(0, "time_fwd"), (1, "time_inv")]:
         buf = np.zeros((nb, 4), dtype=np.int64)
         assert lib.fpc_debug_phases_t(buf.ctypes.data, kid, nb) == 0

@@ -12,7 +12,7 @@ pytestmark = pytest.mark.gpu
 # the DST (M = n+1) and the time FFT (Nt)
 SIZES = [(1.5, 3, 4), (1.5, 7, 8), (1.3, 15, 16), (1.8, 31, 8), (1.5, 63, 32), (1.2, 127, 64),
          (1.7, 255, 128), (1.5, 511, 16), (1.5, 1023, 256), (1.9, 2047, 32), (1.4, 4095, 16),
-         (1.2, 8191, 8)]
+         (1.2, 8191, 8), (1.5, 16383, 4), (1.3, 32767, 4), (1.7, 65535, 4)]
 
 
 def make(gamma, ns, nt, kappa=1.0):
@@ -65,7 +65,7 @@ def test_pc_apply_zero_is_zero():
 
 
 @pytest.mark.parametrize("gamma,ns,nt,restart", [(1.5, 63, 16, 0), (1.5, 255, 64, 0), (1.5, 1023, 256, 20),
-                                                 (1.5, 1023, 256, 5), (1.8, 511, 128, 0)])
+                                                 (1.5, 1023, 256, 5), (1.8, 511, 128, 0), (1.5, 16383, 8, 0)])
 def test_gmres_1d(oracle, gamma, ns, nt, restart):
     w = problems.workload_1d(gamma, ns + 1, nt)
     op = fp.AllAtOnceOperator(fp.TimeStencil(nt), fp.RieszJacobian1D(gamma, 1.0, w.h, ns), w.dt)
@@ -118,7 +118,8 @@ def test_unsupported_sizes_fail_loudly():
         fp.AllAtOnceOperator(fp.TimeStencil(8), fp.RieszJacobian1D(1.5, -1.0, 0.1, 7), 0.1)
 
 
-@pytest.mark.parametrize("gamma,ns,nt", [(1.9, 7, 8), (1.5, 63, 16), (1.5, 1023, 64), (1.2, 8191, 8)])
+@pytest.mark.parametrize("gamma,ns,nt", [(1.9, 7, 8), (1.5, 63, 16), (1.5, 1023, 64), (1.2, 8191, 8),
+                                         (1.4, 32767, 4)])
 def test_pc_forward_1d(oracle, gamma, ns, nt):
     # apply_forward (alpha_circulant.hpp:212-215) vs the oracle, and the round trip P^{-1} P v = v
     op, h, dt = make(gamma, ns, nt)
@@ -130,7 +131,8 @@ def test_pc_forward_1d(oracle, gamma, ns, nt):
     assert rel(fp.apply_inverse(plan, pv), v) <= 1e-10
 
 
-@pytest.mark.parametrize("gamma,ns,nt", [(1.5, 15, 8), (1.7, 63, 16), (1.5, 1023, 64), (1.2, 8191, 8)])
+@pytest.mark.parametrize("gamma,ns,nt", [(1.5, 15, 8), (1.7, 63, 16), (1.5, 1023, 64), (1.2, 8191, 8),
+                                         (1.5, 16383, 4)])
 def test_full_sweep_1d(oracle, gamma, ns, nt):
     # InnerSweep::full (alpha_circulant.hpp:158-159) vs the oracle's full sweep, and the reference's
     # half == full property (test_pint.cpp:203-216)
