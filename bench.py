@@ -6,6 +6,7 @@ with b resident in HBM: the reference's timed span krylov.hpp:87-190 (k+1 PC app
 matvecs, the Gram-Schmidt work, x = P^{-1} V y and the fresh TRR).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--gamma 1.2]
+  python bench.py --sweep [--sweep-nx 1023,65535] [--sweep-nt 256,8192]   (config 4, one line per point)
 
 N > 1 (torchrun): ONE solve frequency-sharded over the N ranks (paper_2003_07020_b200/distributed.py:
 NCCL all-to-all around the tau solves, all-reduce for the dots; scaling "strong"); --replicas
@@ -199,6 +200,95 @@ def run_sharded(args, w, rank, world, local):
     dist.destroy_process_group()
 
 
+# ------------------------------------------------------------------------------------ config-4 sweep
+SWEEP_NX = [1023, 2047, 4095, 8191, 16383, 32767, 65535]
+SWEEP_NT = [256, 512, 1024, 2048, 4096, 8192]
+
+
+def run_sweep(args):
+    """BASELINE config 4: isolated BC preconditioner apply + matvec, 1D gamma=1.5, Nx x Nt grid,
+    complex128 seeded Gaussian input = a batch of two real vectors (Re, Im) since the operators are
+    real-linear; `reps` applications each, device-resident, CUDA events on the
+    library stream.  One JSON line per point (not the headline metric)."""
+    import torch
+    import paper_2003_07020_b200 as fp
+    dev = torch.device("cuda", 0)
+    stream = torch.cuda.Stream(device=dev)
+    ctx = fp.Context(0, stream)
+    peak, peak_kind = load_peaks()
+    nxs = [int(x) for x in args.sweep_nx.split(",")] if args.sweep_nx else SWEEP_NX
+    nts = [int(x) for x in args.sweep_nt.split(",")] if args.sweep_nt else SWEEP_NT
+    ref = None
+    if not args.no_cpu_baseline:
+        try:
+            from oracle import oracle as O
+            ref = O.Reference()
+            ref.set_threads(os.cpu_count() or 1)
+        except Exception:  # noqa: BLE001
+            ref = None
+    for nx in nxs:
+        for nt in nts:
+            h, dt = 1.0 / (nx + 1), 1.0 / nt
+            op = fp.AllAtOnceOperator(fp.TimeStencil(nt), fp.RieszJacobian1D(1.5, 1.0, h, nx), dt, ctx)
+            plan = fp.build_plan(fp.PreconditionerKind.generalized(), nt, dt, op)
+            N = nx * nt
+            gen = torch.Generator(device=dev)
+            gen.manual_seed(20260819 + nx * 131 + nt)
+            with torch.cuda.stream(stream):
+                xr = torch.randn(N, dtype=torch.float64, device=dev, generator=gen)
+                xi = torch.randn(N, dtype=torch.float64, device=dev, generator=gen)
+                yr = torch.empty_like(xr)
+                yi = torch.empty_like(xi)
+            stream.synchronize()
+
+            def timed(fn, reps):
+                for _ in range(args.warmup):
+                    fn()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                for _ in range(reps):
+                    fn()
+                e1.record(stream)
+                torch.cuda.synchronize()
+                return e0.elapsed_time(e1) * 1e-3 / reps
+
+            def pc():
+                fp.apply_inverse(plan, xr, yr)
+                fp.apply_inverse(plan, xi, yi)
+
+            def mv():
+                op.apply(xr, yr)
+                op.apply(xi, yi)
+
+            with ClockSampler(0) as clk:
+                t_pc = timed(pc, args.sweep_reps)
+                t_mv = timed(mv, args.sweep_reps)
+            H = nt // 2 + 1
+            B_pc = 2 * (16.0 * N + 64.0 * H * nx)   # SURVEY §8(d), two real vectors per complex input
+            B_mv = 2 * 16.0 * N
+            cpu = None
+            if ref is not None and N <= args.sweep_cpu_max:
+                p = ref.problem_1d(1.5, 1.0, h, nx, nt, dt)
+                p.build_plan()
+                xh = xr.cpu().numpy()
+                t0 = time.perf_counter()
+                p.pc_apply(xh)
+                t_ref = 2 * (time.perf_counter() - t0)
+                cpu = {"value": 1.0 / t_ref, "unit": "complex PC applies/s", "cores": os.cpu_count(),
+                       "kind": "reference", "sample": "one real apply_inverse of oracle/_ref, x2 for (Re, Im)"}
+            line = {"metric": "config-4 sweep: BC PC applies/s and matvecs/s (complex128 input)",
+                    "config": {"workload": "cfg4_sweep", "n_space": nx, "n_time": nt, "gamma": 1.5, "reps": args.sweep_reps,
+                               "input": "complex128 Gaussian = (Re, Im) real batch of 2"},
+                    "pc_applies_per_s": 1.0 / t_pc, "matvecs_per_s": 1.0 / t_mv,
+                    "pc_apply_gbs": B_pc / t_pc / 1e9, "matvec_gbs": B_mv / t_mv / 1e9,
+                    "pc_apply_hbm_frac": B_pc / t_pc / 1e9 / peak, "matvec_hbm_frac": B_mv / t_mv / 1e9 / peak,
+                    "peak_gbs": peak, "peak_source": peak_kind, "l2_resident": 32.0 * N < 100e6,
+                    "clocks": clk.summary(), "cpu_baseline": cpu}
+            print(json.dumps(line), flush=True)
+            del op, plan, xr, xi, yr, yi
+            torch.cuda.empty_cache()
+
+
 # ------------------------------------------------------------------------------------ our arm
 def main():
     ap = argparse.ArgumentParser()
@@ -212,7 +302,15 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--replicas", action="store_true",
                     help="N > 1: independent replicas instead of the frequency-sharded solve")
+    ap.add_argument("--sweep", action="store_true", help="BASELINE config 4: PC apply + matvec sweep (JSON per point)")
+    ap.add_argument("--sweep-nx", default="", help="comma list (default 1023..65535)")
+    ap.add_argument("--sweep-nt", default="", help="comma list (default 256..8192)")
+    ap.add_argument("--sweep-reps", type=int, default=50)
+    ap.add_argument("--sweep-cpu-max", type=float, default=4e6, help="largest N timed on the CPU reference")
     args = ap.parse_args()
+    if args.sweep:
+        run_sweep(args)
+        return
     args.steps_ref = max(1, min(args.steps, 3))
     args.warmup_ref = 0
 

@@ -17,11 +17,11 @@ cudaError_t launch_matvec_1d(const double* v, double* y, int n_space, int n_time
                              const double* eig_scaled, const double2* tw_base, cudaStream_t st,
                              int koff = 0);
 
-// M = 8192 (Ns up to 8191) on a 2-CTA cluster (kernels_mv.cu)
-cudaError_t launch_matvec_split13(const double* v, double* y, int n_space, int n_time, int koff,
-                                  const double* eig_scaled, const double2* tw_base, cudaStream_t st);
+// M = 8192 / 16384 (Ns up to 8191 / 16383) on a 2-CTA cluster (kernels_mv.cu)
+cudaError_t launch_matvec_split(const double* v, double* y, int n_space, int n_time, int log_m, int koff,
+                                const double* eig_scaled, const double2* tw_base, cudaStream_t st);
 
-// Ns + 1 = 16384 .. 65536 (kernels_large.cu): clusters of C = L/8192 CTAs (4, 8, 16)
+// Ns + 1 = 32768 .. 65536 (kernels_large.cu): clusters of C = L/8192 CTAs (8, 16)
 cudaError_t launch_matvec_large(const double* v, double* y, int n_space, int n_time, int log_m, int koff,
                                 const double* eig_scaled, const double2* tw_base, cudaStream_t st);
 

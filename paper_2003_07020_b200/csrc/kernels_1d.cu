@@ -454,9 +454,9 @@ cudaError_t launch_matvec_1d(const double* v, double* y, int n_space, int n_time
                              const double* eig_scaled, const double2* tw_base, cudaStream_t st,
                              int koff) {
   cudaError_t err = cudaSuccess;
-  if (log_m == 13)  // kernels_mv.cu: 2-CTA cluster, half-length FFTs
-    return launch_matvec_split13(v, y, n_space, n_time, koff, eig_scaled, tw_base, st);
-  if (log_m >= 14)  // kernels_large.cu: 4..16-CTA clusters
+  if (log_m == 13 || log_m == 14)  // kernels_mv.cu: 2-CTA cluster, half-length FFTs
+    return launch_matvec_split(v, y, n_space, n_time, log_m, koff, eig_scaled, tw_base, st);
+  if (log_m >= 15)  // kernels_large.cu: 8..16-CTA clusters
     return launch_matvec_large(v, y, n_space, n_time, log_m, koff, eig_scaled, tw_base, st);
   (void)err;
   return launch_matvec_rows(v, y, n_space, n_time, 1, n_space, log_m, eig_scaled, tw_base, st, koff);

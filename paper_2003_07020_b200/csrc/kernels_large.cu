@@ -199,11 +199,10 @@ cudaError_t launch_cl(K kernel, int C, int nclusters, cudaStream_t st, void** ar
 
 cudaError_t launch_matvec_large(const double* v, double* y, int n_space, int n_time, int log_m, int koff,
                                 const double* eig_scaled, const double2* tw_base, cudaStream_t st) {
-  // L = 2M = C * 8192
+  // L = 2M = C * 8192 (M = 16384 runs on kernels_mv.cu's packed 2-CTA split instead)
   const int C = 1 << (log_m + 1 - kLogS);
   void* args[] = {(void*)&v, (void*)&y, (void*)&n_space, (void*)&koff, (void*)&eig_scaled, (void*)&tw_base};
   switch (C) {
-    case 4: return launch_cl(k_matvec_cl<4>, 4, n_time, st, args);
     case 8: return launch_cl(k_matvec_cl<8>, 8, n_time, st, args);
     case 16: return launch_cl(k_matvec_cl<16>, 16, n_time, st, args);
     default: return cudaErrorInvalidValue;

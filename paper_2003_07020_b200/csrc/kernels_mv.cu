@@ -45,8 +45,9 @@ __device__ __forceinline__ void cpa8(void* smem, const void* gmem, bool valid) {
 }
 }  // namespace
 
+// two CTAs per SM for M = 8192 (4096-point halves); one for M = 16384 (8192-point halves)
 template <int LOGM>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((1 << (LOGM - 1)) / 16, 2)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((1 << (LOGM - 1)) / 16, LOGM <= 13 ? 2 : 1)
     k_matvec_split(const double* __restrict__ v, double* __restrict__ y, int ns, int koff,
                    const double* __restrict__ eig, const double2* __restrict__ twb) {
   constexpr int M = 1 << LOGM, H = M / 2, L = 2 * M, NT = H / 16, BS = padded(H);
@@ -165,15 +166,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((1 << (LOGM - 1)) / 
   cluster.sync();  // keep both buffers alive until the partner has read them
 }
 
-cudaError_t launch_matvec_split13(const double* v, double* y, int n_space, int n_time, int koff,
-                                  const double* eig_scaled, const double2* tw_base, cudaStream_t st) {
-  constexpr size_t smem = size_t(padded(4096)) * sizeof(double2);
-  cudaError_t err = cudaFuncSetAttribute(k_matvec_split<13>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+template <int LOGM>
+static cudaError_t launch_split(const double* v, double* y, int n_space, int n_time, int koff,
+                                const double* eig_scaled, const double2* tw_base, cudaStream_t st) {
+  constexpr int H = 1 << (LOGM - 1);
+  constexpr size_t smem = size_t(padded(H)) * sizeof(double2);
+  cudaError_t err = cudaFuncSetAttribute(k_matvec_split<LOGM>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
   if (err != cudaSuccess) return err;
-  err = cudaFuncSetAttribute(k_matvec_split<13>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  err = cudaFuncSetAttribute(k_matvec_split<LOGM>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   if (err != cudaSuccess) return err;
-  k_matvec_split<13><<<2 * n_time, 256, smem, st>>>(v, y, n_space, koff, eig_scaled, tw_base);
+  k_matvec_split<LOGM><<<2 * n_time, H / 16, smem, st>>>(v, y, n_space, koff, eig_scaled, tw_base);
   return cudaGetLastError();
+}
+
+cudaError_t launch_matvec_split(const double* v, double* y, int n_space, int n_time, int log_m, int koff,
+                                const double* eig_scaled, const double2* tw_base, cudaStream_t st) {
+  if (log_m == 13) return launch_split<13>(v, y, n_space, n_time, koff, eig_scaled, tw_base, st);
+  if (log_m == 14) return launch_split<14>(v, y, n_space, n_time, koff, eig_scaled, tw_base, st);
+  return cudaErrorInvalidValue;
 }
 
 }  // namespace fpc
