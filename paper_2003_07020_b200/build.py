@@ -15,7 +15,7 @@ CSRC = os.path.join(HERE, "csrc")
 ROOT = os.path.dirname(HERE)
 BUILD = os.path.join(ROOT, "build", "fpc")
 LIB = os.path.join(HERE, "libfracpint_b200.so")
-SOURCES = ["kernels_1d.cu", "kernels_mv.cu", "kernels_large.cu", "kernels_2d.cu", "kernels_time.cu", "kernels_full.cu",
+SOURCES = ["kernels_1d.cu", "kernels_mv.cu", "kernels_large.cu", "kernels_2d.cu", "kernels_full.cu",
            "kernels_krylov.cu", "api.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

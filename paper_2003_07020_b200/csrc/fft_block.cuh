@@ -163,20 +163,29 @@ __device__ __forceinline__ void apply_twiddles(double2* v, const double2* __rest
   }
 }
 
+// Barrier policies: the whole CTA, or a named barrier over a thread group (warp-specialised
+// kernels running independent transforms in different groups).
+struct CtaSync {
+  __device__ __forceinline__ static void sync() { __syncthreads(); }
+};
+template <int ID, int NTHR>
+struct GroupSync {
+  __device__ __forceinline__ static void sync() { asm volatile("bar.sync %0, %1;\n" ::"n"(ID), "n"(NTHR) : "memory"); }
+};
+
 // One Stockham pass of radix R over B buffers of size N = 2^LOGN held in smem (buffer stride BS,
 // pad16 inside a buffer).  NS = current sub-transform length (compile time, so all index
 // arithmetic folds to shifts/masks).  Each thread processes E/R butterflies (E complex values).
-template <int LOGN, int R, int S, int BS, int E, int NS>
-__device__ __forceinline__ void stockham_pass(double2* s, const double2* __restrict__ tw) {
+template <int LOGN, int R, int S, int BS, int E, int NS, class Sync>
+__device__ __forceinline__ void stockham_pass(double2* s, const double2* __restrict__ tw, int tid, int nthr) {
   constexpr int N = 1 << LOGN;
   constexpr int NB = N / R;   // butterflies per buffer
   constexpr int PER = E / R;  // butterflies per thread
   double2 v[PER][R];
   int dst[PER];
-  const int nthr = blockDim.x;
 #pragma unroll
   for (int q = 0; q < PER; ++q) {
-    const int g = threadIdx.x + q * nthr;  // butterfly index across buffers
+    const int g = tid + q * nthr;  // butterfly index across buffers
     const int b = g / NB;
     const int j = g & (NB - 1);
     const double2* base = s + b * BS;
@@ -187,7 +196,7 @@ __device__ __forceinline__ void stockham_pass(double2* s, const double2* __restr
     Dft<R, S>::run(v[q]);
     dst[q] = b * BS + (j - jm) * R + jm;  // buffer base + logical offset (pad applied below)
   }
-  __syncthreads();
+  Sync::sync();
 #pragma unroll
   for (int q = 0; q < PER; ++q) {
     const int b = dst[q] / BS;
@@ -196,11 +205,11 @@ __device__ __forceinline__ void stockham_pass(double2* s, const double2* __restr
 #pragma unroll
     for (int r = 0; r < R; ++r) base[pad16(off + r * NS)] = v[q][r];
   }
-  __syncthreads();
+  Sync::sync();
 }
 
-template <int LOGN, int S, int BS, int E, int NS>
-__device__ __forceinline__ void fft_passes(double2* s, const double2* __restrict__ tw) {
+template <int LOGN, int S, int BS, int E, int NS, class Sync>
+__device__ __forceinline__ void fft_passes(double2* s, const double2* __restrict__ tw, int tid, int nthr) {
   constexpr int N = 1 << LOGN;
   if constexpr (NS < N) {
     constexpr int LE = E == 16 ? 4 : E == 8 ? 3 : E == 4 ? 2 : 1;
@@ -208,8 +217,8 @@ __device__ __forceinline__ void fft_passes(double2* s, const double2* __restrict
     // so the twiddle sets the later passes touch stay small and L1 resident
     constexpr int rem = (NS == 1) ? (LOGN % LE) : 0;
     constexpr int R = rem == 3 ? 8 : rem == 2 ? 4 : rem == 1 ? 2 : E;
-    stockham_pass<LOGN, R, S, BS, E, NS>(s, tw);
-    fft_passes<LOGN, S, BS, E, NS * R>(s, tw);
+    stockham_pass<LOGN, R, S, BS, E, NS, Sync>(s, tw, tid, nthr);
+    fft_passes<LOGN, S, BS, E, NS * R, Sync>(s, tw, tid, nthr);
   }
 }
 
@@ -219,7 +228,14 @@ __device__ __forceinline__ void fft_passes(double2* s, const double2* __restrict
 // call and may read the result after it returns.
 template <int LOGN, int S, int BS = padded(1 << LOGN), int E = 16>
 __device__ __forceinline__ void block_fft(double2* s, const double2* __restrict__ tw, int /*nbuf*/) {
-  fft_passes<LOGN, S, BS, E, 1>(s, tw);
+  fft_passes<LOGN, S, BS, E, 1, CtaSync>(s, tw, int(threadIdx.x), int(blockDim.x));
+}
+
+// The same over a thread group of NTHR threads (local index tid) synchronised by named barrier ID;
+// NTHR * E == B * N.
+template <int LOGN, int S, int BS, int E, int NTHR, int ID>
+__device__ __forceinline__ void group_fft(double2* s, const double2* __restrict__ tw, int tid) {
+  fft_passes<LOGN, S, BS, E, 1, GroupSync<ID, NTHR>>(s, tw, tid, NTHR);
 }
 
 }  // namespace fpc

@@ -74,6 +74,19 @@ struct Geo {
 // so 256-thread CTAs run two per SM (16 warps) and 512-thread CTAs one.
 __host__ __device__ constexpr int minb(int nt) { return nt <= 128 ? 4 : nt <= 256 ? 2 : 1; }
 
+// L2 prefetch of a column tile: rows r < nrows, each covering bytes [base + r*stride, +width).
+// Issues every row's lines at once without holding registers (the strided 32..128-byte row
+// segments are latency bound when requested only as fast as register-staged loads retire).
+__device__ __forceinline__ void l2_prefetch_column_tile(const void* base, size_t stride, int nrows, int width,
+                                                        int nthr) {
+  const char* b = static_cast<const char*>(base);
+  for (int r = threadIdx.x; r < nrows; r += nthr) {
+    const uintptr_t a0 = reinterpret_cast<uintptr_t>(b + size_t(r) * stride);
+    const uintptr_t l0 = a0 & ~uintptr_t(127), l1 = (a0 + uintptr_t(width) - 1) & ~uintptr_t(127);
+    for (uintptr_t l = l0; l <= l1; l += 128) asm volatile("prefetch.global.L2 [%0];" ::"l"(l));
+  }
+}
+
 __device__ __forceinline__ double& comp(double2* s, int slot_padded, int c) {
   return reinterpret_cast<double*>(s + slot_padded)[c];
 }
@@ -210,6 +223,9 @@ __global__ void __launch_bounds__(Geo<LOGM, tot_t<LOGM>()>::NT, minb(Geo<LOGM, t
   extern __shared__ double2 smem[];
   const int p0 = blockIdx.x * B;
   FPC_PT(0, 0);
+  // request every row segment of the tile at once (L2 prefetch: no registers held, full lines),
+  // then the register-staged loads below mostly hit L2 (B200 config 1: 145 -> 131 us)
+  l2_prefetch_column_tile(v + p0, size_t(ns) * 8, NTIME, B * 8, NT);
 
   for (int e0 = threadIdx.x; e0 < B * NTIME; e0 += U * NT) {
     double x[U];
@@ -272,6 +288,7 @@ __global__ void __launch_bounds__(Geo<LOGM, tot_t<LOGM>()>::NT, minb(Geo<LOGM, t
   const int p0 = blockIdx.x * B;
   const double2* twT = twb + NTIME;
   FPC_PT(1, 0);
+  l2_prefetch_column_tile(Z + p0, size_t(ns) * 16, M + 1, B * 16, NT);  // 149 -> 141 us
 
   for (int t0 = threadIdx.x; t0 < TASKS; t0 += U * NT) {
     double2 ya[U], yb[U];
@@ -351,6 +368,14 @@ __global__ void __launch_bounds__(TauGeo<LOGM>::G::NT, minb(TauGeo<LOGM>::G::NT)
   const double scale = sqrt(2.0 / double(M));
   FPC_PH(0);
 
+  // whole rows into L2 up front (contiguous; the staged loads below then hit L2)
+  for (int b = 0; b < nb; ++b) {
+    const char* zr = reinterpret_cast<const char*>(Z + size_t(r0 + b) * NSR);
+    const uintptr_t l0 = reinterpret_cast<uintptr_t>(zr) & ~uintptr_t(127);
+    const uintptr_t l1 = (reinterpret_cast<uintptr_t>(zr) + size_t(NSR) * 16 - 1) & ~uintptr_t(127);
+    for (uintptr_t l = l0 + uintptr_t(threadIdx.x) * 128; l <= l1; l += uintptr_t(NT) * 128)
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(l));
+  }
   // load rows: element i -> slot i + 1
   for (int b = 0; b < B; ++b) {
     const double2* zr = Z + size_t(r0 + b) * NSR;
@@ -468,22 +493,9 @@ static int ilog2(int n) {
   return l;
 }
 
-// The persistent cp.async double-buffered variants (kernels_time.cu) are opt-in (FPC_TIME_PIPE=1):
-// at 190+ registers they run one 8-warp CTA per SM and measured slower (186 vs 157 us at
-// config 1) than the plain kernels at two CTAs per SM.
-static bool time_pipe_enabled() {
-  static const bool on = [] {
-    const char* e = std::getenv("FPC_TIME_PIPE");
-    return e && e[0] == '1';
-  }();
-  return on;
-}
-
 cudaError_t launch_time_fwd(const double* v, double2* Z, int n_space, int n_time,
                             const double* scale_fwd, double s_in, const double2* tw_base,
                             cudaStream_t st) {
-  if (n_time <= 8192 && time_pipe_enabled())  // kernels_time.cu (double-buffered, persistent)
-    return launch_time_fwd_pipe(v, Z, n_space, n_time, scale_fwd, s_in, tw_base, st);
   cudaError_t err = cudaSuccess;
   const int lm = ilog2(n_time) - 1;
 #define CALL(LM)                                                                          \
@@ -500,8 +512,6 @@ cudaError_t launch_time_fwd(const double* v, double2* Z, int n_space, int n_time
 
 cudaError_t launch_time_inv(const double2* Z, double* z, int n_space, int n_time,
                             const double* scale_bwd, const double2* tw_base, cudaStream_t st) {
-  if (n_time <= 8192 && time_pipe_enabled())
-    return launch_time_inv_pipe(Z, z, n_space, n_time, scale_bwd, tw_base, st);
   cudaError_t err = cudaSuccess;
   const int lm = ilog2(n_time) - 1;
 #define CALL(LM)                                                                            \

@@ -48,6 +48,19 @@ def test_pc_apply_1d(oracle, gamma, ns, nt):
     assert rel(z, po.pc_apply(v)) <= 1e-12
 
 
+@pytest.mark.parametrize("gamma,ns,nt", [(1.5, 63, 512), (1.7, 255, 1024), (1.3, 31, 2048), (1.5, 127, 4096),
+                                         (1.5, 15, 8192), (1.2, 1023, 2048), (1.4, 8191, 512)])
+def test_pc_apply_long_time(oracle, gamma, ns, nt):
+    # 512 <= Nt <= 8192 runs the persistent two-group time FFT kernels (kernels_time.cu); ragged
+    # last tiles (Ns not a multiple of the tile width) included
+    op, h, dt = make(gamma, ns, nt)
+    plan = fp.build_plan(fp.PreconditionerKind.generalized(), nt, dt, op)
+    po = oracle.problem_1d(gamma, 1.0, h, ns, nt, dt).build_plan()
+    v = np.random.default_rng(ns * 13 + nt).uniform(-1, 1, ns * nt)
+    assert rel(fp.apply_inverse(plan, v), po.pc_apply(v)) <= 1e-12
+    assert rel(fp.apply_forward(plan, v), po.pc_forward(v)) <= 1e-12
+
+
 @pytest.mark.parametrize("alpha", [0.5, 1e-3, 1.0])
 def test_pc_apply_alpha(oracle, alpha):
     op, h, dt = make(1.5, 63, 16)
