@@ -29,7 +29,73 @@ namespace fpc {
 // slot j, slot 0 ignored) and an M-slot scratch buffer at h + b*BH.  Output: DST(f)_i * scale at
 // slot i + OUT_SHIFT of the N-slot buffer (slot 0 zeroed when OUT_SHIFT = 1, so the buffer is
 // again a valid input).
-template <int LOGN, int BS, int BH, int OUT_SHIFT>
+// One row per CTA with the N-point FFT's radix-2 remainder pass (N = 2^(4k+1)) folded into the
+// pre-twiddle: the quadruple (j, N-j, M-j, M+j) holds both radix-2 pairs (j, j+M) and (M-j, N-j),
+// so the pre-phase writes the first Stockham pass's outputs directly (one shared-memory pass and
+// two barriers less per DST).
+template <int LOGN, int BH>
+__device__ __forceinline__ void dst_pre_folded(double2* r, double2* hv, const double2* __restrict__ tw2N) {
+  constexpr int N = 1 << LOGN, M = N / 2, NT = N / 16;
+  constexpr int KQ = (M / 2) / NT;  // quadruples j < M/2 per thread; j = M/2 goes to thread 0
+  static_assert(KQ * NT == M / 2, "quadruple count must divide the thread count");
+  double2 o[KQ][4], mid[2];
+#pragma unroll
+  for (int u = 0; u < KQ; ++u) {
+    const int j = int(threadIdx.x) + u * NT;
+    if (j == 0) {  // y_0 = 0, y_M = 2 f_M, V_0 = f_M
+      const double2 fm = r[pad16(M)];
+      o[u][0] = cscale(fm, 2.0);
+      o[u][1] = cscale(fm, -2.0);
+      hv[0] = fm;
+      continue;
+    }
+    const double2 wj = __ldg(tw2N + j);
+    const double2 wm = __ldg(tw2N + M - j);
+    const double2 f1 = r[pad16(j)], f2 = r[pad16(N - j)];
+    const double2 g1 = r[pad16(M - j)], g2 = r[pad16(M + j)];
+    const double2 sj = cadd(f1, f2), dj = csub(f1, f2), sm = cadd(g1, g2), dm = csub(g1, g2);
+    const double sinj = -wj.y, sinm = -wm.y;
+    const double2 yj = make_double2(fma(sinj, sj.x, 0.5 * dj.x), fma(sinj, sj.y, 0.5 * dj.y));
+    const double2 yNj = make_double2(fma(sinj, sj.x, -0.5 * dj.x), fma(sinj, sj.y, -0.5 * dj.y));
+    const double2 yMj = make_double2(fma(sinm, sm.x, 0.5 * dm.x), fma(sinm, sm.y, 0.5 * dm.y));
+    const double2 yPj = make_double2(fma(sinm, sm.x, -0.5 * dm.x), fma(sinm, sm.y, -0.5 * dm.y));
+    o[u][0] = cadd(yj, yPj);  // pair (j, j+M)
+    o[u][1] = csub(yj, yPj);
+    o[u][2] = cadd(yMj, yNj);  // pair (M-j, N-j)
+    o[u][3] = csub(yMj, yNj);
+    hv[pad16(j)] = cscale(cmul(cconj(wj), csub(sm, mul_si<1>(sj))), 0.5);
+    hv[pad16(M - j)] = cscale(cmul(cconj(wm), csub(sj, mul_si<1>(sm))), 0.5);
+  }
+  if (threadIdx.x == 0) {  // j = M/2: its own mirror, pair (M/2, 3M/2)
+    constexpr int j = M / 2;
+    const double2 wj = __ldg(tw2N + j);
+    const double2 f1 = r[pad16(j)], f2 = r[pad16(N - j)];
+    const double2 sj = cadd(f1, f2), dj = csub(f1, f2);
+    const double sinj = -wj.y;
+    const double2 yj = make_double2(fma(sinj, sj.x, 0.5 * dj.x), fma(sinj, sj.y, 0.5 * dj.y));
+    const double2 yNj = make_double2(fma(sinj, sj.x, -0.5 * dj.x), fma(sinj, sj.y, -0.5 * dj.y));
+    mid[0] = cadd(yj, yNj);
+    mid[1] = csub(yj, yNj);
+    hv[pad16(j)] = cscale(cmul(cconj(wj), csub(sj, mul_si<1>(sj))), 0.5);
+  }
+  __syncthreads();  // every f has been read before the pass outputs overwrite the row
+#pragma unroll
+  for (int u = 0; u < KQ; ++u) {
+    const int j = int(threadIdx.x) + u * NT;
+    r[pad16(2 * j)] = o[u][0];
+    r[pad16(2 * j + 1)] = o[u][1];
+    if (j != 0) {
+      r[pad16(2 * (M - j))] = o[u][2];
+      r[pad16(2 * (M - j) + 1)] = o[u][3];
+    }
+  }
+  if (threadIdx.x == 0) {
+    r[pad16(M)] = mid[0];
+    r[pad16(M + 1)] = mid[1];
+  }
+}
+
+template <int LOGN, int BS, int BH, int OUT_SHIFT, bool FOLD = false>
 __device__ __forceinline__ void block_dst(double2* s, double2* h, const double2* __restrict__ twb,
                                           double scale) {
   constexpr int N = 1 << LOGN, M = N / 2;
@@ -39,6 +105,16 @@ __device__ __forceinline__ void block_dst(double2* s, double2* h, const double2*
   const int nthr = blockDim.x;
   const int nrow = nthr / TPB;
   const double2* tw2N = twb + 2 * N;  // e^{-i pi j/N}
+  if constexpr (FOLD) {
+    static_assert(LOGN % 4 == 1 && LOGN >= 5, "fold needs N = 2 * 16^k");
+    dst_pre_folded<LOGN, BH>(s, h, tw2N);
+    __syncthreads();
+    FPC_DST_PH(0);
+    fft_passes<LOGN, 1, BS, E, 2, CtaSync>(s, twb + N, int(threadIdx.x), nthr);
+    FPC_DST_PH(1);
+    block_fft<LOGN - 1, 1, BH, E / 2>(h, twb + M, 0);
+    FPC_DST_PH(2);
+  } else {
   // 1. pre: quadruples (j, N-j, M-j, M+j), j = 1..M/2 (degenerate at j = M/2 and for j = M)
   for (int t = threadIdx.x; t < nrow * (M / 2 + 1); t += nthr) {
     const int b = t / (M / 2 + 1), j = t - b * (M / 2 + 1);
@@ -81,6 +157,7 @@ __device__ __forceinline__ void block_dst(double2* s, double2* h, const double2*
   FPC_DST_PH(1);
   block_fft<LOGN - 1, 1, BH, E / 2>(h, twb + M, 0);
   FPC_DST_PH(2);
+  }
 
   // 2. post: thread handles k = tb*KP .. tb*KP + KP-1 of its row
   const int b = threadIdx.x / TPB, tb = threadIdx.x - b * TPB;

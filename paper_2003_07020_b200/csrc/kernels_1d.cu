@@ -397,7 +397,7 @@ __global__ void __launch_bounds__(TauGeo<LOGM>::G::NT, minb(TauGeo<LOGM>::G::NT)
   __syncthreads();
   FPC_PH(1);
   if constexpr (MODE != 0) {
-    block_dst<LOGM, BS, BH, 1>(smem, hbuf, twb, scale);
+    block_dst<LOGM, BS, BH, 1, LOGM == 13>(smem, hbuf, twb, scale);
     FPC_PH(2);
     // divide by the shifted tau eigenvalues (slot i + 1 <-> index i)
     for (int b = 0; b < B; ++b) {
@@ -417,7 +417,7 @@ __global__ void __launch_bounds__(TauGeo<LOGM>::G::NT, minb(TauGeo<LOGM>::G::NT)
     __syncthreads();
   }
   FPC_PH(3);
-  block_dst<LOGM, BS, BH, 0>(smem, hbuf, twb, scale);
+  block_dst<LOGM, BS, BH, 0, LOGM == 13>(smem, hbuf, twb, scale);
   FPC_PH(4);
 
   // store rows (slot i <-> index i), coalesced
