@@ -33,8 +33,12 @@ namespace fpc {
 // pre-twiddle: the quadruple (j, N-j, M-j, M+j) holds both radix-2 pairs (j, j+M) and (M-j, N-j),
 // so the pre-phase writes the first Stockham pass's outputs directly (one shared-memory pass and
 // two barriers less per DST).
+// gsrc != nullptr: the row is read straight from global memory (f_j = gsrc[j-1]) instead of the
+// buffer (saves the staging pass of the first DST of a tau solve)
 template <int LOGN, int BH>
-__device__ __forceinline__ void dst_pre_folded(double2* r, double2* hv, const double2* __restrict__ tw2N) {
+__device__ __forceinline__ void dst_pre_folded(double2* r, double2* hv, const double2* __restrict__ tw2N,
+                                               const double2* gsrc) {
+  auto f = [&](int j) -> double2 { return gsrc ? gsrc[j - 1] : r[pad16(j)]; };
   constexpr int N = 1 << LOGN, M = N / 2, NT = N / 16;
   constexpr int KQ = (M / 2) / NT;  // quadruples j < M/2 per thread; j = M/2 goes to thread 0
   static_assert(KQ * NT == M / 2, "quadruple count must divide the thread count");
@@ -43,7 +47,7 @@ __device__ __forceinline__ void dst_pre_folded(double2* r, double2* hv, const do
   for (int u = 0; u < KQ; ++u) {
     const int j = int(threadIdx.x) + u * NT;
     if (j == 0) {  // y_0 = 0, y_M = 2 f_M, V_0 = f_M
-      const double2 fm = r[pad16(M)];
+      const double2 fm = f(M);
       o[u][0] = cscale(fm, 2.0);
       o[u][1] = cscale(fm, -2.0);
       hv[0] = fm;
@@ -51,8 +55,8 @@ __device__ __forceinline__ void dst_pre_folded(double2* r, double2* hv, const do
     }
     const double2 wj = __ldg(tw2N + j);
     const double2 wm = __ldg(tw2N + M - j);
-    const double2 f1 = r[pad16(j)], f2 = r[pad16(N - j)];
-    const double2 g1 = r[pad16(M - j)], g2 = r[pad16(M + j)];
+    const double2 f1 = f(j), f2 = f(N - j);
+    const double2 g1 = f(M - j), g2 = f(M + j);
     const double2 sj = cadd(f1, f2), dj = csub(f1, f2), sm = cadd(g1, g2), dm = csub(g1, g2);
     const double sinj = -wj.y, sinm = -wm.y;
     const double2 yj = make_double2(fma(sinj, sj.x, 0.5 * dj.x), fma(sinj, sj.y, 0.5 * dj.y));
@@ -69,7 +73,7 @@ __device__ __forceinline__ void dst_pre_folded(double2* r, double2* hv, const do
   if (threadIdx.x == 0) {  // j = M/2: its own mirror, pair (M/2, 3M/2)
     constexpr int j = M / 2;
     const double2 wj = __ldg(tw2N + j);
-    const double2 f1 = r[pad16(j)], f2 = r[pad16(N - j)];
+    const double2 f1 = f(j), f2 = f(N - j);
     const double2 sj = cadd(f1, f2), dj = csub(f1, f2);
     const double sinj = -wj.y;
     const double2 yj = make_double2(fma(sinj, sj.x, 0.5 * dj.x), fma(sinj, sj.y, 0.5 * dj.y));
@@ -97,7 +101,7 @@ __device__ __forceinline__ void dst_pre_folded(double2* r, double2* hv, const do
 
 template <int LOGN, int BS, int BH, int OUT_SHIFT, bool FOLD = false>
 __device__ __forceinline__ void block_dst(double2* s, double2* h, const double2* __restrict__ twb,
-                                          double scale) {
+                                          double scale, const double2* gsrc = nullptr) {
   constexpr int N = 1 << LOGN, M = N / 2;
   constexpr int E = N < 16 ? N : 16;  // complex values per thread in the N-point FFT
   constexpr int TPB = N / E;          // threads per row
@@ -107,7 +111,7 @@ __device__ __forceinline__ void block_dst(double2* s, double2* h, const double2*
   const double2* tw2N = twb + 2 * N;  // e^{-i pi j/N}
   if constexpr (FOLD) {
     static_assert(LOGN % 4 == 1 && LOGN >= 5, "fold needs N = 2 * 16^k");
-    dst_pre_folded<LOGN, BH>(s, h, tw2N);
+    dst_pre_folded<LOGN, BH>(s, h, tw2N, gsrc);
     __syncthreads();
     FPC_DST_PH(0);
     fft_passes<LOGN, 1, BS, E, 2, CtaSync>(s, twb + N, int(threadIdx.x), nthr);

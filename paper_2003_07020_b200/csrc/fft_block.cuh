@@ -231,6 +231,36 @@ __device__ __forceinline__ void block_fft(double2* s, const double2* __restrict_
   fft_passes<LOGN, S, BS, E, 1, CtaSync>(s, tw, int(threadIdx.x), int(blockDim.x));
 }
 
+// Full transform of one buffer whose input is produced by load(i) (i = logical index, e.g. straight
+// from global memory): the first Stockham pass (NS = 1, no twiddles) takes its operands from the
+// loader instead of shared memory, which saves the staging write, one read pass and a barrier.
+// Requires blockDim.x * E == N.  Ends with the result in s (natural order).
+template <int LOGN, int S, int BS, int E, class Load>
+__device__ __forceinline__ void block_fft_from(double2* s, const double2* __restrict__ tw, Load load) {
+  constexpr int N = 1 << LOGN;
+  constexpr int LE = E == 16 ? 4 : E == 8 ? 3 : E == 4 ? 2 : 1;
+  constexpr int rem = LOGN % LE;
+  constexpr int R = rem == 3 ? 8 : rem == 2 ? 4 : rem == 1 ? 2 : E;
+  constexpr int NB = N / R, PER = E / R;
+  const int tid = int(threadIdx.x), nthr = int(blockDim.x);
+  double2 v[PER][R];
+#pragma unroll
+  for (int q = 0; q < PER; ++q) {
+    const int j = tid + q * nthr;
+#pragma unroll
+    for (int r = 0; r < R; ++r) v[q][r] = load(j + r * NB);
+  }
+#pragma unroll
+  for (int q = 0; q < PER; ++q) {
+    const int j = tid + q * nthr;
+    Dft<R, S>::run(v[q]);
+#pragma unroll
+    for (int r = 0; r < R; ++r) s[pad16(j * R + r)] = v[q][r];
+  }
+  __syncthreads();
+  fft_passes<LOGN, S, BS, E, R, CtaSync>(s, tw, tid, nthr);
+}
+
 // The same over a thread group of NTHR threads (local index tid) synchronised by named barrier ID;
 // NTHR * E == B * N.
 template <int LOGN, int S, int BS, int E, int NTHR, int ID>

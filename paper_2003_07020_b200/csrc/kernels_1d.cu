@@ -376,8 +376,10 @@ __global__ void __launch_bounds__(TauGeo<LOGM>::G::NT, minb(TauGeo<LOGM>::G::NT)
     for (uintptr_t l = l0 + uintptr_t(threadIdx.x) * 128; l <= l1; l += uintptr_t(NT) * 128)
       asm volatile("prefetch.global.L2 [%0];" ::"l"(l));
   }
+  // one row, folded DST: the first DST reads the row from global memory directly
+  constexpr bool kDirect = (LOGM == 13 && B == 1 && MODE != 0);
   // load rows: element i -> slot i + 1
-  for (int b = 0; b < B; ++b) {
+  for (int b = 0; b < (kDirect ? 0 : B); ++b) {
     const double2* zr = Z + size_t(r0 + b) * NSR;
     double2* s = smem + b * BS;
     for (int i0 = threadIdx.x; i0 < NSR; i0 += U * NT) {
@@ -397,7 +399,7 @@ __global__ void __launch_bounds__(TauGeo<LOGM>::G::NT, minb(TauGeo<LOGM>::G::NT)
   __syncthreads();
   FPC_PH(1);
   if constexpr (MODE != 0) {
-    block_dst<LOGM, BS, BH, 1, LOGM == 13>(smem, hbuf, twb, scale);
+    block_dst<LOGM, BS, BH, 1, LOGM == 13>(smem, hbuf, twb, scale, kDirect ? Z + size_t(r0) * NSR : nullptr);
     FPC_PH(2);
     // divide by the shifted tau eigenvalues (slot i + 1 <-> index i)
     for (int b = 0; b < B; ++b) {

@@ -11,7 +11,8 @@
 // Memory phases are asynchronous or batched so their latency is paid once per CTA (measured with
 // clock64 phase stamps: the first version spent ~60% of its cycles waiting on loads and the
 // cluster barrier):
-//   * the packed FFT input lands by cp.async (8-byte granules, zero-filled past Ns);
+//   * the packed FFT input is read from global memory straight into the first radix-16 pass
+//     (block_fft_from: no shared-memory staging pass);
 //   * the post-twiddle of the odd half is applied by whichever rank assembles the output, so the
 //     two ranks reach the cluster barrier with equal work;
 //   * the BDF2 stencil inputs, both spectral halves and the twiddles of a thread's outputs are all
@@ -38,12 +39,6 @@ extern "C" int fpc_debug_phases_mv(long long* out, int nblocks) {
   } while (0)
 #endif
 
-namespace {
-__device__ __forceinline__ void cpa8(void* smem, const void* gmem, bool valid) {
-  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(valid ? 8 : 0));
-}
-}  // namespace
 
 // two CTAs per SM for M = 8192 (4096-point halves); one for M = 16384 (8192-point halves)
 template <int LOGM>
@@ -60,19 +55,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((1 << (LOGM - 1)) / 
   const double2* twM = twb + M;
   FPC_PHM(0);
 
-  // 1. packed input by cp.async: real index i -> slot i/2, component i%2
-  for (int i = threadIdx.x; i < 2 * H; i += NT) {
-    double* dst = reinterpret_cast<double*>(smem + pad16(i >> 1)) + (i & 1);
-    cpa8(dst, i < ns ? vk + i : vk, i < ns);
-  }
-  asm volatile("cp.async.commit_group;\n" ::);
-  asm volatile("cp.async.wait_group 0;\n" ::);
-  __syncthreads();
-  if (q == 1)  // odd bins: b_m = z_m e^{-2 pi i m/M}
-    for (int m = threadIdx.x; m < H; m += NT) smem[pad16(m)] = cmul(smem[pad16(m)], __ldg(twM + m));
-  __syncthreads();
+  // 1. forward FFT of the packed input z_m = v[2m] + i v[2m+1] (rank 1: b_m = z_m e^{-2 pi i m/M},
+  //    the odd bins); the first radix pass takes its operands straight from global memory
   FPC_PHM(1);
-  block_fft<LOGM - 1, -1, BS, 16>(smem, twb + H, 1);
+  auto load_z = [&](int m) -> double2 {
+    const int i = 2 * m;
+    const double2 zm = make_double2(i < ns ? vk[i] : 0.0, i + 1 < ns ? vk[i + 1] : 0.0);
+    return q == 1 ? cmul(zm, __ldg(twM + m)) : zm;
+  };
+  block_fft_from<LOGM - 1, -1, BS, 16>(smem, twb + H, load_z);
   FPC_PHM(2);
 
   // 2. eigenvalue product on (kappa, M - kappa) pairs; slot j of rank q holds bin 2j + q.
