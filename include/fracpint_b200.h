@@ -15,6 +15,7 @@
  *   fpc_pc_apply           <- apply_inverse(plan, v, out, sw)   alpha_circulant.hpp:206
  *   fpc_pc_forward         <- apply_forward(plan, v, out)       alpha_circulant.hpp:212
  *   fpc_gmres              <- gmres_right(n, A, P^{-1}, b, cfg) krylov.hpp:84 (+ restart m)
+ *   fpc_bicgstab           <- bicgstab_left(n, A, P^{-1}, b, cfg) krylov.hpp:204
  *
  * Plain pointers and sizes only.  Vectors are time-major fp64, v[k*n_space + p] (2D: p = ix*n+iy,
  * x slow; problems.hpp:164-165).  `where` = FPC_HOST (pointers are host memory: copied in and out,
@@ -59,7 +60,8 @@ typedef struct {
   int sweep;
 } fpc_solver_config;
 
-/* SolveReport (krylov.hpp:30-37). */
+/* SolveReport (krylov.hpp:30-37).  iterations_exact is the reference's double `iterations`
+ * (BiCGSTAB converging at a half step reports k + 0.5); `iterations` is its integer part. */
 typedef struct {
   int converged;
   int iterations;
@@ -69,6 +71,7 @@ typedef struct {
   double true_relative_residual;
   double seconds;
   int history_len;
+  double iterations_exact;
 } fpc_report;
 
 int fpc_abi_version(void);
@@ -109,6 +112,10 @@ int fpc_pc_forward(fpc_plan_t plan, const double* v, double* out, int where);
 /* right-preconditioned GMRES on the plan's operator, x0 = 0 */
 int fpc_gmres(fpc_plan_t plan, const double* b, double* x, const fpc_solver_config* cfg,
               fpc_report* report, double* history, int history_cap, int where);
+
+/* left-preconditioned BiCGSTAB on the plan's operator, x0 = 0 (cfg->restart is ignored) */
+int fpc_bicgstab(fpc_plan_t plan, const double* b, double* x, const fpc_solver_config* cfg,
+                 fpc_report* report, double* history, int history_cap, int where);
 
 /* shard level: the per-rank pieces of the frequency-sharded multi-GPU solve
  * (paper_2003_07020_b200/distributed.py).  Device pointers, stream-ordered; sizes are local.

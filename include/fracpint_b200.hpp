@@ -231,6 +231,19 @@ struct KrylovResult {
   SolveReport report;
 };
 
+namespace detail {
+inline void fill_report(SolveReport& out, const fpc_report& rep, const std::vector<double>& hist) {
+  out.converged = rep.converged != 0;
+  out.iterations = rep.iterations_exact;
+  out.residual_history.assign(hist.begin(),
+                              hist.begin() + std::min<std::size_t>(rep.history_len, hist.size()));
+  out.final_relative_residual = rep.final_relative_residual;
+  out.true_relative_residual = rep.true_relative_residual;
+  out.seconds = rep.seconds;
+  out.restarts = rep.restarts;
+}
+}  // namespace detail
+
 // device-resident right-preconditioned GMRES (krylov.hpp:83-192), x0 = 0
 template <class Jacobian>
 KrylovResult gmres_right(const AllAtOnceOperator<Jacobian>& op, const AlphaCirculantPlan& plan,
@@ -243,14 +256,23 @@ KrylovResult gmres_right(const AllAtOnceOperator<Jacobian>& op, const AlphaCircu
   std::vector<double> hist(std::size_t(std::max(cfg.max_iter, 1)) + 1);
   detail::check(fpc_gmres(plan.handle(), b.data(), r.x.data(), &c, &rep, hist.data(),
                           int(hist.size()), FPC_HOST));
-  r.report.converged = rep.converged != 0;
-  r.report.iterations = rep.iterations;
-  r.report.residual_history.assign(hist.begin(),
-                                   hist.begin() + std::min<std::size_t>(rep.history_len, hist.size()));
-  r.report.final_relative_residual = rep.final_relative_residual;
-  r.report.true_relative_residual = rep.true_relative_residual;
-  r.report.seconds = rep.seconds;
-  r.report.restarts = rep.restarts;
+  detail::fill_report(r.report, rep, hist);
+  return r;
+}
+
+// device-resident left-preconditioned BiCGSTAB (krylov.hpp:204-280), x0 = 0
+template <class Jacobian>
+KrylovResult bicgstab_left(const AllAtOnceOperator<Jacobian>& op, const AlphaCirculantPlan& plan,
+                           std::span<const double> b, const SolverConfig& cfg = {}) {
+  if (b.size() != op.dim()) throw std::invalid_argument("bicgstab_left: size mismatch");
+  KrylovResult r;
+  r.x.assign(op.dim(), 0.0);
+  fpc_solver_config c{cfg.tol, cfg.max_iter, 0, FPC_SWEEP_HALF};
+  fpc_report rep{};
+  std::vector<double> hist(2 * std::size_t(std::max(cfg.max_iter, 1)) + 2);
+  detail::check(fpc_bicgstab(plan.handle(), b.data(), r.x.data(), &c, &rep, hist.data(),
+                             int(hist.size()), FPC_HOST));
+  detail::fill_report(r.report, rep, hist);
   return r;
 }
 

@@ -823,3 +823,98 @@ int orc_gmres(const orc_problem* p, const double* b, double* x, double tol, int 
   rep->true_relative_residual = sqrt(s) / norm_b;
   return 0;
 }
+
+/* ---------------------------------------------------------------- BiCGSTAB (krylov.hpp:204-280) */
+
+/* bicgstab_left: BiCGSTAB on P^{-1} A x = P^{-1} b, x0 = 0, the unpreconditioned residual carried
+ * alongside from the same matvec outputs (q = A p, t_orig = A s).  *iterations counts a half-step
+ * convergence as k + 0.5 (krylov.hpp:244-249). */
+int orc_bicgstab(const orc_problem* p, const double* b, double* x, double tol, int max_iter,
+                 int full_sweep, double* iterations, orc_report* rep, double* history,
+                 int history_cap) {
+  const size_t n = orc_problem_dim(p);
+  memset(rep, 0, sizeof *rep);
+  memset(x, 0, n * sizeof(double));
+  *iterations = 0.0;
+  int hl = 0, rc = 0;
+  const double norm_b = norm2(b, n); /* :210 */
+  if (norm_b == 0.0) {
+    rep->converged = 1;
+    return 0;
+  }
+  const double floor_ = 1e-300; /* :215 */
+  double* r = (double*)malloc(n * sizeof(double));
+  double* rt = (double*)malloc(n * sizeof(double));
+  double* rhat = (double*)malloc(n * sizeof(double));
+  double* pp = (double*)calloc(n, sizeof(double));
+  double* q = (double*)calloc(n, sizeof(double));
+  double* v = (double*)calloc(n, sizeof(double));
+  double* s = (double*)calloc(n, sizeof(double));
+  double* st = (double*)calloc(n, sizeof(double));
+  double* to = (double*)calloc(n, sizeof(double));
+  double* t = (double*)calloc(n, sizeof(double));
+  memcpy(rt, b, n * sizeof(double));
+  if ((rc = orc_pc_apply(p, b, r, full_sweep))) goto done; /* :219 */
+  memcpy(rhat, r, n * sizeof(double));
+  double rho_prev = 1.0, alpha = 1.0, omega = 1.0;
+  for (int k = 0; k < max_iter; ++k) {
+    const double rho = dot(rhat, r, n); /* :224 */
+    if (fabs(rho) < floor_) break;
+    if (k == 0) {
+      memcpy(pp, r, n * sizeof(double));
+    } else {
+      const double beta = (rho / rho_prev) * (alpha / omega);
+      for (size_t i = 0; i < n; ++i) pp[i] = r[i] + beta * (pp[i] - omega * v[i]);
+    }
+    orc_matvec(p, pp, q); /* :234-235 */
+    if ((rc = orc_pc_apply(p, q, v, full_sweep))) break;
+    const double denom = dot(rhat, v, n);
+    if (fabs(denom) < floor_) break;
+    alpha = rho / denom;
+    for (size_t i = 0; i < n; ++i) { /* :239-242 */
+      s[i] = r[i] - alpha * v[i];
+      st[i] = rt[i] - alpha * q[i];
+    }
+    const double rel_half = norm2(st, n) / norm_b;
+    if (history && hl < history_cap) history[hl] = rel_half;
+    ++hl;
+    if (rel_half <= tol) { /* :244-250 */
+      axpy(alpha, pp, x, n);
+      *iterations = k + 0.5;
+      rep->converged = 1;
+      rep->final_relative_residual = rel_half;
+      break;
+    }
+    orc_matvec(p, s, to); /* :251-252 */
+    if ((rc = orc_pc_apply(p, to, t, full_sweep))) break;
+    const double tt = dot(t, t, n);
+    if (tt < floor_) break;
+    omega = dot(t, s, n) / tt;
+    for (size_t i = 0; i < n; ++i) { /* :256-260 */
+      x[i] += alpha * pp[i] + omega * s[i];
+      r[i] = s[i] - omega * t[i];
+      rt[i] = st[i] - omega * to[i];
+    }
+    const double rel = norm2(rt, n) / norm_b;
+    if (history && hl < history_cap) history[hl] = rel;
+    ++hl;
+    *iterations = k + 1.0;
+    rep->final_relative_residual = rel;
+    if (rel <= tol) {
+      rep->converged = 1;
+      break;
+    }
+    if (fabs(omega) < floor_) break;
+    rho_prev = rho;
+  }
+  if (!rc) { /* :274-275 fresh residual */
+    orc_matvec(p, x, q);
+    for (size_t i = 0; i < n; ++i) q[i] = b[i] - q[i];
+    rep->true_relative_residual = norm2(q, n) / norm_b;
+  }
+done:
+  rep->iterations = (int)*iterations;
+  rep->history_len = hl;
+  free(r); free(rt); free(rhat); free(pp); free(q); free(v); free(s); free(st); free(to); free(t);
+  return rc;
+}

@@ -77,6 +77,12 @@ typedef struct {
 int orc_gmres(const orc_problem* p, const double* b, double* x, double tol, int max_iter,
               int restart, int full_sweep, orc_report* rep, double* history, int history_cap);
 
+/* BiCGSTAB (krylov.hpp:204-280), x0 = 0; *iterations = the reference's double count (k + 0.5
+ * for a half-step convergence) */
+int orc_bicgstab(const orc_problem* p, const double* b, double* x, double tol, int max_iter,
+                 int full_sweep, double* iterations, orc_report* rep, double* history,
+                 int history_cap);
+
 #ifdef __cplusplus
 }
 #endif

@@ -96,6 +96,8 @@ def _load(path: str, kind: str):
         lib.orc_jacobian_column.argtypes = [C.c_void_p, C.c_int, _dp]
         lib.orc_gmres.argtypes = [C.c_void_p, _dp, _dp, C.c_double, C.c_int, C.c_int, C.c_int,
                                   C.POINTER(_ORep), _dp, C.c_int]
+        lib.orc_bicgstab.argtypes = [C.c_void_p, _dp, _dp, C.c_double, C.c_int, C.c_int, _dp,
+                                     C.POINTER(_ORep), _dp, C.c_int]
         lib.orc_fft_inplace.argtypes = [_dp, C.c_size_t, C.c_int]
         lib.orc_dst1_real.argtypes = [_dp, _dp, C.c_size_t]
         lib.orc_dst1_complex.argtypes = [_dp, _dp, C.c_size_t]
@@ -121,6 +123,10 @@ def _load(path: str, kind: str):
         lib.ref_tau_sigma.argtypes = [C.c_void_p, _dp]
         lib.ref_gmres.argtypes = [C.c_void_p, _dp, _dp, C.c_double, C.c_int, C.POINTER(C.c_int),
                                   C.POINTER(C.c_int), _dp, _dp, _dp, _dp, C.c_int, C.POINTER(C.c_int)]
+        lib.ref_bicgstab.argtypes = [C.c_void_p, _dp, _dp, C.c_double, C.c_int, C.POINTER(C.c_int),
+                                     _dp, _dp, _dp, _dp, _dp, C.c_int, C.POINTER(C.c_int)]
+        lib.ref_run_problem.argtypes = [C.c_int, C.c_double, C.c_double, C.c_int, C.c_int, C.c_int, C.c_int,
+                                        C.c_double, C.c_int, _dp, C.POINTER(C.c_int), _dp, _dp, _dp, _dp]
         lib.ref_fft_inplace.argtypes = [_dp, C.c_size_t, C.c_int]
         lib.ref_dst1_real.argtypes = [_dp, _dp, C.c_size_t]
         lib.ref_dst1_complex.argtypes = [_dp, _dp, C.c_size_t]
@@ -307,6 +313,19 @@ class OracleProblem(_ProblemBase):
                               rep.true_relative_residual, list(hist[:min(rep.history_len, cap)]),
                               0.0, rep.restarts)
 
+    def bicgstab(self, b, tol=1e-9, max_iter=200, full_sweep=False):
+        """bicgstab_left (krylov.hpp:204-280); report.iterations is the reference's float count."""
+        b = np.ascontiguousarray(b, dtype=np.float64)
+        x = np.empty_like(b)
+        rep = _ORep()
+        it = np.zeros(1)
+        cap = 2 * max(max_iter, 1) + 2
+        hist = np.zeros(cap)
+        self.be._chk(self.be.lib.orc_bicgstab(self.h, _ptr(b), _ptr(x), tol, max_iter, int(full_sweep), _ptr(it),
+                                              C.byref(rep), _ptr(hist), cap))
+        return x, SolveReport(bool(rep.converged), float(it[0]), rep.final_relative_residual,
+                              rep.true_relative_residual, list(hist[:min(rep.history_len, cap)]))
+
 
 class Reference(_Backend):
     """The unmodified reference, compiled from /root/reference headers (oracle/_ref)."""
@@ -318,6 +337,20 @@ class Reference(_Backend):
 
     def set_threads(self, n: int):
         self.lib.ref_set_threads(int(n))
+
+    def run_problem(self, dim, gx, gy, nt, h_inv, method="gmres", strang=False, tol=1e-9, max_iter=200):
+        """run_problem(example1(gx) | example2(gx, gy), RunConfig) (driver.hpp:84-112).
+        Returns dict(iterations, converged, err_inf, rhs, exact, final)."""
+        n = h_inv - 1
+        ns = n if dim == 1 else n * n
+        it, err = np.zeros(1), np.zeros(1)
+        conv = C.c_int()
+        rhs, ex, fin = np.zeros(nt * ns), np.zeros(ns), np.zeros(ns)
+        self._chk(self.lib.ref_run_problem(dim, gx, gy, nt, h_inv, 1 if method == "bicgstab" else 0, int(strang),
+                                           tol, max_iter, _ptr(it), C.byref(conv), _ptr(err), _ptr(rhs), _ptr(ex),
+                                           _ptr(fin)))
+        return {"iterations": float(it[0]), "converged": bool(conv.value), "err_inf": float(err[0]),
+                "rhs": rhs, "exact": ex, "final": fin}
 
     def problem_1d(self, gamma, kappa, h, n, nt, dt):
         hd = self.lib.ref_problem_1d(gamma, kappa, h, n, nt, dt)
@@ -356,4 +389,16 @@ class RefProblem(_ProblemBase):
         self.be._chk(self.be.lib.ref_gmres(self.h, _ptr(b), _ptr(x), tol, max_iter, C.byref(conv), C.byref(it),
                                            _ptr(fr), _ptr(tr), _ptr(sec), _ptr(hist), cap, C.byref(hl)))
         return x, SolveReport(bool(conv.value), it.value, float(fr[0]), float(tr[0]),
+                              list(hist[:min(hl.value, cap)]), float(sec[0]))
+
+    def bicgstab(self, b, tol=1e-9, max_iter=200):
+        b = np.ascontiguousarray(b, dtype=np.float64)
+        x = np.empty_like(b)
+        conv, hl = C.c_int(), C.c_int()
+        it, fr, tr, sec = np.zeros(1), np.zeros(1), np.zeros(1), np.zeros(1)
+        cap = 2 * max_iter + 2
+        hist = np.zeros(cap)
+        self.be._chk(self.be.lib.ref_bicgstab(self.h, _ptr(b), _ptr(x), tol, max_iter, C.byref(conv), _ptr(it),
+                                              _ptr(fr), _ptr(tr), _ptr(sec), _ptr(hist), cap, C.byref(hl)))
+        return x, SolveReport(bool(conv.value), float(it[0]), float(fr[0]), float(tr[0]),
                               list(hist[:min(hl.value, cap)]), float(sec[0]))

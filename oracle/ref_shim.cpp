@@ -6,6 +6,8 @@
 // No reference source is copied: this file only calls the reference's public API
 // (driver.hpp:49-92 orchestration pattern).
 #include <fracpint/all_at_once.hpp>
+#include <fracpint/driver.hpp>
+#include <fracpint/problems.hpp>
 #include <fracpint/alpha_circulant.hpp>
 #include <fracpint/dst.hpp>
 #include <fracpint/jacobian.hpp>
@@ -165,6 +167,85 @@ int ref_pc_forward(void* hp, const double* v, double* out) {
   return guarded([&] {
     if (!p->plan) throw std::invalid_argument("no plan");
     fracpint::apply_forward(*p->plan, {v, n}, {out, n});
+  });
+}
+
+// Manufactured benchmarks (problems.hpp:68-131) through the reference's run_problem
+// (driver.hpp:84-112): dim 1 = example1(gx), dim 2 = example2(gx, gy).  strang != 0 selects
+// PreconditionerKind::strang(), method 1 = bicgstab.  rhs_out (nt*ns) gets the assembled all-at-once
+// right-hand side, exact_out (ns) the exact final state, final_out (ns) the computed one.
+int ref_run_problem(int dim, double gx, double gy, int nt, int h_inv, int method, int strang,
+                    double tol, int max_iter, double* iterations, int* converged, double* err_inf,
+                    double* rhs_out, double* exact_out, double* final_out) {
+  return guarded([&] {
+    fracpint::RunConfig cfg;
+    cfg.n_time = nt;
+    cfg.h_inv = h_inv;
+    cfg.kind = strang ? fracpint::PreconditionerKind::strang() : fracpint::PreconditionerKind::generalized();
+    cfg.method = method == 1 ? fracpint::KrylovMethod::bicgstab : fracpint::KrylovMethod::gmres;
+    cfg.solver.tol = tol;
+    cfg.solver.max_iter = max_iter;
+    fracpint::RunResult r;
+    std::vector<double> u0, f, ex;
+    double dt = 0.0;
+    if (dim == 1) {
+      const auto p = fracpint::example1(gx);
+      fracpint::Grid1D g(p.a, p.b, h_inv);
+      dt = p.t_final / nt;
+      u0 = fracpint::sample_initial(p, g);
+      f = fracpint::sample_source(p, g, dt, nt);
+      ex = fracpint::sample_exact(p, g, p.t_final);
+      r = fracpint::run_problem(p, cfg);
+    } else {
+      const auto p = fracpint::example2(gx, gy);
+      fracpint::Grid2D g(p.ax, p.bx, p.ay, p.by, h_inv);
+      dt = p.t_final / nt;
+      u0 = fracpint::sample_initial(p, g);
+      f = fracpint::sample_source(p, g, dt, nt);
+      ex = fracpint::sample_exact(p, g, p.t_final);
+      r = fracpint::run_problem(p, cfg);
+    }
+    *iterations = r.report.iterations;
+    *converged = r.report.converged ? 1 : 0;
+    *err_inf = r.err_inf;
+    if (rhs_out) {
+      auto b = fracpint::assemble_rhs(fracpint::TimeStencil(nt), dt, f, u0);
+      std::copy(b.begin(), b.end(), rhs_out);
+    }
+    if (exact_out) std::copy(ex.begin(), ex.end(), exact_out);
+    if (final_out) std::copy(r.final_state.begin(), r.final_state.end(), final_out);
+  });
+}
+
+// bicgstab_left exactly as driver.hpp:68-71 wires it (KrylovMethod::bicgstab).
+int ref_bicgstab(void* hp, const double* b, double* x, double tol, int max_iter, int* converged,
+                 double* iterations, double* final_rel, double* true_rel, double* seconds,
+                 double* history, int history_cap, int* history_len) {
+  auto* p = static_cast<RefProblem*>(hp);
+  const std::size_t n = p->dim();
+  return guarded([&] {
+    if (!p->plan) throw std::invalid_argument("no plan");
+    fracpint::SolverConfig cfg;
+    cfg.tol = tol;
+    cfg.max_iter = max_iter;
+    auto apply_pinv = [p](std::span<const double> in, std::span<double> out) {
+      fracpint::apply_inverse(*p->plan, in, out);
+    };
+    fracpint::KrylovResult r = std::visit(
+        [&](const auto& o) {
+          auto apply_a = [&o](std::span<const double> in, std::span<double> out) { o.apply(in, out); };
+          return fracpint::bicgstab_left(n, apply_a, apply_pinv, {b, n}, cfg);
+        },
+        p->op);
+    std::copy(r.x.begin(), r.x.end(), x);
+    *converged = r.report.converged ? 1 : 0;
+    *iterations = r.report.iterations;
+    *final_rel = r.report.final_relative_residual;
+    *true_rel = r.report.true_relative_residual;
+    *seconds = r.report.seconds;
+    const int h = static_cast<int>(r.report.residual_history.size());
+    *history_len = h;
+    for (int i = 0; i < h && i < history_cap; ++i) history[i] = r.report.residual_history[i];
   });
 }
 

@@ -5,12 +5,12 @@ include/fracpint_b200.h); this package is the Python mirror of the reference int
 """
 from .solver import (AllAtOnceOperator, AlphaCirculantPlan, Context, InnerSweep, KrylovResult,
                      PreconditionerKind, RieszJacobian1D, RieszJacobian2D, SolveReport, SolverConfig,
-                     TimeStencil, apply_forward, apply_inverse, assemble_rhs, build_plan,
+                     TimeStencil, apply_forward, apply_inverse, assemble_rhs, bicgstab_left, build_plan,
                      centred_weights, gmres_right, kernel_launches, KernelProfile)
 
 __all__ = [
     "AllAtOnceOperator", "AlphaCirculantPlan", "Context", "InnerSweep", "KrylovResult",
     "PreconditionerKind", "RieszJacobian1D", "RieszJacobian2D", "SolveReport", "SolverConfig",
-    "TimeStencil", "apply_forward", "apply_inverse", "assemble_rhs", "build_plan", "centred_weights",
+    "TimeStencil", "apply_forward", "apply_inverse", "assemble_rhs", "bicgstab_left", "build_plan", "centred_weights",
     "gmres_right", "kernel_launches", "KernelProfile",
 ]

@@ -23,7 +23,7 @@ EXPORTS = [
     "fpc_device_free", "fpc_problem_create_1d", "fpc_problem_create_2d", "fpc_problem_destroy",
     "fpc_problem_dims", "fpc_problem_first_column", "fpc_problem_tau_sigma", "fpc_matvec",
     "fpc_assemble_rhs", "fpc_plan_create", "fpc_plan_destroy", "fpc_plan_info", "fpc_plan_lambda",
-    "fpc_pc_apply", "fpc_pc_forward", "fpc_gmres", "fpc_kernel_launches", "fpc_profile_start",
+    "fpc_pc_apply", "fpc_pc_forward", "fpc_gmres", "fpc_bicgstab", "fpc_kernel_launches", "fpc_profile_start",
     "fpc_profile_stop", "fpc_profile_entry", "fpc_shard_matvec", "fpc_shard_time_fwd", "fpc_shard_tau",
     "fpc_shard_time_inv", "fpc_shard_dots", "fpc_shard_update", "fpc_shard_lincomb",
 ]
@@ -37,7 +37,7 @@ class ReportC(C.Structure):
     _fields_ = [("converged", C.c_int), ("iterations", C.c_int), ("restarts", C.c_int),
                 ("reorthogonalizations", C.c_int), ("final_relative_residual", C.c_double),
                 ("true_relative_residual", C.c_double), ("seconds", C.c_double),
-                ("history_len", C.c_int)]
+                ("history_len", C.c_int), ("iterations_exact", C.c_double)]
 
 
 _lib = None
@@ -78,6 +78,7 @@ def load():
     lib.fpc_pc_apply.argtypes = [vp, dp, dp, C.c_int, C.c_int]
     lib.fpc_pc_forward.argtypes = [vp, dp, dp, C.c_int]
     lib.fpc_gmres.argtypes = [vp, dp, dp, C.POINTER(SolverConfigC), C.POINTER(ReportC), dp, C.c_int, C.c_int]
+    lib.fpc_bicgstab.argtypes = [vp, dp, dp, C.POINTER(SolverConfigC), C.POINTER(ReportC), dp, C.c_int, C.c_int]
     lib.fpc_kernel_launches.restype = C.c_ulonglong
     lib.fpc_profile_entry.argtypes = [C.c_int, C.c_char_p, C.c_int, C.POINTER(d), C.POINTER(C.c_longlong)]
     lib.fpc_shard_matvec.argtypes = [vp, vp, vp, C.c_int, C.c_int]

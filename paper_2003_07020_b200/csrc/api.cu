@@ -263,7 +263,7 @@ struct fpc_context_s {
   const double** dvptr = nullptr;  // device pointer table for update/lincomb
   double* dscales = nullptr;
   static constexpr int kPartialStride = 264;
-  static constexpr int kScal = 1024;
+  static constexpr int kScal = 2048;  // [1024, 1280): unit scales for x = Z y
 };
 
 struct DeviceGuard {
@@ -315,6 +315,7 @@ struct fpc_plan_s {
   int sweep_mode = FPC_SWEEP_HALF;
   // GMRES workspace (grown on demand, reused across solves)
   std::vector<double*> basis;
+  std::vector<double*> zbasis;  // z_j = P^{-1} V_j kept for x = Z y (see gmres_inner)
   double* d_z = nullptr;
   double* d_u = nullptr;
   double* d_r = nullptr;
@@ -342,7 +343,7 @@ void upload(void* dst, const void* src, size_t bytes, cudaStream_t st) {
 
 extern "C" {
 
-int fpc_abi_version(void) { return 1; }
+int fpc_abi_version(void) { return 2; }
 const char* fpc_last_error(void) { return g_err.c_str(); }
 unsigned long long fpc_kernel_launches(void) { return g_launches.load(); }
 
@@ -716,6 +717,7 @@ int fpc_plan_destroy(fpc_plan_t pl) {
     DeviceGuard g(p->ctx->device);
     cudaStreamSynchronize(p->ctx->stream);
     for (double* b : pl->basis) cudaFree(b);
+    for (double* b : pl->zbasis) cudaFree(b);
     for (void* q : {(void*)pl->d_sf, (void*)pl->d_sb, (void*)pl->d_lambda, (void*)pl->d_sigma,
                     (void*)pl->d_Z, (void*)pl->d_z, (void*)pl->d_u, (void*)pl->d_r, (void*)pl->d_x,
                     (void*)pl->d_d, (void*)pl->d_b, (void*)pl->d_Zf})
@@ -858,6 +860,28 @@ double* basis_buf(fpc_plan_s* pl, size_t i, size_t n) {
   return pl->basis[i];
 }
 
+// Slot i of the preconditioned basis Z (z_i = P^{-1} V_i), or nullptr when keeping it would
+// crowd out the Krylov basis: the basis slots the solve may still need (up to `basis_need`) plus
+// 1 GiB of headroom must stay free.  Config 3 (8.6 GB vectors, GMRES(10)) does not keep Z.
+double* zbasis_buf(fpc_plan_s* pl, size_t i, size_t n, size_t basis_need) {
+  if (pl->zbasis.size() > i) return pl->zbasis[i];
+  size_t free_b = 0, total_b = 0;
+  if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) return nullptr;
+  const size_t vec = (n + 2) * sizeof(double);
+  const size_t more_basis = basis_need > pl->basis.size() ? basis_need - pl->basis.size() : 0;
+  while (pl->zbasis.size() <= i) {
+    if (free_b < vec * (more_basis + 1) + (size_t(1) << 30)) return nullptr;
+    void* q = nullptr;
+    if (cudaMalloc(&q, vec) != cudaSuccess) {
+      cudaGetLastError();
+      return nullptr;
+    }
+    pl->zbasis.push_back(static_cast<double*>(q));
+    free_b -= vec;
+  }
+  return pl->zbasis[i];
+}
+
 // h[col0..col0+nv) (+ norm) into ctx->dscal[out_off...] via dots + deterministic reduce
 void dots_into(GmresState& S, const std::vector<const double*>& V, int nv, const double* w,
                bool with_norm, int out_off) {
@@ -912,10 +936,19 @@ static void gmres_inner(fpc_plan_s* pl, const double* b, double* x, double tol, 
   if (!pl->d_z) pl->d_z = dalloc<double>(n + 2);
   const double reorth_threshold = 0.70710678118654752;
   int steps = 0;
+  // z_j = P^{-1} V_j is kept (when memory allows) so that x = Z y needs no extra preconditioner
+  // apply: the reference forms x = P^{-1}(V y) (krylov.hpp:180-183); by linearity both are the same
+  // x up to rounding, and Z costs no extra traffic (z_j is written by the PC apply either way).
+  bool keep_z = true;
   for (int j = 0; j < max_iter; ++j) {
-    pc_apply_dev(pl, V[size_t(j)], pl->d_z, S.scales[size_t(j)]);
+    double* zj = keep_z ? zbasis_buf(pl, size_t(j), n, size_t(max_iter)) : nullptr;
+    if (!zj) {
+      keep_z = false;
+      zj = pl->d_z;
+    }
+    pc_apply_dev(pl, V[size_t(j)], zj, S.scales[size_t(j)]);
     double* w = basis_buf(pl, size_t(j), n);  // basis slot j holds V_{j+1} (V_0 = b)
-    matvec_dev(p, pl->d_z, w);
+    matvec_dev(p, zj, w);
     const int nv = j + 1;
     // CGS pass: h_i = <V_i, w>, norm_before^2
     dots_into(S, V, nv, w, true, 0);
@@ -1017,17 +1050,28 @@ static void gmres_inner(fpc_plan_s* pl, const double* b, double* x, double tol, 
     for (int k = i + 1; k < steps; ++k) s -= hcols[size_t(k)][size_t(i)] * y[size_t(k)];
     y[size_t(i)] = s / hcols[size_t(i)][size_t(i)];
   }
-  // u = V y lives in the z buffer (z is dead after the loop): one 8N buffer less at config 3
-  double* u = pl->d_z;
-  std::vector<const double*> vp(V.begin(), V.begin() + steps);
-  ck(cudaMemcpyAsync(c->dvptr, vp.data(), vp.size() * sizeof(double*), cudaMemcpyHostToDevice, S.st), "vptr");
-  ck(cudaMemcpyAsync(c->dscales, S.scales.data(), size_t(steps) * sizeof(double), cudaMemcpyHostToDevice, S.st),
-     "scales");
   std::memcpy(c->hpin + 600, y.data(), y.size() * sizeof(double));
   ck(cudaMemcpyAsync(c->dscal + 600, c->hpin + 600, y.size() * sizeof(double), cudaMemcpyHostToDevice, S.st),
      "y");
-  LAUNCH("lincomb", S.st, fpc::launch_lincomb(c->dvptr, c->dscales, c->dscal + 600, steps, u, n, S.st));
-  pc_apply_dev(pl, u, x, 1.0);
+  if (keep_z && steps > 0) {
+    // x = Z y (z_i already carries the basis scale)
+    std::vector<const double*> zp(pl->zbasis.begin(), pl->zbasis.begin() + steps);
+    std::vector<double> ones(size_t(steps), 1.0);
+    ck(cudaMemcpyAsync(c->dvptr, zp.data(), zp.size() * sizeof(double*), cudaMemcpyHostToDevice, S.st), "vptr");
+    std::memcpy(c->hpin + 1024, ones.data(), ones.size() * sizeof(double));
+    ck(cudaMemcpyAsync(c->dscales, c->hpin + 1024, size_t(steps) * sizeof(double), cudaMemcpyHostToDevice, S.st),
+       "scales");
+    LAUNCH("lincomb", S.st, fpc::launch_lincomb(c->dvptr, c->dscales, c->dscal + 600, steps, x, n, S.st));
+  } else {
+    // u = V y lives in the z buffer (z is dead after the loop): one 8N buffer less at config 3
+    double* u = pl->d_z;
+    std::vector<const double*> vp(V.begin(), V.begin() + steps);
+    ck(cudaMemcpyAsync(c->dvptr, vp.data(), vp.size() * sizeof(double*), cudaMemcpyHostToDevice, S.st), "vptr");
+    ck(cudaMemcpyAsync(c->dscales, S.scales.data(), size_t(steps) * sizeof(double), cudaMemcpyHostToDevice, S.st),
+       "scales");
+    LAUNCH("lincomb", S.st, fpc::launch_lincomb(c->dvptr, c->dscales, c->dscal + 600, steps, u, n, S.st));
+    pc_apply_dev(pl, u, x, 1.0);
+  }
   *steps_out = steps;
   ck(cudaStreamSynchronize(S.st), "sync");  // hpin reuse boundary
 }
@@ -1149,6 +1193,142 @@ int fpc_gmres(fpc_plan_t pl, const double* b, double* x, const fpc_solver_config
       ck(cudaMemcpyAsync(x, p->d_out, n * sizeof(double), cudaMemcpyDeviceToHost, st), "D2H");
       ck(cudaStreamSynchronize(st), "sync");
     }
+    rep->iterations_exact = rep->iterations;
+    rep->history_len = int(hist.size());
+    for (int i = 0; i < int(hist.size()) && i < history_cap; ++i) history[i] = hist[size_t(i)];
+    rep->seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  });
+}
+
+// ---------------------------------------------------------------------------- BiCGSTAB
+// bicgstab_left (krylov.hpp:204-280) on the device: the recurrence on preconditioned vectors with
+// the true residual carried alongside from the same matvec outputs.  Scalars go to the host at
+// three sync points per iteration (the half-step test, omega, the full-step test); alpha is formed
+// on the device from rho and the denominator so the s update needs no extra round trip.
+static void bicgstab_dev(fpc_plan_s* pl, const double* b, double* x, const fpc_solver_config& cfg,
+                         fpc_report* rep, std::vector<double>& hist) {
+  fpc_problem_s* p = pl->prob;
+  fpc_context_s* c = p->ctx;
+  const size_t n = p->dim();
+  cudaStream_t st = c->stream;
+  GmresState S{pl, c, n, st, {}, 0};
+  ck(cudaMemsetAsync(x, 0, n * sizeof(double), st), "memset");
+  dots_into(S, {}, 0, b, true, 0);
+  ck(cudaMemcpyAsync(c->hpin, c->dscal, sizeof(double), cudaMemcpyDeviceToHost, st), "D2H");
+  ck(cudaStreamSynchronize(st), "sync");
+  const double norm_b = std::sqrt(c->hpin[0]);
+  rep->iterations_exact = 0.0;
+  if (norm_b == 0.0) {
+    rep->converged = 1;
+    return;
+  }
+  constexpr double kFloor = 1e-300;  // krylov.hpp:215
+  // workspace in the plan's basis slots: r (= s), r_true (= s_true), rhat, p, q (= t_orig), v, t
+  double* r = basis_buf(pl, 0, n);
+  double* rt = basis_buf(pl, 1, n);
+  double* rhat = basis_buf(pl, 2, n);
+  double* pv = basis_buf(pl, 3, n);
+  double* q = basis_buf(pl, 4, n);
+  double* v = basis_buf(pl, 5, n);
+  double* t = basis_buf(pl, 6, n);
+  // device scalar slots: [kR] rho, [kD] denom (adjacent: k_bicg_s reads both), [kS] ||s_true||^2,
+  // [kT] <s,t>, ||t||^2, [kN] ||r_true||^2, next rho
+  constexpr int kR = 1100, kD = 1101, kS = 1104, kT = 1108, kN = 1112;
+  const int stride = fpc_context_s::kPartialStride;
+  ck(cudaMemcpyAsync(rt, b, n * sizeof(double), cudaMemcpyDeviceToDevice, st), "copy");
+  pc_apply_dev(pl, b, r, 1.0);
+  ck(cudaMemcpyAsync(rhat, r, n * sizeof(double), cudaMemcpyDeviceToDevice, st), "copy");
+  dots_into(S, {}, 0, r, true, kR);  // rho_0 = <rhat, r> = ||r||^2
+  ck(cudaMemcpyAsync(c->hpin + kR, c->dscal + kR, sizeof(double), cudaMemcpyDeviceToHost, st), "D2H");
+  ck(cudaStreamSynchronize(st), "sync");
+  double rho = c->hpin[kR], rho_prev = 1.0, alpha = 1.0, omega = 1.0;
+  for (int k = 0; k < cfg.max_iter; ++k) {
+    if (std::abs(rho) < kFloor) break;
+    const double beta = k == 0 ? 0.0 : (rho / rho_prev) * (alpha / omega);
+    LAUNCH("bicg_p", st, fpc::launch_bicg_p(r, v, pv, beta, omega, n, k == 0, st));
+    matvec_dev(p, pv, q);
+    pc_apply_dev(pl, q, v, 1.0);
+    fpc::VecSet vs{};
+    vs.v[0] = rhat;
+    vs.s[0] = 1.0;
+    LAUNCH("dots", st, fpc::launch_dots(vs, 1, v, n, c->partial, stride, 0, false, st));
+    LAUNCH("reduce", st, fpc::launch_reduce(c->partial, stride, 1, c->dscal + kD, false, st));
+    LAUNCH("bicg_s", st, fpc::launch_bicg_s(r, rt, v, q, c->dscal + kR, n, c->partial, st));
+    LAUNCH("reduce", st, fpc::launch_reduce(c->partial, 1, 1, c->dscal + kS, false, st));
+    ck(cudaMemcpyAsync(c->hpin + kD, c->dscal + kD, sizeof(double), cudaMemcpyDeviceToHost, st), "D2H");
+    ck(cudaMemcpyAsync(c->hpin + kS, c->dscal + kS, sizeof(double), cudaMemcpyDeviceToHost, st), "D2H");
+    ck(cudaStreamSynchronize(st), "sync");
+    const double denom = c->hpin[kD];
+    if (std::abs(denom) < kFloor) break;
+    alpha = rho / denom;
+    const double rel_half = std::sqrt(c->hpin[kS]) / norm_b;
+    hist.push_back(rel_half);
+    if (rel_half <= cfg.tol) {
+      LAUNCH("axpy", st, fpc::launch_axpy(alpha, pv, x, n, st));
+      rep->iterations_exact = k + 0.5;
+      rep->converged = 1;
+      rep->final_relative_residual = rel_half;
+      break;
+    }
+    matvec_dev(p, r, q);  // t_orig = A s (s lives in r; t_orig over q)
+    pc_apply_dev(pl, q, t, 1.0);
+    vs.v[0] = r;  // <s, t> and ||t||^2
+    LAUNCH("dots", st, fpc::launch_dots(vs, 1, t, n, c->partial, stride, 0, true, st));
+    LAUNCH("reduce", st, fpc::launch_reduce(c->partial, stride, 2, c->dscal + kT, false, st));
+    ck(cudaMemcpyAsync(c->hpin + kT, c->dscal + kT, 2 * sizeof(double), cudaMemcpyDeviceToHost, st), "D2H");
+    ck(cudaStreamSynchronize(st), "sync");
+    const double tt = c->hpin[kT + 1];
+    if (tt < kFloor) break;
+    omega = c->hpin[kT] / tt;
+    LAUNCH("bicg_x", st, fpc::launch_bicg_x(x, pv, r, t, rt, q, rhat, alpha, omega, n, c->partial, st));
+    LAUNCH("reduce", st, fpc::launch_reduce(c->partial, 2, 2, c->dscal + kN, false, st));
+    ck(cudaMemcpyAsync(c->hpin + kN, c->dscal + kN, 2 * sizeof(double), cudaMemcpyDeviceToHost, st), "D2H");
+    ck(cudaStreamSynchronize(st), "sync");
+    const double rel = std::sqrt(c->hpin[kN]) / norm_b;
+    hist.push_back(rel);
+    rep->iterations_exact = k + 1.0;
+    rep->final_relative_residual = rel;
+    if (rel <= cfg.tol) {
+      rep->converged = 1;
+      break;
+    }
+    if (std::abs(omega) < kFloor) break;
+    rho_prev = rho;
+    rho = c->hpin[kN + 1];
+    ck(cudaMemcpyAsync(c->dscal + kR, c->dscal + kN + 1, sizeof(double), cudaMemcpyDeviceToDevice, st), "rho");
+  }
+  rep->true_relative_residual = resid_norm_dev(pl, b, x) / norm_b;
+}
+
+int fpc_bicgstab(fpc_plan_t pl, const double* b, double* x, const fpc_solver_config* cfg_in,
+                 fpc_report* rep, double* history, int history_cap, int where) {
+  if (!pl || !rep) return set_err(FPC_INVALID_ARGUMENT, "null argument");
+  return guarded([&] {
+    check_ptr(b, "fpc_bicgstab");
+    check_ptr(x, "fpc_bicgstab");
+    fpc_solver_config cfg{1e-9, 200, 0, FPC_SWEEP_HALF};
+    if (cfg_in) cfg = *cfg_in;
+    if (cfg.sweep != FPC_SWEEP_HALF && cfg.sweep != FPC_SWEEP_FULL) throw InvalidArg{"fpc_bicgstab: bad sweep"};
+    pl->sweep_mode = cfg.sweep;
+    fpc_problem_s* p = pl->prob;
+    DeviceGuard g(p->ctx->device);
+    const auto t0 = std::chrono::steady_clock::now();
+    std::memset(rep, 0, sizeof *rep);
+    std::vector<double> hist;
+    const size_t n = p->dim();
+    cudaStream_t st = p->ctx->stream;
+    if (where == FPC_DEVICE) {
+      check_dev_aligned(b, "fpc_bicgstab");
+      check_dev_aligned(x, "fpc_bicgstab");
+      bicgstab_dev(pl, b, x, cfg, rep, hist);
+    } else {
+      ensure_staging(p);
+      upload(p->d_in, b, n * sizeof(double), st);
+      bicgstab_dev(pl, p->d_in, p->d_out, cfg, rep, hist);
+      ck(cudaMemcpyAsync(x, p->d_out, n * sizeof(double), cudaMemcpyDeviceToHost, st), "D2H");
+      ck(cudaStreamSynchronize(st), "sync");
+    }
+    rep->iterations = int(rep->iterations_exact);
     rep->history_len = int(hist.size());
     for (int i = 0; i < int(hist.size()) && i < history_cap; ++i) history[i] = hist[size_t(i)];
     rep->seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();

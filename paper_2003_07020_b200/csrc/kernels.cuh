@@ -102,4 +102,18 @@ cudaError_t launch_axpy(double a, const double* x, double* y, size_t n, cudaStre
 // y = b - y
 cudaError_t launch_rsub(const double* b, double* y, size_t n, cudaStream_t st);
 
+// ---- BiCGSTAB vector kernels (krylov.hpp:204-280) -------------------------------------------
+// p = r (first) or r + beta (p - omega v)
+cudaError_t launch_bicg_p(const double* r, const double* v, double* p, double beta, double omega,
+                          size_t n, bool first, cudaStream_t st);
+// alpha = rho_denom[0]/rho_denom[1]; r <- r - alpha v (= s); rt <- rt - alpha q (= s_true);
+// partial[blk] = ||s_true||^2
+cudaError_t launch_bicg_s(double* r, double* rt, const double* v, const double* q,
+                          const double* rho_denom, size_t n, double* partial, cudaStream_t st);
+// x += alpha p + omega s; r <- s - omega t; rt <- s_true - omega t_orig;
+// partial[blk*2] = ||rt||^2, partial[blk*2+1] = <rhat, r>
+cudaError_t launch_bicg_x(double* x, const double* p, double* r, const double* t, double* rt,
+                          const double* to, const double* rhat, double alpha, double omega,
+                          size_t n, double* partial, cudaStream_t st);
+
 }  // namespace fpc

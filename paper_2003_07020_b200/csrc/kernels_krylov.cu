@@ -311,3 +311,82 @@ cudaError_t launch_update_dots(const VecSetN& vs, int nv, const double* coef, do
 }
 
 }  // namespace fpc
+
+// ---------------------------------------------------------------------------------------------
+// BiCGSTAB vector kernels (krylov.hpp:204-280, bicgstab_left).  Elementwise, so the in-place
+// aliasing below (s over r, s_true over r_true, t_orig over q) keeps the reference's values.
+namespace fpc {
+
+// p = r (first) or p = r + beta (p - omega v)                                 krylov.hpp:228-233
+__global__ void __launch_bounds__(kDotsThreads)
+    k_bicg_p(const double* __restrict__ r, const double* __restrict__ v, double* __restrict__ p,
+             double beta, double omega, size_t n, int first) {
+  for (size_t e = size_t(blockIdx.x) * kDotsThreads + threadIdx.x; e < n;
+       e += size_t(kDotsGrid) * kDotsThreads)
+    p[e] = first ? r[e] : r[e] + beta * (p[e] - omega * v[e]);
+}
+
+// alpha = rho / denom (device scalars); s = r - alpha v (into r); s_true = r_true - alpha q (into
+// r_true); partial[blk] = ||s_true||^2                                          krylov.hpp:236-243
+__global__ void __launch_bounds__(kDotsThreads)
+    k_bicg_s(double* __restrict__ r, double* __restrict__ rt, const double* __restrict__ v,
+             const double* __restrict__ q, const double* __restrict__ rho_denom, size_t n,
+             double* __restrict__ partial) {
+  const double alpha = rho_denom[0] / rho_denom[1];
+  double acc[1] = {0.0};
+  for (size_t e = size_t(blockIdx.x) * kDotsThreads + threadIdx.x; e < n;
+       e += size_t(kDotsGrid) * kDotsThreads) {
+    r[e] = r[e] - alpha * v[e];
+    const double st = rt[e] - alpha * q[e];
+    rt[e] = st;
+    acc[0] = fma(st, st, acc[0]);
+  }
+  __shared__ double outb[1];
+  block_reduce_store<1>(acc, outb);
+  __syncthreads();
+  if (threadIdx.x == 0) partial[blockIdx.x] = outb[0];
+}
+
+// x += alpha p + omega s; r = s - omega t (s lives in r); r_true = s_true - omega t_orig;
+// partial[blk*2 + 0] = ||r_true||^2, partial[blk*2 + 1] = <rhat, r> (the next rho)  :253-259, 221
+__global__ void __launch_bounds__(kDotsThreads)
+    k_bicg_x(double* __restrict__ x, const double* __restrict__ p, double* __restrict__ r,
+             const double* __restrict__ t, double* __restrict__ rt, const double* __restrict__ to,
+             const double* __restrict__ rhat, double alpha, double omega, size_t n,
+             double* __restrict__ partial) {
+  double acc[2] = {0.0, 0.0};
+  for (size_t e = size_t(blockIdx.x) * kDotsThreads + threadIdx.x; e < n;
+       e += size_t(kDotsGrid) * kDotsThreads) {
+    const double s = r[e];
+    x[e] += alpha * p[e] + omega * s;
+    const double rn = s - omega * t[e];
+    r[e] = rn;
+    const double rtn = rt[e] - omega * to[e];
+    rt[e] = rtn;
+    acc[0] = fma(rtn, rtn, acc[0]);
+    acc[1] = fma(rhat[e], rn, acc[1]);
+  }
+  __shared__ double outb[2];
+  block_reduce_store<2>(acc, outb);
+  __syncthreads();
+  if (threadIdx.x < 2) partial[size_t(blockIdx.x) * 2 + threadIdx.x] = outb[threadIdx.x];
+}
+
+cudaError_t launch_bicg_p(const double* r, const double* v, double* p, double beta, double omega,
+                          size_t n, bool first, cudaStream_t st) {
+  k_bicg_p<<<kDotsGrid, kDotsThreads, 0, st>>>(r, v, p, beta, omega, n, first ? 1 : 0);
+  return cudaGetLastError();
+}
+cudaError_t launch_bicg_s(double* r, double* rt, const double* v, const double* q,
+                          const double* rho_denom, size_t n, double* partial, cudaStream_t st) {
+  k_bicg_s<<<kDotsGrid, kDotsThreads, 0, st>>>(r, rt, v, q, rho_denom, n, partial);
+  return cudaGetLastError();
+}
+cudaError_t launch_bicg_x(double* x, const double* p, double* r, const double* t, double* rt,
+                          const double* to, const double* rhat, double alpha, double omega,
+                          size_t n, double* partial, cudaStream_t st) {
+  k_bicg_x<<<kDotsGrid, kDotsThreads, 0, st>>>(x, p, r, t, rt, to, rhat, alpha, omega, n, partial);
+  return cudaGetLastError();
+}
+
+}  // namespace fpc

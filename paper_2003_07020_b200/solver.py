@@ -387,34 +387,49 @@ class KrylovResult:
     report: SolveReport
 
 
+def _krylov(fn, name, op, plan, b, cfg, out):
+    if not isinstance(op, AllAtOnceOperator) or not isinstance(plan, AlphaCirculantPlan):
+        raise TypeError(f"{name}(op, plan, b, cfg): device operator and plan required")
+    if plan.op.h.value != op.h.value:
+        raise ValueError(f"{name}: the plan was built for a different operator")
+    cfg = cfg or SolverConfig()
+    n = op.dim()
+    c = N.SolverConfigC(float(cfg.tol), int(cfg.max_iter), int(cfg.restart), int(cfg.sweep))
+    rep = N.ReportC()
+    cap = 2 * max(int(cfg.max_iter), 1) + 2
+    hist = np.zeros(cap)
+    if _is_torch(b):
+        import torch
+        bin_ = _dev_in(b, n)
+        x = torch.empty_like(bin_) if out is None else _dev_in(out, n)
+        N.check(fn(plan.h, C.c_void_p(bin_.data_ptr()), C.c_void_p(x.data_ptr()), C.byref(c),
+                   C.byref(rep), C.c_void_p(hist.ctypes.data), cap, N.FPC_DEVICE))
+    else:
+        bin_ = _host_in(b, n)
+        x = np.empty(n) if out is None else out
+        N.check(fn(plan.h, C.c_void_p(bin_.ctypes.data), C.c_void_p(x.ctypes.data), C.byref(c),
+                   C.byref(rep), C.c_void_p(hist.ctypes.data), cap, N.FPC_HOST))
+    r = SolveReport(bool(rep.converged), float(rep.iterations_exact), list(hist[:min(rep.history_len, cap)]),
+                    rep.final_relative_residual, rep.true_relative_residual, rep.seconds, rep.restarts,
+                    rep.reorthogonalizations)
+    return KrylovResult(x, r)
+
+
 def gmres_right(op: AllAtOnceOperator, plan: AlphaCirculantPlan, b, cfg: SolverConfig | None = None,
                 out=None) -> KrylovResult:
     """Right-preconditioned GMRES on the device (krylov.hpp:83-192), x0 = 0.
 
     This is the non-generic overload of the reference's gmres_right(n, apply_a, apply_pinv, b, cfg):
     the operator and the plan are the device objects, so the whole iteration stays in HBM."""
-    if not isinstance(op, AllAtOnceOperator) or not isinstance(plan, AlphaCirculantPlan):
-        raise TypeError("gmres_right(op, plan, b, cfg): device operator and plan required")
-    if plan.op.h.value != op.h.value:
-        raise ValueError("gmres_right: the plan was built for a different operator")
-    cfg = cfg or SolverConfig()
-    n = op.dim()
-    c = N.SolverConfigC(float(cfg.tol), int(cfg.max_iter), int(cfg.restart), int(cfg.sweep))
-    rep = N.ReportC()
-    cap = max(int(cfg.max_iter), 1) + 1
-    hist = np.zeros(cap)
-    if _is_torch(b):
-        import torch
-        bin_ = _dev_in(b, n)
-        x = torch.empty_like(bin_) if out is None else _dev_in(out, n)
-        N.check(plan.lib.fpc_gmres(plan.h, C.c_void_p(bin_.data_ptr()), C.c_void_p(x.data_ptr()), C.byref(c),
-                                   C.byref(rep), C.c_void_p(hist.ctypes.data), cap, N.FPC_DEVICE))
-    else:
-        bin_ = _host_in(b, n)
-        x = np.empty(n) if out is None else out
-        N.check(plan.lib.fpc_gmres(plan.h, C.c_void_p(bin_.ctypes.data), C.c_void_p(x.ctypes.data), C.byref(c),
-                                   C.byref(rep), C.c_void_p(hist.ctypes.data), cap, N.FPC_HOST))
-    r = SolveReport(bool(rep.converged), float(rep.iterations), list(hist[:min(rep.history_len, cap)]),
-                    rep.final_relative_residual, rep.true_relative_residual, rep.seconds, rep.restarts,
-                    rep.reorthogonalizations)
-    return KrylovResult(x, r)
+    return _krylov(plan.lib.fpc_gmres if isinstance(plan, AlphaCirculantPlan) else None, "gmres_right",
+                   op, plan, b, cfg, out)
+
+
+def bicgstab_left(op: AllAtOnceOperator, plan: AlphaCirculantPlan, b, cfg: SolverConfig | None = None,
+                  out=None) -> KrylovResult:
+    """Left-preconditioned BiCGSTAB on the device (krylov.hpp:204-280), x0 = 0: the recurrence on
+    P^{-1}-preconditioned vectors, convergence tested on the true residual carried alongside;
+    `report.iterations` counts a half-step convergence as k + 0.5 like the reference.
+    `cfg.restart` is ignored."""
+    return _krylov(plan.lib.fpc_bicgstab if isinstance(plan, AlphaCirculantPlan) else None, "bicgstab_left",
+                   op, plan, b, cfg, out)

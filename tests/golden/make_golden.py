@@ -52,6 +52,9 @@ def main():
         ("p2a", 2, (1.3, 1.7), (1.0, 1.0), 1.0 / 8, 7, 8, 1.0 / 8, 0.0),
         ("p2b", 2, (1.4, 1.8), (0.03, 0.05), 0.25, 7, 8, 0.2, 0.6),
         ("p2c", 2, (1.5, 1.5), (1.0, 1.0), 1.0 / 16, 15, 16, 1.0 / 16, 0.0),
+        # Strang P1 (alpha = 1, lambda_0 = 0; alpha_circulant.hpp:26)
+        ("p1s", 1, (1.5,), (1.0,), 1.0 / 32, 31, 16, 1.0 / 16, 1.0),
+        ("p2s", 2, (1.3, 1.7), (1.0, 1.0), 1.0 / 8, 7, 8, 1.0 / 8, 1.0),
     ]
     for tag, dim, gm, kp, h, n, nt, dt, alpha in cases:
         if dim == 1:
@@ -78,6 +81,32 @@ def main():
         g[f"{tag}_iters"] = np.array([rep.iterations])
         g[f"{tag}_history"] = np.array(rep.residual_history)
         g[f"{tag}_trr"] = np.array([rep.true_relative_residual])
+        # bicgstab_left (krylov.hpp:204-280) on the same system
+        xb, rb = p.bicgstab(b, 1e-10, 200)
+        g[f"{tag}_bicg_x"] = xb
+        g[f"{tag}_bicg_iters"] = np.array([rb.iterations])
+        g[f"{tag}_bicg_history"] = np.array(rb.residual_history)
+        g[f"{tag}_bicg_trr"] = np.array([rb.true_relative_residual])
+    # paper-table path: run_problem on the manufactured benchmarks (driver.hpp:94-112).
+    # (tag, dim, gx, gy, nt, h_inv, method, strang, keep_rhs)
+    rows = [
+        ("rp1a", 1, 1.2, 0.0, 64, 128, "gmres", False, True),
+        ("rp1b", 1, 1.2, 0.0, 64, 128, "gmres", True, False),
+        ("rp1c", 1, 1.9, 0.0, 64, 128, "gmres", False, False),
+        ("rp1d", 1, 1.5, 0.0, 16, 32, "bicgstab", False, True),
+        ("rp2a", 2, 1.4, 1.2, 16, 16, "bicgstab", False, True),
+        ("rp2b", 2, 1.5, 1.5, 64, 64, "bicgstab", False, False),
+        ("rp2c", 2, 1.5, 1.5, 64, 64, "bicgstab", True, False),
+        ("rp2d", 2, 1.7, 1.9, 16, 16, "gmres", False, False),
+    ]
+    for tag, dim, gx, gy, nt, h_inv, method, strang, keep in rows:
+        out = r.run_problem(dim, gx, gy, nt, h_inv, method, strang)
+        g[f"{tag}_params"] = np.array([dim, gx, gy, nt, h_inv, 1 if method == "bicgstab" else 0, int(strang)])
+        g[f"{tag}_result"] = np.array([out["iterations"], float(out["converged"]), out["err_inf"]])
+        g[f"{tag}_final"] = out["final"]
+        g[f"{tag}_exact"] = out["exact"]
+        if keep:
+            g[f"{tag}_rhs"] = out["rhs"]
     np.savez_compressed(OUT, **g)
     print("wrote", OUT, os.path.getsize(OUT), "bytes,", len(g), "arrays")
 

@@ -31,7 +31,7 @@ def test_library_loads_and_exports_every_declared_symbol():
 
 def test_abi_version_and_error_string():
     lib = N.load()
-    assert lib.fpc_abi_version() == 1
+    assert lib.fpc_abi_version() == 2
     assert isinstance(lib.fpc_last_error(), bytes)
 
 

@@ -11,7 +11,7 @@ import paper_2003_07020_b200 as fp
 pytestmark = pytest.mark.gpu
 
 GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "fracpint_ref_golden.npz")
-TAGS = ["p1a", "p1b", "p1c", "p1d", "p2a", "p2b", "p2c"]
+TAGS = ["p1a", "p1b", "p1c", "p1d", "p2a", "p2b", "p2c", "p1s", "p2s"]  # p?s: Strang alpha = 1
 
 
 @pytest.fixture(scope="module")
@@ -51,3 +51,14 @@ def test_gpu_vs_reference_golden(gold, tag):
     g = gold[f"{tag}_history"]
     k = min(len(h), len(g))
     assert np.allclose(h[:k], g[:k], rtol=1e-6, atol=1e-13)
+
+
+@pytest.mark.parametrize("tag", TAGS)
+def test_gpu_bicgstab_vs_reference_golden(gold, tag):
+    """bicgstab_left (krylov.hpp:204-280) on the device vs the reference's own solve."""
+    op, plan = make(gold[f"{tag}_params"])
+    res = fp.bicgstab_left(op, plan, gold[f"{tag}_b"], fp.SolverConfig(tol=1e-10, max_iter=200))
+    assert res.report.converged
+    assert abs(res.report.iterations - float(gold[f"{tag}_bicg_iters"][0])) <= 1.0
+    assert rel(res.x, gold[f"{tag}_bicg_x"]) <= 1e-10
+    assert res.report.true_relative_residual <= 10 * max(float(gold[f"{tag}_bicg_trr"][0]), 1e-11)

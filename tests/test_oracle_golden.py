@@ -7,7 +7,7 @@ import numpy as np
 import pytest
 
 GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "fracpint_ref_golden.npz")
-TAGS = ["p1a", "p1b", "p1c", "p1d", "p2a", "p2b", "p2c"]
+TAGS = ["p1a", "p1b", "p1c", "p1d", "p2a", "p2b", "p2c", "p1s", "p2s"]
 
 
 @pytest.fixture(scope="module")
@@ -67,6 +67,18 @@ def test_gmres_golden(oracle, gold, tag):
     assert np.abs(np.array(rep.residual_history) - gold[f"{tag}_history"]).max() <= 1e-12
 
 
+@pytest.mark.parametrize("tag", TAGS)
+def test_bicgstab_golden(oracle, gold, tag):
+    """bicgstab_left (krylov.hpp:204-280): half-step iteration counts, x, history."""
+    p = make(oracle, gold[f"{tag}_params"])
+    x, rep = p.bicgstab(gold[f"{tag}_b"], 1e-10, 200)
+    assert rep.iterations == float(gold[f"{tag}_bicg_iters"][0])
+    assert rel(x, gold[f"{tag}_bicg_x"]) <= 1e-10
+    h, g = np.array(rep.residual_history), gold[f"{tag}_bicg_history"]
+    # late entries are norms of nearly cancelled residuals: compare them in units of ||b||
+    assert len(h) == len(g) and np.allclose(h, g, rtol=1e-6, atol=1e-12)
+
+
 def test_live_reference_pins(oracle, reference):
     """Random cases against the reference compiled here (skipped where oracle/_ref is absent)."""
     rng = np.random.default_rng(11)
@@ -84,3 +96,15 @@ def test_live_reference_pins(oracle, reference):
     pr = reference.problem_2d(1.3, 1.7, 1, 1, 1 / 8, 7, 8, 1 / 8).build_plan()
     v = rng.uniform(-1, 1, 49 * 8)
     assert rel(po.matvec(v), pr.matvec(v)) <= 1e-14 and rel(po.pc_apply(v), pr.pc_apply(v)) <= 1e-12
+
+
+def test_live_reference_bicgstab(oracle, reference):
+    rng = np.random.default_rng(12)
+    for gamma, ns, nt, alpha in [(1.3, 31, 8, 0.0), (1.7, 63, 16, 1.0)]:
+        h, dt = 1.0 / (ns + 1), 1.0 / nt
+        po = oracle.problem_1d(gamma, 1.0, h, ns, nt, dt).build_plan(alpha)
+        pr = reference.problem_1d(gamma, 1.0, h, ns, nt, dt).build_plan(alpha)
+        b = rng.uniform(-1, 1, ns * nt)
+        xo, ro = po.bicgstab(b, 1e-10, 200)
+        xr, rr = pr.bicgstab(b, 1e-10, 200)
+        assert ro.iterations == rr.iterations and rel(xo, xr) <= 1e-10
