@@ -48,6 +48,9 @@ extern "C" {
 #define FPC_SWEEP_HALF 0 /* InnerSweep::half (alpha_circulant.hpp:128) */
 #define FPC_SWEEP_FULL 1 /* InnerSweep::full */
 
+#define FPC_ORDER_REFERENCE 0 /* time FFT -> tau solves per frequency -> inverse time FFT (default) */
+#define FPC_ORDER_COMMUTED 1  /* DST per time level -> per-mode time solve -> DST */
+
 typedef struct fpc_context_s* fpc_context_t;
 typedef struct fpc_problem_s* fpc_problem_t;
 typedef struct fpc_plan_s* fpc_plan_t;
@@ -106,6 +109,9 @@ int fpc_plan_destroy(fpc_plan_t plan);
 int fpc_plan_info(fpc_plan_t plan, double* alpha, double* min_shift_margin, int* solve_count,
                   int* n_warnings);
 int fpc_plan_lambda(fpc_plan_t plan, double* lambda_interleaved);
+/* half-sweep factor ordering of fpc_pc_apply / fpc_pc_forward / the Krylov solvers (the same
+ * operator up to rounding; FPC_UNSUPPORTED for 2D or n_space + 1 > 8192 when commuted) */
+int fpc_plan_set_ordering(fpc_plan_t plan, int ordering);
 int fpc_pc_apply(fpc_plan_t plan, const double* v, double* out, int sweep, int where);
 int fpc_pc_forward(fpc_plan_t plan, const double* v, double* out, int where);
 

@@ -3,13 +3,13 @@ Riesz fractional diffusion system (arXiv 2003.07020), drop-in for the reference'
 solver API.  The compute lives in libfracpint_b200.so (hand-written sm_100a CUDA behind the C-ABI
 include/fracpint_b200.h); this package is the Python mirror of the reference interface.
 """
-from .solver import (AllAtOnceOperator, AlphaCirculantPlan, Context, InnerSweep, KrylovResult,
+from .solver import (AllAtOnceOperator, AlphaCirculantPlan, Context, InnerSweep, KrylovResult, Ordering,
                      PreconditionerKind, RieszJacobian1D, RieszJacobian2D, SolveReport, SolverConfig,
                      TimeStencil, apply_forward, apply_inverse, assemble_rhs, bicgstab_left, build_plan,
                      centred_weights, gmres_right, kernel_launches, KernelProfile)
 
 __all__ = [
-    "AllAtOnceOperator", "AlphaCirculantPlan", "Context", "InnerSweep", "KrylovResult",
+    "AllAtOnceOperator", "AlphaCirculantPlan", "Context", "InnerSweep", "KrylovResult", "Ordering",
     "PreconditionerKind", "RieszJacobian1D", "RieszJacobian2D", "SolveReport", "SolverConfig",
     "TimeStencil", "apply_forward", "apply_inverse", "assemble_rhs", "bicgstab_left", "build_plan", "centred_weights",
     "gmres_right", "kernel_launches", "KernelProfile",

@@ -15,6 +15,7 @@ LIB_PATH = os.environ.get("FPC_LIB") or os.path.join(HERE, "libfracpint_b200.so"
 FPC_OK, FPC_INVALID_ARGUMENT, FPC_RUNTIME_ERROR, FPC_CUDA_ERROR, FPC_UNSUPPORTED = 0, 1, 2, 3, 4
 FPC_HOST, FPC_DEVICE = 0, 1
 FPC_SWEEP_HALF, FPC_SWEEP_FULL = 0, 1
+FPC_ORDER_REFERENCE, FPC_ORDER_COMMUTED = 0, 1
 
 # every symbol include/fracpint_b200.h declares (checked by tests/test_abi.py)
 EXPORTS = [
@@ -23,7 +24,7 @@ EXPORTS = [
     "fpc_device_free", "fpc_problem_create_1d", "fpc_problem_create_2d", "fpc_problem_destroy",
     "fpc_problem_dims", "fpc_problem_first_column", "fpc_problem_tau_sigma", "fpc_matvec",
     "fpc_assemble_rhs", "fpc_plan_create", "fpc_plan_destroy", "fpc_plan_info", "fpc_plan_lambda",
-    "fpc_pc_apply", "fpc_pc_forward", "fpc_gmres", "fpc_bicgstab", "fpc_kernel_launches", "fpc_profile_start",
+    "fpc_plan_set_ordering", "fpc_pc_apply", "fpc_pc_forward", "fpc_gmres", "fpc_bicgstab", "fpc_kernel_launches", "fpc_profile_start",
     "fpc_profile_stop", "fpc_profile_entry", "fpc_shard_matvec", "fpc_shard_time_fwd", "fpc_shard_tau",
     "fpc_shard_time_inv", "fpc_shard_dots", "fpc_shard_update", "fpc_shard_lincomb",
 ]
@@ -75,6 +76,7 @@ def load():
     lib.fpc_plan_destroy.argtypes = [vp]
     lib.fpc_plan_info.argtypes = [vp, C.POINTER(d), C.POINTER(d), ip, ip]
     lib.fpc_plan_lambda.argtypes = [vp, dp]
+    lib.fpc_plan_set_ordering.argtypes = [vp, C.c_int]
     lib.fpc_pc_apply.argtypes = [vp, dp, dp, C.c_int, C.c_int]
     lib.fpc_pc_forward.argtypes = [vp, dp, dp, C.c_int]
     lib.fpc_gmres.argtypes = [vp, dp, dp, C.POINTER(SolverConfigC), C.POINTER(ReportC), dp, C.c_int, C.c_int]

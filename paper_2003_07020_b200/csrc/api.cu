@@ -313,6 +313,7 @@ struct fpc_plan_s {
   double2* d_Z = nullptr;  // half spectrum scratch (H x ns complex)
   double2* d_Zf = nullptr; // full spectrum (Nt x ns complex), InnerSweep::full only
   int sweep_mode = FPC_SWEEP_HALF;
+  int ordering = FPC_ORDER_REFERENCE;  // FPC_ORDER_COMMUTED: DST-first (kernels_commuted.cu)
   // GMRES workspace (grown on demand, reused across solves)
   std::vector<double*> basis;
   std::vector<double*> zbasis;  // z_j = P^{-1} V_j kept for x = Z y (see gmres_inner)
@@ -728,6 +729,18 @@ int fpc_plan_destroy(fpc_plan_t pl) {
   return FPC_OK;
 }
 
+int fpc_plan_set_ordering(fpc_plan_t pl, int ordering) {
+  if (!pl) return set_err(FPC_INVALID_ARGUMENT, "null plan");
+  return guarded([&] {
+    if (ordering != FPC_ORDER_REFERENCE && ordering != FPC_ORDER_COMMUTED)
+      throw InvalidArg{"fpc_plan_set_ordering: bad ordering"};
+    const fpc_problem_s* p = pl->prob;
+    if (ordering == FPC_ORDER_COMMUTED && (p->two_dim || p->ns + 1 > 8192))
+      throw Unsupported{"commuted ordering: 1D with n_space + 1 <= 8192 only"};
+    pl->ordering = ordering;
+  });
+}
+
 int fpc_plan_info(fpc_plan_t pl, double* alpha, double* margin, int* solve_count, int* n_warn) {
   if (!pl) return set_err(FPC_INVALID_ARGUMENT, "null plan");
   if (alpha) *alpha = pl->alpha;
@@ -756,6 +769,16 @@ static void pc_apply_dev(fpc_plan_s* pl, const double* v, double* z, double s_in
   }
   fpc_problem_s* p = pl->prob;
   cudaStream_t st = p->ctx->stream;
+  if (pl->ordering == FPC_ORDER_COMMUTED) {
+    // S per time level -> per-column time solve -> S per time level
+    double* U = reinterpret_cast<double*>(pl->d_Z);
+    LAUNCH("dst_pairs", st, fpc::launch_dst_pairs(v, U, p->ns, p->nt, s_in, p->ctx->tw, st));
+    LAUNCH("time_solve", st,
+           fpc::launch_time_solve(U, U, p->ns, p->nt, pl->d_sf, pl->d_sb, 1.0, pl->d_lambda, pl->d_sigma, p->dt,
+                                  p->ctx->tw, st, forward));
+    LAUNCH("dst_pairs", st, fpc::launch_dst_pairs(U, z, p->ns, p->nt, 1.0, p->ctx->tw, st));
+    return;
+  }
   LAUNCH("time_fwd", st, fpc::launch_time_fwd(v, pl->d_Z, p->ns, p->nt, pl->d_sf, s_in, p->ctx->tw, st));
   if (!p->two_dim)
     LAUNCH("tau_solve_1d", st,
@@ -1076,6 +1099,250 @@ static void gmres_inner(fpc_plan_s* pl, const double* b, double* x, double tol, 
   ck(cudaStreamSynchronize(S.st), "sync");  // hpin reuse boundary
 }
 
+// GMRES with delayed re-orthogonalisation (classical Gram-Schmidt twice, the second pass lagged
+// one step; the low-synchronisation DCGS2 of Bielich et al., in the Arnoldi form).  Same Krylov
+// space and the same least-squares problem as the reference's gmres_right (krylov.hpp:83-192:
+// Gram-Schmidt with re-orthogonalisation, which fires on every step of this preconditioned
+// system); per step the basis is read twice instead of three times:
+//   iteration j >= 1 has the once-orthogonalised candidate u~ (norm nu) of v_j in a buffer and
+//   runs w = A P^{-1} (u~/nu), then
+//   Q1  one pass: a = V^T u~, b = V^T w, <u~,w>, ||u~||^2, ||w||^2          (one sync)
+//       host: v_j = (u~ - V a)/rho, rho^2 = ||u~||^2 - ||a||^2 finalises Hessenberg column j-1;
+//       A P^{-1} v_j = (nu w - V_{0..j} H a)/rho by the Arnoldi relation, so the projections
+//       e = V_{0..j}^T A P^{-1} v_j follow from a, b and H without touching the vectors;
+//   Q2  one pass: u~ <- rho v_j, w <- A P^{-1} v_j - V_{0..j} e (the next candidate), ||w||^2.
+// The step's convergence test uses the candidate's norm for H_{j+1,j}; the next Q1 replaces it by
+// the re-orthogonalised value and redoes that Givens rotation (a 1e-13-relative change here).
+// With Z kept, z~_j = P^{-1}(u~_j/nu_j) and x = Z~ (T y), T upper triangular from the same a's.
+static void gmres_inner_lagged(fpc_plan_s* pl, const double* b, double* x, double tol, int max_iter,
+                               int* conv, int* steps_out, std::vector<double>& hist, double* last_rel,
+                               int* reorth_count) {
+  fpc_problem_s* p = pl->prob;
+  fpc_context_s* c = p->ctx;
+  GmresState S{pl, c, p->dim(), c->stream, {}, 0};
+  const size_t n = S.n;
+  cudaStream_t st = S.st;
+  const int stride = fpc_context_s::kPartialStride;
+  *conv = 0;
+  *steps_out = 0;
+  dots_into(S, {}, 0, b, true, 0);
+  ck(cudaMemcpyAsync(c->hpin, c->dscal, sizeof(double), cudaMemcpyDeviceToHost, st), "D2H");
+  ck(cudaStreamSynchronize(st), "sync");
+  const double norm_b = std::sqrt(c->hpin[0]);
+  if (norm_b == 0.0) {
+    ck(cudaMemsetAsync(x, 0, n * sizeof(double), st), "memset");
+    *conv = 1;
+    return;
+  }
+  if (!pl->d_z) pl->d_z = dalloc<double>(n + 2);
+  // V[i]: buffer of basis vector i (V[0] = b, read only); v_i = sc[i] * V[i] once final
+  std::vector<double*> V{const_cast<double*>(b)};
+  std::vector<double> sc{1.0 / norm_b};
+  std::vector<std::vector<double>> R;   // raw Hessenberg columns (final, except the newest)
+  std::vector<std::vector<double>> T;   // T[j][i]: Z_j = sum_i T[j][i] z~_i
+  std::vector<double> gc, gs, g{norm_b}, g_pre, nb_before;
+  bool keep_z = true;
+  std::vector<double*> zt;
+  auto rotate_column = [&](int j, std::vector<double> h) {
+    // apply the final rotations 0..j-1 to raw column j, then form rotation j; g[j], g[j+1] from g_pre[j]
+    for (int i = 0; i < j; ++i) {
+      const double hi = h[size_t(i)], hi1 = h[size_t(i) + 1];
+      h[size_t(i)] = gc[size_t(i)] * hi + gs[size_t(i)] * hi1;
+      h[size_t(i) + 1] = -gs[size_t(i)] * hi + gc[size_t(i)] * hi1;
+    }
+    const double hj = h[size_t(j)], hj1 = h[size_t(j) + 1];
+    const double rad = std::hypot(hj, hj1);
+    const double cs = rad > 0.0 ? hj / rad : 1.0;
+    const double sn = rad > 0.0 ? hj1 / rad : 0.0;
+    if (gc.size() <= size_t(j)) {
+      gc.push_back(cs);
+      gs.push_back(sn);
+      g_pre.push_back(g[size_t(j)]);
+      g.push_back(0.0);
+    } else {
+      gc[size_t(j)] = cs;
+      gs[size_t(j)] = sn;
+    }
+    g[size_t(j) + 1] = -sn * g_pre[size_t(j)];
+    g[size_t(j)] = cs * g_pre[size_t(j)];
+    h[size_t(j)] = rad;
+    h[size_t(j) + 1] = 0.0;
+    return h;
+  };
+  std::vector<std::vector<double>> Hr;  // rotated columns (for the back substitution)
+  int steps = 0;
+  double nu = 0.0;  // norm of the candidate in V[j]
+  for (int j = 0; j < max_iter; ++j) {
+    double* zj = keep_z ? zbasis_buf(pl, size_t(j), n, size_t(max_iter)) : nullptr;
+    if (!zj) {
+      keep_z = false;
+      zj = pl->d_z;
+    }
+    zt.push_back(zj);
+    double* W = basis_buf(pl, size_t(j), n);  // slot j holds basis vector j + 1
+    pc_apply_dev(pl, V[size_t(j)], zj, j == 0 ? sc[0] : 1.0 / nu);
+    matvec_dev(p, zj, W);
+    std::vector<double> col(size_t(j) + 2, 0.0);
+    double norm_before = 0.0, nu_next = 0.0;
+    if (j == 0) {
+      // first vector: plain pass h_0 = <v_0, w>, w -= h_0 v_0 (v_0 = b/||b|| is exact)
+      S.scales.assign(1, sc[0]);
+      dots_into(S, {b}, 1, W, true, 0);
+      ck(cudaMemcpyAsync(c->dvptr, V.data(), sizeof(double*), cudaMemcpyHostToDevice, st), "vptr");
+      ck(cudaMemcpyAsync(c->dscales, sc.data(), sizeof(double), cudaMemcpyHostToDevice, st), "scales");
+      LAUNCH("update", st, fpc::launch_update(c->dvptr, c->dscales, c->dscal, 1, W, n, c->partial, st));
+      LAUNCH("reduce", st, fpc::launch_reduce(c->partial, 1, 1, c->dscal + 512, false, st));
+      ck(cudaMemcpyAsync(c->hpin, c->dscal, 2 * sizeof(double), cudaMemcpyDeviceToHost, st), "D2H");
+      ck(cudaMemcpyAsync(c->hpin + 512, c->dscal + 512, sizeof(double), cudaMemcpyDeviceToHost, st), "D2H");
+      ck(cudaStreamSynchronize(st), "sync");
+      col[0] = c->hpin[0];
+      norm_before = std::sqrt(c->hpin[1]);
+      nu_next = std::sqrt(c->hpin[512]);
+      T.push_back({1.0});
+    } else {
+      // Q1: a = V^T u~, b = V^T w (+ <u~,w>, ||u~||^2, ||w||^2)
+      double* U = V[size_t(j)];
+      for (int g0 = 0; g0 < j; g0 += 16) {
+        const int cnt = std::min(16, j - g0);
+        fpc::VecSet16 vs{};
+        for (int i = 0; i < cnt; ++i) {
+          vs.v[i] = V[size_t(g0 + i)];
+          vs.s[i] = sc[size_t(g0 + i)];
+        }
+        LAUNCH("dots2", st, fpc::launch_dots2(vs, cnt, U, W, n, c->partial, stride, g0, g0 == 0, st));
+      }
+      LAUNCH("reduce", st, fpc::launch_reduce(c->partial, stride, fpc::kDots2X + 3, c->dscal, false, st));
+      ck(cudaMemcpyAsync(c->hpin, c->dscal, (fpc::kDots2X + 3) * sizeof(double), cudaMemcpyDeviceToHost, st),
+         "D2H");
+      ck(cudaStreamSynchronize(st), "sync");
+      std::vector<double> a(static_cast<size_t>(j)), bb(static_cast<size_t>(j));
+      double aa = 0.0, ab = 0.0;
+      for (int i = 0; i < j; ++i) {
+        a[size_t(i)] = c->hpin[i];
+        bb[size_t(i)] = c->hpin[fpc::kDots2B + i];
+        aa += a[size_t(i)] * a[size_t(i)];
+        ab += a[size_t(i)] * bb[size_t(i)];
+      }
+      const double beta = c->hpin[fpc::kDots2X], uu = c->hpin[fpc::kDots2X + 1], ww = c->hpin[fpc::kDots2X + 2];
+      const double rho = std::sqrt(std::max(uu - aa, 0.0));
+      ++*reorth_count;
+      // finalise column j-1 with the re-orthogonalised v_j and redo its rotation
+      std::vector<double>& rc = R[size_t(j) - 1];
+      for (int i = 0; i < j; ++i) rc[size_t(i)] += a[size_t(i)];
+      rc[size_t(j)] = rho;
+      Hr[size_t(j) - 1] = rotate_column(j - 1, rc);
+      const double rel_c = std::abs(g[size_t(j)]) / norm_b;
+      hist.back() = rel_c;
+      *last_rel = rel_c;
+      if (rel_c <= tol) {  // converged at step j after all (the estimate was just above tol)
+        *conv = 1;
+        break;
+      }
+      if (rho <= 1e-14 * std::max(1.0, nb_before[size_t(j) - 1])) break;  // krylov.hpp:160-165
+      sc.push_back(1.0 / rho);
+      // T column j: Z_j = (nu z~_j - sum_l a_l Z_l)/rho
+      std::vector<double> tj(size_t(j) + 1, 0.0);
+      tj[size_t(j)] = nu / rho;
+      for (int l = 0; l < j; ++l)
+        for (int i = 0; i <= l; ++i) tj[size_t(i)] -= a[size_t(l)] * T[size_t(l)][size_t(i)] / rho;
+      T.push_back(tj);
+      // gg = H_{0..j, 0..j-1} a (Arnoldi relation), e = V_{0..j}^T A P^{-1} v_j
+      std::vector<double> gg(size_t(j) + 1, 0.0);
+      for (int l = 0; l < j; ++l)
+        for (int k = 0; k <= l + 1; ++k) gg[size_t(k)] += R[size_t(l)][size_t(k)] * a[size_t(l)];
+      for (int k = 0; k < j; ++k) col[size_t(k)] = (nu * bb[size_t(k)] - gg[size_t(k)]) / rho;
+      col[size_t(j)] = (nu * (beta - ab) / rho - gg[size_t(j)]) / rho;
+      // Q2: U <- U - V a (= rho v_j);  W <- cw W + cu U + V cd (= the next candidate)
+      const double t = gg[size_t(j)] / rho + col[size_t(j)];
+      const double cw = nu / rho, cu = -t / rho;
+      for (int g0 = 0; g0 < j || g0 == 0; g0 += fpc::kMaxUpd2) {
+        const int cnt = std::min(fpc::kMaxUpd2, j - g0);
+        fpc::Update2Args ua{};
+        ua.cw = cw;
+        ua.cu = cu;
+        for (int i = 0; i < cnt; ++i) {
+          const int k = g0 + i;
+          ua.v[i] = V[size_t(k)];
+          ua.ca[i] = a[size_t(k)] * sc[size_t(k)];
+          ua.cd[i] = (-gg[size_t(k)] / rho - col[size_t(k)] + t * a[size_t(k)] / rho) * sc[size_t(k)];
+        }
+        const bool last = g0 + cnt >= j;
+        LAUNCH("update2", st, fpc::launch_update2(ua, cnt, g0 == 0, last, U, W, n, c->partial, st));
+        if (last) break;
+      }
+      LAUNCH("reduce", st, fpc::launch_reduce(c->partial, 1, 1, c->dscal + 512, false, st));
+      ck(cudaMemcpyAsync(c->hpin + 512, c->dscal + 512, sizeof(double), cudaMemcpyDeviceToHost, st), "D2H");
+      ck(cudaStreamSynchronize(st), "sync");
+      nu_next = std::sqrt(c->hpin[512]);
+      double e2 = 0.0;
+      for (int k = 0; k <= j; ++k) e2 += col[size_t(k)] * col[size_t(k)];
+      norm_before = std::sqrt(e2 + nu_next * nu_next);  // ||A P^{-1} v_j||
+      (void)ww;
+    }
+    col[size_t(j) + 1] = nu_next;  // estimate until the next Q1 re-orthogonalises
+    R.push_back(col);
+    nb_before.push_back(norm_before);
+    Hr.push_back(rotate_column(j, col));
+    steps = j + 1;
+    const double rel = std::abs(g[size_t(j) + 1]) / norm_b;
+    hist.push_back(rel);
+    *last_rel = rel;
+    if (rel <= tol) {
+      *conv = 1;
+      break;
+    }
+    if (nu_next <= 1e-14 * std::max(1.0, norm_before)) break;
+    V.push_back(W);
+    nu = nu_next;
+  }
+  // back substitution (krylov.hpp:171-179) on the rotated columns
+  std::vector<double> y(size_t(steps), 0.0);
+  for (int i = steps - 1; i >= 0; --i) {
+    double sacc = g[size_t(i)];
+    for (int k = i + 1; k < steps; ++k) sacc -= Hr[size_t(k)][size_t(i)] * y[size_t(k)];
+    y[size_t(i)] = sacc / Hr[size_t(i)][size_t(i)];
+  }
+  std::vector<double> coef(size_t(steps), 0.0), scales(size_t(steps), 1.0);
+  std::vector<const double*> ptr(static_cast<size_t>(steps));
+  if (keep_z) {
+    // x = Z y = Z~ (T y)
+    for (int jj = 0; jj < steps; ++jj)
+      for (int i = 0; i <= jj; ++i) coef[size_t(i)] += T[size_t(jj)][size_t(i)] * y[size_t(jj)];
+    for (int i = 0; i < steps; ++i) ptr[size_t(i)] = zt[size_t(i)];
+  } else {
+    for (int i = 0; i < steps; ++i) {
+      coef[size_t(i)] = y[size_t(i)];
+      scales[size_t(i)] = sc[size_t(i)];
+      ptr[size_t(i)] = V[size_t(i)];
+    }
+  }
+  ck(cudaMemcpyAsync(c->dvptr, ptr.data(), ptr.size() * sizeof(double*), cudaMemcpyHostToDevice, st), "vptr");
+  std::memcpy(c->hpin + 1024, scales.data(), scales.size() * sizeof(double));
+  ck(cudaMemcpyAsync(c->dscales, c->hpin + 1024, scales.size() * sizeof(double), cudaMemcpyHostToDevice, st),
+     "scales");
+  std::memcpy(c->hpin + 600, coef.data(), coef.size() * sizeof(double));
+  ck(cudaMemcpyAsync(c->dscal + 600, c->hpin + 600, coef.size() * sizeof(double), cudaMemcpyHostToDevice, st),
+     "coef");
+  if (keep_z) {
+    LAUNCH("lincomb", st, fpc::launch_lincomb(c->dvptr, c->dscales, c->dscal + 600, steps, x, n, st));
+  } else {
+    double* u = pl->d_z;
+    LAUNCH("lincomb", st, fpc::launch_lincomb(c->dvptr, c->dscales, c->dscal + 600, steps, u, n, st));
+    pc_apply_dev(pl, u, x, 1.0);
+  }
+  *steps_out = steps;
+  ck(cudaStreamSynchronize(st), "sync");
+}
+
+// GS scheme: FPC_GS=cgs2 selects the reference-shaped CGS + conditional re-orthogonalisation loop
+static bool use_lagged_gs(int max_iter) {
+  static const int mode = [] {
+    const char* e = std::getenv("FPC_GS");
+    return (e && std::string(e) == "cgs2") ? 0 : 1;
+  }();
+  return mode == 1 && max_iter <= 120;
+}
+
 static double resid_norm_dev(fpc_plan_s* pl, const double* b, const double* x) {
   fpc_problem_s* p = pl->prob;
   fpc_context_s* c = p->ctx;
@@ -1099,7 +1366,8 @@ static void gmres_dev(fpc_plan_s* pl, const double* b, double* x, const fpc_solv
   int reorth = 0;
   if (cfg.restart <= 0 || cfg.restart >= cfg.max_iter) {
     int conv = 0, steps = 0;
-    gmres_inner(pl, b, x, cfg.tol, cfg.max_iter, &conv, &steps, hist, &last_rel, &reorth);
+    (use_lagged_gs(cfg.max_iter) ? gmres_inner_lagged : gmres_inner)(pl, b, x, cfg.tol, cfg.max_iter, &conv, &steps,
+                                                                     hist, &last_rel, &reorth);
     rep->converged = conv;
     rep->iterations = steps;
   } else {
@@ -1128,7 +1396,8 @@ static void gmres_dev(fpc_plan_s* pl, const double* b, double* x, const fpc_solv
       const int m = std::min(cfg.restart, budget);
       int conv = 0, steps = 0;
       const size_t h0 = hist.size();
-      gmres_inner(pl, r, pl->d_d, cfg.tol * norm_b / norm_r, m, &conv, &steps, hist, &last_rel, &reorth);
+      (use_lagged_gs(m) ? gmres_inner_lagged : gmres_inner)(pl, r, pl->d_d, cfg.tol * norm_b / norm_r, m, &conv, &steps,
+                                                            hist, &last_rel, &reorth);
       for (size_t i = h0; i < hist.size(); ++i) hist[i] *= norm_r / norm_b;
       if (last_rel >= 0.0) last_rel *= norm_r / norm_b;
       LAUNCH("axpy", c->stream, fpc::launch_axpy(1.0, pl->d_d, x, n, c->stream));

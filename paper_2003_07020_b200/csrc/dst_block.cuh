@@ -15,6 +15,8 @@
 // grows like sqrt(N); that is measurably worse than the reference at large N, so it is not used.)
 // The identities are real-linear with real coefficients, so they hold for complex rows directly.
 #pragma once
+#include <type_traits>
+
 #include "fft_block.cuh"
 
 #ifndef FPC_DST_PH
@@ -35,10 +37,10 @@ namespace fpc {
 // two barriers less per DST).
 // gsrc != nullptr: the row is read straight from global memory (f_j = gsrc[j-1]) instead of the
 // buffer (saves the staging pass of the first DST of a tau solve)
-template <int LOGN, int BH>
+// Src: f(j) -> f_j, j = 1..N-1 (the buffer, a global row, or a gather of two real rows)
+template <int LOGN, int BH, class Src>
 __device__ __forceinline__ void dst_pre_folded(double2* r, double2* hv, const double2* __restrict__ tw2N,
-                                               const double2* gsrc) {
-  auto f = [&](int j) -> double2 { return gsrc ? gsrc[j - 1] : r[pad16(j)]; };
+                                               Src f) {
   constexpr int N = 1 << LOGN, M = N / 2, NT = N / 16;
   constexpr int KQ = (M / 2) / NT;  // quadruples j < M/2 per thread; j = M/2 goes to thread 0
   static_assert(KQ * NT == M / 2, "quadruple count must divide the thread count");
@@ -99,9 +101,9 @@ __device__ __forceinline__ void dst_pre_folded(double2* r, double2* hv, const do
   }
 }
 
-template <int LOGN, int BS, int BH, int OUT_SHIFT, bool FOLD = false>
+template <int LOGN, int BS, int BH, int OUT_SHIFT, bool FOLD = false, class Src = void*>
 __device__ __forceinline__ void block_dst(double2* s, double2* h, const double2* __restrict__ twb,
-                                          double scale, const double2* gsrc = nullptr) {
+                                          double scale, const double2* gsrc = nullptr, Src src = nullptr) {
   constexpr int N = 1 << LOGN, M = N / 2;
   constexpr int E = N < 16 ? N : 16;  // complex values per thread in the N-point FFT
   constexpr int TPB = N / E;          // threads per row
@@ -111,7 +113,12 @@ __device__ __forceinline__ void block_dst(double2* s, double2* h, const double2*
   const double2* tw2N = twb + 2 * N;  // e^{-i pi j/N}
   if constexpr (FOLD) {
     static_assert(LOGN % 4 == 1 && LOGN >= 5, "fold needs N = 2 * 16^k");
-    dst_pre_folded<LOGN, BH>(s, h, tw2N, gsrc);
+    if constexpr (!std::is_same<Src, void*>::value)
+      dst_pre_folded<LOGN, BH>(s, h, tw2N, src);
+    else if (gsrc)
+      dst_pre_folded<LOGN, BH>(s, h, tw2N, [&](int j) { return gsrc[j - 1]; });
+    else
+      dst_pre_folded<LOGN, BH>(s, h, tw2N, [&](int j) { return s[pad16(j)]; });
     __syncthreads();
     FPC_DST_PH(0);
     fft_passes<LOGN, 1, BS, E, 2, CtaSync>(s, twb + N, int(threadIdx.x), nthr);

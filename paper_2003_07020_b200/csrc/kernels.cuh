@@ -102,6 +102,37 @@ cudaError_t launch_axpy(double a, const double* x, double* y, size_t n, cudaStre
 // y = b - y
 cudaError_t launch_rsub(const double* b, double* y, size_t n, cudaStream_t st);
 
+// ---- delayed re-orthogonalisation Gram-Schmidt (api.cu gmres_inner_lagged) ----------------
+constexpr int kDots2B = 128;  // partial column offset of the b_i = <v_i, W> block
+constexpr int kDots2X = 256;  // partial columns of <U,W>, <U,U>, <W,W>
+struct VecSet16 {
+  const double* v[16];
+  double s[16];
+};
+// partial[blk*stride + col0 + i] = s_i <v_i, U>, [.. + kDots2B + col0 + i] = s_i <v_i, W> (i < nv <= 16),
+// extra: [.. + kDots2X + 0..2] = <U,W>, <U,U>, <W,W>
+cudaError_t launch_dots2(const VecSet16& vs, int nv, const double* U, const double* W, size_t n,
+                         double* partial, int stride, int col0, bool extra, cudaStream_t st);
+constexpr int kMaxUpd2 = 24;
+struct Update2Args {
+  const double* v[kMaxUpd2];
+  double ca[kMaxUpd2];
+  double cd[kMaxUpd2];
+  double cu, cw;
+};
+// U <- U - sum ca_i v_i; W <- (first ? cw W + cu U_old : W) + sum cd_i v_i; norm: partial = ||W||^2
+cudaError_t launch_update2(const Update2Args& a, int nv, bool first, bool norm, double* U, double* W,
+                           size_t n, double* partial, cudaStream_t st);
+
+// ---- commuted preconditioner ordering (kernels_commuted.cu), 1D --------------
+// out = S v per time level, levels (k, k + Nt/2) paired in one complex row; scale s_in
+cudaError_t launch_dst_pairs(const double* v, double* out, int n_space, int n_time, double s_in,
+                             const double2* tw_base, cudaStream_t st);
+// per spatial column p: z = D^{-1} F^* diag(1/(lambda_n - dt sigma_p)) F D (s_in u)  (forward: multiply)
+cudaError_t launch_time_solve(const double* u, double* z, int n_space, int n_time, const double* scale_fwd,
+                              const double* scale_bwd, double s_in, const double2* lambda, const double* sigma,
+                              double dt, const double2* tw_base, cudaStream_t st, bool forward);
+
 // ---- BiCGSTAB vector kernels (krylov.hpp:204-280) -------------------------------------------
 // p = r (first) or r + beta (p - omega v)
 cudaError_t launch_bicg_p(const double* r, const double* v, double* p, double beta, double omega,

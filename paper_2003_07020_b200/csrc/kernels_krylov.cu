@@ -390,3 +390,174 @@ cudaError_t launch_bicg_x(double* x, const double* p, double* r, const double* t
 }
 
 }  // namespace fpc
+
+// ---------------------------------------------------------------------------------------------
+// Delayed re-orthogonalisation Gram-Schmidt (two basis passes per Arnoldi step; api.cu
+// gmres_inner_lagged).  Q1 = k_dots2: a_i = s_i <v_i, U>, b_i = s_i <v_i, W> (+ <U,W>, <U,U>,
+// <W,W>).  Q2 = k_update2: U' = U - sum ca_i v_i, W' = cw W + cu U + sum cd_i v_i, ||W'||^2.
+namespace fpc {
+
+// partial[blk*stride + col0 + i] = a_i, [.. + kDots2B + col0 + i] = b_i, [.. + kDots2X + 0..2] =
+// <U,W>, <U,U>, <W,W> (EXTRA only)
+template <int NV, bool EXTRA>
+__global__ void __launch_bounds__(kDotsThreads)
+    k_dots2(VecSet16 vs, const double* __restrict__ U, const double* __restrict__ W, size_t n,
+            double* __restrict__ partial, int stride, int col0) {
+  constexpr int NACC = 2 * NV + (EXTRA ? 3 : 0);
+  double acc[NACC > 0 ? NACC : 1];
+#pragma unroll
+  for (int i = 0; i < NACC; ++i) acc[i] = 0.0;
+  const size_t n2 = n / 2;
+  const double2* u2 = reinterpret_cast<const double2*>(U);
+  const double2* w2 = reinterpret_cast<const double2*>(W);
+  for (size_t e = size_t(blockIdx.x) * kDotsThreads + threadIdx.x; e < n2;
+       e += size_t(kDotsGrid) * kDotsThreads) {
+    const double2 uv = u2[e], wv = w2[e];
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      const double2 x = reinterpret_cast<const double2*>(vs.v[i])[e];
+      acc[i] = fma(x.x, uv.x, acc[i]);
+      acc[i] = fma(x.y, uv.y, acc[i]);
+      acc[NV + i] = fma(x.x, wv.x, acc[NV + i]);
+      acc[NV + i] = fma(x.y, wv.y, acc[NV + i]);
+    }
+    if (EXTRA) {
+      acc[2 * NV] = fma(uv.x, wv.x, acc[2 * NV]);
+      acc[2 * NV] = fma(uv.y, wv.y, acc[2 * NV]);
+      acc[2 * NV + 1] = fma(uv.x, uv.x, acc[2 * NV + 1]);
+      acc[2 * NV + 1] = fma(uv.y, uv.y, acc[2 * NV + 1]);
+      acc[2 * NV + 2] = fma(wv.x, wv.x, acc[2 * NV + 2]);
+      acc[2 * NV + 2] = fma(wv.y, wv.y, acc[2 * NV + 2]);
+    }
+  }
+  if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
+    const double ul = U[n - 1], wl = W[n - 1];
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      const double x = vs.v[i][n - 1];
+      acc[i] = fma(x, ul, acc[i]);
+      acc[NV + i] = fma(x, wl, acc[NV + i]);
+    }
+    if (EXTRA) {
+      acc[2 * NV] = fma(ul, wl, acc[2 * NV]);
+      acc[2 * NV + 1] = fma(ul, ul, acc[2 * NV + 1]);
+      acc[2 * NV + 2] = fma(wl, wl, acc[2 * NV + 2]);
+    }
+  }
+  __shared__ double outb[NACC > 0 ? NACC : 1];
+  block_reduce_store<NACC>(acc, outb);
+  __syncthreads();
+  for (int t = threadIdx.x; t < NACC; t += kDotsThreads) {
+    double* prow = partial + size_t(blockIdx.x) * stride;
+    if (t < NV)
+      prow[col0 + t] = outb[t] * vs.s[t];
+    else if (t < 2 * NV)
+      prow[kDots2B + col0 + (t - NV)] = outb[t] * vs.s[t - NV];
+    else
+      prow[kDots2X + (t - 2 * NV)] = outb[t];
+  }
+}
+
+cudaError_t launch_dots2(const VecSet16& vs, int nv, const double* U, const double* W, size_t n,
+                         double* partial, int stride, int col0, bool extra, cudaStream_t st) {
+#define D2(NVV)                                                                                      \
+  case NVV:                                                                                          \
+    if (extra)                                                                                       \
+      k_dots2<NVV, true><<<kDotsGrid, kDotsThreads, 0, st>>>(vs, U, W, n, partial, stride, col0);    \
+    else                                                                                             \
+      k_dots2<NVV, false><<<kDotsGrid, kDotsThreads, 0, st>>>(vs, U, W, n, partial, stride, col0);   \
+    break;
+  switch (nv) {
+    case 0:
+      k_dots2<0, true><<<kDotsGrid, kDotsThreads, 0, st>>>(vs, U, W, n, partial, stride, col0);
+      break;
+    D2(1) D2(2) D2(3) D2(4) D2(5) D2(6) D2(7) D2(8)
+    D2(9) D2(10) D2(11) D2(12) D2(13) D2(14) D2(15) D2(16)
+    default:
+      return cudaErrorInvalidValue;
+  }
+#undef D2
+  return cudaGetLastError();
+}
+
+// U <- U - sum_i ca_i v_i ; W <- cw W + cu U_old + sum_i cd_i v_i  (coefficients already carry the
+// basis scales); NORM: partial[blk] = ||W_new||^2.  FIRST: the cw/cu terms are applied (a later
+// group of basis vectors only adds its sums in place).
+template <int NV, bool FIRST, bool NORM>
+__global__ void __launch_bounds__(kDotsThreads)
+    k_update2(Update2Args a, double* __restrict__ U, double* __restrict__ W, size_t n,
+              double* __restrict__ partial) {
+  double acc[1] = {0.0};
+  const size_t n2 = n / 2;
+  double2* u2 = reinterpret_cast<double2*>(U);
+  double2* w2 = reinterpret_cast<double2*>(W);
+  for (size_t e = size_t(blockIdx.x) * kDotsThreads + threadIdx.x; e < n2;
+       e += size_t(kDotsGrid) * kDotsThreads) {
+    const double2 uv = u2[e], wv = w2[e];
+    double2 nu = uv, nw;
+    if (FIRST) {
+      nw.x = fma(a.cw, wv.x, a.cu * uv.x);
+      nw.y = fma(a.cw, wv.y, a.cu * uv.y);
+    } else {
+      nw = wv;
+    }
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      const double2 x = reinterpret_cast<const double2*>(a.v[i])[e];
+      nu.x = fma(-a.ca[i], x.x, nu.x);
+      nu.y = fma(-a.ca[i], x.y, nu.y);
+      nw.x = fma(a.cd[i], x.x, nw.x);
+      nw.y = fma(a.cd[i], x.y, nw.y);
+    }
+    u2[e] = nu;
+    w2[e] = nw;
+    if (NORM) {
+      acc[0] = fma(nw.x, nw.x, acc[0]);
+      acc[0] = fma(nw.y, nw.y, acc[0]);
+    }
+  }
+  if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
+    const double ul = U[n - 1], wl = W[n - 1];
+    double nu = ul, nw = FIRST ? fma(a.cw, wl, a.cu * ul) : wl;
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      const double x = a.v[i][n - 1];
+      nu = fma(-a.ca[i], x, nu);
+      nw = fma(a.cd[i], x, nw);
+    }
+    U[n - 1] = nu;
+    W[n - 1] = nw;
+    if (NORM) acc[0] = fma(nw, nw, acc[0]);
+  }
+  if (NORM) {
+    __shared__ double outb[1];
+    block_reduce_store<1>(acc, outb);
+    __syncthreads();
+    if (threadIdx.x == 0) partial[blockIdx.x] = outb[0];
+  }
+}
+
+cudaError_t launch_update2(const Update2Args& a, int nv, bool first, bool norm, double* U, double* W,
+                           size_t n, double* partial, cudaStream_t st) {
+#define U2(NVV)                                                                                        \
+  case NVV:                                                                                            \
+    if (first && norm)                                                                                 \
+      k_update2<NVV, true, true><<<kDotsGrid, kDotsThreads, 0, st>>>(a, U, W, n, partial);             \
+    else if (first)                                                                                    \
+      k_update2<NVV, true, false><<<kDotsGrid, kDotsThreads, 0, st>>>(a, U, W, n, partial);            \
+    else if (norm)                                                                                     \
+      k_update2<NVV, false, true><<<kDotsGrid, kDotsThreads, 0, st>>>(a, U, W, n, partial);            \
+    else                                                                                               \
+      k_update2<NVV, false, false><<<kDotsGrid, kDotsThreads, 0, st>>>(a, U, W, n, partial);           \
+    break;
+  switch (nv) {
+    U2(0) U2(1) U2(2) U2(3) U2(4) U2(5) U2(6) U2(7) U2(8) U2(9) U2(10) U2(11) U2(12)
+    U2(13) U2(14) U2(15) U2(16) U2(17) U2(18) U2(19) U2(20) U2(21) U2(22) U2(23) U2(24)
+    default:
+      return cudaErrorInvalidValue;
+  }
+#undef U2
+  return cudaGetLastError();
+}
+
+}  // namespace fpc

@@ -296,6 +296,15 @@ class PreconditionerKind:
         return self._auto
 
 
+class Ordering(IntEnum):
+    """Factor ordering of the half-sweep preconditioner apply.  `reference`: time FFT, tau solves
+    per retained frequency, inverse time FFT (alpha_circulant.hpp:137-199).  `commuted`: DST per
+    time level, per-mode time solve, DST per time level (same operator up to
+    rounding, 1D only)."""
+    reference = N.FPC_ORDER_REFERENCE
+    commuted = N.FPC_ORDER_COMMUTED
+
+
 class InnerSweep(IntEnum):
     half = N.FPC_SWEEP_HALF
     full = N.FPC_SWEEP_FULL
@@ -322,6 +331,11 @@ class AlphaCirculantPlan:
         k = np.arange(self.n_time) / self.n_time
         self.scale_fwd = self.alpha ** k
         self.scale_bwd = self.alpha ** (-k)
+        self.ordering = Ordering.reference
+
+    def set_ordering(self, ordering: "Ordering") -> None:
+        N.check(self.lib.fpc_plan_set_ordering(self.h, int(ordering)))
+        self.ordering = Ordering(ordering)
 
     def mirror_index(self, n: int) -> int:
         return self.n_time - n + 2
@@ -334,7 +348,8 @@ class AlphaCirculantPlan:
             pass
 
 
-def build_plan(kind: PreconditionerKind, n_time: int, dt: float, op) -> AlphaCirculantPlan:
+def build_plan(kind: PreconditionerKind, n_time: int, dt: float, op,
+               ordering: Ordering = Ordering.reference) -> AlphaCirculantPlan:
     """alpha_circulant.hpp:83-126.  `op` is the AllAtOnceOperator whose Jacobian the reference
     passes (the device plan shares its spectra)."""
     if n_time < 3:
@@ -345,7 +360,10 @@ def build_plan(kind: PreconditionerKind, n_time: int, dt: float, op) -> AlphaCir
         raise TypeError("build_plan: pass the AllAtOnceOperator (device operator)")
     if op.n_time() != n_time or abs(op.dt() - dt) > 0.0:
         raise ValueError("build_plan: n_time/dt must match the operator")
-    return AlphaCirculantPlan(op, kind.alpha_for(dt))
+    plan = AlphaCirculantPlan(op, kind.alpha_for(dt))
+    if ordering != Ordering.reference:
+        plan.set_ordering(ordering)
+    return plan
 
 
 def apply_inverse(plan: AlphaCirculantPlan, v, out=None, sweep: InnerSweep = InnerSweep.half):

@@ -1,0 +1,60 @@
+"""Commuted preconditioner ordering on the B200 (kernels_commuted.cu) vs the C
+oracle's reference-ordering apply: same operator up to rounding.  PC apply / forward at sizes across
+every kernel instantiation, GMRES iteration counts and x, and the 2D / oversize rejections."""
+import numpy as np
+import pytest
+
+import paper_2003_07020_b200 as fp
+from paper_2003_07020_b200 import problems
+
+pytestmark = pytest.mark.gpu
+
+
+def rel(a, b):
+    return np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300)
+
+
+def make(gamma, ns, nt, alpha=0.0):
+    h, dt = 1.0 / (ns + 1), 1.0 / nt
+    op = fp.AllAtOnceOperator(fp.TimeStencil(nt), fp.RieszJacobian1D(gamma, 1.0, h, ns), dt)
+    kind = fp.PreconditionerKind.generalized() if alpha <= 0 else fp.PreconditionerKind.with_alpha(alpha)
+    return op, fp.build_plan(kind, nt, dt, op, ordering=fp.Ordering.commuted), h, dt
+
+
+@pytest.mark.parametrize("ns,nt", [(3, 4), (15, 8), (31, 64), (255, 16), (1023, 256), (4095, 32),
+                                   (8191, 64), (511, 2048), (63, 16384)])
+def test_commuted_pc_vs_oracle(oracle, ns, nt):
+    op, plan, h, dt = make(1.5, ns, nt)
+    po = oracle.problem_1d(1.5, 1.0, h, ns, nt, dt).build_plan()
+    v = np.random.default_rng(ns * 7 + nt).uniform(-1, 1, ns * nt)
+    assert rel(fp.apply_inverse(plan, v), po.pc_apply(v)) <= 1e-12
+    assert rel(fp.apply_forward(plan, v), po.pc_forward(v)) <= 1e-12
+
+
+@pytest.mark.parametrize("gamma,alpha", [(1.2, 0.0), (1.8, 1.0)])
+def test_commuted_gmres_vs_oracle(oracle, gamma, alpha):
+    ns, nt = 1023, 128
+    op, plan, h, dt = make(gamma, ns, nt, alpha)
+    po = oracle.problem_1d(gamma, 1.0, h, ns, nt, dt).build_plan(alpha)
+    b = np.random.default_rng(3).uniform(-1, 1, ns * nt)
+    res = fp.gmres_right(op, plan, b, fp.SolverConfig(tol=1e-10, max_iter=200, restart=20))
+    xo, ro = po.gmres(b, 1e-10, 200, restart=20)
+    assert abs(res.report.iterations - ro.iterations) <= 1
+    assert rel(res.x, xo) <= 1e-10
+    bi = fp.bicgstab_left(op, plan, b, fp.SolverConfig(tol=1e-10, max_iter=200))
+    xb, rb = po.bicgstab(b, 1e-10, 200)
+    assert abs(bi.report.iterations - rb.iterations) <= 1 and rel(bi.x, xb) <= 1e-10
+
+
+def test_commuted_switch_and_rejections():
+    op, plan, h, dt = make(1.5, 255, 64)
+    v = np.random.default_rng(1).uniform(-1, 1, 255 * 64)
+    zc = fp.apply_inverse(plan, v)
+    plan.set_ordering(fp.Ordering.reference)
+    zr = fp.apply_inverse(plan, v)
+    assert rel(zc, zr) <= 1e-12
+    op2 = fp.AllAtOnceOperator(fp.TimeStencil(8), fp.RieszJacobian2D(1.5, 1.5, 1, 1, 1 / 8, 7), 1 / 8)
+    with pytest.raises(NotImplementedError):
+        fp.build_plan(fp.PreconditionerKind.generalized(), 8, 1 / 8, op2, ordering=fp.Ordering.commuted)
+    with pytest.raises(ValueError):
+        plan.set_ordering(7)
