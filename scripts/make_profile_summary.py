@@ -14,7 +14,7 @@ col = lambda r, name: r[hdr.index(name)] if name in hdr else ""
 # map kernel names to the library's launch categories (bench.py roofline keys)
 cats = [("k_matvec_split", "matvec_1d"), ("k_matvec_1d_split", "matvec_1d"), ("k_matvec_1d", "matvec_1d"), ("k_matvec_2d", "matvec_2d"),
         ("k_time_fwd", "time_fwd"), ("k_time_inv", "time_inv"), ("k_tau_solve_1d", "tau_solve_1d"),
-        ("k_tau_2d", "tau_solve_2d"), ("k_update_dots", "update_dots"), ("k_dots", "dots"), ("k_update", "update")]
+        ("k_tau_2d", "tau_solve_2d"), ("k_update_dots", "update_dots"), ("k_dots2", "dots2"), ("k_update2", "update2"), ("k_dots", "dots"), ("k_update", "update")]
 out = [f"# ncu summary `{tag}` (B200, `--set full --clock-control none`, config 1 bench)\n",
        "Per-kernel figures of one launch each (ncu replays: cold-cache, serialised).\n",
        "| kernel | time (us) | DRAM read (MB) | DRAM write (MB) | DRAM % peak | fp64 pipe % | L1/smem % | warps active % | regs | top stalls |",
