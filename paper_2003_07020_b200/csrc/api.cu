@@ -498,6 +498,19 @@ int fpc_problem_create_1d(fpc_context_t c, double gamma, double kappa, double h,
     p->log_m = ilog2_exact(L / 2);
     std::vector<double> e = circulant_eigs(p->colx);
     for (double& x : e) x *= -dt / (2.0 * double(L));
+    if (p->log_m == 13 || p->log_m == 14) {
+      // the 2-CTA matvec's per-rank pair table (kernels_mv.cu): at double offset eigq_offset(M),
+      // {eig[kap], eig[M - kap]} for task t of rank q, kap = q ? 2t + 1 : 2t + 2
+      const size_t M = L / 2, H = M / 2;
+      e.resize(fpc::eigq_offset(int(M)) + 4 * (H / 2), 0.0);
+      double* eq = e.data() + fpc::eigq_offset(int(M));
+      for (int q = 0; q < 2; ++q)
+        for (size_t t = 0; t < H / 2; ++t) {
+          const size_t kap = q ? 2 * t + 1 : 2 * t + 2;
+          eq[2 * (q * (H / 2) + t)] = e[kap];
+          eq[2 * (q * (H / 2) + t) + 1] = e[M - kap];
+        }
+    }
     p->d_eig = dalloc<double>(e.size());
     ck(cudaMemcpy(p->d_eig, e.data(), e.size() * sizeof(double), cudaMemcpyHostToDevice), "eig");
     *out = p;

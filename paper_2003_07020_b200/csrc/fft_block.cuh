@@ -115,7 +115,8 @@ struct Dft<4, S> {
   }
 };
 
-// Twiddle table access: tw points at the size-N table, tw[t] = e^{-2 pi i t / N}, 0 <= t < N.
+// Twiddle table access: tw points at a size-N table, tw[t] = e^{-2 pi i t / N}, 0 <= t < N (every
+// table lives at tw_base + N, so the tables of all sizes are reachable from any one of them).
 template <int S>
 __device__ __forceinline__ double2 twid(const double2* __restrict__ tw, int t) {
   const double2 w = __ldg(tw + t);
@@ -192,7 +193,10 @@ __device__ __forceinline__ void stockham_pass(double2* s, const double2* __restr
 #pragma unroll
     for (int r = 0; r < R; ++r) v[q][r] = base[pad16(j + r * NB)];
     const int jm = j & (NS - 1);
-    if constexpr (NS > 1) apply_twiddles<R, S>(v[q], tw, jm * (N / (NS * R)));
+    // w = e^{-2 pi i jm/(NS R)}: read from the dense size-(NS R) table (tw_base + NS R), not the
+    // size-N table at stride N/(NS R) -- the same doubles (power-of-two index scaling), a much
+    // smaller L1 footprint
+    if constexpr (NS > 1) apply_twiddles<R, S>(v[q], tw - N + NS * R, jm);
     Dft<R, S>::run(v[q]);
     dst[q] = b * BS + (j - jm) * R + jm;  // buffer base + logical offset (pad applied below)
   }

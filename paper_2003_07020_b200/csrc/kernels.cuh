@@ -9,6 +9,13 @@ namespace fpc {
 // t < N, lives at tw_base + N.
 constexpr int kMaxLogTw = 17;
 
+// Shared-memory carveout for a kernel: the smallest supported shared-memory capacity (sm_100: 0, 8,
+// 16, 32, 64, 100, 132, 164, 196, 228 KB per SM) that still holds the CTAs per SM the kernel's
+// register budget allows (threads: <=128 -> 4, <=256 -> 2, else 1), so the rest of the 256 KB
+// L1/shared array stays L1 for the twiddle and eigenvalue tables.  FPC_CARVEOUT=max restores
+// the maximum shared-memory carveout.
+int carveout_pct(size_t dyn_smem, int threads);
+
 // ---- 1D all-at-once matvec (all_at_once.hpp:33-55 + toeplitz.hpp:41-57) --------------------
 // y_k = C-stencil(v)_k + IFFT(eig' .* FFT(pad(v_k)))  with eig' = -dt*eig/(2L) pre-folded.
 // koff = global time level of v's first block (time-sharded callers: the two previous blocks
@@ -17,7 +24,10 @@ cudaError_t launch_matvec_1d(const double* v, double* y, int n_space, int n_time
                              const double* eig_scaled, const double2* tw_base, cudaStream_t st,
                              int koff = 0);
 
-// M = 8192 / 16384 (Ns up to 8191 / 16383) on a 2-CTA cluster (kernels_mv.cu)
+// M = 8192 / 16384 (Ns up to 8191 / 16383) on a 2-CTA cluster (kernels_mv.cu).  eig_scaled also
+// holds, at double offset eigq_offset(M), the per-rank table {eig'[kap], eig'[M - kap]} (kap = 2t+2
+// for rank 0, 2t+1 for rank 1, t < M/4) the kernel's spectral product reads contiguously.
+__host__ __device__ constexpr int eigq_offset(int m) { return (m + 1 + 1) & ~1; }
 cudaError_t launch_matvec_split(const double* v, double* y, int n_space, int n_time, int log_m, int koff,
                                 const double* eig_scaled, const double2* tw_base, cudaStream_t st);
 

@@ -435,8 +435,8 @@ __global__ void __launch_bounds__(TauGeo<LOGM>::G::NT, minb(TauGeo<LOGM>::G::NT)
 // launchers
 // =====================================================================================
 template <class K>
-static cudaError_t prep(K kernel, size_t smem) {
-  cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+static cudaError_t prep(K kernel, size_t smem, int threads = 1024) {
+  cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, carveout_pct(smem, threads));
   if (e != cudaSuccess) return e;
   if (smem > 48 * 1024)
     return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
@@ -468,7 +468,7 @@ cudaError_t launch_matvec_rows(const double* v, double* y, int len, int nrows, i
 #define CALL(LM)                                                                          \
   {                                                                                       \
     using G = Geo<LM, kTotMv, 16>;                                                        \
-    if ((err = prep(k_matvec_1d<LM>, MvGeo<LM>::SMEM)) != cudaSuccess) return err;        \
+    if ((err = prep(k_matvec_1d<LM>, MvGeo<LM>::SMEM, Geo<LM, kTotMv, 16>::NT)) != cudaSuccess) return err;        \
     k_matvec_1d<LM><<<(nrows + G::B - 1) / G::B, G::NT, MvGeo<LM>::SMEM, st>>>(           \
         v, y, len, nrows, rpt, sstride, koff, eig_scaled, tw_base);                       \
   }
@@ -503,7 +503,7 @@ cudaError_t launch_time_fwd(const double* v, double2* Z, int n_space, int n_time
 #define CALL(LM)                                                                          \
   {                                                                                       \
     using G = Geo<LM, tot_t<LM>()>;                                                             \
-    if ((err = prep(k_time_fwd<LM>, G::SMEM)) != cudaSuccess) return err;                 \
+    if ((err = prep(k_time_fwd<LM>, G::SMEM, G::NT)) != cudaSuccess) return err;                 \
     k_time_fwd<LM><<<(n_space + G::B - 1) / G::B, G::NT, G::SMEM, st>>>(                  \
         v, Z, n_space, scale_fwd, s_in, tw_base);                                         \
   }
@@ -519,7 +519,7 @@ cudaError_t launch_time_inv(const double2* Z, double* z, int n_space, int n_time
 #define CALL(LM)                                                                            \
   {                                                                                         \
     using G = Geo<LM, tot_t<LM>()>;                                                               \
-    if ((err = prep(k_time_inv<LM>, G::SMEM)) != cudaSuccess) return err;                   \
+    if ((err = prep(k_time_inv<LM>, G::SMEM, G::NT)) != cudaSuccess) return err;                   \
     k_time_inv<LM><<<(n_space + G::B - 1) / G::B, G::NT, G::SMEM, st>>>(Z, z, n_space,       \
                                                                         scale_bwd, tw_base); \
   }
@@ -535,7 +535,7 @@ cudaError_t launch_dst_rows(double2* Z, int n, int n_rows, const double2* tw_bas
 #define CALL(LM)                                                                          \
   {                                                                                       \
     using TG = TauGeo<LM>;                                                                \
-    if ((err = prep(k_tau_solve_1d<LM, 0>, TG::SMEM)) != cudaSuccess) return err;     \
+    if ((err = prep(k_tau_solve_1d<LM, 0>, TG::SMEM, TG::G::NT)) != cudaSuccess) return err;     \
     const int grid = (n_rows + TG::G::B - 1) / TG::G::B;                                  \
     k_tau_solve_1d<LM, 0><<<grid, TG::G::NT, TG::SMEM, st>>>(Z, n_rows, nullptr, nullptr, \
                                                                  0.0, tw_base);           \
@@ -549,7 +549,7 @@ template <int LM, int MODE>
 static cudaError_t tau1d(double2* Z, int n_rows, const double2* lambda, const double* sigma,
                          double dt, const double2* tw_base, cudaStream_t st) {
   using TG = TauGeo<LM>;
-  cudaError_t err = prep(k_tau_solve_1d<LM, MODE>, TG::SMEM);
+  cudaError_t err = prep(k_tau_solve_1d<LM, MODE>, TG::SMEM, TG::G::NT);
   if (err != cudaSuccess) return err;
   const int grid = (n_rows + TG::G::B - 1) / TG::G::B;
   k_tau_solve_1d<LM, MODE><<<grid, TG::G::NT, TG::SMEM, st>>>(Z, n_rows, lambda, sigma, dt, tw_base);

@@ -22,8 +22,8 @@ __device__ __forceinline__ double& comp2(double2* s, int slot_padded, int c) {
 }
 
 template <class K>
-cudaError_t prep2(K kernel, size_t smem) {
-  cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+cudaError_t prep2(K kernel, size_t smem, int threads = 1024) {
+  cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, carveout_pct(smem, threads));
   if (e != cudaSuccess) return e;
   if (smem > 48 * 1024)
     return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
@@ -212,7 +212,7 @@ cudaError_t launch_matvec_2d(const double* v, double* y, int n, int n_time, int 
 #define CALL(LM)                                                                          \
   {                                                                                       \
     using G = ColGeo<LM>;                                                                 \
-    if ((err = prep2(k_matvec_2d_cols<LM>, G::SMEM)) != cudaSuccess) return err;          \
+    if ((err = prep2(k_matvec_2d_cols<LM>, G::SMEM, G::NT)) != cudaSuccess) return err;          \
     const int tiles = (n + G::C - 1) / G::C;                                              \
     k_matvec_2d_cols<LM><<<n_time * tiles, G::NT, G::SMEM, st>>>(v, y, n, eig_x_scaled, tw_base); \
   }
@@ -226,7 +226,7 @@ static cudaError_t tau2d_cols(double2* Z, int n, int n_rows, const double2* lamb
                               const double* sigma, double dt, const double2* tw_base,
                               cudaStream_t st) {
   using G = ColGeo<LM>;
-  cudaError_t err = prep2(k_tau_2d_cols<LM, MODE>, G::SMEM);
+  cudaError_t err = prep2(k_tau_2d_cols<LM, MODE>, G::SMEM, G::NT);
   if (err != cudaSuccess) return err;
   const int tiles = (n + G::C - 1) / G::C;
   k_tau_2d_cols<LM, MODE><<<n_rows * tiles, G::NT, G::SMEM, st>>>(Z, n, lambda, sigma, dt, tw_base);

@@ -212,8 +212,8 @@ __global__ void __launch_bounds__(CGeo<LOGM, tot_c<LOGM>()>::NT, minb_c(CGeo<LOG
 // launchers
 // ---------------------------------------------------------------------------------------------
 template <class K>
-static cudaError_t prep_c(K kernel, size_t smem) {
-  cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+static cudaError_t prep_c(K kernel, size_t smem, int threads = 1024) {
+  cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, carveout_pct(smem, threads));
   if (e != cudaSuccess) return e;
   if (smem > 48 * 1024) return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   return cudaSuccess;
@@ -252,7 +252,7 @@ cudaError_t launch_dst_pairs(const double* v, double* out, int n_space, int n_ti
 #define CALL(LN)                                                                              \
   {                                                                                           \
     using PG = PairGeo<LN>;                                                                   \
-    if ((err = prep_c(k_dst_pairs<LN>, PG::SMEM)) != cudaSuccess) return err;                 \
+    if ((err = prep_c(k_dst_pairs<LN>, PG::SMEM, PG::G::NT)) != cudaSuccess) return err;                 \
     k_dst_pairs<LN><<<(n_pairs + PG::G::B - 1) / PG::G::B, PG::G::NT, PG::SMEM, st>>>(v, out, n_pairs, \
                                                                                     scale, tw_base); \
   }
@@ -270,7 +270,7 @@ cudaError_t launch_time_solve(const double* u, double* z, int n_space, int n_tim
   {                                                                                                   \
     using G = CGeo<LM, tot_c<LM>()>;                                                                  \
     auto kern = forward ? k_time_solve<LM, 2> : k_time_solve<LM, 1>;                                  \
-    if ((err = prep_c(kern, G::SMEM)) != cudaSuccess) return err;                                     \
+    if ((err = prep_c(kern, G::SMEM, G::NT)) != cudaSuccess) return err;                                     \
     kern<<<(n_space + G::B - 1) / G::B, G::NT, G::SMEM, st>>>(u, z, n_space, scale_fwd, scale_bwd, s_in, \
                                                               lambda, sigma, dt, tw_base);            \
   }

@@ -5,9 +5,29 @@
 // grid-stride assignment, reduces in-CTA by a fixed shuffle/shared-memory tree, and a single-CTA
 // kernel sums the per-CTA partials in index order.  Vectors are 16-byte aligned (double2 loads);
 // an odd tail element is handled by CTA 0.
+#include <cstdlib>
+#include <string>
+
 #include "kernels.cuh"
 
 namespace fpc {
+
+int carveout_pct(size_t dyn_smem, int threads) {
+  static const bool maxed = [] {
+    const char* e = std::getenv("FPC_CARVEOUT");
+    return e && std::string(e) == "max";
+  }();
+  if (maxed) return 100;
+  const int by_regs = threads <= 128 ? 4 : threads <= 256 ? 2 : 1;
+  const size_t per_cta = dyn_smem + 2048;  // + static shared memory and the 1 KB system reserve
+  const int by_smem = int((228u * 1024u) / per_cta);
+  const int ctas = by_smem < by_regs ? (by_smem > 0 ? by_smem : 1) : by_regs;
+  const size_t need = size_t(ctas) * per_cta;
+  static const int caps[] = {0, 8, 16, 32, 64, 100, 132, 164, 196, 228};
+  for (int c : caps)
+    if (size_t(c) * 1024 >= need) return (c * 100 + 227) / 228;
+  return 100;
+}
 
 constexpr int kDotsThreads = 256;
 constexpr int kDotsGrid = 148 * 4;

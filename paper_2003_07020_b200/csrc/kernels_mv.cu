@@ -58,10 +58,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((1 << (LOGM - 1)) / 
   // 1. forward FFT of the packed input z_m = v[2m] + i v[2m+1] (rank 1: b_m = z_m e^{-2 pi i m/M},
   //    the odd bins); the first radix pass takes its operands straight from global memory
   FPC_PHM(1);
+  // e^{-2 pi i m/M} = tw_{M/64}[m >> 6] * tw_M[m & 63]: two small L1-resident tables instead of a
+  // 64 KB stretch of the size-M table per row
+  const double2* twMh = twb + M / 64;
+  auto twm = [&](int m) -> double2 { return cmul(__ldg(twMh + (m >> 6)), __ldg(twM + (m & 63))); };
   auto load_z = [&](int m) -> double2 {
     const int i = 2 * m;
     const double2 zm = make_double2(i < ns ? vk[i] : 0.0, i + 1 < ns ? vk[i + 1] : 0.0);
-    return q == 1 ? cmul(zm, __ldg(twM + m)) : zm;
+    return q == 1 ? cmul(zm, twm(m)) : zm;
   };
   block_fft_from<LOGM - 1, -1, BS, 16>(smem, twb + H, load_z);
   FPC_PHM(2);
@@ -69,6 +73,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((1 << (LOGM - 1)) / 
   // 2. eigenvalue product on (kappa, M - kappa) pairs; slot j of rank q holds bin 2j + q.
   //    task t: rank 0 -> (slot t+1, slot H-t-1, kappa 2t+2); rank 1 -> (t, H-1-t, 2t+1)
   const double2* twL = twb + L;
+  const double2* twLh = twb + L / 128;  // e^{-2 pi i kappa/L} = tw_{L/128}[kappa >> 7] tw_L[kappa & 127]
+  const double2* eigq = reinterpret_cast<const double2*>(eig + eigq_offset(M)) + q * (H / 2);
   constexpr int UP = 4;
   constexpr int ntask = H / 2;
   if (q == 0 && threadIdx.x == 0) {
@@ -85,9 +91,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((1 << (LOGM - 1)) / 
       const int t = t0 + u * NT;
       const int kap = q == 0 ? 2 * (t + 1) : 2 * t + 1;
       const bool ok = t < ntask;
-      wv[u] = ok ? __ldg(twL + kap) : make_double2(1.0, 0.0);  // e^{-2 pi i kappa/L}
-      ek[u] = ok ? __ldg(eig + kap) : 0.0;
-      em[u] = ok ? __ldg(eig + M - kap) : 0.0;
+      wv[u] = ok ? cmul(__ldg(twLh + (kap >> 7)), __ldg(twL + (kap & 127))) : make_double2(1.0, 0.0);
+      const double2 ee = ok ? __ldg(eigq + t) : make_double2(0.0, 0.0);
+      ek[u] = ee.x;
+      em[u] = ee.y;
     }
 #pragma unroll
     for (int u = 0; u < UP; ++u) {
@@ -129,7 +136,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((1 << (LOGM - 1)) / 
       const int j0 = 2 * m;
       e[u] = Eb[pad16(m)];
       o[u] = Ob[pad16(m)];
-      w[u] = __ldg(twM + m);
+      w[u] = twm(m);
       const bool ok0 = j0 < ns, ok1 = j0 + 1 < ns;
       c0[u] = make_double2(ok0 ? vk[j0] : 0.0, ok1 ? vk[j0 + 1] : 0.0);
       c1[u] = make_double2(ok0 && kg >= 1 ? vk[long(j0) - ns] : 0.0, ok1 && kg >= 1 ? vk[long(j0) + 1 - ns] : 0.0);
@@ -162,7 +169,8 @@ static cudaError_t launch_split(const double* v, double* y, int n_space, int n_t
                                 const double* eig_scaled, const double2* tw_base, cudaStream_t st) {
   constexpr int H = 1 << (LOGM - 1);
   constexpr size_t smem = size_t(padded(H)) * sizeof(double2);
-  cudaError_t err = cudaFuncSetAttribute(k_matvec_split<LOGM>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+  cudaError_t err = cudaFuncSetAttribute(k_matvec_split<LOGM>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                         carveout_pct(smem, H / 16));
   if (err != cudaSuccess) return err;
   err = cudaFuncSetAttribute(k_matvec_split<LOGM>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   if (err != cudaSuccess) return err;
