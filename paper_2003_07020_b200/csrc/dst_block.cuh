@@ -56,7 +56,7 @@ __device__ __forceinline__ void dst_pre_folded(double2* r, double2* hv, const do
       continue;
     }
     const double2 wj = __ldg(tw2N + j);
-    const double2 wm = __ldg(tw2N + M - j);
+    const double2 wm = make_double2(-wj.y, -wj.x);  // e^{-i pi (M-j)/N} = -i conj(e^{-i pi j/N}), M = N/2
     const double2 f1 = f(j), f2 = f(N - j);
     const double2 g1 = f(M - j), g2 = f(M + j);
     const double2 sj = cadd(f1, f2), dj = csub(f1, f2), sm = cadd(g1, g2), dm = csub(g1, g2);
@@ -138,8 +138,8 @@ __device__ __forceinline__ void block_dst(double2* s, double2* h, const double2*
       hv[0] = fm;
       continue;
     }
-    const double2 wj = __ldg(tw2N + j);       // e^{-i pi j/N}: sin(pi j/N) = -wj.y
-    const double2 wm = __ldg(tw2N + M - j);   // e^{-i pi (M-j)/N}
+    const double2 wj = __ldg(tw2N + j);            // e^{-i pi j/N}: sin(pi j/N) = -wj.y
+    const double2 wm = make_double2(-wj.y, -wj.x);  // e^{-i pi (M-j)/N} = -i conj(wj)
     const double2 f1 = r[pad16(j)], f2 = r[pad16(N - j)];
     const double2 sj = cadd(f1, f2), dj = csub(f1, f2);
     const double sinj = -wj.y, sinm = -wm.y;

@@ -123,10 +123,12 @@ __device__ __forceinline__ double2 twid(const double2* __restrict__ tw, int t) {
   return S > 0 ? cconj(w) : w;
 }
 
-// Multiply v[r] (r = 1..R-1) by w^r, w = tw[t1] (w4 = tw[4 t1] when R > 4).  t1 = 0 gives the
-// identity through the table (tw[0] = 1), so there is no divergent early exit.
+// Multiply v[r] (r = 1..R-1) by w^r, w = tw[t1] (w4 = tw4[t1] = w^4 when R > 4: tw4 is the table a
+// quarter the size of tw's, so w4 is the same double as tw[4 t1]).  t1 = 0 gives the identity
+// through the table (tw[0] = 1), so there is no divergent early exit.
 template <int R, int S>
-__device__ __forceinline__ void apply_twiddles(double2* v, const double2* __restrict__ tw, int t1) {
+__device__ __forceinline__ void apply_twiddles(double2* v, const double2* __restrict__ tw,
+                                               const double2* __restrict__ tw4, int t1) {
   const double2 w1 = twid<S>(tw, t1);
   if constexpr (R == 2) {
     v[1] = cmul(v[1], w1);
@@ -139,7 +141,7 @@ __device__ __forceinline__ void apply_twiddles(double2* v, const double2* __rest
   } else {
     // powers built and applied on the fly (few live twiddles -> fewer registers):
     // w^{4a+b} = (w^4)^a w^b, at most three products deep
-    const double2 w4 = twid<S>(tw, 4 * t1);
+    const double2 w4 = twid<S>(tw4, t1);
     const double2 w2 = cmul(w1, w1);
     const double2 w3 = cmul(w2, w1);
     v[1] = cmul(v[1], w1);
@@ -196,7 +198,7 @@ __device__ __forceinline__ void stockham_pass(double2* s, const double2* __restr
     // w = e^{-2 pi i jm/(NS R)}: read from the dense size-(NS R) table (tw_base + NS R), not the
     // size-N table at stride N/(NS R) -- the same doubles (power-of-two index scaling), a much
     // smaller L1 footprint
-    if constexpr (NS > 1) apply_twiddles<R, S>(v[q], tw - N + NS * R, jm);
+    if constexpr (NS > 1) apply_twiddles<R, S>(v[q], tw - N + NS * R, tw - N + (NS * R) / 4, jm);
     Dft<R, S>::run(v[q]);
     dst[q] = b * BS + (j - jm) * R + jm;  // buffer base + logical offset (pad applied below)
   }
