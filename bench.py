@@ -152,8 +152,9 @@ def run_sharded(args, w, rank, world, local):
     jac = (fp.RieszJacobian2D(w.gamma[0], w.gamma[1], 1.0, 1.0, w.h, w.n) if w.two_dim
            else fp.RieszJacobian1D(w.gamma[0], 1.0, w.h, w.n))
     op = fp.AllAtOnceOperator(fp.TimeStencil(w.n_time), jac, w.dt, ctx)
-    plan = fp.build_plan(fp.PreconditionerKind.generalized(), w.n_time, w.dt, op)
-    s = ShardedSolver(w.n_time, w.n_space, CudaShardKernels(op, plan))
+    plan = fp.build_plan(fp.PreconditionerKind.generalized(), w.n_time, w.dt, op,
+                         ordering=fp.Ordering[args.ordering])
+    s = ShardedSolver(w.n_time, w.n_space, CudaShardKernels(op, plan), ordering=args.ordering)
     b_host = problems.rhs(w)
     lo, hi = s.koff * w.n_space, (s.koff + s.nt_loc) * w.n_space
     b_loc_host = np.ascontiguousarray(b_host[lo:hi])
@@ -192,7 +193,8 @@ def run_sharded(args, w, rank, world, local):
             "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded uniform[-1,1] source)",
             "config": {"workload": w.name, "n_space": w.n, "n_time": w.n_time, "tol": w.tol, "restart": w.restart,
-                       "parallelism": f"frequency-sharded x{world} (NCCL all-to-all + all-reduce)"},
+                       "parallelism": f"frequency-sharded x{world} (NCCL all-to-all + all-reduce)",
+                       "pc_ordering": args.ordering},
             "iterations": rep.iterations, "true_relative_residual": rep.true_relative_residual,
             "e2e": {"value": 1.0 / te, "unit": UNIT, "h2d_bytes_per_step": 8 * (hi - lo),
                     "d2h_bytes_per_step": 8 * (hi - lo)},

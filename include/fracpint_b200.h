@@ -130,7 +130,11 @@ int fpc_bicgstab(fpc_plan_t plan, const double* b, double* x, const fpc_solver_c
  *   time_fwd / time_inv on ns_local spatial columns (row stride ns_local), Z half spectrum
  *     [Nt/2+1][ns_local] complex                                      alpha_circulant.hpp:146-198
  *   tau on frequency rows [row0, row0+nrows) of a [nrows][n_space] complex block  tau.hpp:98-136
- *   dots / update / lincomb: the Gram-Schmidt vector kernels on local shards   krylov.hpp:116-183 */
+ *   dots / update / lincomb: the Gram-Schmidt vector kernels on local shards   krylov.hpp:116-183
+ * commuted ordering (n_space + 1 <= 8192), two all-to-alls per apply:
+ *   dst_levels: out = s_in * S v for nt_local contiguous time levels (nt_local even)  dst.hpp:21-43
+ *   time_solve: per spatial column p in [col0, col0 + ns_local) of a [Nt][ns_local] block,
+ *     z = D^-1 F^* diag(1/(lambda_n - dt sigma_p)) F D u (forward != 0: multiply)  alpha_circulant.hpp:137-199 */
 int fpc_shard_matvec(fpc_problem_t p, const double* v, double* y, int nt_local, int k_offset);
 int fpc_shard_time_fwd(fpc_plan_t plan, const double* v, double* Z, int ns_local, double s_in);
 int fpc_shard_tau(fpc_plan_t plan, double* Z, int row0, int nrows, int forward);
@@ -141,6 +145,8 @@ int fpc_shard_update(fpc_context_t ctx, const double* const* V, const double* co
                      double* w, size_t n, double* norm2_host);
 int fpc_shard_lincomb(fpc_context_t ctx, const double* const* V, const double* coef, int nv,
                       double* u, size_t n);
+int fpc_shard_dst_levels(fpc_plan_t plan, const double* v, double* out, int nt_local, double s_in);
+int fpc_shard_time_solve(fpc_plan_t plan, const double* u, double* z, int col0, int ns_local, int forward);
 
 /* instrumentation: number of kernels this library launched in this process */
 unsigned long long fpc_kernel_launches(void);

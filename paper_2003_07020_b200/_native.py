@@ -27,6 +27,7 @@ EXPORTS = [
     "fpc_plan_set_ordering", "fpc_pc_apply", "fpc_pc_forward", "fpc_gmres", "fpc_bicgstab", "fpc_kernel_launches", "fpc_profile_start",
     "fpc_profile_stop", "fpc_profile_entry", "fpc_shard_matvec", "fpc_shard_time_fwd", "fpc_shard_tau",
     "fpc_shard_time_inv", "fpc_shard_dots", "fpc_shard_update", "fpc_shard_lincomb",
+    "fpc_shard_dst_levels", "fpc_shard_time_solve",
 ]
 
 
@@ -90,6 +91,8 @@ def load():
     lib.fpc_shard_dots.argtypes = [vp, vp, vp, C.c_int, vp, C.c_size_t, C.c_int, vp]
     lib.fpc_shard_update.argtypes = [vp, vp, vp, C.c_int, vp, C.c_size_t, vp]
     lib.fpc_shard_lincomb.argtypes = [vp, vp, vp, C.c_int, vp, C.c_size_t]
+    lib.fpc_shard_dst_levels.argtypes = [vp, vp, vp, C.c_int, d]
+    lib.fpc_shard_time_solve.argtypes = [vp, vp, vp, C.c_int, C.c_int, C.c_int]
     _lib = lib
     return lib
 

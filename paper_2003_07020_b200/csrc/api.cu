@@ -1676,6 +1676,39 @@ int fpc_shard_time_inv(fpc_plan_t pl, const double* Z, double* z, int ns_local) 
   });
 }
 
+static void check_commuted_shard(const fpc_problem_s* p, const char* who) {
+  if (p->two_dim || p->ns + 1 > 8192) throw Unsupported{std::string(who) + ": 1D with n_space + 1 <= 8192 only"};
+}
+
+int fpc_shard_dst_levels(fpc_plan_t pl, const double* v, double* out, int nt_local, double s_in) {
+  if (!pl || !v || !out) return set_err(FPC_INVALID_ARGUMENT, "null argument");
+  return guarded([&] {
+    fpc_problem_s* p = pl->prob;
+    check_commuted_shard(p, "fpc_shard_dst_levels");
+    if (nt_local < 2 || nt_local % 2 || nt_local > p->nt)
+      throw InvalidArg{"fpc_shard_dst_levels: nt_local must be even and <= n_time"};
+    if (v == out) throw InvalidArg{"fpc_shard_dst_levels: input and output must be disjoint"};
+    DeviceGuard g(p->ctx->device);
+    cudaStream_t st = p->ctx->stream;
+    // any pairing of levels into complex rows is valid: (k, k + nt_local/2) of the local block
+    LAUNCH("dst_pairs", st, fpc::launch_dst_pairs(v, out, p->ns, nt_local, s_in, p->ctx->tw, st));
+  });
+}
+
+int fpc_shard_time_solve(fpc_plan_t pl, const double* u, double* z, int col0, int ns_local, int forward) {
+  if (!pl || !u || !z) return set_err(FPC_INVALID_ARGUMENT, "null argument");
+  return guarded([&] {
+    fpc_problem_s* p = pl->prob;
+    check_commuted_shard(p, "fpc_shard_time_solve");
+    if (col0 < 0 || ns_local < 1 || col0 + ns_local > p->ns) throw InvalidArg{"fpc_shard_time_solve: bad column range"};
+    DeviceGuard g(p->ctx->device);
+    cudaStream_t st = p->ctx->stream;
+    LAUNCH("time_solve", st,
+           fpc::launch_time_solve(u, z, ns_local, p->nt, pl->d_sf, pl->d_sb, 1.0, pl->d_lambda, pl->d_sigma + col0,
+                                  p->dt, p->ctx->tw, st, forward != 0));
+  });
+}
+
 // out_host[i] = s_i <V_i, w> (i < nv), out_host[nv] = <w, w> when with_norm; synchronous.
 int fpc_shard_dots(fpc_context_t c, const double* const* V, const double* scales, int nv,
                    const double* w, size_t n, int with_norm, double* out_host) {

@@ -10,6 +10,10 @@ Layouts (G ranks, N = Nt*Ns, H = Nt/2 + 1):
       all-to-all time -> space columns; time FFT (local columns); all-to-all space -> frequency rows;
       tau solves (local rows, alpha_circulant.hpp:160 -- the independent PinT work);
       all-to-all back to space; inverse time FFT; all-to-all back to time.
+  * PC apply, commuted ordering (ordering="commuted", 1D): DST of every local time
+    level; all-to-all time -> space columns; per-column time solve (FFT, divide, inverse FFT);
+    all-to-all back to time; DST of every local time level -- two all-to-alls instead of four,
+    real-valued in flight, rounding-level difference from the reference ordering.
   * Gram-Schmidt dots / norms: local partials + all_reduce (krylov.hpp:116-131).
 Every rank runs the same host-side Hessenberg/Givens recurrence on the reduced values.
 
@@ -87,6 +91,16 @@ class CudaShardKernels:
         N.check(self.lib.fpc_shard_time_inv(self.plan.h, self._p(Z), self._p(z), ns_local))
         return z
 
+    def dst_levels(self, v, nt_local, s_in):
+        out = self.empty(v.numel())
+        N.check(self.lib.fpc_shard_dst_levels(self.plan.h, self._p(v), self._p(out), nt_local, float(s_in)))
+        return out
+
+    def time_solve(self, cols, col0, ns_local, forward=False):
+        z = self.empty(cols.numel())
+        N.check(self.lib.fpc_shard_time_solve(self.plan.h, self._p(cols), self._p(z), col0, ns_local, int(forward)))
+        return z
+
     def _ptrs(self, V):
         arr = (C.c_void_p * max(len(V), 1))(*[v.data_ptr() for v in V])
         return arr
@@ -119,7 +133,10 @@ class CudaShardKernels:
 class ShardedSolver:
     """Right-preconditioned GMRES (krylov.hpp:83-192, + GMRES(m) restarts) over G ranks."""
 
-    def __init__(self, n_time: int, n_space: int, kernels, group=None):
+    def __init__(self, n_time: int, n_space: int, kernels, group=None, ordering: str = "reference"):
+        if ordering not in ("reference", "commuted"):
+            raise ValueError("ShardedSolver: ordering must be 'reference' or 'commuted'")
+        self.ordering = ordering
         self.k = kernels
         self.group = group
         self.G = dist.get_world_size(group) if dist.is_initialized() else 1
@@ -179,6 +196,8 @@ class ShardedSolver:
         return self.k.matvec(v_loc, self.nt_loc, self.koff, False)
 
     def pc_apply(self, v_loc, s_in=1.0, forward=False):
+        if self.ordering == "commuted":
+            return self._pc_apply_commuted(v_loc, s_in, forward)
         G, r, ns, nt_loc = self.G, self.rank, self.ns, self.nt_loc
         V = v_loc.view(nt_loc, ns)
         # 1. time -> space columns
@@ -203,6 +222,23 @@ class ShardedSolver:
         parts = self._a2a([z[d * nt_loc:(d + 1) * nt_loc] for d in range(G)],
                           [nt_loc * self.cs[s] for s in range(G)], z)
         return torch.cat([p.view(nt_loc, self.cs[s]) for s, p in enumerate(parts)], dim=1).reshape(-1).contiguous()
+
+    def _pc_apply_commuted(self, v_loc, s_in=1.0, forward=False):
+        G, r, ns, nt_loc = self.G, self.rank, self.ns, self.nt_loc
+        # 1. S on every local time level (no communication)
+        u = self.k.dst_levels(v_loc, nt_loc, s_in).view(nt_loc, ns)
+        # 2. time -> space columns
+        parts = self._a2a([u[:, self.co[d]:self.co[d] + self.cs[d]] for d in range(G)],
+                          [nt_loc * self.cs[r]] * G, u)
+        cols = torch.cat([p.view(nt_loc, self.cs[r]) for p in parts]).reshape(-1)
+        # 3. per spatial mode: time FFT, divide by (lambda_n - dt sigma_p), inverse FFT
+        z = self.k.time_solve(cols, self.co[r], self.cs[r], forward).view(self.nt, self.cs[r])
+        # 4. space -> time
+        parts = self._a2a([z[d * nt_loc:(d + 1) * nt_loc] for d in range(G)],
+                          [nt_loc * self.cs[s] for s in range(G)], z)
+        w = torch.cat([p.view(nt_loc, self.cs[s]) for s, p in enumerate(parts)], dim=1).reshape(-1).contiguous()
+        # 5. S on every local time level
+        return self.k.dst_levels(w, nt_loc, 1.0)
 
     # ------------------------------------------------------------------ GMRES
     def _norm(self, w):

@@ -81,6 +81,23 @@ class NumpyShardKernels:
         z = np.fft.fft(F, axis=0).real * (self.sb / self.nt)[:, None]
         return torch.from_numpy(np.ascontiguousarray(z).ravel())
 
+    # commuted ordering (1D): S per time level; per-column time solve over all Nt frequencies
+    def dst_levels(self, v, nt_local, s_in):
+        X = v.numpy().reshape(nt_local, self.ns)
+        return torch.from_numpy(np.ascontiguousarray((X @ self.Q.T) * s_in).ravel())
+
+    def time_solve(self, cols, col0, ns_local, forward=False):
+        X = cols.numpy().reshape(self.nt, ns_local) * self.sf[:, None]
+        F = np.fft.ifft(X, axis=0) * self.nt  # e^{+2 pi i kn/Nt}
+        lam = np.empty(self.nt, complex)
+        lam[:self.H] = self.lam[:self.H]
+        for n in range(self.H, self.nt):
+            lam[n] = np.conj(self.lam[self.nt - n])
+        d = lam[:, None] - self.dt * self.sigma[None, col0:col0 + ns_local]
+        Y = F * d if forward else F / d
+        z = np.fft.fft(Y, axis=0).real * (self.sb / self.nt)[:, None]
+        return torch.from_numpy(np.ascontiguousarray(z).ravel())
+
     def dots(self, V, scales, w, with_norm):
         wn = w.numpy()
         out = [s * float(v.numpy() @ wn) for v, s in zip(V, scales)]

@@ -30,7 +30,8 @@ def _worker(rank, world, port, case, out_dir):
     from dist_cpu_kernels import NumpyShardKernels
     from oracle.oracle import Oracle
     from paper_2003_07020_b200.distributed import ShardedSolver
-    two_dim, g, n, nt, restart = case
+    two_dim, g, n, nt, restart = case[:5]
+    ordering = case[5] if len(case) > 5 else "reference"
     dt = 1.0 / nt
     o = Oracle()
     if two_dim:
@@ -41,7 +42,7 @@ def _worker(rank, world, port, case, out_dir):
         po = o.problem_1d(g[0], 1.0, 1.0 / (n + 1), n, nt, dt).build_plan()
         ns = n
     k = NumpyShardKernels(po, nt, dt, two_dim, n)
-    s = ShardedSolver(nt, ns, k)
+    s = ShardedSolver(nt, ns, k, ordering=ordering)
     rng = np.random.default_rng(5)
     v = rng.uniform(-1, 1, nt * ns)
     lo, hi = s.koff * ns, (s.koff + s.nt_loc) * ns
@@ -56,12 +57,13 @@ def _worker(rank, world, port, case, out_dir):
 
 
 @pytest.mark.parametrize("case", [(False, (1.5,), 31, 16, 0), (False, (1.3,), 63, 8, 5),
-                                  (True, (1.3, 1.7), 7, 8, 0)])
+                                  (True, (1.3, 1.7), 7, 8, 0),
+                                  (False, (1.5,), 31, 16, 0, "commuted"), (False, (1.7,), 15, 32, 5, "commuted")])
 def test_sharded_solve_matches_oracle(tmp_path, oracle, case):
     world = 2
     mp.spawn(_worker, args=(world, free_port(), case, str(tmp_path)), nprocs=world, join=True)
     parts = [np.load(tmp_path / f"r{r}.npz") for r in range(world)]
-    two_dim, g, n, nt, restart = case
+    two_dim, g, n, nt, restart = case[:5]
     dt = 1.0 / nt
     if two_dim:
         po = oracle.problem_2d(g[0], g[1], 1.0, 1.0, 1.0 / (n + 1), n, nt, dt).build_plan()

@@ -10,8 +10,8 @@ from paper_2003_07020_b200 import problems
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("two_dim", [False, True])
-def test_sharded_world1_matches_single_gpu(oracle, two_dim):
+@pytest.mark.parametrize("two_dim,ordering", [(False, "reference"), (True, "reference"), (False, "commuted")])
+def test_sharded_world1_matches_single_gpu(oracle, two_dim, ordering):
     torch = pytest.importorskip("torch")
     from paper_2003_07020_b200.distributed import CudaShardKernels, ShardedSolver
     if two_dim:
@@ -22,10 +22,11 @@ def test_sharded_world1_matches_single_gpu(oracle, two_dim):
         jac = fp.RieszJacobian1D(1.5, 1.0, w.h, w.n)
     ctx = fp.Context(0, torch.cuda.current_stream())
     op = fp.AllAtOnceOperator(fp.TimeStencil(w.n_time), jac, w.dt, ctx)
-    plan = fp.build_plan(fp.PreconditionerKind.generalized(), w.n_time, w.dt, op)
+    plan = fp.build_plan(fp.PreconditionerKind.generalized(), w.n_time, w.dt, op,
+                         ordering=fp.Ordering[ordering])
     b = problems.rhs(w)
     bt = torch.from_numpy(b).cuda()
-    s = ShardedSolver(w.n_time, w.n_space, CudaShardKernels(op, plan))
+    s = ShardedSolver(w.n_time, w.n_space, CudaShardKernels(op, plan), ordering=ordering)
     rel = lambda a, c: np.linalg.norm(a - c) / np.linalg.norm(c)
     assert rel(s.matvec(bt).cpu().numpy(), op.apply(b)) <= 1e-14
     assert rel(s.pc_apply(bt).cpu().numpy(), fp.apply_inverse(plan, b)) <= 1e-14
