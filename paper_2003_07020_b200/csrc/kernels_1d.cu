@@ -100,10 +100,15 @@ __device__ __forceinline__ double& comp(double2* s, int slot_padded, int c) {
 // =====================================================================================
 constexpr int kTotMv = 4096;
 
+#ifndef FPC_MV_CST_SMEM
+#define FPC_MV_CST_SMEM 0
+#endif
+// FPC_MV_CST_SMEM = 1: the stencil part is formed in the load phase and parked in shared memory;
+// 0: the epilogue re-reads the three (L2-resident) rows, leaving the smem for L1 (carveout)
 template <int LOGM>
 struct MvGeo {
   using G = Geo<LOGM, kTotMv, 16>;
-  static constexpr size_t SMEM = G::SMEM + size_t(G::B) * G::M * sizeof(double);
+  static constexpr size_t SMEM = G::SMEM + (FPC_MV_CST_SMEM ? size_t(G::B) * G::M * sizeof(double) : 0);
 };
 
 template <int LOGM>
@@ -134,8 +139,10 @@ __global__ void __launch_bounds__(Geo<LOGM, kTotMv, 16>::NT, minb(Geo<LOGM, kTot
       const bool ok = e < B * L && b < nb && idx < ns;
       const size_t o = size_t(k0 + b) * ns + idx;
       x0[u] = ok ? v[o] : 0.0;
-      x1[u] = (ok && k >= 1) ? v[o - sstride] : 0.0;
-      x2[u] = (ok && k >= 2) ? v[o - 2 * size_t(sstride)] : 0.0;
+      if (FPC_MV_CST_SMEM) {
+        x1[u] = (ok && k >= 1) ? v[o - sstride] : 0.0;
+        x2[u] = (ok && k >= 2) ? v[o - 2 * size_t(sstride)] : 0.0;
+      }
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
@@ -144,7 +151,7 @@ __global__ void __launch_bounds__(Geo<LOGM, kTotMv, 16>::NT, minb(Geo<LOGM, kTot
         const int b = e / L, idx = e - b * L;
         const int k = (k0 + b) / rpt + koff;
         comp(smem, b * BS + pad16(idx >> 1), idx & 1) = x0[u];
-        if (idx < ns) {
+        if (FPC_MV_CST_SMEM && idx < ns) {
           double c;
           if (k == 0)
             c = x0[u];
@@ -190,11 +197,43 @@ __global__ void __launch_bounds__(Geo<LOGM, kTotMv, 16>::NT, minb(Geo<LOGM, kTot
   block_fft<LOGM, 1, BS, G::E>(smem, twb + M, B);
 
   // epilogue: stencil part + spatial term
-  for (int b = 0; b < nb; ++b) {
-    double* yb = y + size_t(k0 + b) * ns;
-    for (int idx = threadIdx.x; idx < ns; idx += NT) {
-      const double tv = comp(smem, b * BS + pad16(idx >> 1), idx & 1);
-      yb[idx] = cst[b * M + idx] + tv;
+  if (FPC_MV_CST_SMEM) {
+    for (int b = 0; b < nb; ++b) {
+      double* yb = y + size_t(k0 + b) * ns;
+      for (int idx = threadIdx.x; idx < ns; idx += NT) {
+        const double tv = comp(smem, b * BS + pad16(idx >> 1), idx & 1);
+        yb[idx] = cst[b * M + idx] + tv;
+      }
+    }
+  } else {
+    for (int e0 = threadIdx.x; e0 < nb * ns; e0 += U * NT) {
+      double x0[U], x1[U], x2[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int e = e0 + u * NT;
+        const int b = e / ns, idx = e - b * ns;
+        const int k = (k0 + b) / rpt + koff;
+        const bool ok = e < nb * ns;
+        const size_t o = size_t(k0 + b) * ns + idx;
+        x0[u] = ok ? v[o] : 0.0;
+        x1[u] = (ok && k >= 1) ? v[o - sstride] : 0.0;
+        x2[u] = (ok && k >= 2) ? v[o - 2 * size_t(sstride)] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int e = e0 + u * NT;
+        if (e >= nb * ns) continue;
+        const int b = e / ns, idx = e - b * ns;
+        const int k = (k0 + b) / rpt + koff;
+        double c;  // time_stencil.hpp:16-26 (same association as all_at_once.hpp:44-53)
+        if (k == 0)
+          c = x0[u];
+        else if (k == 1)
+          c = 1.5 * x0[u] + -2.0 * x1[u];
+        else
+          c = 1.5 * x0[u] + -2.0 * x1[u] + 0.5 * x2[u];
+        y[size_t(k0 + b) * ns + idx] = c + comp(smem, b * BS + pad16(idx >> 1), idx & 1);
+      }
     }
   }
 }

@@ -46,7 +46,8 @@ struct ColGeo {
   static constexpr int NT = C * M / E;
   static constexpr int BS = C > 1 ? skew2(M) : padded(M);
   static constexpr int BH = C > 1 ? skew2(M / 2) : padded(M / 2);  // DCT-III scratch (tau)
-  static constexpr size_t SMEM = size_t(C) * (BS + BH) * sizeof(double2);
+  static constexpr size_t SMEM = size_t(C) * (BS + BH) * sizeof(double2);  // tau: FFT + DCT-III buffers
+  static constexpr size_t SMEM_MV = size_t(C) * BS * sizeof(double2);      // matvec: FFT buffers only
 };
 
 }  // namespace
@@ -212,9 +213,9 @@ cudaError_t launch_matvec_2d(const double* v, double* y, int n, int n_time, int 
 #define CALL(LM)                                                                          \
   {                                                                                       \
     using G = ColGeo<LM>;                                                                 \
-    if ((err = prep2(k_matvec_2d_cols<LM>, G::SMEM, G::NT)) != cudaSuccess) return err;          \
+    if ((err = prep2(k_matvec_2d_cols<LM>, G::SMEM_MV, G::NT)) != cudaSuccess) return err;       \
     const int tiles = (n + G::C - 1) / G::C;                                              \
-    k_matvec_2d_cols<LM><<<n_time * tiles, G::NT, G::SMEM, st>>>(v, y, n, eig_x_scaled, tw_base); \
+    k_matvec_2d_cols<LM><<<n_time * tiles, G::NT, G::SMEM_MV, st>>>(v, y, n, eig_x_scaled, tw_base); \
   }
   FPC_DISPATCH_2D(log_m, CALL)
 #undef CALL
