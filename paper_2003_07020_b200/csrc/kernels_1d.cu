@@ -101,14 +101,18 @@ __device__ __forceinline__ double& comp(double2* s, int slot_padded, int c) {
 constexpr int kTotMv = 4096;
 
 #ifndef FPC_MV_CST_SMEM
-#define FPC_MV_CST_SMEM 0
+#define FPC_MV_CST_SMEM 2
 #endif
-// FPC_MV_CST_SMEM = 1: the stencil part is formed in the load phase and parked in shared memory;
-// 0: the epilogue re-reads the three (L2-resident) rows, leaving the smem for L1 (carveout)
+// Stencil part of the rows matvec.  Parked: formed in the load phase and kept in shared memory
+// (fewest dependent memory round trips: best for the small grids of M >= 1024, config 0).  Not
+// parked: the rows are loaded 16 deep, and the epilogue re-reads the three L2-resident rows
+// (B200 config 2, M = 256: 2D matvec 1182 -> 932 us).  FPC_MV_CST_SMEM = 0 / 1 forces either.
+template <int LOGM>
+constexpr bool mv_cst_parked() { return FPC_MV_CST_SMEM == 1 || (FPC_MV_CST_SMEM == 2 && LOGM >= 10); }
 template <int LOGM>
 struct MvGeo {
   using G = Geo<LOGM, kTotMv, 16>;
-  static constexpr size_t SMEM = G::SMEM + (FPC_MV_CST_SMEM ? size_t(G::B) * G::M * sizeof(double) : 0);
+  static constexpr size_t SMEM = G::SMEM + (mv_cst_parked<LOGM>() ? size_t(G::B) * G::M * sizeof(double) : 0);
 };
 
 template <int LOGM>
@@ -129,7 +133,38 @@ __global__ void __launch_bounds__(Geo<LOGM, kTotMv, 16>::NT, minb(Geo<LOGM, kTot
   const int k0 = blockIdx.x * B;
   const int nb = min(B, nrows - k0);
 
-  for (int e0 = threadIdx.x; e0 < B * L; e0 += U * NT) {
+  constexpr bool kParked = mv_cst_parked<LOGM>();
+  if (!kParked) {
+    // rows k0 .. k0+nb-1 are one contiguous stretch of nb*ns doubles: 16 loads in flight per
+    // thread (the load phase is latency bound), then the packed-slot stores
+    constexpr int UL = 16;
+    const int nreal = nb * ns;
+    const double* src = v + size_t(k0) * ns;
+    for (int e0 = threadIdx.x; e0 < nreal; e0 += UL * NT) {
+      double x[UL];
+#pragma unroll
+      for (int u = 0; u < UL; ++u) {
+        const int e = e0 + u * NT;
+        x[u] = e < nreal ? src[e] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < UL; ++u) {
+        const int e = e0 + u * NT;
+        if (e < nreal) {
+          const int b = e / ns, idx = e - b * ns;
+          comp(smem, b * BS + pad16(idx >> 1), idx & 1) = x[u];
+        }
+      }
+    }
+    // zero padding: slots whose both entries lie at idx >= ns, the odd half-slot, unused rows
+    const int s0 = (ns + 1) >> 1;
+    for (int t = threadIdx.x; t < B * M; t += NT) {
+      const int b = t / M, m = t - b * M;
+      if (b >= nb || m >= s0) smem[b * BS + pad16(m)] = make_double2(0.0, 0.0);
+      else if ((ns & 1) && m == s0 - 1) comp(smem, b * BS + pad16(m), 1) = 0.0;
+    }
+  }
+  for (int e0 = threadIdx.x; e0 < (kParked ? B * L : 0); e0 += U * NT) {
     double x0[U], x1[U], x2[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
@@ -139,7 +174,7 @@ __global__ void __launch_bounds__(Geo<LOGM, kTotMv, 16>::NT, minb(Geo<LOGM, kTot
       const bool ok = e < B * L && b < nb && idx < ns;
       const size_t o = size_t(k0 + b) * ns + idx;
       x0[u] = ok ? v[o] : 0.0;
-      if (FPC_MV_CST_SMEM) {
+      if (kParked) {
         x1[u] = (ok && k >= 1) ? v[o - sstride] : 0.0;
         x2[u] = (ok && k >= 2) ? v[o - 2 * size_t(sstride)] : 0.0;
       }
@@ -151,7 +186,7 @@ __global__ void __launch_bounds__(Geo<LOGM, kTotMv, 16>::NT, minb(Geo<LOGM, kTot
         const int b = e / L, idx = e - b * L;
         const int k = (k0 + b) / rpt + koff;
         comp(smem, b * BS + pad16(idx >> 1), idx & 1) = x0[u];
-        if (FPC_MV_CST_SMEM && idx < ns) {
+        if (kParked && idx < ns) {
           double c;
           if (k == 0)
             c = x0[u];
@@ -197,7 +232,7 @@ __global__ void __launch_bounds__(Geo<LOGM, kTotMv, 16>::NT, minb(Geo<LOGM, kTot
   block_fft<LOGM, 1, BS, G::E>(smem, twb + M, B);
 
   // epilogue: stencil part + spatial term
-  if (FPC_MV_CST_SMEM) {
+  if (kParked) {
     for (int b = 0; b < nb; ++b) {
       double* yb = y + size_t(k0 + b) * ns;
       for (int idx = threadIdx.x; idx < ns; idx += NT) {
@@ -206,10 +241,11 @@ __global__ void __launch_bounds__(Geo<LOGM, kTotMv, 16>::NT, minb(Geo<LOGM, kTot
       }
     }
   } else {
-    for (int e0 = threadIdx.x; e0 < nb * ns; e0 += U * NT) {
-      double x0[U], x1[U], x2[U];
+    constexpr int UE = 8;
+    for (int e0 = threadIdx.x; e0 < nb * ns; e0 += UE * NT) {
+      double x0[UE], x1[UE], x2[UE];
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
+      for (int u = 0; u < UE; ++u) {
         const int e = e0 + u * NT;
         const int b = e / ns, idx = e - b * ns;
         const int k = (k0 + b) / rpt + koff;
@@ -220,7 +256,7 @@ __global__ void __launch_bounds__(Geo<LOGM, kTotMv, 16>::NT, minb(Geo<LOGM, kTot
         x2[u] = (ok && k >= 2) ? v[o - 2 * size_t(sstride)] : 0.0;
       }
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
+      for (int u = 0; u < UE; ++u) {
         const int e = e0 + u * NT;
         if (e >= nb * ns) continue;
         const int b = e / ns, idx = e - b * ns;
@@ -417,21 +453,25 @@ __global__ void __launch_bounds__(TauGeo<LOGM>::G::NT, minb(TauGeo<LOGM>::G::NT)
   }
   // one row, folded DST: the first DST reads the row from global memory directly
   constexpr bool kDirect = (LOGM == 13 && B == 1 && MODE != 0);
-  // load rows: element i -> slot i + 1
-  for (int b = 0; b < (kDirect ? 0 : B); ++b) {
-    const double2* zr = Z + size_t(r0 + b) * NSR;
-    double2* s = smem + b * BS;
-    for (int i0 = threadIdx.x; i0 < NSR; i0 += U * NT) {
-      double2 x[U];
+  // load rows: element i of row b -> slot i + 1.  The nb rows are one contiguous stretch, read 16
+  // deep per thread (one memory round trip instead of one per row); rows b >= nb are zeroed
+  if constexpr (!kDirect) {
+    constexpr int UL = 16;
+    const double2* zr = Z + size_t(r0) * NSR;
+    for (int e0 = threadIdx.x; e0 < B * NSR; e0 += UL * NT) {
+      double2 x[UL];
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int i = i0 + u * NT;
-        x[u] = (i < NSR && b < nb) ? zr[i] : make_double2(0.0, 0.0);
+      for (int u = 0; u < UL; ++u) {
+        const int e = e0 + u * NT;
+        x[u] = e < nb * NSR ? zr[e] : make_double2(0.0, 0.0);
       }
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int i = i0 + u * NT;
-        if (i < NSR) s[pad16(i + 1)] = x[u];
+      for (int u = 0; u < UL; ++u) {
+        const int e = e0 + u * NT;
+        if (e < B * NSR) {
+          const int b = e / NSR, i = e - b * NSR;
+          smem[b * BS + pad16(i + 1)] = x[u];
+        }
       }
     }
   }
@@ -441,7 +481,27 @@ __global__ void __launch_bounds__(TauGeo<LOGM>::G::NT, minb(TauGeo<LOGM>::G::NT)
     block_dst<LOGM, BS, BH, 1, LOGM == 13>(smem, hbuf, twb, scale, kDirect ? Z + size_t(r0) * NSR : nullptr);
     FPC_PH(2);
     // divide by the shifted tau eigenvalues (slot i + 1 <-> index i)
-    for (int b = 0; b < B; ++b) {
+    if constexpr (B > 1) {  // several short rows: one flattened, 16-deep pass over all of them
+      constexpr int UD = 16;
+      for (int e0 = threadIdx.x; e0 < B * NSR; e0 += UD * NT) {
+        double sg[UD];
+#pragma unroll
+        for (int u = 0; u < UD; ++u) {
+          const int e = e0 + u * NT;
+          sg[u] = e < B * NSR ? __ldg(sigma + (e % NSR)) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < UD; ++u) {
+          const int e = e0 + u * NT;
+          if (e >= B * NSR) continue;
+          const int b = e / NSR, i = e - b * NSR;
+          const double2 l = (b < nb) ? __ldg(lam + r0 + b) : make_double2(1.0, 0.0);
+          double2* sl = smem + b * BS + pad16(i + 1);
+          *sl = shift_apply<MODE>(*sl, l.x - dt * sg[u], l.y);
+        }
+      }
+    }
+    for (int b = 0; b < (B > 1 ? 0 : B); ++b) {
       double2* s = smem + b * BS;
       const double2 l = (b < nb) ? __ldg(lam + r0 + b) : make_double2(1.0, 0.0);
       for (int i0 = threadIdx.x; i0 < NSR; i0 += 4 * U * NT) {  // sigma loads batched ahead of use

@@ -69,23 +69,33 @@ __global__ void __launch_bounds__(ColGeo<LOGM>::NT, (ColGeo<LOGM>::NT <= 256 ? 2
   const int iy0 = (blockIdx.x - k * tiles) * C;
   const size_t base = size_t(k) * n * n;
 
-  // load columns: element (ix, c) -> buffer c, packed slot ix/2 (real packing of length L)
-  for (int e0 = threadIdx.x; e0 < C * L; e0 += U * NT) {
-    double x[U];
+  // load columns: element (ix, c) -> buffer c, packed slot ix/2 (real packing of length L); only
+  // the n real rows are read (16 loads in flight per thread), the padding is zero-filled apart
+  constexpr int UL = 16;
+  for (int e0 = threadIdx.x; e0 < C * n; e0 += UL * NT) {
+    double x[UL];
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
+    for (int u = 0; u < UL; ++u) {
       const int e = e0 + u * NT;
       const int c = e % C, ix = e / C;
       const int iy = iy0 + c;
-      x[u] = (e < C * L && ix < n && iy < n) ? v[base + size_t(ix) * n + iy] : 0.0;
+      x[u] = (e < C * n && iy < n) ? v[base + size_t(ix) * n + iy] : 0.0;
     }
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
+    for (int u = 0; u < UL; ++u) {
       const int e = e0 + u * NT;
-      if (e < C * L) {
+      if (e < C * n) {
         const int c = e % C, ix = e / C;
         comp2(smem, c * BS + pad16(ix >> 1), ix & 1) = x[u];
       }
+    }
+  }
+  {
+    const int s0 = (n + 1) >> 1;  // first slot with both entries at ix >= n
+    for (int t = threadIdx.x; t < C * M; t += NT) {
+      const int c = t / M, m = t - c * M;
+      if (m >= s0) smem[c * BS + pad16(m)] = make_double2(0.0, 0.0);
+      else if ((n & 1) && m == s0 - 1) comp2(smem, c * BS + pad16(m), 1) = 0.0;
     }
   }
   __syncthreads();
@@ -116,12 +126,24 @@ __global__ void __launch_bounds__(ColGeo<LOGM>::NT, (ColGeo<LOGM>::NT <= 256 ? 2
   }
   __syncthreads();
   block_fft<LOGM, 1, BS, E>(smem, twb + M, C);
-  for (int e = threadIdx.x; e < C * n; e += NT) {
-    const int c = e % C, ix = e / C;
-    const int iy = iy0 + c;
-    if (iy >= n) continue;
-    const size_t o = base + size_t(ix) * n + iy;
-    y[o] += comp2(smem, c * BS + pad16(ix >> 1), ix & 1);
+  // y += x-direction term: the read-modify-write batched 8 deep (latency bound otherwise)
+  constexpr int UE = 8;
+  for (int e0 = threadIdx.x; e0 < C * n; e0 += UE * NT) {
+    double yo[UE];
+#pragma unroll
+    for (int u = 0; u < UE; ++u) {
+      const int e = e0 + u * NT;
+      const int c = e % C, ix = e / C;
+      const int iy = iy0 + c;
+      yo[u] = (e < C * n && iy < n) ? y[base + size_t(ix) * n + iy] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < UE; ++u) {
+      const int e = e0 + u * NT;
+      const int c = e % C, ix = e / C;
+      const int iy = iy0 + c;
+      if (e < C * n && iy < n) y[base + size_t(ix) * n + iy] = yo[u] + comp2(smem, c * BS + pad16(ix >> 1), ix & 1);
+    }
   }
 }
 
@@ -137,7 +159,7 @@ __global__ void __launch_bounds__(ColGeo<LOGM>::NT, (ColGeo<LOGM>::NT <= 256 ? 2
   using G = ColGeo<LOGM>;
   constexpr int M = G::M, C = G::C, NT = G::NT, BS = G::BS, E = G::E;
   constexpr int NSR = M - 1;  // column length n
-  constexpr int U = 4;
+  constexpr int U = 16;       // loads in flight per thread (these phases are latency bound)
   extern __shared__ double2 smem[];
   double2* hbuf = smem + C * BS;  // DCT-III scratch columns (dst_block.cuh)
   constexpr int BH = G::BH;
@@ -169,12 +191,24 @@ __global__ void __launch_bounds__(ColGeo<LOGM>::NT, (ColGeo<LOGM>::NT <= 256 ? 2
   __syncthreads();
   block_dst<LOGM, BS, BH, 1>(smem, hbuf, twb, scale);
   const double2 l = __ldg(lam + r);
-  for (int e = threadIdx.x; e < C * NSR; e += NT) {
-    const int c = e % C, ix = e / C;
-    const int iy = iy0 + c;
-    if (iy >= NSR) continue;
-    double2* s = smem + c * BS + pad16(ix + 1);
-    *s = shift_apply<MODE>(*s, l.x - dt * __ldg(sigma + size_t(ix) * NSR + iy), l.y);
+  for (int e0 = threadIdx.x; e0 < C * NSR; e0 += U * NT) {
+    double sg[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int e = e0 + u * NT;
+      const int c = e % C, ix = e / C;
+      const int iy = iy0 + c;
+      sg[u] = (e < C * NSR && iy < NSR) ? __ldg(sigma + size_t(ix) * NSR + iy) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int e = e0 + u * NT;
+      const int c = e % C, ix = e / C;
+      const int iy = iy0 + c;
+      if (e >= C * NSR || iy >= NSR) continue;
+      double2* s = smem + c * BS + pad16(ix + 1);
+      *s = shift_apply<MODE>(*s, l.x - dt * sg[u], l.y);
+    }
   }
   __syncthreads();
   block_dst<LOGM, BS, BH, 0>(smem, hbuf, twb, scale);
