@@ -123,7 +123,19 @@ __device__ __forceinline__ void block_dst(double2* s, double2* h, const double2*
     FPC_DST_PH(0);
     fft_passes<LOGN, 1, BS, E, 2, CtaSync>(s, twb + N, int(threadIdx.x), nthr);
     FPC_DST_PH(1);
-    block_fft<LOGN - 1, 1, BH, E / 2>(h, twb + M, 0);
+#ifndef FPC_DCT_HALF_GROUP
+#define FPC_DCT_HALF_GROUP 1
+#endif
+    if constexpr (FPC_DCT_HALF_GROUP && E == 16) {
+      // the M-point DCT FFT in radix-16 passes by half the CTA (named barrier): fewer passes, i.e.
+      // less shared-memory traffic, than radix-8 passes over all threads -- these kernels are
+      // bound by the shared-memory pipe
+      constexpr int NH = (N / 2) / 16;
+      if (int(threadIdx.x) < NH) group_fft<LOGN - 1, 1, BH, 16, NH, 1>(h, twb + M, int(threadIdx.x));
+      __syncthreads();
+    } else {
+      block_fft<LOGN - 1, 1, BH, E / 2>(h, twb + M, 0);
+    }
     FPC_DST_PH(2);
   } else {
   // 1. pre: quadruples (j, N-j, M-j, M+j), j = 1..M/2 (degenerate at j = M/2 and for j = M)
