@@ -25,6 +25,10 @@
   } while (0)
 #endif
 
+#ifndef FPC_DCT_HALF_GROUP
+#define FPC_DCT_HALF_GROUP 1
+#endif
+
 namespace fpc {
 
 // Buffers: B = blockDim.x * 16 / N rows; row b has an N-slot buffer at s + b*BS (input f_j at
@@ -123,9 +127,6 @@ __device__ __forceinline__ void block_dst(double2* s, double2* h, const double2*
     FPC_DST_PH(0);
     fft_passes<LOGN, 1, BS, E, 2, CtaSync>(s, twb + N, int(threadIdx.x), nthr);
     FPC_DST_PH(1);
-#ifndef FPC_DCT_HALF_GROUP
-#define FPC_DCT_HALF_GROUP 1
-#endif
     if constexpr (FPC_DCT_HALF_GROUP && E == 16) {
       // the M-point DCT FFT in radix-16 passes by half the CTA (named barrier): fewer passes, i.e.
       // less shared-memory traffic, than radix-8 passes over all threads -- these kernels are
@@ -178,7 +179,18 @@ __device__ __forceinline__ void block_dst(double2* s, double2* h, const double2*
   FPC_DST_PH(0);
   block_fft<LOGN, 1, BS, E>(s, twb + N, 0);
   FPC_DST_PH(1);
-  block_fft<LOGN - 1, 1, BH, E / 2>(h, twb + M, 0);
+  // the M-point DCT FFTs of all rows: radix-16 passes on half the CTA when the CTA size allows
+  // (fewer shared-memory passes, as in the folded path; N <= 512: the larger-N small grids are
+  // latency bound and lose more to the idle half), else radix-8 passes on all threads
+  if (FPC_DCT_HALF_GROUP && E == 16 && LOGN >= 5 && LOGN <= 9 && nthr == 256) {
+    if (int(threadIdx.x) < 128) group_fft<LOGN - 1, 1, BH, 16, 128, 1>(h, twb + M, int(threadIdx.x));
+    __syncthreads();
+  } else if (FPC_DCT_HALF_GROUP && E == 16 && LOGN >= 5 && LOGN <= 9 && nthr == 512) {
+    if (int(threadIdx.x) < 256) group_fft<LOGN - 1, 1, BH, 16, 256, 1>(h, twb + M, int(threadIdx.x));
+    __syncthreads();
+  } else {
+    block_fft<LOGN - 1, 1, BH, E / 2>(h, twb + M, 0);
+  }
   FPC_DST_PH(2);
   }
 
