@@ -267,6 +267,44 @@ __device__ __forceinline__ void block_fft_from(double2* s, const double2* __rest
   fft_passes<LOGN, S, BS, E, R, CtaSync>(s, tw, tid, nthr);
 }
 
+// B real columns of length 2N packed into B complex N-point buffers (slot m = x[2m] + i x[2m+1]),
+// transformed with the first Stockham pass taken straight from the loader: load(b, k) returns
+// element k of column b (already scaled).  Threads map to butterflies column-fastest, so the
+// loads of consecutive threads hit consecutive columns of one row (the caller's coalescing unit),
+// and every thread issues all 2E of its loads before the first use.  Saves the staging write, one
+// shared-memory read pass and a barrier against packing into shared memory first.
+// Requires blockDim.x * E == B * N.  Ends with the spectra in s (natural order).
+template <int LOGN, int S, int B, int BS, int E, class Load>
+__device__ __forceinline__ void block_fft_columns_from(double2* s, const double2* __restrict__ tw, Load load) {
+  constexpr int N = 1 << LOGN;
+  constexpr int LE = E == 16 ? 4 : E == 8 ? 3 : E == 4 ? 2 : 1;
+  constexpr int rem = LOGN % LE;
+  constexpr int R = rem == 3 ? 8 : rem == 2 ? 4 : rem == 1 ? 2 : E;
+  constexpr int NB = N / R, PER = E / R;
+  const int tid = int(threadIdx.x), nthr = int(blockDim.x);
+  double2 v[PER][R];
+#pragma unroll
+  for (int q = 0; q < PER; ++q) {
+    const int g = tid + q * nthr;
+    const int b = g % B, j = g / B;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int m = j + r * NB;
+      v[q][r] = make_double2(load(b, 2 * m), load(b, 2 * m + 1));
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < PER; ++q) {
+    const int g = tid + q * nthr;
+    const int b = g % B, j = g / B;
+    Dft<R, S>::run(v[q]);
+#pragma unroll
+    for (int r = 0; r < R; ++r) s[b * BS + pad16(j * R + r)] = v[q][r];
+  }
+  __syncthreads();
+  fft_passes<LOGN, S, BS, E, R, CtaSync>(s, tw, tid, nthr);
+}
+
 // The same over a thread group of NTHR threads (local index tid) synchronised by named barrier ID;
 // NTHR * E == B * N.
 template <int LOGN, int S, int BS, int E, int NTHR, int ID>

@@ -302,6 +302,16 @@ __global__ void __launch_bounds__(Geo<LOGM, tot_t<LOGM>()>::NT, minb(Geo<LOGM, t
   // then the register-staged loads below mostly hit L2 (B200 config 1: 145 -> 131 us)
   l2_prefetch_column_tile(v + p0, size_t(ns) * 8, NTIME, B * 8, NT);
 
+#ifndef FPC_TF_FUSED
+#define FPC_TF_FUSED 1
+#endif
+  if (FPC_TF_FUSED) {
+    FPC_PT(0, 1);
+    block_fft_columns_from<LOGM, 1, B, BS, G::E>(smem, twb + M, [&](int c, int kk) {
+      const int p = p0 + c;
+      return p < ns ? __ldg(sf + kk) * (s_in * v[size_t(kk) * ns + p]) : 0.0;
+    });
+  } else {
   for (int e0 = threadIdx.x; e0 < B * NTIME; e0 += U * NT) {
     double x[U];
 #pragma unroll
@@ -323,6 +333,7 @@ __global__ void __launch_bounds__(Geo<LOGM, tot_t<LOGM>()>::NT, minb(Geo<LOGM, t
   __syncthreads();
   FPC_PT(0, 1);
   block_fft<LOGM, 1, BS, G::E>(smem, twb + M, B);
+  }
   FPC_PT(0, 2);
 
   const double2* twT = twb + NTIME;  // e^{-2 pi i n/Nt}; the forward kernel here is e^{+...}

@@ -145,6 +145,15 @@ __global__ void __launch_bounds__(CGeo<LOGM, tot_c<LOGM>()>::NT, minb_c(CGeo<LOG
   const int p0 = blockIdx.x * B;
   l2_prefetch_tile(u + p0, size_t(ns) * 8, NTIME, B * 8, NT);
 
+#ifndef FPC_TF_FUSED
+#define FPC_TF_FUSED 1
+#endif
+  if (FPC_TF_FUSED) {
+    block_fft_columns_from<LOGM, 1, B, BS, G::E>(smem, twb + M, [&](int c, int kk) {
+      const int p = p0 + c;
+      return p < ns ? __ldg(sf + kk) * (s_in * u[size_t(kk) * ns + p]) : 0.0;
+    });
+  } else {
   for (int e0 = threadIdx.x; e0 < B * NTIME; e0 += U * NT) {
     double x[U];
 #pragma unroll
@@ -165,6 +174,7 @@ __global__ void __launch_bounds__(CGeo<LOGM, tot_c<LOGM>()>::NT, minb_c(CGeo<LOG
   }
   __syncthreads();
   block_fft<LOGM, 1, BS, G::E>(smem, twb + M, B);
+  }
 
   // unpack (n, M-n) -> Z_n, Z_{M-n}; divide; repack for the inverse (K2 / K4 formulas)
   const double2* twT = twb + NTIME;  // e^{-2 pi i n/Nt}
