@@ -1715,6 +1715,8 @@ int fpc_shard_dots(fpc_context_t c, const double* const* V, const double* scales
   if (!c || !out_host) return set_err(FPC_INVALID_ARGUMENT, "null argument");
   return guarded([&] {
     if (nv < 0 || nv > 250) throw InvalidArg{"fpc_shard_dots: 0 <= nv <= 250"};
+    for (int i = 0; i < nv; ++i) check_dev_aligned(V[i], "fpc_shard_dots");
+    check_dev_aligned(w, "fpc_shard_dots");
     DeviceGuard g(c->device);
     GmresState S{nullptr, c, n, c->stream, std::vector<double>(scales, scales + nv), 0};
     std::vector<const double*> vv(V, V + nv);
@@ -1732,6 +1734,8 @@ int fpc_shard_update(fpc_context_t c, const double* const* V, const double* coef
   if (!c || !norm2_host) return set_err(FPC_INVALID_ARGUMENT, "null argument");
   return guarded([&] {
     if (nv < 0 || nv > 250) throw InvalidArg{"fpc_shard_update: 0 <= nv <= 250"};
+    for (int i = 0; i < nv; ++i) check_dev_aligned(V[i], "fpc_shard_update");
+    check_dev_aligned(w, "fpc_shard_update");
     DeviceGuard g(c->device);
     std::vector<double> ones(size_t(nv), 1.0);
     ck(cudaMemcpyAsync(c->dvptr, V, size_t(nv) * sizeof(double*), cudaMemcpyHostToDevice, c->stream), "vptr");
@@ -1752,6 +1756,8 @@ int fpc_shard_lincomb(fpc_context_t c, const double* const* V, const double* coe
   if (!c) return set_err(FPC_INVALID_ARGUMENT, "null context");
   return guarded([&] {
     if (nv < 1 || nv > 250) throw InvalidArg{"fpc_shard_lincomb: 1 <= nv <= 250"};
+    for (int i = 0; i < nv; ++i) check_dev_aligned(V[i], "fpc_shard_lincomb");
+    check_dev_aligned(u, "fpc_shard_lincomb");
     DeviceGuard g(c->device);
     std::vector<double> ones(size_t(nv), 1.0);
     ck(cudaMemcpyAsync(c->dvptr, V, size_t(nv) * sizeof(double*), cudaMemcpyHostToDevice, c->stream), "vptr");

@@ -30,7 +30,10 @@ int carveout_pct(size_t dyn_smem, int threads) {
 }
 
 constexpr int kDotsThreads = 256;
-constexpr int kDotsGrid = 148 * 4;
+#ifndef FPC_DOTS_GRID
+#define FPC_DOTS_GRID (148 * 8)  // B200 config 1: Q1 200 -> 187 us, lincomb 347 -> 281 us vs 148 * 4
+#endif
+constexpr int kDotsGrid = FPC_DOTS_GRID;
 int dots_grid() { return kDotsGrid; }
 
 template <int NACC>
