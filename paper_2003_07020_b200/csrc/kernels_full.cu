@@ -8,7 +8,7 @@
 namespace fpc {
 
 namespace {
-constexpr int kGridF = 148 * 4;  // == dots_grid(): the partials reduce with launch_reduce
+// grid = dots_grid(): the per-CTA partials are summed by launch_reduce over dots_grid() rows
 
 __host__ __device__ constexpr int skew_f(int m) {
   return m < 16 ? padded(m) : padded(m) + ((9 - padded(m) % 8) % 8);
@@ -114,7 +114,7 @@ cudaError_t launch_time_inv_full(const double2* Z, double* z, int n_space, int n
   {                                                                                        \
     using G = FGeo<LN>;                                                                    \
     if ((err = prep_f(k_time_inv_full<LN>, G::SMEM)) != cudaSuccess) return err;           \
-    k_time_inv_full<LN><<<kGridF, G::NT, G::SMEM, st>>>(Z, z, n_space, scale_bwd, tw_base, partial); \
+    k_time_inv_full<LN><<<dots_grid(), G::NT, G::SMEM, st>>>(Z, z, n_space, scale_bwd, tw_base, partial); \
   }
   switch (l) {
     case 2: CALL(2); break;
