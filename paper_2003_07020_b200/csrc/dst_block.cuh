@@ -28,6 +28,9 @@
 #ifndef FPC_DCT_HALF_GROUP
 #define FPC_DCT_HALF_GROUP 1
 #endif
+#ifndef FPC_DCT_HALF_MAXLOG
+#define FPC_DCT_HALF_MAXLOG 9
+#endif
 
 namespace fpc {
 
@@ -182,10 +185,10 @@ __device__ __forceinline__ void block_dst(double2* s, double2* h, const double2*
   // the M-point DCT FFTs of all rows: radix-16 passes on half the CTA when the CTA size allows
   // (fewer shared-memory passes, as in the folded path; N <= 512: the larger-N small grids are
   // latency bound and lose more to the idle half), else radix-8 passes on all threads
-  if (FPC_DCT_HALF_GROUP && E == 16 && LOGN >= 5 && LOGN <= 9 && nthr == 256) {
+  if (FPC_DCT_HALF_GROUP && E == 16 && LOGN >= 5 && LOGN <= FPC_DCT_HALF_MAXLOG && nthr == 256) {
     if (int(threadIdx.x) < 128) group_fft<LOGN - 1, 1, BH, 16, 128, 1>(h, twb + M, int(threadIdx.x));
     __syncthreads();
-  } else if (FPC_DCT_HALF_GROUP && E == 16 && LOGN >= 5 && LOGN <= 9 && nthr == 512) {
+  } else if (FPC_DCT_HALF_GROUP && E == 16 && LOGN >= 5 && LOGN <= FPC_DCT_HALF_MAXLOG && nthr == 512) {
     if (int(threadIdx.x) < 256) group_fft<LOGN - 1, 1, BH, 16, 256, 1>(h, twb + M, int(threadIdx.x));
     __syncthreads();
   } else {
