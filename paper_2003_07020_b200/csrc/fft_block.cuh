@@ -166,6 +166,23 @@ __device__ __forceinline__ void apply_twiddles(double2* v, const double2* __rest
   }
 }
 
+// Cluster barrier without memory ordering (barrier.cluster.arrive.relaxed): for barriers that only
+// order execution -- "every CTA of the cluster has started" or "the partner has finished reading my
+// shared memory" (its DSMEM loads have returned: their values were consumed before it arrived).
+// cg::cluster_group::sync() is arrive.release, i.e. MEMBAR.ALL.GPU, which waits for every
+// outstanding global store of the thread (the epilogue's) before the CTA can retire.
+// FPC_CLUSTER_RELAXED=0 restores cluster.sync() everywhere (A/B).
+#ifndef FPC_CLUSTER_RELAXED
+#define FPC_CLUSTER_RELAXED 1
+#endif
+template <class Cluster>
+__device__ __forceinline__ void cluster_sync_relaxed(Cluster& cluster) {
+  if constexpr (FPC_CLUSTER_RELAXED)
+    asm volatile("barrier.cluster.arrive.relaxed.aligned;\n\tbarrier.cluster.wait.aligned;\n" ::: "memory");
+  else
+    cluster.sync();
+}
+
 // Barrier policies: the whole CTA, or a named barrier over a thread group (warp-specialised
 // kernels running independent transforms in different groups).
 struct CtaSync {

@@ -143,6 +143,18 @@ cudaError_t launch_time_solve(const double* u, double* z, int n_space, int n_tim
                               const double* scale_bwd, double s_in, const double2* lambda, const double* sigma,
                               double dt, const double2* tw_base, cudaStream_t st, bool forward);
 
+// ---- time FFTs on 2-CTA clusters split by time parity (kernels_tsplit.cu), Nt = 1024 / 2048:
+// the launchers above dispatch to these when time_split_supported(n_time)
+bool time_split_supported(int n_time);
+cudaError_t launch_time_fwd_split(const double* v, double2* Z, int n_space, int n_time, const double* scale_fwd,
+                                  double s_in, const double2* tw_base, cudaStream_t st);
+cudaError_t launch_time_inv_split(const double2* Z, double* z, int n_space, int n_time, const double* scale_bwd,
+                                  const double2* tw_base, cudaStream_t st);
+cudaError_t launch_time_solve_split(const double* u, double* z, int n_space, int n_time, const double* scale_fwd,
+                                    const double* scale_bwd, double s_in, const double2* lambda,
+                                    const double* sigma, double dt, const double2* tw_base, cudaStream_t st,
+                                    bool forward);
+
 // ---- BiCGSTAB vector kernels (krylov.hpp:204-280) -------------------------------------------
 // p = r (first) or r + beta (p - omega v)
 cudaError_t launch_bicg_p(const double* r, const double* v, double* p, double beta, double omega,

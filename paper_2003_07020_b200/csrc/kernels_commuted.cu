@@ -275,6 +275,9 @@ cudaError_t launch_time_solve(const double* u, double* z, int n_space, int n_tim
                               const double* scale_bwd, double s_in, const double2* lambda, const double* sigma,
                               double dt, const double2* tw_base, cudaStream_t st, bool forward) {
   cudaError_t err = cudaSuccess;
+  if (time_split_supported(n_time))
+    return launch_time_solve_split(u, z, n_space, n_time, scale_fwd, scale_bwd, s_in, lambda, sigma, dt, tw_base, st,
+                                   forward);
   const int lm = ilog2_c(n_time) - 1;
 #define CALL(LM)                                                                                      \
   {                                                                                                   \

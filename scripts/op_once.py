@@ -14,3 +14,7 @@ y = torch.empty_like(b)
 op.apply(b, y)
 fp.apply_inverse(plan, b, y)
 torch.cuda.synchronize()
+if len(sys.argv) > 2 and sys.argv[2] == "commuted":
+    planc = fp.build_plan(fp.PreconditionerKind.generalized(), w.n_time, w.dt, op, ordering=fp.Ordering.commuted)
+    fp.apply_inverse(planc, b, y)
+    torch.cuda.synchronize()
