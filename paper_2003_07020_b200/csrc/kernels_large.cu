@@ -46,7 +46,7 @@ __global__ void __launch_bounds__(kThr, 1)
   const long kg = long(k) + koff;
   const double* vk = v + k * ns;
   const double2* twL = twb + L;  // e^{-2 pi i t/L}
-  cluster.sync();  // every CTA of the cluster is running before its shared memory is written
+  cluster_sync_relaxed(cluster);  // every CTA of the cluster is running before its shared memory is written
 
   // 1. fold: for my m-slice, the C-point DFT over r of x_{m+rS} (x = 0 for index >= Ns, so only
   //    r < C/2 contribute), twiddled by w_L^{m q} and stored into CTA q's buffer
@@ -102,13 +102,13 @@ __global__ void __launch_bounds__(kThr, 1)
       yk[j] = c + t[r].x;
     }
   }
-  cluster.sync();  // partners have read this CTA's buffer
+  cluster_sync_relaxed(cluster);  // partners have read this CTA's buffer (no wait on the y stores)
 }
 
 // ---------------------------------------------------------------------------------- tau solve
 // one DST-I of the row (in place), scaled by sqrt(2/N); MODE 1/2: divided/multiplied by the
 // shifted eigenvalue (tau.hpp:109-118) on the way out
-template <int C, int MODE>
+template <int C, int MODE, bool LAST = false>
 __device__ __forceinline__ void dst_cl(double2* row, double2* smem, cg::cluster_group& cluster, int q,
                                        const double2* __restrict__ twb, double2 l,
                                        const double* __restrict__ sigma, double dt) {
@@ -152,7 +152,12 @@ __device__ __forceinline__ void dst_cl(double2* row, double2* smem, cg::cluster_
       row[kk - 1] = val;
     }
   }
-  cluster.sync();  // row writes visible to the cluster; partners are done with this buffer
+  // row writes visible to the cluster (the next DST's fold reads them); after the last DST only
+  // "partners are done with this buffer" is needed
+  if constexpr (LAST)
+    cluster_sync_relaxed(cluster);
+  else
+    cluster.sync();
 }
 
 template <int C, int MODE>
@@ -165,9 +170,9 @@ __global__ void __launch_bounds__(kThr, 1)
   const int rowi = blockIdx.x / C;
   double2* row = Z + size_t(rowi) * ns;
   const double2 l = MODE != 0 ? __ldg(lam + rowi) : make_double2(1.0, 0.0);
-  cluster.sync();  // every CTA of the cluster is running before its shared memory is written
+  cluster_sync_relaxed(cluster);  // every CTA of the cluster is running before its shared memory is written
   dst_cl<C, MODE>(row, smem, cluster, q, twb, l, sigma, dt);
-  dst_cl<C, 0>(row, smem, cluster, q, twb, l, sigma, dt);
+  dst_cl<C, 0, true>(row, smem, cluster, q, twb, l, sigma, dt);
 }
 
 template <class K>
