@@ -105,6 +105,115 @@ __global__ void __launch_bounds__(kThr, 1)
   cluster_sync_relaxed(cluster);  // partners have read this CTA's buffer (no wait on the y stores)
 }
 
+// ------------------------------------------------------------------ matvec, packed residue split
+// The 2-CTA split of kernels_mv.cu generalised to C = M/S CTAs (C = 4: Ns = 32767, C = 8: Ns = 65535):
+// the real length-L embedding is packed into M = L/2 complex points z_m = v_{2m} + i v_{2m+1}
+// (z_m = 0 for m >= H = M/2), and the M-point transform is split by residue classes of the bins,
+// k = C k' + q:
+//   X_{Ck'+q} = sum_{m'<S} e^{-2 pi i m'k'/S} [ w_M^{m'q} sum_{j<C/2} z_{m'+jS} e^{-2 pi i jq/C} ],
+// one S-point FFT per rank (only j < C/2 of the C-point DFT is non-zero: half the fold work of the
+// unpacked k_matvec_cl, whose L-point transform is twice as long).  The spectral product pairs
+// bins k and M-k: residues q and C-q, so ranks 0 and C/2 pair within themselves and rank q pairs
+// with rank C-q through DSMEM (each rank of a pair handles the pairs whose own slot is < S/2, so
+// no slot is touched by both).  Inverse: rank q inverts its residue class, then
+//   y_{m'+jS} = sum_q e^{+2 pi i jq/C} [ w_M^{-m'q} a^{(q)}_{m'} ]   (j < C/2: the outputs needed),
+// a C-point DFT over the ranks' values of one m', gathered through DSMEM.
+template <int C>
+__global__ void __launch_bounds__(kThr, 1)
+    k_matvec_splitc(const double* __restrict__ v, double* __restrict__ y, int ns, int koff,
+                    const double* __restrict__ eig, const double2* __restrict__ twb) {
+  constexpr int S = kS, M = C * S, L = 2 * M;
+  extern __shared__ double2 smem[];
+  cg::cluster_group cluster = cg::this_cluster();
+  const int q = int(cluster.block_rank());
+  const size_t k = blockIdx.x / C;
+  const long kg = long(k) + koff;
+  const double* vk = v + k * ns;
+  const double2* twM = twb + M;        // e^{-2 pi i t/M} = twMh[t >> 6] * twM[t & 63]
+  const double2* twMh = twb + M / 64;
+  auto wm = [&](int t) -> double2 { return cmul(__ldg(twMh + (t >> 6)), __ldg(twM + (t & 63))); };
+  const double2* twC = twb + C;        // e^{-2 pi i t/C}
+  cluster_sync_relaxed(cluster);       // every CTA of the cluster is running (DSMEM targets exist)
+
+  // 1. forward: u_{m'} = w_M^{m'q} sum_{j<C/2} z_{m'+jS} e^{-2 pi i jq/C}, S-point FFT (-)
+  auto load_u = [&](int mp) -> double2 {
+    double2 acc = make_double2(0.0, 0.0);
+#pragma unroll
+    for (int j = 0; j < C / 2; ++j) {
+      const int i = 2 * (mp + j * S);
+      const double2 zm = make_double2(i < ns ? vk[i] : 0.0, i + 1 < ns ? vk[i + 1] : 0.0);
+      acc = j == 0 ? zm : cadd(acc, q == 0 ? zm : cmul(zm, __ldg(twC + ((j * q) & (C - 1)))));
+    }
+    return q == 0 ? acc : cmul(acc, wm(mp * q));
+  };
+  block_fft_from<kLogS, -1, kBS, 16>(smem, twb + S, load_u);
+  cluster.sync();  // both ranks of every pair have their spectra
+
+  // 2. eigenvalue product on (kappa, M - kappa) pairs (kernels_mv.cu formulas)
+  const double2* twL = twb + L;
+  const double2* twLh = twb + L / 128;  // e^{-2 pi i kappa/L} = twLh[kappa >> 7] twL[kappa & 127]
+  const int qp = (C - q) & (C - 1);      // partner rank (0 -> 0, C/2 -> C/2)
+  double2* own = smem;
+  double2* par = cluster.map_shared_rank(smem, qp);
+  const int ntask = q == 0 ? S / 2 + 1 : S / 2;
+  for (int t = int(threadIdx.x); t < ntask; t += kThr) {
+    const int kap = C * t + q;
+    if (kap == 0) {
+      const double2 z = own[0];
+      const double y0 = __ldg(eig) * (2.0 * (z.x + z.y));
+      const double ym = __ldg(eig + M) * (2.0 * (z.x - z.y));
+      own[0] = make_double2(y0 + ym, y0 - ym);
+      continue;
+    }
+    // partner slot of M - kappa: rank 0 -> S - t, others -> S - 1 - t (in rank qp)
+    const int s2 = q == 0 ? S - t : S - 1 - t;
+    const double2 w = cmul(__ldg(twLh + (kap >> 7)), __ldg(twL + (kap & 127)));
+    const double ek = __ldg(eig + kap), em = __ldg(eig + (M - kap));
+    const double2 a = own[pad16(t)], bq = par[pad16(s2)];
+    const double2 P = cadd(a, cconj(bq)), Q = csub(a, cconj(bq));
+    const double2 iwQ = mul_si<1>(cmul(w, Q));
+    const double2 Yk = cscale(csub(P, iwQ), ek);
+    const double2 Ym = cscale(cconj(cadd(P, iwQ)), em);
+    const double2 A = cadd(Yk, cconj(Ym));
+    const double2 D = csub(Yk, cconj(Ym));
+    own[pad16(t)] = cadd(A, mul_si<1>(cmul(D, cconj(w))));
+    if (!(q == 0 && s2 == t)) par[pad16(s2)] = cadd(cconj(A), mul_si<1>(cmul(cconj(D), w)));
+  }
+  cluster.sync();  // the partner's writes into my slots >= S/2 are done
+  block_fft<kLogS, 1, kBS, 16>(smem, twb + S, 1);
+  cluster.sync();  // every rank's inverse is done
+
+  // 3. y_{m'+jS} = sum_r e^{+2 pi i jr/C} w_M^{-m'r} a^{(r)}_{m'}, j < C/2; + BDF2 stencil
+  double* yk = y + k * ns;
+  for (int mp = q * (S / C) + int(threadIdx.x); mp < (q + 1) * (S / C); mp += kThr) {
+    double2 b[C];
+#pragma unroll
+    for (int r = 0; r < C; ++r) {
+      const double2 p = cluster.map_shared_rank(smem, r)[pad16(mp)];
+      b[r] = r == 0 ? p : cmul(p, cconj(wm(mp * r)));
+    }
+    Dft<C, 1>::run(b);
+#pragma unroll
+    for (int j = 0; j < C / 2; ++j) {
+#pragma unroll
+      for (int part = 0; part < 2; ++part) {
+        const int i = 2 * (mp + j * S) + part;
+        if (i >= ns) continue;
+        const double c0 = vk[i];
+        double c;  // time_stencil.hpp:16-26 (same association as all_at_once.hpp:44-53)
+        if (kg == 0)
+          c = c0;
+        else if (kg == 1)
+          c = 1.5 * c0 + -2.0 * vk[long(i) - ns];
+        else
+          c = 1.5 * c0 + -2.0 * vk[long(i) - ns] + 0.5 * vk[long(i) - 2 * long(ns)];
+        yk[i] = c + (part ? b[j].y : b[j].x);
+      }
+    }
+  }
+  cluster_sync_relaxed(cluster);  // partners have read this CTA's buffer
+}
+
 // ---------------------------------------------------------------------------------- tau solve
 // one DST-I of the row (in place), scaled by sqrt(2/N); MODE 1/2: divided/multiplied by the
 // shifted eigenvalue (tau.hpp:109-118) on the way out
@@ -204,9 +313,20 @@ cudaError_t launch_cl(K kernel, int C, int nclusters, cudaStream_t st, void** ar
 
 cudaError_t launch_matvec_large(const double* v, double* y, int n_space, int n_time, int log_m, int koff,
                                 const double* eig_scaled, const double2* tw_base, cudaStream_t st) {
-  // L = 2M = C * 8192 (M = 16384 runs on kernels_mv.cu's packed 2-CTA split instead)
-  const int C = 1 << (log_m + 1 - kLogS);
   void* args[] = {(void*)&v, (void*)&y, (void*)&n_space, (void*)&koff, (void*)&eig_scaled, (void*)&tw_base};
+#ifndef FPC_MV_LARGE_SPLIT
+#define FPC_MV_LARGE_SPLIT 1
+#endif
+  if (FPC_MV_LARGE_SPLIT) {  // packed residue split: M = C * 8192
+    const int Cp = 1 << (log_m - kLogS);
+    switch (Cp) {
+      case 4: return launch_cl(k_matvec_splitc<4>, 4, n_time, st, args);
+      case 8: return launch_cl(k_matvec_splitc<8>, 8, n_time, st, args);
+      default: return cudaErrorInvalidValue;
+    }
+  }
+  // unpacked: L = 2M = C * 8192 (M = 16384 runs on kernels_mv.cu's packed 2-CTA split instead)
+  const int C = 1 << (log_m + 1 - kLogS);
   switch (C) {
     case 8: return launch_cl(k_matvec_cl<8>, 8, n_time, st, args);
     case 16: return launch_cl(k_matvec_cl<16>, 16, n_time, st, args);
