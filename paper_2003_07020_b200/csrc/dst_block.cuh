@@ -28,6 +28,9 @@
 #ifndef FPC_DCT_HALF_GROUP
 #define FPC_DCT_HALF_GROUP 1
 #endif
+#ifndef FPC_DST_PRE_SEL
+#define FPC_DST_PRE_SEL 1
+#endif
 #ifndef FPC_DCT_HALF_MAXLOG
 #define FPC_DCT_HALF_MAXLOG 9
 #endif
@@ -92,11 +95,14 @@ __device__ __forceinline__ void dst_pre_folded(double2* r, double2* hv, const do
     hv[pad16(j)] = cscale(cmul(cconj(wj), csub(sj, mul_si<1>(sj))), 0.5);
   }
   __syncthreads();  // every f has been read before the pass outputs overwrite the row
+  // the pair (2j, 2j+1) is written as two stores whose slot parity alternates with lane bit 2: each
+  // store then covers eight bank groups per quarter warp (2j alone hits four, twice)
+  const int sel = FPC_DST_PRE_SEL ? (int(threadIdx.x) >> 2) & 1 : 0;
 #pragma unroll
   for (int u = 0; u < KQ; ++u) {
     const int j = int(threadIdx.x) + u * NT;
-    r[pad16(2 * j)] = o[u][0];
-    r[pad16(2 * j + 1)] = o[u][1];
+    r[pad16(2 * j + sel)] = sel ? o[u][1] : o[u][0];
+    r[pad16(2 * j + 1 - sel)] = sel ? o[u][0] : o[u][1];
     if (j != 0) {
       r[pad16(2 * (M - j))] = o[u][2];
       r[pad16(2 * (M - j) + 1)] = o[u][3];
