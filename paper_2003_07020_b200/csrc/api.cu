@@ -1224,7 +1224,7 @@ static void gmres_inner_lagged(fpc_plan_s* pl, const double* b, double* x, doubl
         }
         LAUNCH("dots2", st, fpc::launch_dots2(vs, cnt, U, W, n, c->partial, stride, g0, g0 == 0, st));
       }
-      LAUNCH("reduce", st, fpc::launch_reduce(c->partial, stride, fpc::kDots2X + 3, c->dscal, false, st));
+      LAUNCH("reduce", st, fpc::launch_reduce_dots2(c->partial, stride, j, c->dscal, st));
       ck(cudaMemcpyAsync(c->hpin, c->dscal, (fpc::kDots2X + 3) * sizeof(double), cudaMemcpyDeviceToHost, st),
          "D2H");
       ck(cudaStreamSynchronize(st), "sync");

@@ -123,6 +123,9 @@ struct VecSet16 {
 // extra: [.. + kDots2X + 0..2] = <U,W>, <U,U>, <W,W>
 cudaError_t launch_dots2(const VecSet16& vs, int nv, const double* U, const double* W, size_t n,
                          double* partial, int stride, int col0, bool extra, cudaStream_t st);
+// out[c] for the used columns of a dots2 reduction only (c = 0..nab-1, kDots2B + 0..nab-1,
+// kDots2X + 0..2), same per-column arithmetic as launch_reduce
+cudaError_t launch_reduce_dots2(const double* partial, int stride, int nab, double* out, cudaStream_t st);
 constexpr int kMaxUpd2 = 24;
 struct Update2Args {
   const double* v[kMaxUpd2];

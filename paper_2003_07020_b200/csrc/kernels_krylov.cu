@@ -121,13 +121,27 @@ cudaError_t launch_dots(const VecSet& vs, int nv, const double* w, size_t n, dou
 }
 
 // One CTA per output: thread t sums partials b = t, t+256, ... in order, then a fixed
-// shuffle/smem tree -> the result is independent of scheduling (deterministic).
+// shuffle/smem tree -> the result is independent of scheduling (deterministic).  The thread's
+// loads are all issued before the first add (same summation order).  Column of CTA i: i, or for a
+// Q1 reduction (nab > 0) the used columns only: a_0..a_{nab-1}, b_0..b_{nab-1}, the three extras.
 __global__ void __launch_bounds__(kDotsThreads)
     k_reduce(const double* __restrict__ partial, int stride, int count, double* __restrict__ out,
-             int accumulate) {
-  const int i = blockIdx.x;
+             int accumulate, int nab) {
+  const int i = nab > 0 ? (int(blockIdx.x) < nab       ? int(blockIdx.x)
+                           : int(blockIdx.x) < 2 * nab ? kDots2B + int(blockIdx.x) - nab
+                                                       : kDots2X + int(blockIdx.x) - 2 * nab)
+                        : int(blockIdx.x);
+  constexpr int PER = (kDotsGrid + kDotsThreads - 1) / kDotsThreads;
+  double x[PER];
+#pragma unroll
+  for (int u = 0; u < PER; ++u) {
+    const int b = int(threadIdx.x) + u * kDotsThreads;
+    x[u] = b < kDotsGrid ? partial[size_t(b) * stride + i] : 0.0;
+  }
   double acc[1] = {0.0};
-  for (int b = threadIdx.x; b < kDotsGrid; b += kDotsThreads) acc[0] += partial[size_t(b) * stride + i];
+#pragma unroll
+  for (int u = 0; u < PER; ++u)
+    if (int(threadIdx.x) + u * kDotsThreads < kDotsGrid) acc[0] += x[u];
   __shared__ double outb[1];
   block_reduce_store<1>(acc, outb);
   __syncthreads();
@@ -137,7 +151,13 @@ __global__ void __launch_bounds__(kDotsThreads)
 cudaError_t launch_reduce(const double* partial, int stride, int count, double* out,
                           bool accumulate, cudaStream_t st) {
   if (count <= 0) return cudaSuccess;
-  k_reduce<<<count, kDotsThreads, 0, st>>>(partial, stride, count, out, accumulate ? 1 : 0);
+  k_reduce<<<count, kDotsThreads, 0, st>>>(partial, stride, count, out, accumulate ? 1 : 0, 0);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_reduce_dots2(const double* partial, int stride, int nab, double* out, cudaStream_t st) {
+  if (nab <= 0 || nab > kDots2B) return cudaErrorInvalidValue;
+  k_reduce<<<2 * nab + 3, kDotsThreads, 0, st>>>(partial, stride, 2 * nab + 3, out, 0, nab);
   return cudaGetLastError();
 }
 
