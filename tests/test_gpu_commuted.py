@@ -22,7 +22,8 @@ def make(gamma, ns, nt, alpha=0.0):
 
 
 @pytest.mark.parametrize("ns,nt", [(3, 4), (15, 8), (31, 64), (255, 16), (1023, 256), (4095, 32),
-                                   (8191, 64), (511, 2048), (127, 1024), (255, 2048), (63, 16384)])
+                                   (8191, 64), (511, 2048), (127, 1024), (255, 2048), (127, 4096), (63, 8192),
+                                   (63, 16384)])
 def test_commuted_pc_vs_oracle(oracle, ns, nt):
     op, plan, h, dt = make(1.5, ns, nt)
     po = oracle.problem_1d(1.5, 1.0, h, ns, nt, dt).build_plan()
