@@ -115,6 +115,16 @@ struct MvGeo {
   static constexpr size_t SMEM = G::SMEM + (mv_cst_parked<LOGM>() ? size_t(G::B) * G::M * sizeof(double) : 0);
 };
 
+// e / d for 0 <= e < 2^24 by a float reciprocal and one correction step (a runtime integer
+// division is a ~20-instruction dependent chain; these index splits sit in the latency-bound
+// load and epilogue loops of the rows matvec, where ns and rows-per-level are runtime values)
+__device__ __forceinline__ int div_small(int e, int d, float inv_d) {
+  int q = __float2int_rz(__int2float_rn(e) * inv_d);
+  q -= (q * d > e) ? 1 : 0;
+  q += ((q + 1) * d <= e) ? 1 : 0;
+  return q;
+}
+
 template <int LOGM>
 __global__ void __launch_bounds__(Geo<LOGM, kTotMv, 16>::NT, minb(Geo<LOGM, kTotMv, 16>::NT))
     k_matvec_1d(const double* __restrict__ v, double* __restrict__ y, int ns, int nrows, int rpt,
@@ -132,6 +142,7 @@ __global__ void __launch_bounds__(Geo<LOGM, kTotMv, 16>::NT, minb(Geo<LOGM, kTot
   double* cst = reinterpret_cast<double*>(smem + B * BS);  // stencil part, B x M
   const int k0 = blockIdx.x * B;
   const int nb = min(B, nrows - k0);
+  const float inv_ns = 1.0f / float(ns), inv_rpt = 1.0f / float(rpt);
 
   constexpr bool kParked = mv_cst_parked<LOGM>();
   if (!kParked) {
@@ -151,7 +162,7 @@ __global__ void __launch_bounds__(Geo<LOGM, kTotMv, 16>::NT, minb(Geo<LOGM, kTot
       for (int u = 0; u < UL; ++u) {
         const int e = e0 + u * NT;
         if (e < nreal) {
-          const int b = e / ns, idx = e - b * ns;
+          const int b = div_small(e, ns, inv_ns), idx = e - b * ns;
           comp(smem, b * BS + pad16(idx >> 1), idx & 1) = x[u];
         }
       }
@@ -170,7 +181,7 @@ __global__ void __launch_bounds__(Geo<LOGM, kTotMv, 16>::NT, minb(Geo<LOGM, kTot
     for (int u = 0; u < U; ++u) {
       const int e = e0 + u * NT;
       const int b = e / L, idx = e - b * L;
-      const int k = (k0 + b) / rpt + koff;
+      const int k = div_small(k0 + b, rpt, inv_rpt) + koff;
       const bool ok = e < B * L && b < nb && idx < ns;
       const size_t o = size_t(k0 + b) * ns + idx;
       x0[u] = ok ? v[o] : 0.0;
@@ -184,7 +195,7 @@ __global__ void __launch_bounds__(Geo<LOGM, kTotMv, 16>::NT, minb(Geo<LOGM, kTot
       const int e = e0 + u * NT;
       if (e < B * L) {
         const int b = e / L, idx = e - b * L;
-        const int k = (k0 + b) / rpt + koff;
+        const int k = div_small(k0 + b, rpt, inv_rpt) + koff;
         comp(smem, b * BS + pad16(idx >> 1), idx & 1) = x0[u];
         if (kParked && idx < ns) {
           double c;
@@ -247,8 +258,8 @@ __global__ void __launch_bounds__(Geo<LOGM, kTotMv, 16>::NT, minb(Geo<LOGM, kTot
 #pragma unroll
       for (int u = 0; u < UE; ++u) {
         const int e = e0 + u * NT;
-        const int b = e / ns, idx = e - b * ns;
-        const int k = (k0 + b) / rpt + koff;
+        const int b = div_small(e, ns, inv_ns), idx = e - b * ns;
+        const int k = div_small(k0 + b, rpt, inv_rpt) + koff;
         const bool ok = e < nb * ns;
         const size_t o = size_t(k0 + b) * ns + idx;
         x0[u] = ok ? v[o] : 0.0;
@@ -259,8 +270,8 @@ __global__ void __launch_bounds__(Geo<LOGM, kTotMv, 16>::NT, minb(Geo<LOGM, kTot
       for (int u = 0; u < UE; ++u) {
         const int e = e0 + u * NT;
         if (e >= nb * ns) continue;
-        const int b = e / ns, idx = e - b * ns;
-        const int k = (k0 + b) / rpt + koff;
+        const int b = div_small(e, ns, inv_ns), idx = e - b * ns;
+        const int k = div_small(k0 + b, rpt, inv_rpt) + koff;
         double c;  // time_stencil.hpp:16-26 (same association as all_at_once.hpp:44-53)
         if (k == 0)
           c = x0[u];
