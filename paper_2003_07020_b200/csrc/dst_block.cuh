@@ -211,11 +211,16 @@ __device__ __forceinline__ void block_dst(double2* s, double2* h, const double2*
   // thread tb owns k = tb*KP .. tb*KP + KP-1, visited in a per-thread rotated order: at step u the
   // eight lanes of a quarter warp then hit eight different bank groups in the reads of Y_k, Y_{N-k},
   // the DCT slot and the two output writes (1.05 wavefronts per access against 1.6 unrotated,
-  // KP = 8, one row per 32+ threads)
+  // KP = 8)
 #ifndef FPC_DST_POST_ROT
 #define FPC_DST_POST_ROT 1
 #endif
-  const int rot = (FPC_DST_POST_ROT && TPB >= 32) ? (4 * tb + 4 * (tb >> 1)) : 0;
+  // (rows of TPB < 32 threads share a warp at skewed buffer strides: same rotation for TPB >= 8,
+  // (4 tb + 5 floor(tb/2)) for TPB = 4: 2.8 -> 1.6 wavefronts)
+  const int rot = !FPC_DST_POST_ROT ? 0
+                  : TPB >= 8        ? 4 * tb + 4 * (tb >> 1)
+                  : TPB == 4        ? 4 * tb + 5 * (tb >> 1)
+                                    : 0;
 #pragma unroll
   for (int u = 0; u < KP; ++u) {
     const int k = tb * KP + ((u + rot) & (KP - 1));
