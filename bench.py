@@ -451,6 +451,14 @@ def main():
     B_pc = 16.0 * N + 64.0 * H * w.n_space
     peak, peak_kind = load_peaks()
 
+    # whole-solve roofline: compulsory bytes of the reference algorithm for k
+    # iterations -- (k+1)(B_mv + B_pc) + sum_j 8N(2j+5) (one Gram-Schmidt pass per step, j counted
+    # within a restart cycle) + 8N(k+1) (x = P^{-1} sum y_k V_k) + 16N (TRR) + (B_mv + 24N) per restart
+    rcyc = w.restart if w.restart else k + 1
+    n_restarts = max(0, (k - 1) // rcyc) if k > 0 else 0
+    B_tot = ((k + 1) * (B_mv + B_pc) + sum(8.0 * N * (2 * (j % rcyc) + 5) for j in range(k))
+             + 8.0 * N * (k + 1) + 16.0 * N + n_restarts * (B_mv + 24.0 * N))
+
     # dominant kernel by live device time inside the solve
     dom = max(table.items(), key=lambda kv: kv[1][0])
     dom_name, (dom_ms, dom_cnt) = dom
@@ -507,6 +515,10 @@ def main():
                          "frac": (achieved / peak) if achieved else None, "traffic": traffic,
                          "algorithmic_bytes_per_launch": dom_bytes, "avg_launch_us": dom_t * 1e6,
                          "peak_source": peak_kind},
+            "solve_roofline": {"bound": "hbm", "algorithmic_bytes": B_tot, "achieved": B_tot / t_step / 1e9,
+                               "peak": peak, "unit": "GB/s", "frac": B_tot / t_step / 1e9 / peak,
+                               "formula": "SURVEY 8(d) B_tot, one Gram-Schmidt pass per step (the reference "
+                                          "re-orthogonalises every step here, which doubles that term)"},
             "kernel_time_ms_per_solve": {k_: v[0] for k_, v in table.items()},
             "kernel_launches_per_solve": {k_: v[1] for k_, v in table.items()},
             "clocks": clk.summary(),
