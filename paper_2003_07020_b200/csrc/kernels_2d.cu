@@ -17,6 +17,15 @@ namespace {
 __host__ __device__ constexpr int skew2(int m) {
   return m < 16 ? padded(m) : padded(m) + ((9 - padded(m) % 8) % 8);
 }
+// Column-buffer stride for the column-fastest phases (loads, eigenvalue product, divide, stores:
+// lane = column c fastest, then the slot).  A quarter warp of 16-byte accesses covers 8/C slots of
+// each of C buffers (C <= 8), so the buffers must start 8/C bank groups apart (stride = 8/C mod 8):
+// C = 4 -> 2, C = 2 -> 4.  The 8-byte halves of the loads/epilogue then also land in distinct banks
+// (C = 4: 8 banks apart).  C >= 8 keeps the one-group skew (same slot, 8 consecutive buffers).
+__host__ __device__ constexpr int skew_cols(int m, int c) {
+  return m < 16 ? padded(m)
+                : padded(m) + (((c == 4 ? 2 : c == 2 ? 4 : 1) - padded(m) % 8 + 8) % 8);
+}
 __device__ __forceinline__ double& comp2(double2* s, int slot_padded, int c) {
   return reinterpret_cast<double*>(s + slot_padded)[c];
 }
@@ -44,7 +53,7 @@ struct ColGeo {
   static constexpr int E = M < 16 ? M : 16;
   static constexpr int C = kTot2 / M > 0 ? kTot2 / M : 1;  // columns per CTA
   static constexpr int NT = C * M / E;
-  static constexpr int BS = C > 1 ? skew2(M) : padded(M);
+  static constexpr int BS = C > 1 ? skew_cols(M, C) : padded(M);
   static constexpr int BH = C > 1 ? skew2(M / 2) : padded(M / 2);  // DCT-III scratch (tau)
   static constexpr size_t SMEM = size_t(C) * (BS + BH) * sizeof(double2);  // tau: FFT + DCT-III buffers
   static constexpr size_t SMEM_MV = size_t(C) * BS * sizeof(double2);      // matvec: FFT buffers only
