@@ -75,7 +75,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((1 << (LOGM - 1)) / 
   const double2* twL = twb + L;
   const double2* twLh = twb + L / 128;  // e^{-2 pi i kappa/L} = tw_{L/128}[kappa >> 7] tw_L[kappa & 127]
   const double2* eigq = reinterpret_cast<const double2*>(eig + eigq_offset(M)) + q * (H / 2);
-  constexpr int UP = 4;
+#ifndef FPC_MV_UP
+#define FPC_MV_UP 4
+#endif
+  constexpr int UP = FPC_MV_UP;
   constexpr int ntask = H / 2;
   if (q == 0 && threadIdx.x == 0) {
     const double2 z = smem[0];
@@ -126,7 +129,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((1 << (LOGM - 1)) / 
   double* yk = y + k * ns;
   constexpr int PER = (H / 2) / NT;  // m values per thread
   static_assert(PER * NT == H / 2, "H/2 must be a multiple of the thread count");
-  constexpr int UB = 2;              // m values whose loads are in flight together
+#ifndef FPC_MV_UB
+#define FPC_MV_UB 2
+#endif
+  constexpr int UB = FPC_MV_UB;      // m values whose loads are in flight together
 #pragma unroll 1
   for (int u0 = 0; u0 < PER; u0 += UB) {
     double2 e[UB], o[UB], w[UB], c0[UB], c1[UB], c2[UB];

@@ -9,7 +9,7 @@ pytestmark = pytest.mark.gpu
 
 SIZES = [(1.4, 1.8, 3, 4), (1.3, 1.7, 7, 8), (1.5, 1.5, 15, 16), (1.3, 1.7, 31, 8), (1.9, 1.2, 63, 4),
          (1.3, 1.7, 127, 8), (1.3, 1.7, 255, 8), (1.5, 1.5, 511, 4), (1.5, 1.5, 1023, 4),
-         (1.4, 1.6, 2047, 2)]
+         (1.4, 1.6, 2047, 4)]
 
 
 def make(gx, gy, n, nt, kx=1.0, ky=1.0):
