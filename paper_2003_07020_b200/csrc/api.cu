@@ -262,6 +262,8 @@ struct fpc_context_s {
   double* hpin = nullptr;       // pinned host mirror of dscal
   const double** dvptr = nullptr;  // device pointer table for update/lincomb
   double* dscales = nullptr;
+  cudaStream_t aux = nullptr;   // host-path result copy overlapped with the true-residual check
+  cudaEvent_t aux_ev = nullptr;
   static constexpr int kPartialStride = 264;
   static constexpr int kScal = 2048;  // [1024, 1280): unit scales for x = Z y
 };
@@ -419,6 +421,11 @@ static void release_ctx(fpc_context_s* c) {
   cudaFreeHost(c->hpin);
   cudaFree(c->dvptr);
   cudaFree(c->dscales);
+  if (c->aux) {
+    cudaStreamSynchronize(c->aux);
+    cudaStreamDestroy(c->aux);
+    cudaEventDestroy(c->aux_ev);
+  }
   if (c->own_stream) cudaStreamDestroy(c->stream);
   delete c;
 }
@@ -1370,8 +1377,21 @@ static double resid_norm_dev(fpc_plan_s* pl, const double* b, const double* x) {
   return std::sqrt(c->hpin[900]);
 }
 
+// Host-path result copy: x (final once the Krylov loop ends) goes to the caller's buffer on a side
+// stream while the main stream runs the true-residual check (krylov.hpp:188, a matvec and a norm,
+// which only read x).  The caller synchronises the side stream before returning.
+static void copy_out_async(fpc_context_s* c, double* host_x, const double* x, size_t n) {
+  if (!c->aux) {
+    ck(cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking), "cudaStreamCreate");
+    ck(cudaEventCreateWithFlags(&c->aux_ev, cudaEventDisableTiming), "cudaEventCreate");
+  }
+  ck(cudaEventRecord(c->aux_ev, c->stream), "event");
+  ck(cudaStreamWaitEvent(c->aux, c->aux_ev, 0), "wait");
+  ck(cudaMemcpyAsync(host_x, x, n * sizeof(double), cudaMemcpyDeviceToHost, c->aux), "D2H");
+}
+
 static void gmres_dev(fpc_plan_s* pl, const double* b, double* x, const fpc_solver_config& cfg,
-                      fpc_report* rep, std::vector<double>& hist) {
+                      fpc_report* rep, std::vector<double>& hist, double* host_x = nullptr) {
   fpc_problem_s* p = pl->prob;
   fpc_context_s* c = p->ctx;
   const size_t n = p->dim();
@@ -1430,6 +1450,7 @@ static void gmres_dev(fpc_plan_s* pl, const double* b, double* x, const fpc_solv
   }
   rep->reorthogonalizations = reorth;
   rep->final_relative_residual = hist.empty() ? 1.0 : last_rel;
+  if (host_x) copy_out_async(c, host_x, x, n);
   // fresh_relative_residual (krylov.hpp:64-75)
   GmresState S{pl, c, n, c->stream, {}, 0};
   dots_into(S, {}, 0, b, true, 0);
@@ -1471,9 +1492,14 @@ int fpc_gmres(fpc_plan_t pl, const double* b, double* x, const fpc_solver_config
     } else {
       ensure_staging(p);
       upload(p->d_in, b, n * sizeof(double), st);
-      gmres_dev(pl, p->d_in, p->d_out, cfg, rep, hist);
-      ck(cudaMemcpyAsync(x, p->d_out, n * sizeof(double), cudaMemcpyDeviceToHost, st), "D2H");
+      try {
+        gmres_dev(pl, p->d_in, p->d_out, cfg, rep, hist, x);
+      } catch (...) {
+        if (p->ctx->aux) cudaStreamSynchronize(p->ctx->aux);
+        throw;
+      }
       ck(cudaStreamSynchronize(st), "sync");
+      ck(cudaStreamSynchronize(p->ctx->aux), "sync");
     }
     rep->iterations_exact = rep->iterations;
     rep->history_len = int(hist.size());

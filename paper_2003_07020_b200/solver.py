@@ -425,6 +425,9 @@ def _krylov(fn, name, op, plan, b, cfg, out):
     else:
         bin_ = _host_in(b, n)
         x = np.empty(n) if out is None else out
+        if not (isinstance(x, np.ndarray) and x.dtype == np.float64 and x.size == n
+                and x.flags.c_contiguous and x.flags.writeable):
+            raise ValueError(f"{name}: out must be a writable contiguous float64 array of size {n}")
         N.check(fn(plan.h, C.c_void_p(bin_.ctypes.data), C.c_void_p(x.ctypes.data), C.byref(c),
                    C.byref(rep), C.c_void_p(hist.ctypes.data), cap, N.FPC_HOST))
     r = SolveReport(bool(rep.converged), float(rep.iterations_exact), list(hist[:min(rep.history_len, cap)]),

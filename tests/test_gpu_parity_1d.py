@@ -124,6 +124,33 @@ def test_device_tensors_roundtrip(oracle):
     assert rel(z.cpu().numpy(), fp.apply_inverse(plan, v)) == 0.0
 
 
+@pytest.mark.parametrize("pinned", [False, True])
+def test_gmres_host_buffers_match_device(pinned):
+    # host path: upload, solve, x copied back on a side stream while the true-residual check runs
+    torch = pytest.importorskip("torch")
+    w = problems.workload_1d(1.5, 1024, 64)
+    op = fp.AllAtOnceOperator(fp.TimeStencil(64), fp.RieszJacobian1D(1.5, 1.0, w.h, w.n), w.dt)
+    plan = fp.build_plan(fp.PreconditionerKind.generalized(), 64, w.dt, op)
+    b = problems.rhs(w)
+    cfg = fp.SolverConfig(tol=1e-10, max_iter=200, restart=20)
+    rd = fp.gmres_right(op, plan, torch.from_numpy(b).cuda(), cfg)
+    op.ctx.synchronize()
+    if pinned:
+        bh = torch.from_numpy(b).pin_memory().numpy()
+        xh = torch.empty(b.size, dtype=torch.float64).pin_memory().numpy()
+    else:
+        bh, xh = b.copy(), np.full(b.size, np.nan)
+    for _ in range(2):  # the second call reuses the side stream and the staging buffers
+        xh[:] = np.nan
+        rh = fp.gmres_right(op, plan, bh, cfg, out=xh)
+        assert rh.x is xh
+        assert np.array_equal(xh, rd.x.cpu().numpy())
+        assert rh.report.iterations == rd.report.iterations
+        assert rh.report.true_relative_residual == rd.report.true_relative_residual
+    with pytest.raises(ValueError):
+        fp.gmres_right(op, plan, bh, cfg, out=np.empty(b.size, dtype=np.float32))
+
+
 def test_unsupported_sizes_fail_loudly():
     with pytest.raises(NotImplementedError):
         fp.AllAtOnceOperator(fp.TimeStencil(6), fp.RieszJacobian1D(1.5, 1.0, 0.1, 9), 0.1)
