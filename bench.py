@@ -378,6 +378,7 @@ def main():
         torch.cuda.synchronize()
         barrier()
     launches = fp.kernel_launches() - launches0
+    x_sample = x[::1009].cpu().numpy()  # checked against the e2e (host-buffer) solve below
     t_step = ev0.elapsed_time(ev1) * 1e-3 / args.steps
     if world > 1:
         tt = torch.tensor([t_step], device=dev)
@@ -402,27 +403,6 @@ def main():
         alt = {other: {"ms_per_step": t_alt * 1e3, "value": 1.0 / t_alt, "iterations": int(r2.report.iterations),
                        "true_relative_residual": r2.report.true_relative_residual}}
         del plan2
-
-    # e2e: the public API with HOST buffers (pinned): the C-ABI's host path uploads b, solves, and
-    # copies x back (overlapped with the true-residual check); wall clock around synchronous calls
-    b_pin = torch.from_numpy(b_host).pin_memory()
-    x_pin = torch.empty_like(b_pin).pin_memory()
-    b_pin_np, x_pin_np = b_pin.numpy(), x_pin.numpy()
-    with torch.cuda.stream(stream):
-        def e2e_step():
-            return fp.gmres_right(op, plan, b_pin_np, cfg, out=x_pin_np)
-        e2e_step()
-        t0 = time.perf_counter()
-        for _ in range(args.steps):
-            r_e2e = e2e_step()
-        t_e2e = (time.perf_counter() - t0) / args.steps
-        fp.gmres_right(op, plan, b, cfg, out=x)  # host path == device path, bit for bit
-        stream.synchronize()
-        e2e_same_x = bool(np.array_equal(x_pin_np, x.cpu().numpy()))
-    if world > 1:
-        tt = torch.tensor([t_e2e], device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        t_e2e = float(tt.item())
 
     # live per-kernel device time inside one solve (events around every launch)
     with fp.KernelProfile() as prof:
@@ -476,6 +456,33 @@ def main():
         except Exception:
             traffic = None
 
+    # e2e: the public API with HOST buffers (pinned): the C-ABI's host path uploads b, solves, and
+    # copies x back (overlapped with the true-residual check); wall clock around synchronous calls
+    # (the device-resident b and x are released first: the host path stages through its own buffers,
+    # and config 3 has no room for both pairs next to the basis)
+    trr = res.report.true_relative_residual
+    res = r2 = None  # results hold the device x
+    del b, x, y
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+    b_pin = torch.from_numpy(b_host).pin_memory()
+    x_pin = torch.empty_like(b_pin).pin_memory()
+    b_pin_np, x_pin_np = b_pin.numpy(), x_pin.numpy()
+    with torch.cuda.stream(stream):
+        def e2e_step():
+            return fp.gmres_right(op, plan, b_pin_np, cfg, out=x_pin_np)
+        e2e_step()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            r_e2e = e2e_step()
+        t_e2e = (time.perf_counter() - t0) / args.steps
+        stream.synchronize()
+        e2e_same_x = bool(np.array_equal(x_pin_np[::1009], x_sample))  # host path == device path
+    if world > 1:
+        tt = torch.tensor([t_e2e], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_e2e = float(tt.item())
+
     # CPU baseline: the reference on this host, bounded sample (rank 0, N = 1 only)
     cpu = None
     if rank == 0 and world == 1 and w.dim > 2e8:
@@ -504,7 +511,7 @@ def main():
                        "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
                        "pc_ordering": args.ordering,
                        "l2": "inputs larger than L2 (134 MB per Krylov vector vs 126 MB L2)"},
-            "time_to_tol_s": t_step, "iterations": k, "true_relative_residual": res.report.true_relative_residual,
+            "time_to_tol_s": t_step, "iterations": k, "true_relative_residual": trr,
             "pc_applies_per_s": 1.0 / t_pc, "matvecs_per_s": 1.0 / t_mv,
             "pc_apply_gbs": B_pc / t_pc / 1e9, "matvec_gbs": B_mv / t_mv / 1e9,
             "e2e": {"value": world / t_e2e, "unit": UNIT, "h2d_bytes_per_step": 8 * N, "d2h_bytes_per_step": 8 * N,

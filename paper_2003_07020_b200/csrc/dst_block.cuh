@@ -31,6 +31,9 @@
 #ifndef FPC_DST_PRE_SEL
 #define FPC_DST_PRE_SEL 1
 #endif
+#ifndef FPC_DST_DUAL
+#define FPC_DST_DUAL 0  // measured slower (config-1 tau 3.18 -> 3.35 ms per solve), kept for A/B
+#endif
 #ifndef FPC_DCT_HALF_MAXLOG
 #define FPC_DCT_HALF_MAXLOG 9
 #endif
@@ -134,6 +137,11 @@ __device__ __forceinline__ void block_dst(double2* s, double2* h, const double2*
       dst_pre_folded<LOGN, BH>(s, h, tw2N, [&](int j) { return s[pad16(j)]; });
     __syncthreads();
     FPC_DST_PH(0);
+    if constexpr (FPC_DST_DUAL && E == 16) {
+      // the N-point FFT (after the folded radix-2 pass) and the M-point DCT FFT, both k radix-16
+      // passes, pipelined against each other (fft_block.cuh dual_fft_passes)
+      dual_fft_passes<LOGN, BS, 2, LOGN - 1, BH, 1, 1>(s, twb + N, h, twb + M, int(threadIdx.x), nthr, nthr / 2);
+    } else {
     fft_passes<LOGN, 1, BS, E, 2, CtaSync>(s, twb + N, int(threadIdx.x), nthr);
     FPC_DST_PH(1);
     if constexpr (FPC_DCT_HALF_GROUP && E == 16) {
@@ -145,6 +153,7 @@ __device__ __forceinline__ void block_dst(double2* s, double2* h, const double2*
       __syncthreads();
     } else {
       block_fft<LOGN - 1, 1, BH, E / 2>(h, twb + M, 0);
+    }
     }
     FPC_DST_PH(2);
   } else {

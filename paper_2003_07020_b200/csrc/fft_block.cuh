@@ -196,6 +196,41 @@ struct GroupSync {
 // One Stockham pass of radix R over B buffers of size N = 2^LOGN held in smem (buffer stride BS,
 // pad16 inside a buffer).  NS = current sub-transform length (compile time, so all index
 // arithmetic folds to shifts/masks).  Each thread processes E/R butterflies (E complex values).
+// The pass in two halves (operands read + butterflies into registers; autosorted writes), so a
+// caller can interleave the halves of independent transforms between its own barriers.
+template <int LOGN, int R, int S, int BS, int E, int NS>
+__device__ __forceinline__ void stockham_load(const double2* s, const double2* __restrict__ tw, int tid, int nthr,
+                                              double2 (&v)[E / R][R], int (&dst)[E / R]) {
+  constexpr int N = 1 << LOGN;
+  constexpr int NB = N / R;
+  constexpr int PER = E / R;
+#pragma unroll
+  for (int q = 0; q < PER; ++q) {
+    const int g = tid + q * nthr;
+    const int b = g / NB;
+    const int j = g & (NB - 1);
+    const double2* base = s + b * BS;
+#pragma unroll
+    for (int r = 0; r < R; ++r) v[q][r] = base[pad16(j + r * NB)];
+    const int jm = j & (NS - 1);
+    if constexpr (NS > 1) apply_twiddles<R, S>(v[q], tw - N + NS * R, tw - N + (NS * R) / 4, jm);
+    Dft<R, S>::run(v[q]);
+    dst[q] = b * BS + (j - jm) * R + jm;
+  }
+}
+
+template <int R, int BS, int E, int NS>
+__device__ __forceinline__ void stockham_store(double2* s, const double2 (&v)[E / R][R], const int (&dst)[E / R]) {
+#pragma unroll
+  for (int q = 0; q < E / R; ++q) {
+    const int b = dst[q] / BS;
+    const int off = dst[q] - b * BS;
+    double2* base = s + b * BS;
+#pragma unroll
+    for (int r = 0; r < R; ++r) base[pad16(off + r * NS)] = v[q][r];
+  }
+}
+
 template <int LOGN, int R, int S, int BS, int E, int NS, class Sync>
 __device__ __forceinline__ void stockham_pass(double2* s, const double2* __restrict__ tw, int tid, int nthr) {
   constexpr int N = 1 << LOGN;
@@ -320,6 +355,35 @@ __device__ __forceinline__ void block_fft_columns_from(double2* s, const double2
   }
   __syncthreads();
   fft_passes<LOGN, S, BS, E, R, CtaSync>(s, tw, tid, nthr);
+}
+
+// Two independent single-buffer transforms in radix-16 passes, software pipelined between CTA
+// barriers: the N = 2^LOGA point transform of `a` on all nthr threads (passes from NSA) and the
+// 2^LOGB point transform of `b` on threads tid < nb (passes from NSB), the same number of passes
+// each.  Interval order: load a_p | store a_p, load b_p | store b_p, load a_{p+1} | ... | store
+// b_last: every in-place pass still reads all its operands before any write (a barrier between),
+// a thread holds one pass's 16 values at a time, and 2k+1 barriers replace the 4k of the two
+// transforms run one after the other (the second on half the CTA, the other half idle).
+// Requires nthr * 16 == 2^LOGA and nb * 16 == 2^LOGB.  Ends with a barrier.
+template <int LOGA, int BSA, int NSA, int LOGB, int BSB, int NSB, int S>
+__device__ __forceinline__ void dual_fft_passes(double2* a, const double2* __restrict__ twa, double2* b,
+                                                const double2* __restrict__ twb, int tid, int nthr, int nb) {
+  if constexpr (NSA < (1 << LOGA)) {
+    static_assert(NSB < (1 << LOGB) && NSA * 16 <= (1 << LOGA) && NSB * 16 <= (1 << LOGB), "pass counts differ");
+    double2 va[1][16];
+    int da[1];
+    stockham_load<LOGA, 16, S, BSA, 16, NSA>(a, twa, tid, nthr, va, da);
+    __syncthreads();
+    stockham_store<16, BSA, 16, NSA>(a, va, da);
+    double2 vb[1][16];
+    int db[1];
+    if (tid < nb) stockham_load<LOGB, 16, S, BSB, 16, NSB>(b, twb, tid, nb, vb, db);
+    __syncthreads();
+    if (tid < nb) stockham_store<16, BSB, 16, NSB>(b, vb, db);
+    dual_fft_passes<LOGA, BSA, NSA * 16, LOGB, BSB, NSB * 16, S>(a, twa, b, twb, tid, nthr, nb);
+  } else {
+    __syncthreads();
+  }
 }
 
 // The same over a thread group of NTHR threads (local index tid) synchronised by named barrier ID;
