@@ -456,6 +456,14 @@ def main():
         except Exception:
             traffic = None
 
+    onchip = None  # the on-chip pipe that bounds an FFT kernel (ncu, per launch), beside the HBM roofline
+    ofile = os.path.join(ROOT, "profiles", "onchip.json")
+    if os.path.exists(ofile):
+        try:
+            onchip = json.load(open(ofile)).get(dom_name)
+        except Exception:
+            onchip = None
+
     # e2e: the public API with HOST buffers (pinned): the C-ABI's host path uploads b, solves, and
     # copies x back (overlapped with the true-residual check); wall clock around synchronous calls
     # (the device-resident b and x are released first: the host path stages through its own buffers,
@@ -521,7 +529,7 @@ def main():
             "roofline": {"bound": "hbm", "kernel": dom_name, "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": (achieved / peak) if achieved else None, "traffic": traffic,
                          "algorithmic_bytes_per_launch": dom_bytes, "avg_launch_us": dom_t * 1e6,
-                         "peak_source": peak_kind},
+                         "peak_source": peak_kind, "onchip": onchip},
             "solve_roofline": {"bound": "hbm", "algorithmic_bytes": B_tot, "achieved": B_tot / t_step / 1e9,
                                "peak": peak, "unit": "GB/s", "frac": B_tot / t_step / 1e9 / peak,
                                "formula": "SURVEY 8(d) B_tot, one Gram-Schmidt pass per step (the reference "

@@ -20,6 +20,7 @@ out = [f"# ncu summary `{tag}` (B200, `--set full --clock-control none`, config 
        "| kernel | time (us) | DRAM read (MB) | DRAM write (MB) | DRAM % peak | fp64 pipe % | L1/smem % | warps active % | regs | top stalls |",
        "|---|---|---|---|---|---|---|---|---|---|"]
 traffic = {}
+onchip = {}  # per category: the on-chip pipes that bound the FFT kernels (bench.py roofline.onchip)
 for r in rows[2:]:
     name = col(r, "Kernel Name")
     st = []
@@ -44,6 +45,11 @@ for r in rows[2:]:
     for pat, cat in cats:
         if pat in name:
             traffic.setdefault(cat, (rd + wr) * scale)
+            onchip.setdefault(cat, {
+                "l1_smem_pct": float(col(r, 'l1tex__throughput.avg.pct_of_peak_sustained_active') or 0),
+                "fp64_pipe_pct": float(col(r, 'sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active') or 0),
+                "dram_pct": float(col(r, 'gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed') or 0),
+                "source": f"ncu --set full, profiles/{tag}_summary.md"})
             break
 # launch list: share of device time per kernel family over the captured launches
 share = defaultdict(float)
@@ -62,4 +68,5 @@ for k, v in sorted(share.items(), key=lambda kv: -kv[1]):
 os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
 open(os.path.join(ROOT, "profiles", f"{tag}_summary.md"), "w").write("\n".join(out) + "\n")
 json.dump(traffic, open(os.path.join(ROOT, "profiles", "traffic.json"), "w"), indent=1)
+json.dump(onchip, open(os.path.join(ROOT, "profiles", "onchip.json"), "w"), indent=1)
 print("\n".join(out))
