@@ -266,17 +266,17 @@ __device__ __forceinline__ void stockham_pass(double2* s, const double2* __restr
   Sync::sync();
 }
 
-template <int LOGN, int S, int BS, int E, int NS, class Sync>
+// Passes from sub-transform length NS up to (not including) NEND (default: the whole transform).
+template <int LOGN, int S, int BS, int E, int NS, class Sync, int NEND = (1 << LOGN)>
 __device__ __forceinline__ void fft_passes(double2* s, const double2* __restrict__ tw, int tid, int nthr) {
-  constexpr int N = 1 << LOGN;
-  if constexpr (NS < N) {
+  if constexpr (NS < NEND) {
     constexpr int LE = E == 16 ? 4 : E == 8 ? 3 : E == 4 ? 2 : 1;
     // the remainder radix goes first (NS = 1 needs no twiddles), full radix-E passes after it,
     // so the twiddle sets the later passes touch stay small and L1 resident
     constexpr int rem = (NS == 1) ? (LOGN % LE) : 0;
     constexpr int R = rem == 3 ? 8 : rem == 2 ? 4 : rem == 1 ? 2 : E;
     stockham_pass<LOGN, R, S, BS, E, NS, Sync>(s, tw, tid, nthr);
-    fft_passes<LOGN, S, BS, E, NS * R, Sync>(s, tw, tid, nthr);
+    fft_passes<LOGN, S, BS, E, NS * R, Sync, NEND>(s, tw, tid, nthr);
   }
 }
 
@@ -293,7 +293,7 @@ __device__ __forceinline__ void block_fft(double2* s, const double2* __restrict_
 // from global memory): the first Stockham pass (NS = 1, no twiddles) takes its operands from the
 // loader instead of shared memory, which saves the staging write, one read pass and a barrier.
 // Requires blockDim.x * E == N.  Ends with the result in s (natural order).
-template <int LOGN, int S, int BS, int E, class Load>
+template <int LOGN, int S, int BS, int E, class Load, int NEND = (1 << LOGN)>
 __device__ __forceinline__ void block_fft_from(double2* s, const double2* __restrict__ tw, Load load) {
   constexpr int N = 1 << LOGN;
   constexpr int LE = E == 16 ? 4 : E == 8 ? 3 : E == 4 ? 2 : 1;
@@ -316,7 +316,7 @@ __device__ __forceinline__ void block_fft_from(double2* s, const double2* __rest
     for (int r = 0; r < R; ++r) s[pad16(j * R + r)] = v[q][r];
   }
   __syncthreads();
-  fft_passes<LOGN, S, BS, E, R, CtaSync>(s, tw, tid, nthr);
+  fft_passes<LOGN, S, BS, E, R, CtaSync, NEND>(s, tw, tid, nthr);
 }
 
 // B real columns of length 2N packed into B complex N-point buffers (slot m = x[2m] + i x[2m+1]),

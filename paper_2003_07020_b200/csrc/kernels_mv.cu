@@ -40,6 +40,80 @@ extern "C" int fpc_debug_phases_mv(long long* out, int nblocks) {
 #endif
 
 
+// Fused middle of the split matvec for H = M/2 = 16^k (called after every forward pass but the
+// last): thread j finishes the forward FFT's last radix-16 pass in registers -- it then holds the
+// spectrum slots p_r = j + r H/16, r = 0..15 -- stores them, and reads the 16 mirror slots of its
+// pairs (rank 0: H - p, rank 1: H - 1 - p; all held by one other thread).  Each own slot's output of
+// the eigenvalue product is formed from (own, mirror) with the pair's canonical twiddle and
+// eigenvalues, exactly the arithmetic of the unfused product (the pair's primary slot gets
+// A + i D conj(w), the mirror slot conj(A) + i conj(D) w); the 16 outputs are exactly the operands
+// of the inverse FFT's first radix-16 pass (no twiddles at NS = 1), which runs in registers too.
+// Against the three separate phases: one shared-memory read and one write per element less, and one
+// barrier less.
+template <int LOGM>
+__device__ __forceinline__ void mv_fused_product(double2* smem, int q, const double* __restrict__ eig,
+                                                 const double2* __restrict__ twb) {
+  constexpr int M = 1 << LOGM, H = M / 2, L = 2 * M, NB = H / 16, BS = padded(H);
+  const int j = int(threadIdx.x);
+  double2 v[1][16];
+  int dst[1];
+  stockham_load<LOGM - 1, 16, -1, BS, 16, NB>(smem, twb + H, j, NB, v, dst);
+  __syncthreads();
+  stockham_store<16, BS, 16, NB>(smem, v, dst);  // slot j + r NB <- v[0][r]
+  __syncthreads();
+  const double2* twL = twb + L;
+  const double2* twLh = twb + L / 128;
+  const double2* eigq = reinterpret_cast<const double2*>(eig + eigq_offset(M)) + q * (H / 2);
+#ifndef FPC_MV_FG
+#define FPC_MV_FG 4
+#endif
+  constexpr int G = FPC_MV_FG;  // slots whose mirror / table loads are in flight together
+#pragma unroll
+  for (int r0 = 0; r0 < 16; r0 += G) {
+    double2 bm[G], wv[G], ee[G];
+#pragma unroll
+    for (int u = 0; u < G; ++u) {
+      const int s = j + (r0 + u) * NB;
+      const int ms = q == 0 ? ((H - s) & (H - 1)) : H - 1 - s;  // mirror slot (rank 0 slot 0: itself)
+      const bool prim = q == 0 ? s <= H / 2 : s < H / 2;
+      const int s1 = prim ? s : ms;                             // the pair's primary slot
+      const int t = q == 0 ? s1 - 1 : s1;                       // its task index
+      const int kap = 2 * s1 + q;
+      bm[u] = smem[pad16(ms)];
+      const bool ok = !(q == 0 && s == 0);
+      wv[u] = ok ? cmul(__ldg(twLh + (kap >> 7)), __ldg(twL + (kap & 127))) : make_double2(1.0, 0.0);
+      ee[u] = ok ? __ldg(eigq + t) : make_double2(0.0, 0.0);
+    }
+#pragma unroll
+    for (int u = 0; u < G; ++u) {
+      const int r = r0 + u;
+      const int s = j + r * NB;
+      if (q == 0 && s == 0) {  // bins 0 and M
+        const double2 z = v[0][r];
+        const double y0 = eig[0] * (2.0 * (z.x + z.y));
+        const double ym = eig[M] * (2.0 * (z.x - z.y));
+        v[0][r] = make_double2(y0 + ym, y0 - ym);
+        continue;
+      }
+      const bool prim = q == 0 ? s <= H / 2 : s < H / 2;
+      const double2 a = prim ? v[0][r] : bm[u], bq = prim ? bm[u] : v[0][r];
+      const double2 w = wv[u];
+      const double2 P = cadd(a, cconj(bq)), Q = csub(a, cconj(bq));
+      const double2 iwQ = mul_si<1>(cmul(w, Q));
+      const double2 Yk = cscale(csub(P, iwQ), ee[u].x);
+      const double2 Ym = cscale(cconj(cadd(P, iwQ)), ee[u].y);
+      const double2 A = cadd(Yk, cconj(Ym));
+      const double2 D = csub(Yk, cconj(Ym));
+      v[0][r] = prim ? cadd(A, mul_si<1>(cmul(D, cconj(w)))) : cadd(cconj(A), mul_si<1>(cmul(cconj(D), w)));
+    }
+  }
+  Dft<16, 1>::run(v[0]);  // inverse FFT, first pass (NS = 1: no twiddles)
+  __syncthreads();        // every mirror read is done before the pass outputs overwrite the buffer
+  dst[0] = 16 * j;
+  stockham_store<16, BS, 16, 1>(smem, v, dst);
+  __syncthreads();
+}
+
 // two CTAs per SM for M = 8192 (4096-point halves); one for M = 16384 (8192-point halves)
 template <int LOGM>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((1 << (LOGM - 1)) / 16, LOGM <= 13 ? 2 : 1)
@@ -67,6 +141,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((1 << (LOGM - 1)) / 
     const double2 zm = make_double2(i < ns ? vk[i] : 0.0, i + 1 < ns ? vk[i + 1] : 0.0);
     return q == 1 ? cmul(zm, twm(m)) : zm;
   };
+#ifndef FPC_MV_FUSE
+#define FPC_MV_FUSE 0  // measured slower (262 -> 269 us at config 1), kept for A/B
+#endif
+  // H = 16^k (M = 8192): the forward FFT's last pass, the eigenvalue product and the inverse FFT's
+  // first pass share one register set (see mv_fused_product); otherwise three separate phases
+  constexpr bool kFuse = FPC_MV_FUSE && (LOGM - 1) % 4 == 0;
+  if constexpr (kFuse) {
+    block_fft_from<LOGM - 1, -1, BS, 16, decltype(load_z), H / 16>(smem, twb + H, load_z);
+    FPC_PHM(2);
+    mv_fused_product<LOGM>(smem, q, eig, twb);
+    FPC_PHM(3);
+    fft_passes<LOGM - 1, 1, BS, 16, 16, CtaSync>(smem, twb + H, int(threadIdx.x), NT);
+  } else {
   block_fft_from<LOGM - 1, -1, BS, 16>(smem, twb + H, load_z);
   FPC_PHM(2);
 
@@ -119,6 +206,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((1 << (LOGM - 1)) / 
   __syncthreads();
   FPC_PHM(3);
   block_fft<LOGM - 1, 1, BS, 16>(smem, twb + H, 1);
+  }
   FPC_PHM(4);
   cluster.sync();
   FPC_PHM(5);
