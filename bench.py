@@ -154,7 +154,8 @@ def run_sharded(args, w, rank, world, local):
     op = fp.AllAtOnceOperator(fp.TimeStencil(w.n_time), jac, w.dt, ctx)
     plan = fp.build_plan(fp.PreconditionerKind.generalized(), w.n_time, w.dt, op,
                          ordering=fp.Ordering[args.ordering])
-    s = ShardedSolver(w.n_time, w.n_space, CudaShardKernels(op, plan), ordering=args.ordering)
+    s = ShardedSolver(w.n_time, w.n_space, CudaShardKernels(op, plan), ordering=args.ordering,
+                      transport=args.transport)
     b_host = problems.rhs(w)
     lo, hi = s.koff * w.n_space, (s.koff + s.nt_loc) * w.n_space
     b_loc_host = np.ascontiguousarray(b_host[lo:hi])
@@ -193,7 +194,9 @@ def run_sharded(args, w, rank, world, local):
             "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded uniform[-1,1] source)",
             "config": {"workload": w.name, "n_space": w.n, "n_time": w.n_time, "tol": w.tol, "restart": w.restart,
-                       "parallelism": f"frequency-sharded x{world} (NCCL all-to-all + all-reduce)",
+                       "parallelism": f"frequency-sharded x{world} ("
+                                      + ("NCCL all-to-all" if args.transport == "nccl" else "peer-store exchanges")
+                                      + " + all-reduce)",
                        "pc_ordering": args.ordering},
             "iterations": rep.iterations, "true_relative_residual": rep.true_relative_residual,
             "e2e": {"value": 1.0 / te, "unit": UNIT, "h2d_bytes_per_step": 8 * (hi - lo),
@@ -302,6 +305,9 @@ def main():
     ap.add_argument("--gamma", type=float, default=1.2)
     ap.add_argument("--ref-iters", type=int, default=2, help="reference sample: GMRES iterations per step")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--transport", default="nccl", choices=["nccl", "p2p"],
+                    help="N > 1 sharded solve: NCCL all_to_all exchanges, or peer-store kernels into "
+                         "CUDA-IPC-shared receive buffers (kernels_p2p.cu)")
     ap.add_argument("--ordering", default="reference", choices=["reference", "commuted"],
                     help="PC factor ordering: reference (time FFT, tau solves, inverse FFT) or commuted (SURVEY 8(f)1)")
     ap.add_argument("--replicas", action="store_true",

@@ -148,6 +148,25 @@ int fpc_shard_lincomb(fpc_context_t ctx, const double* const* V, const double* c
 int fpc_shard_dst_levels(fpc_plan_t plan, const double* v, double* out, int nt_local, double s_in);
 int fpc_shard_time_solve(fpc_plan_t plan, const double* u, double* z, int col0, int ns_local, int forward);
 
+/* Peer-store transport for the sharded PC apply's exchanges (replaces NCCL all_to_all_single + the
+ * pack/unpack copies around it; distributed.py ShardedSolver(transport="p2p")).  The receive
+ * buffers are plain device allocations shared by CUDA IPC:
+ *   fpc_ipc_get_handle: 64-byte cudaIpcMemHandle_t of a device allocation (fpc_device_alloc)
+ *   fpc_ipc_open: map a peer's handle (another process, same node) -> device pointer; fpc_ipc_close
+ *   fpc_shard_scatter_p2p: src [rows][cols] elements of es doubles (1 real, 2 complex); the split
+ *     dimension (columns if split_cols, else rows) is partitioned by off[0..nranks) (rank d owns
+ *     [off[d], off[d+1]), off[nranks] = the dimension); element (i, j) owned by d is stored to
+ *       split_cols: dst[d][(row_base + i) * stride[d] + col_base + (j - off[d])]
+ *       split rows: dst[d][(row_base + i - off[d]) * stride[d] + col_base + j]
+ *     (elements of es doubles), stream-ordered on the context stream, ending with a system-scope
+ *     fence; the caller orders consumers behind a cross-rank barrier on the same stream.  nranks <= 8. */
+int fpc_ipc_get_handle(const void* dptr, void* handle64);
+int fpc_ipc_open(fpc_context_t ctx, const void* handle64, void** dptr);
+int fpc_ipc_close(fpc_context_t ctx, void* dptr);
+int fpc_shard_scatter_p2p(fpc_context_t ctx, const double* src, int rows, int cols, int es, int split_cols,
+                          double* const* dst, const int* off, const int* stride, int nranks, int row_base,
+                          int col_base);
+
 /* instrumentation: number of kernels this library launched in this process */
 unsigned long long fpc_kernel_launches(void);
 /* live per-kernel device time: CUDA events on the launching stream around every launch while

@@ -27,7 +27,8 @@ EXPORTS = [
     "fpc_plan_set_ordering", "fpc_pc_apply", "fpc_pc_forward", "fpc_gmres", "fpc_bicgstab", "fpc_kernel_launches", "fpc_profile_start",
     "fpc_profile_stop", "fpc_profile_entry", "fpc_shard_matvec", "fpc_shard_time_fwd", "fpc_shard_tau",
     "fpc_shard_time_inv", "fpc_shard_dots", "fpc_shard_update", "fpc_shard_lincomb",
-    "fpc_shard_dst_levels", "fpc_shard_time_solve",
+    "fpc_shard_dst_levels", "fpc_shard_time_solve", "fpc_ipc_get_handle", "fpc_ipc_open", "fpc_ipc_close",
+    "fpc_shard_scatter_p2p",
 ]
 
 
@@ -65,6 +66,11 @@ def load():
     lib.fpc_synchronize.argtypes = [vp]
     lib.fpc_device_alloc.argtypes = [vp, C.c_size_t, C.POINTER(C.c_void_p)]
     lib.fpc_device_free.argtypes = [vp, vp]
+    lib.fpc_ipc_get_handle.argtypes = [vp, vp]
+    lib.fpc_ipc_open.argtypes = [vp, vp, C.POINTER(C.c_void_p)]
+    lib.fpc_ipc_close.argtypes = [vp, vp]
+    lib.fpc_shard_scatter_p2p.argtypes = [vp, vp, C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_void_p),
+                                          ip, ip, C.c_int, C.c_int, C.c_int]
     lib.fpc_problem_create_1d.argtypes = [vp, d, d, d, C.c_int, C.c_int, d, C.POINTER(C.c_void_p)]
     lib.fpc_problem_create_2d.argtypes = [vp, d, d, d, d, d, C.c_int, C.c_int, d, C.POINTER(C.c_void_p)]
     lib.fpc_problem_destroy.argtypes = [vp]

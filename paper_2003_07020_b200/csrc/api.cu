@@ -1754,6 +1754,62 @@ int fpc_shard_dots(fpc_context_t c, const double* const* V, const double* scales
   });
 }
 
+// ---------------------------------------------------------------------------- peer-store transport
+int fpc_ipc_get_handle(const void* dptr, void* handle64) {
+  if (!dptr || !handle64) return set_err(FPC_INVALID_ARGUMENT, "null argument");
+  return guarded([&] {
+    static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
+    cudaIpcMemHandle_t h;
+    ck(cudaIpcGetMemHandle(&h, const_cast<void*>(dptr)), "cudaIpcGetMemHandle");
+    std::memcpy(handle64, &h, sizeof h);
+  });
+}
+
+int fpc_ipc_open(fpc_context_t c, const void* handle64, void** dptr) {
+  if (!c || !handle64 || !dptr) return set_err(FPC_INVALID_ARGUMENT, "null argument");
+  return guarded([&] {
+    DeviceGuard g(c->device);
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle64, sizeof h);
+    ck(cudaIpcOpenMemHandle(dptr, h, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
+  });
+}
+
+int fpc_ipc_close(fpc_context_t c, void* dptr) {
+  if (!c || !dptr) return set_err(FPC_INVALID_ARGUMENT, "null argument");
+  return guarded([&] {
+    DeviceGuard g(c->device);
+    ck(cudaIpcCloseMemHandle(dptr), "cudaIpcCloseMemHandle");
+  });
+}
+
+int fpc_shard_scatter_p2p(fpc_context_t c, const double* src, int rows, int cols, int es, int split_cols,
+                          double* const* dst, const int* off, const int* stride, int nranks, int row_base,
+                          int col_base) {
+  if (!c || !dst || !off || !stride) return set_err(FPC_INVALID_ARGUMENT, "null argument");
+  return guarded([&] {
+    if (nranks < 1 || nranks > fpc::kP2PMaxRanks) throw InvalidArg{"fpc_shard_scatter_p2p: 1 <= nranks <= 8"};
+    if (es != 1 && es != 2) throw InvalidArg{"fpc_shard_scatter_p2p: es must be 1 or 2"};
+    if (rows < 0 || cols < 0 || row_base < 0 || col_base < 0) throw InvalidArg{"fpc_shard_scatter_p2p: negative size"};
+    if (size_t(rows) * size_t(cols) > 0) check_ptr(src, "fpc_shard_scatter_p2p");
+    fpc::P2PScatter a{};
+    for (int d = 0; d < nranks; ++d) {
+      check_ptr(dst[d], "fpc_shard_scatter_p2p");
+      if (es == 2) check_dev_aligned(dst[d], "fpc_shard_scatter_p2p");
+      if (d > 0 && off[d] < off[d - 1]) throw InvalidArg{"fpc_shard_scatter_p2p: offsets must be non-decreasing"};
+      if (stride[d] < 0) throw InvalidArg{"fpc_shard_scatter_p2p: negative stride"};
+      a.dst[d] = dst[d];
+      a.off[d] = off[d];
+      a.stride[d] = stride[d];
+    }
+    if (off[0] != 0) throw InvalidArg{"fpc_shard_scatter_p2p: off[0] must be 0"};
+    if (es == 2) check_dev_aligned(src, "fpc_shard_scatter_p2p");
+    DeviceGuard g(c->device);
+    LAUNCH("scatter_p2p", c->stream, fpc::launch_p2p_scatter(src, rows, cols, es, split_cols != 0, a, nranks,
+                                                               row_base, col_base, c->stream));
+  });
+}
+
 // w <- w - sum_i coef_i * V_i (coef on the host, scales already folded in); returns ||w||^2.
 int fpc_shard_update(fpc_context_t c, const double* const* V, const double* coef, int nv, double* w,
                      size_t n, double* norm2_host) {

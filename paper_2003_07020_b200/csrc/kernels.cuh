@@ -172,4 +172,14 @@ cudaError_t launch_bicg_x(double* x, const double* p, double* r, const double* t
                           const double* to, const double* rhat, double alpha, double omega,
                           size_t n, double* partial, cudaStream_t st);
 
+// kernels_p2p.cu: one exchange of the sharded PC apply as peer stores (destinations by kernel param)
+constexpr int kP2PMaxRanks = 8;
+struct P2PScatter {
+  double* dst[kP2PMaxRanks];  // receive buffer of each rank (peer-mapped, or local for the own rank)
+  int off[kP2PMaxRanks];      // partition of the split dimension: rank d owns [off[d], off[d+1])
+  int stride[kP2PMaxRanks];   // row stride (elements) of rank d's receive matrix
+};
+cudaError_t launch_p2p_scatter(const double* src, int rows, int cols, int es, bool split_cols, const P2PScatter& a,
+                               int nranks, int row_base, int col_base, cudaStream_t st);
+
 }  // namespace fpc

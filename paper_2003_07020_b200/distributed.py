@@ -129,13 +129,103 @@ class CudaShardKernels:
     def synchronize(self):
         self.ctx.synchronize()
 
+    # peer-store transport (kernels_p2p.cu)
+    def alloc_shared(self, n_doubles):
+        ptr = C.c_void_p()
+        N.check(self.lib.fpc_device_alloc(self.ctx.h, max(8 * int(n_doubles), 16), C.byref(ptr)))
+        return ptr.value
+
+    def free_shared(self, ptr):
+        self.lib.fpc_device_free(self.ctx.h, C.c_void_p(ptr))
+
+    def ipc_handle(self, ptr) -> bytes:
+        h = C.create_string_buffer(64)
+        N.check(self.lib.fpc_ipc_get_handle(C.c_void_p(ptr), h))
+        return h.raw
+
+    def ipc_open(self, handle: bytes):
+        ptr = C.c_void_p()
+        N.check(self.lib.fpc_ipc_open(self.ctx.h, C.create_string_buffer(handle, 64), C.byref(ptr)))
+        return ptr.value
+
+    def ipc_close(self, ptr):
+        self.lib.fpc_ipc_close(self.ctx.h, C.c_void_p(ptr))
+
+    def tensor_at(self, ptr, n_doubles):
+        """A float64 CUDA tensor over n doubles at a device pointer this object owns (zero copy)."""
+        class _Buf:
+            __cuda_array_interface__ = {"shape": (int(n_doubles),), "typestr": "<f8", "data": (int(ptr), False),
+                                        "version": 3, "strides": None}
+        return torch.as_tensor(_Buf(), device=self.device)
+
+    def scatter_p2p(self, src, rows, cols, es, split_cols, dst_ptrs, off, stride, row_base, col_base):
+        G = len(dst_ptrs)
+        d = (C.c_void_p * G)(*dst_ptrs)
+        o = (C.c_int * G)(*off)
+        st = (C.c_int * G)(*stride)
+        N.check(self.lib.fpc_shard_scatter_p2p(self.ctx.h, self._p(src), int(rows), int(cols), int(es),
+                                               int(split_cols), d, o, st, G, int(row_base), int(col_base)))
+
+
+class P2PTransport:
+    """Receive buffers of the sharded PC apply's exchanges, one per exchange, mapped into every rank
+    by CUDA IPC; an exchange is one peer-store kernel (fpc_shard_scatter_p2p: pack, NVLink transfer
+    and unpack in one pass) followed by a stream-ordered barrier (one-element all_reduce on the same
+    stream), replacing all_to_all_single and the copies around it.  Correct by construction for the
+    buffer reuse: each exchange owns its buffer, and a rank rewrites a peer's buffer only after that
+    peer has passed a later barrier, i.e. after its consumer kernel of the previous contents ran."""
+
+    def __init__(self, kernels, group, G: int, rank: int, sizes: dict):
+        self.k, self.group, self.G, self.rank = kernels, group, G, rank
+        self.local, self.ptrs, self._opened = {}, {}, []
+        for name, n in sizes.items():
+            ptr = kernels.alloc_shared(n)
+            self.local[name] = (ptr, int(n))
+            handles = [None] * G
+            if G > 1:
+                dist.all_gather_object(handles, kernels.ipc_handle(ptr), group=group)
+            ptrs = []
+            for d in range(G):
+                if d == rank:
+                    ptrs.append(ptr)
+                else:
+                    q = kernels.ipc_open(handles[d])
+                    self._opened.append(q)
+                    ptrs.append(q)
+            self.ptrs[name] = ptrs
+        self._flag = torch.zeros(1, dtype=torch.float64, device=kernels.device)
+
+    def exchange(self, name, src, rows, cols, es, split_cols, off, stride, row_base, col_base):
+        """Scatter src into every rank's `name` buffer; returns this rank's buffer (float64 view)
+        once every rank's stores into it are complete (stream order)."""
+        self.k.scatter_p2p(src, rows, cols, es, split_cols, self.ptrs[name], off, stride, row_base, col_base)
+        if self.G > 1:
+            dist.all_reduce(self._flag, group=self.group)
+        ptr, n = self.local[name]
+        return self.k.tensor_at(ptr, n)
+
+    def close(self):
+        self.k.synchronize()
+        for q in self._opened:
+            self.k.ipc_close(q)
+        self._opened = []
+        for ptr, _ in self.local.values():
+            self.k.free_shared(ptr)
+        self.local = {}
+
 
 class ShardedSolver:
     """Right-preconditioned GMRES (krylov.hpp:83-192, + GMRES(m) restarts) over G ranks."""
 
-    def __init__(self, n_time: int, n_space: int, kernels, group=None, ordering: str = "reference"):
+    def __init__(self, n_time: int, n_space: int, kernels, group=None, ordering: str = "reference",
+                 transport: str = "nccl"):
         if ordering not in ("reference", "commuted"):
             raise ValueError("ShardedSolver: ordering must be 'reference' or 'commuted'")
+        if transport not in ("nccl", "p2p"):
+            raise ValueError("ShardedSolver: transport must be 'nccl' or 'p2p'")
+        if transport == "p2p" and not isinstance(kernels, CudaShardKernels):
+            raise ValueError("ShardedSolver: the p2p transport needs the CUDA shard kernels")
+        self.transport = transport
         self.ordering = ordering
         self.k = kernels
         self.group = group
@@ -151,6 +241,30 @@ class ShardedSolver:
         self.hs = split_counts(self.H, self.G)
         self.ho = offsets(self.hs)
         self.koff = self.rank * self.nt_loc
+        self.p2p = None
+        if transport == "p2p":
+            r = self.rank
+            self.p2p = P2PTransport(kernels, group, self.G, r, {
+                "cols": n_time * self.cs[r],              # time -> space columns [Nt][cs_r]
+                "rows": 2 * self.hs[r] * n_space,         # space -> frequency rows [hs_r][Ns] complex
+                "Z": 2 * self.H * self.cs[r],             # frequency -> space [H][cs_r] complex
+                "w": self.nt_loc * n_space})              # space -> time [nt_loc][Ns]
+
+    def close(self):
+        if self.p2p is not None:
+            self.p2p.close()
+            self.p2p = None
+
+    # peer-store versions of the exchanges (transport="p2p")
+    def _x_time_to_space(self, v_loc):
+        r = self.rank
+        return self.p2p.exchange("cols", v_loc, self.nt_loc, self.ns, 1, True, self.co, self.cs,
+                                 r * self.nt_loc, 0)
+
+    def _x_space_to_time(self, z):
+        r = self.rank
+        return self.p2p.exchange("w", z, self.nt, self.cs[r], 1, False, [d * self.nt_loc for d in range(self.G)],
+                                 [self.ns] * self.G, 0, self.co[r])
 
     # ------------------------------------------------------------------ collectives
     def _a2a(self, send_chunks, recv_sizes, like):
@@ -199,6 +313,15 @@ class ShardedSolver:
         if self.ordering == "commuted":
             return self._pc_apply_commuted(v_loc, s_in, forward)
         G, r, ns, nt_loc = self.G, self.rank, self.ns, self.nt_loc
+        if self.p2p is not None:
+            cols = self._x_time_to_space(v_loc)
+            Z = self.k.time_fwd(cols, self.cs[r], s_in)
+            rows = self.p2p.exchange("rows", torch.view_as_real(Z).reshape(-1), self.H, self.cs[r], 2, False,
+                                     self.ho, [ns] * G, 0, self.co[r])
+            self.k.tau(torch.view_as_complex(rows.view(-1, 2)), self.ho[r], self.hs[r], forward)
+            Zb = self.p2p.exchange("Z", rows, self.hs[r], ns, 2, True, self.co, self.cs, self.ho[r], 0)
+            z = self.k.time_inv(torch.view_as_complex(Zb.view(-1, 2)), self.cs[r])
+            return self._x_space_to_time(z).clone()  # the buffer is reused by the next apply
         V = v_loc.view(nt_loc, ns)
         # 1. time -> space columns
         parts = self._a2a([V[:, self.co[d]:self.co[d] + self.cs[d]] for d in range(G)],
@@ -225,6 +348,10 @@ class ShardedSolver:
 
     def _pc_apply_commuted(self, v_loc, s_in=1.0, forward=False):
         G, r, ns, nt_loc = self.G, self.rank, self.ns, self.nt_loc
+        if self.p2p is not None:
+            u = self.k.dst_levels(v_loc, nt_loc, s_in)
+            z = self.k.time_solve(self._x_time_to_space(u), self.co[r], self.cs[r], forward)
+            return self.k.dst_levels(self._x_space_to_time(z), nt_loc, 1.0)
         # 1. S on every local time level (no communication)
         u = self.k.dst_levels(v_loc, nt_loc, s_in).view(nt_loc, ns)
         # 2. time -> space columns

@@ -80,3 +80,14 @@ def test_sharded_solve_matches_oracle(tmp_path, oracle, case):
     xo, ro = po.gmres(v, 1e-10, 200, restart=restart)
     assert all(int(p["iters"]) == ro.iterations for p in parts)
     assert rel(cat("x"), xo) <= 1e-10
+
+
+def test_p2p_transport_needs_cuda_kernels():
+    # the peer-store transport maps CUDA receive buffers: the numpy kernels are refused up front
+    import pytest
+    from paper_2003_07020_b200.distributed import ShardedSolver
+    from dist_cpu_kernels import NumpyShardKernels
+    with pytest.raises(ValueError):
+        ShardedSolver(8, 7, NumpyShardKernels.__new__(NumpyShardKernels), transport="p2p")
+    with pytest.raises(ValueError):
+        ShardedSolver(8, 7, NumpyShardKernels.__new__(NumpyShardKernels), transport="mpi")
