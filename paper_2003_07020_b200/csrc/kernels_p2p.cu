@@ -34,39 +34,71 @@ struct Elem<2> {
   using T = double2;
 };
 
+// Tiles of one source row x kChunk columns, one tile per CTA iteration (one division per tile, none
+// per element); every thread issues its kPer loads before its stores.
+constexpr int kP2PThreads = 256, kP2PPer = 8, kP2PChunk = kP2PThreads * kP2PPer;
+
 template <int ES, bool SPLIT_COLS>
-__global__ void __launch_bounds__(256) k_p2p_scatter(const double* __restrict__ src, int rows, int cols,
-                                                     P2PScatter a, int nranks, int row_base, int col_base) {
+__global__ void __launch_bounds__(kP2PThreads) k_p2p_scatter(const double* __restrict__ src, int rows, int cols,
+                                                             P2PScatter a, int nranks, int row_base, int col_base) {
   using T = typename Elem<ES>::T;
   const T* s = reinterpret_cast<const T*>(src);
-  const size_t total = size_t(rows) * size_t(cols);
-  for (size_t e = size_t(blockIdx.x) * blockDim.x + threadIdx.x; e < total; e += size_t(gridDim.x) * blockDim.x) {
-    const int i = int(e / size_t(cols)), j = int(e - size_t(i) * size_t(cols));
-    const int key = SPLIT_COLS ? j : i;
-    int d = 0;
+  const int nchunk = (cols + kP2PChunk - 1) / kP2PChunk;
+  const long ntile = long(rows) * nchunk;
+  for (long tile = blockIdx.x; tile < ntile; tile += gridDim.x) {
+    const int i = int(tile / nchunk), j0 = int(tile - long(i) * nchunk) * kP2PChunk;
+    const T* srow = s + size_t(i) * size_t(cols);
+    T v[kP2PPer];
 #pragma unroll
-    for (int r = 1; r < kP2PMaxRanks; ++r)
-      if (r < nranks && key >= a.off[r]) d = r;
-    const size_t di = SPLIT_COLS ? size_t(row_base + i) * size_t(a.stride[d]) + size_t(col_base + j - a.off[d])
-                                 : size_t(row_base + i - a.off[d]) * size_t(a.stride[d]) + size_t(col_base + j);
-    reinterpret_cast<T*>(a.dst[d])[di] = s[e];
+    for (int u = 0; u < kP2PPer; ++u) {
+      const int j = j0 + int(threadIdx.x) + u * kP2PThreads;
+      if (j < cols) v[u] = srow[j];
+    }
+    if constexpr (SPLIT_COLS) {
+#pragma unroll
+      for (int u = 0; u < kP2PPer; ++u) {
+        const int j = j0 + int(threadIdx.x) + u * kP2PThreads;
+        if (j >= cols) continue;
+        int d = 0;
+#pragma unroll
+        for (int r = 1; r < kP2PMaxRanks; ++r)
+          if (r < nranks && j >= a.off[r]) d = r;
+        reinterpret_cast<T*>(a.dst[d])[size_t(row_base + i) * size_t(a.stride[d]) + size_t(col_base + j - a.off[d])] =
+            v[u];
+      }
+    } else {
+      int d = 0;
+#pragma unroll
+      for (int r = 1; r < kP2PMaxRanks; ++r)
+        if (r < nranks && i >= a.off[r]) d = r;
+      T* drow = reinterpret_cast<T*>(a.dst[d]) + size_t(row_base + i - a.off[d]) * size_t(a.stride[d]) + col_base;
+#pragma unroll
+      for (int u = 0; u < kP2PPer; ++u) {
+        const int j = j0 + int(threadIdx.x) + u * kP2PThreads;
+        if (j < cols) drow[j] = v[u];
+      }
+    }
   }
-  __threadfence_system();
+  // one system-scope fence per CTA, after the CTA barrier (cumulative over the CTA's stores), instead
+  // of one per thread
+  __syncthreads();
+  if (threadIdx.x == 0) __threadfence_system();
 }
 
 cudaError_t launch_p2p_scatter(const double* src, int rows, int cols, int es, bool split_cols, const P2PScatter& a,
                                int nranks, int row_base, int col_base, cudaStream_t st) {
   const size_t total = size_t(rows) * size_t(cols);
   if (total == 0) return cudaSuccess;
-  const int grid = int(std::min<size_t>((total + 255) / 256, size_t(148) * 8));
+  const size_t ntile = size_t(rows) * size_t((cols + kP2PChunk - 1) / kP2PChunk);
+  const int grid = int(std::min<size_t>(ntile, size_t(148) * 8));
   if (es == 1 && split_cols)
-    k_p2p_scatter<1, true><<<grid, 256, 0, st>>>(src, rows, cols, a, nranks, row_base, col_base);
+    k_p2p_scatter<1, true><<<grid, kP2PThreads, 0, st>>>(src, rows, cols, a, nranks, row_base, col_base);
   else if (es == 1)
-    k_p2p_scatter<1, false><<<grid, 256, 0, st>>>(src, rows, cols, a, nranks, row_base, col_base);
+    k_p2p_scatter<1, false><<<grid, kP2PThreads, 0, st>>>(src, rows, cols, a, nranks, row_base, col_base);
   else if (split_cols)
-    k_p2p_scatter<2, true><<<grid, 256, 0, st>>>(src, rows, cols, a, nranks, row_base, col_base);
+    k_p2p_scatter<2, true><<<grid, kP2PThreads, 0, st>>>(src, rows, cols, a, nranks, row_base, col_base);
   else
-    k_p2p_scatter<2, false><<<grid, 256, 0, st>>>(src, rows, cols, a, nranks, row_base, col_base);
+    k_p2p_scatter<2, false><<<grid, kP2PThreads, 0, st>>>(src, rows, cols, a, nranks, row_base, col_base);
   return cudaGetLastError();
 }
 
