@@ -1514,7 +1514,7 @@ int fpc_gmres(fpc_plan_t pl, const double* b, double* x, const fpc_solver_config
 // three sync points per iteration (the half-step test, omega, the full-step test); alpha is formed
 // on the device from rho and the denominator so the s update needs no extra round trip.
 static void bicgstab_dev(fpc_plan_s* pl, const double* b, double* x, const fpc_solver_config& cfg,
-                         fpc_report* rep, std::vector<double>& hist) {
+                         fpc_report* rep, std::vector<double>& hist, double* host_x = nullptr, bool* copied = nullptr) {
   fpc_problem_s* p = pl->prob;
   fpc_context_s* c = p->ctx;
   const size_t n = p->dim();
@@ -1605,6 +1605,10 @@ static void bicgstab_dev(fpc_plan_s* pl, const double* b, double* x, const fpc_s
     rho = c->hpin[kN + 1];
     ck(cudaMemcpyAsync(c->dscal + kR, c->dscal + kN + 1, sizeof(double), cudaMemcpyDeviceToDevice, st), "rho");
   }
+  if (host_x) {  // x is final: copy it back under the true-residual check (as gmres_dev)
+    copy_out_async(c, host_x, x, pl->prob->dim());
+    *copied = true;
+  }
   rep->true_relative_residual = resid_norm_dev(pl, b, x) / norm_b;
 }
 
@@ -1632,9 +1636,16 @@ int fpc_bicgstab(fpc_plan_t pl, const double* b, double* x, const fpc_solver_con
     } else {
       ensure_staging(p);
       upload(p->d_in, b, n * sizeof(double), st);
-      bicgstab_dev(pl, p->d_in, p->d_out, cfg, rep, hist);
-      ck(cudaMemcpyAsync(x, p->d_out, n * sizeof(double), cudaMemcpyDeviceToHost, st), "D2H");
+      bool copied = false;
+      try {
+        bicgstab_dev(pl, p->d_in, p->d_out, cfg, rep, hist, x, &copied);
+      } catch (...) {
+        if (p->ctx->aux) cudaStreamSynchronize(p->ctx->aux);
+        throw;
+      }
+      if (!copied) ck(cudaMemcpyAsync(x, p->d_out, n * sizeof(double), cudaMemcpyDeviceToHost, st), "D2H");
       ck(cudaStreamSynchronize(st), "sync");
+      if (copied) ck(cudaStreamSynchronize(p->ctx->aux), "sync");
     }
     rep->iterations = int(rep->iterations_exact);
     rep->history_len = int(hist.size());
