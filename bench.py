@@ -1,17 +1,21 @@
-"""bench.py -- BC-preconditioned GMRES time-to-tol on B200 (BASELINE.json metric, configs[1]).
+"""bench.py -- BC-preconditioned GMRES time-to-tol on B200 (BASELINE.json metric).
 
-A "step" = one full right-preconditioned GMRES(20) solve to tol 1e-10 of the all-at-once BDF2
-system of config 1 (1D Riesz FDE, gamma=1.2, Nx=8191, Nt=2048, fp64, seeded uniform source),
-with b resident in HBM: the reference's timed span krylov.hpp:87-190 (k+1 PC applies, k+1
-matvecs, the Gram-Schmidt work, x = P^{-1} V y and the fresh TRR).
+Headline (N=1): BASELINE configs[2], the largest configuration that fits one GPU's role in the
+BASELINE list (config 3 is specified as the 8-GPU case): 2D Riesz FDE, gamma 1.3/1.7,
+255^2 x 512 = 33.3 M DoF, GMRES(20) right-preconditioned with the BC preconditioner, tol 1e-10,
+fp64, seeded uniform source.  A "step" = one full solve with b resident in HBM: the reference's
+timed span krylov.hpp:87-190 (k+1 PC applies, k+1 matvecs, the Gram-Schmidt work, x = P^{-1} V y
+and the fresh TRR).  Configs 1 (1D 8191 x 2048, gamma 1.2) and 3 (2D 1023^2 x 1024, GMRES(10),
+tol 1e-9) are measured after it in the same run and reported under "secondary".
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--gamma 1.2]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config 2]
   python bench.py --sweep [--sweep-nx 1023,65535] [--sweep-nt 256,8192]   (config 4, one line per point)
 
-N > 1 (torchrun): ONE solve frequency-sharded over the N ranks (paper_2003_07020_b200/distributed.py:
-NCCL all-to-all around the tau solves, all-reduce for the dots; scaling "strong"); --replicas
-instead runs N independent solves (scaling "weak").  --impl reference times the reference's own
-CPU solver (oracle/_ref, the unmodified reference headers) on this host's cores.
+N > 1 (torchrun): ONE solve sharded over the N ranks (paper_2003_07020_b200/distributed.py:
+time-sharded Krylov vectors, NCCL all-to-all around the tau solves, all-reduce for the dots;
+scaling "strong"); --replicas instead runs N independent solves (scaling "weak").
+--impl reference times the reference's own CPU solver (oracle/_ref: the unmodified reference
+headers compiled by oracle/Makefile) on this host's cores: one full, unextrapolated solve per step.
 """
 from __future__ import annotations
 
@@ -97,44 +101,95 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------------------------ reference arm
-def cpu_reference_sample(w, threads: int, sample_iters: int):
-    """Time the unmodified reference (oracle/_ref) gmres_right on this workload, bounded to
-    `sample_iters` iterations; returns (seconds, sample_iters_done, true iteration count k)."""
+def ref_problem(w):
+    """The unmodified reference (oracle/_ref) on workload w, plan built (driver.hpp:49-73)."""
     from oracle import oracle as O
     ref = O.Reference()
-    ref.set_threads(threads)
     if w.two_dim:
         p = ref.problem_2d(w.gamma[0], w.gamma[1], 1.0, 1.0, w.h, w.n, w.n_time, w.dt).build_plan()
     else:
         p = ref.problem_1d(w.gamma[0], 1.0, w.h, w.n, w.n_time, w.dt).build_plan()
+    return ref, p
+
+
+def cpu_reference_solve(w, threads: int):
+    """ONE full reference solve (gmres_right as driver.hpp:62-73 wires it; GMRES(m) through the
+    restart emulation of SURVEY §8(c) when the solve needs more than m steps).  Returns
+    (seconds of the reference's own timed span krylov.hpp:87-190, iterations)."""
     from paper_2003_07020_b200 import problems
+    ref, p = ref_problem(w)
+    ref.set_threads(threads)
     b = problems.rhs(w)
-    _, rep = p.gmres(b, w.tol, sample_iters)
+    _, rep = p.gmres(b, w.tol, 200)
+    if rep.iterations > w.restart > 0:  # GMRES(m) differs from the unrestarted solve: emulate it
+        _, r2 = p.gmres_restarted(b, w.tol, 200, w.restart)
+        return r2["seconds"], r2["iterations"]
     return rep.seconds, rep.iterations
 
 
-def run_reference(args, w, k_full: int):
+def cpu_reference_ops(w, threads: int):
+    """The reference's apply_inverse and AllAtOnceOperator::apply, one call each, wall-clock."""
+    from paper_2003_07020_b200 import problems
+    ref, p = ref_problem(w)
+    ref.set_threads(threads)
+    b = problems.rhs(w)
+    t0 = time.perf_counter()
+    p.pc_apply(b)
+    t1 = time.perf_counter()
+    p.matvec(b)
+    t2 = time.perf_counter()
+    return t1 - t0, t2 - t1
+
+
+def run_reference(args, w):
     rank, world, _ = dist_env()
     if rank != 0:
         return
     threads = os.cpu_count() or 1
-    times = []
-    for i in range(args.warmup_ref + args.steps_ref):
-        sec, done = cpu_reference_sample(w, threads, args.ref_iters)
-        if i >= args.warmup_ref:
-            times.append(sec * (k_full + 1) / (done + 1))
+    times, iters = [], None
+    for _ in range(args.steps_ref):
+        sec, iters = cpu_reference_solve(w, threads)
+        times.append(sec)
     t = statistics.mean(times)
     val = 1.0 / t
-    sample = (f"reference gmres_right (oracle/_ref, unmodified headers) on {w.name}, max_iter={args.ref_iters} of the "
-              f"{k_full}-iteration solve, time x ({k_full}+1)/({args.ref_iters}+1)")
+    # the single-thread figure (set_thread_count(1), parallel.hpp:24) beside nproc: one PC apply and
+    # one matvec of the same workload at each thread count (a 1-thread full solve is ~16x longer)
+    pc1, mv1 = cpu_reference_ops(w, 1)
+    pcn, mvn = cpu_reference_ops(w, threads)
+    sample = (f"reference gmres_right (oracle/_ref, unmodified headers) on {w.name}: {args.steps_ref} full solves of "
+              f"{iters} iterations, {threads} threads, the reference's own report.seconds (krylov.hpp:87-190)")
     line = {"impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": world,
-            "steps": args.steps_ref, "warmup": args.warmup_ref, "ms_per_step": t * 1e3, "higher_is_better": True,
+            "steps": args.steps_ref, "warmup": 0, "ms_per_step": t * 1e3, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded uniform source)",
-            "config": {"workload": w.name, "n_space": w.n, "n_time": w.n_time, "gamma": w.gamma[0], "tol": w.tol,
-                       "restart": w.restart},
-            "cpu_baseline": {"value": val, "unit": UNIT, "cores": threads, "kind": "reference", "sample": sample},
+            "config": workload_config(w),
+            "iterations": iters, "step_seconds": times,
+            "cpu_baseline": {"value": val, "unit": UNIT, "cores": threads, "kind": "reference", "sample": sample,
+                             "cpu_model": cpu_model()},
+            "single_thread": {"threads": 1, "pc_apply_s": pc1, "matvec_s": mv1,
+                              "nproc": {"threads": threads, "pc_apply_s": pcn, "matvec_s": mvn},
+                              "note": "one apply_inverse and one AllAtOnceOperator::apply of this workload at "
+                                      "set_thread_count(1) and at nproc"},
             "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line))
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
+def workload_config(w):
+    c = {"workload": w.name, "n_space": w.n_space, "n_time": w.n_time, "dof": w.dim,
+         "gamma": list(w.gamma), "kappa": list(w.kappa), "tol": w.tol, "restart": w.restart,
+         "solver": f"GMRES({w.restart}) right-preconditioned, BC alpha=min(0.5, dt/2)", "seed": w.seed}
+    if w.two_dim:
+        c["n_per_dim"] = w.n
+    return c
 
 
 # ------------------------------------------------------------------------------------ sharded
@@ -295,15 +350,191 @@ def run_sweep(args):
 
 
 # ------------------------------------------------------------------------------------ our arm
+def load_onchip_peaks():
+    """fp64 / shared-memory roofs measured on the B200 by scripts/onchip_peaks.cu (profiles/)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "onchip_peaks.json")) as f:
+            return json.load(f)
+    except Exception:  # noqa: BLE001
+        return {}
+
+
+def fft_flops(w):
+    """SURVEY §8(d) algorithmic FLOPs of one matvec (the reference's algorithm: two complex FFTs
+    of the circulant length L per Toeplitz product) -- 1D: Nt (5 L log2 L + L) + 6N; 2D: 2n
+    Toeplitz products per time level."""
+    import math
+    N = w.dim
+    L = 1 << math.ceil(math.log2(2 * w.n))
+    per = 5.0 * L * math.log2(L) + L
+    return w.n_time * (2 * w.n if w.two_dim else 1) * per + (8.0 if w.two_dim else 6.0) * N
+
+
+def solve_bytes(w, k):
+    """SURVEY §8(d) compulsory bytes of a k-iteration solve: (k+1)(B_mv + B_pc) + sum_j 8N(2j+5)
+    (one Gram-Schmidt pass per step, j counted within a restart cycle) + 8N(k+1) + 16N + per
+    restart (B_mv + 24N)."""
+    N = w.dim
+    H = w.n_time // 2 + 1
+    B_mv, B_pc = 16.0 * N, 16.0 * N + 64.0 * H * w.n_space
+    rcyc = w.restart if w.restart else k + 1
+    n_restarts = max(0, (k - 1) // rcyc) if k > 0 else 0
+    return ((k + 1) * (B_mv + B_pc) + sum(8.0 * N * (2 * (j % rcyc) + 5) for j in range(k))
+            + 8.0 * N * (k + 1) + 16.0 * N + n_restarts * (B_mv + 24.0 * N)), B_mv, B_pc
+
+
+def build_ours(fp, w, ctx, ordering="reference"):
+    if w.two_dim:
+        jac = fp.RieszJacobian2D(w.gamma[0], w.gamma[1], 1.0, 1.0, w.h, w.n)
+    else:
+        jac = fp.RieszJacobian1D(w.gamma[0], 1.0, w.h, w.n)
+    op = fp.AllAtOnceOperator(fp.TimeStencil(w.n_time), jac, w.dt, ctx)
+    plan = fp.build_plan(fp.PreconditionerKind.generalized(), w.n_time, w.dt, op, ordering=fp.Ordering[ordering])
+    return op, plan
+
+
+def measure(fp, torch, w, args, stream, ctx, dev, steps, warmup, full, sync=None):
+    """Device-resident time-to-tol of w (K solves between events on the library stream), plus,
+    when `full`: live per-kernel times, operator rates, the roofline of the dominant kernel and the
+    e2e solve through the C-ABI with pinned host buffers."""
+    from paper_2003_07020_b200 import problems
+    op, plan = build_ours(fp, w, ctx, args.ordering)
+    cfg = fp.SolverConfig(tol=w.tol, max_iter=200, restart=w.restart)
+    b_host = problems.rhs(w)
+    N = w.dim
+    with torch.cuda.stream(stream):
+        b = torch.from_numpy(b_host).to(dev)
+        x = torch.empty_like(b)
+    stream.synchronize()
+    for _ in range(warmup):
+        res = fp.gmres_right(op, plan, b, cfg, out=x)
+    torch.cuda.synchronize()
+    k = int(res.report.iterations)
+    launches0 = fp.kernel_launches()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(dev.index) as clk:
+        if sync:
+            sync()
+        torch.cuda.synchronize()
+        ev0.record(stream)
+        for _ in range(steps):
+            res = fp.gmres_right(op, plan, b, cfg, out=x)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        if sync:
+            sync()
+    launches = fp.kernel_launches() - launches0
+    t_step = ev0.elapsed_time(ev1) * 1e-3 / steps
+    out = {"ms_per_step": t_step * 1e3, "value": 1.0 / t_step, "iterations": k, "restarts": int(res.report.restarts),
+           "true_relative_residual": res.report.true_relative_residual, "gpu_launches": launches,
+           "clocks": clk.summary()}
+    B_tot, B_mv, B_pc = solve_bytes(w, k)
+    peak, peak_kind = load_peaks()
+    out["solve_roofline"] = {"bound": "hbm", "algorithmic_bytes": B_tot, "achieved": B_tot / t_step / 1e9,
+                             "peak": peak, "unit": "GB/s", "frac": B_tot / t_step / 1e9 / peak,
+                             "formula": "SURVEY 8(d) B_tot, one Gram-Schmidt pass per step (the reference "
+                                        "re-orthogonalises every step here, which doubles that term)"}
+    if not full:
+        del b, x, res, op, plan
+        torch.cuda.synchronize()
+        torch.cuda.empty_cache()
+        return out
+    x_sample = x[::1009].cpu().numpy()  # checked against the e2e (host-buffer) solve below
+
+    with fp.KernelProfile() as prof:  # live per-kernel device time inside one solve
+        fp.gmres_right(op, plan, b, cfg, out=x)
+    table = prof.table
+
+    def rate(fn, reps=20):
+        for _ in range(3):
+            fn()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(reps):
+            fn()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) * 1e-3 / reps
+
+    y = x  # the solution buffer is free again
+    t_mv = rate(lambda: op.apply(b, y))
+    t_pc = rate(lambda: fp.apply_inverse(plan, b, y))
+    H = w.n_time // 2 + 1
+    out.update({"pc_applies_per_s": 1.0 / t_pc, "matvecs_per_s": 1.0 / t_mv,
+                "pc_apply_gbs": B_pc / t_pc / 1e9, "matvec_gbs": B_mv / t_mv / 1e9})
+
+    # dominant kernel by live device time inside the solve; algorithmic bytes per launch (SURVEY §8(d))
+    dom_name, (dom_ms, dom_cnt) = max(table.items(), key=lambda kv: kv[1][0])
+    per_launch_bytes = {"matvec_1d": B_mv, "matvec_2d": B_mv, "time_fwd": 8.0 * N + 16.0 * H * w.n_space,
+                        "time_inv": 8.0 * N + 16.0 * H * w.n_space, "tau_solve_1d": 32.0 * H * w.n_space,
+                        "tau_solve_2d": 32.0 * H * w.n_space}
+    dom_bytes = per_launch_bytes.get(dom_name)
+    dom_t = dom_ms * 1e-3 / dom_cnt
+    achieved = dom_bytes / dom_t / 1e9 if dom_bytes else None
+    traffic = onchip = None
+    for fname, key in (("traffic.json", "traffic"), ("onchip.json", "onchip")):
+        fpath = os.path.join(ROOT, "profiles", fname)
+        if os.path.exists(fpath):
+            try:
+                val = json.load(open(fpath)).get(w.name, {}).get(dom_name)
+            except Exception:  # noqa: BLE001
+                val = None
+            if key == "traffic":
+                traffic = val
+            else:
+                onchip = val
+    roof = {"bound": "hbm", "kernel": dom_name, "achieved": achieved, "peak": peak, "unit": "GB/s",
+            "frac": (achieved / peak) if achieved else None, "traffic": traffic,
+            "algorithmic_bytes_per_launch": dom_bytes, "avg_launch_us": dom_t * 1e6, "peak_source": peak_kind,
+            "onchip": onchip}
+    ocp = load_onchip_peaks()
+    if dom_name.startswith("matvec") and ocp.get("fp64_fma_tflops"):
+        f = fft_flops(w)
+        roof["fp64"] = {"flops_per_launch": f, "achieved_tflops": f / dom_t / 1e12,
+                        "peak_tflops": ocp["fp64_fma_tflops"], "frac": f / dom_t / 1e12 / ocp["fp64_fma_tflops"],
+                        "formula": "SURVEY 8(d) F_mv (reference algorithm: two complex FFTs of length L per "
+                                   "Toeplitz product)", "peak_source": "profiles/onchip_peaks.json (measured)"}
+    out["roofline"] = roof
+    out["kernel_time_ms_per_solve"] = {k_: v[0] for k_, v in table.items()}
+    out["kernel_launches_per_solve"] = {k_: v[1] for k_, v in table.items()}
+
+    # e2e: the public API with HOST buffers (pinned): the C-ABI's host path uploads b, solves, and
+    # copies x back (overlapped with the true-residual check); wall clock around synchronous calls
+    res = None
+    del b, x, y
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+    b_pin = torch.from_numpy(b_host).pin_memory()
+    x_pin = torch.empty_like(b_pin).pin_memory()
+    b_pin_np, x_pin_np = b_pin.numpy(), x_pin.numpy()
+    with torch.cuda.stream(stream):
+        fp.gmres_right(op, plan, b_pin_np, cfg, out=x_pin_np)
+        if sync:
+            sync()
+        t0 = time.perf_counter()
+        for _ in range(steps):
+            r_e2e = fp.gmres_right(op, plan, b_pin_np, cfg, out=x_pin_np)
+        t_e2e = (time.perf_counter() - t0) / steps
+        stream.synchronize()
+    out["e2e"] = {"value": 1.0 / t_e2e, "unit": UNIT, "h2d_bytes_per_step": 8 * N, "d2h_bytes_per_step": 8 * N,
+                  "iterations": int(r_e2e.report.iterations),
+                  "x_matches_device": bool(np.array_equal(x_pin_np[::1009], x_sample))}
+    del op, plan, b_pin, x_pin
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", type=int, default=1)
-    ap.add_argument("--gamma", type=float, default=1.2)
-    ap.add_argument("--ref-iters", type=int, default=2, help="reference sample: GMRES iterations per step")
+    ap.add_argument("--config", type=int, default=2, help="headline BASELINE config (default 2)")
+    ap.add_argument("--gamma", type=float, default=1.2, help="config 1 only")
+    ap.add_argument("--secondary", default="1,3", help="BASELINE configs measured after the headline ('' = none)")
+    ap.add_argument("--ref-steps", type=int, default=3, help="reference arm: full solves timed (<= --steps)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--transport", default="nccl", choices=["nccl", "p2p"],
                     help="N > 1 sharded solve: NCCL all_to_all exchanges, or peer-store kernels into "
@@ -311,7 +542,7 @@ def main():
     ap.add_argument("--ordering", default="reference", choices=["reference", "commuted"],
                     help="PC factor ordering: reference (time FFT, tau solves, inverse FFT) or commuted (SURVEY 8(f)1)")
     ap.add_argument("--replicas", action="store_true",
-                    help="N > 1: independent replicas instead of the frequency-sharded solve")
+                    help="N > 1: independent replicas instead of the sharded solve")
     ap.add_argument("--sweep", action="store_true", help="BASELINE config 4: PC apply + matvec sweep (JSON per point)")
     ap.add_argument("--sweep-nx", default="", help="comma list (default 1023..65535)")
     ap.add_argument("--sweep-nt", default="", help="comma list (default 256..8192)")
@@ -321,15 +552,13 @@ def main():
     if args.sweep:
         run_sweep(args)
         return
-    args.steps_ref = max(1, min(args.steps, 3))
-    args.warmup_ref = 0
+    args.steps_ref = max(1, min(args.steps, args.ref_steps))
 
     from paper_2003_07020_b200 import problems
     w = problems.config(args.config, args.gamma if args.config == 1 else None)
-    k_full_known = {1: 13}.get(args.config, 12)
 
     if args.impl == "reference":
-        run_reference(args, w, k_full_known)
+        run_reference(args, w)
         return
 
     import torch
@@ -346,205 +575,66 @@ def main():
     import paper_2003_07020_b200 as fp
     stream = torch.cuda.Stream(device=dev)
     ctx = fp.Context(local, stream)
-    if w.two_dim:
-        jac = fp.RieszJacobian2D(w.gamma[0], w.gamma[1], 1.0, 1.0, w.h, w.n)
-    else:
-        jac = fp.RieszJacobian1D(w.gamma[0], 1.0, w.h, w.n)
-    op = fp.AllAtOnceOperator(fp.TimeStencil(w.n_time), jac, w.dt, ctx)
-    plan = fp.build_plan(fp.PreconditionerKind.generalized(), w.n_time, w.dt, op,
-                         ordering=fp.Ordering[args.ordering])
-    cfg = fp.SolverConfig(tol=w.tol, max_iter=200, restart=w.restart)
-    b_host = problems.rhs(w)
-    N = w.dim
-    with torch.cuda.stream(stream):
-        b = torch.from_numpy(b_host).to(dev)
-        x = torch.empty_like(b)
-    stream.synchronize()
+    sync = dist.barrier if world > 1 else None
 
-    def barrier():
-        if world > 1:
-            dist.barrier()
-
-    # warm-up (untimed)
-    for _ in range(args.warmup):
-        res = fp.gmres_right(op, plan, b, cfg, out=x)
-    torch.cuda.synchronize()
-    k = int(res.report.iterations)
-
-    # timed region: K device-resident solves; inputs (134 MB vectors) exceed the 126 MB L2
-    launches0 = fp.kernel_launches()
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clk:
-        barrier()
-        torch.cuda.synchronize()
-        ev0.record(stream)
-        for _ in range(args.steps):
-            res = fp.gmres_right(op, plan, b, cfg, out=x)
-        ev1.record(stream)
-        torch.cuda.synchronize()
-        barrier()
-    launches = fp.kernel_launches() - launches0
-    x_sample = x[::1009].cpu().numpy()  # checked against the e2e (host-buffer) solve below
-    t_step = ev0.elapsed_time(ev1) * 1e-3 / args.steps
-    if world > 1:
-        tt = torch.tensor([t_step], device=dev)
+    def max_over_ranks(t):
+        if world == 1:
+            return t
+        tt = torch.tensor([t], device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        t_step = float(tt.item())
-    value = world / t_step
+        return float(tt.item())
 
-    # the other factor ordering of the PC apply (rounding-level different), same solve
-    alt = None
-    if world == 1 and not w.two_dim and w.n + 1 <= 8192:
-        other = "commuted" if args.ordering == "reference" else "reference"
-        plan2 = fp.build_plan(fp.PreconditionerKind.generalized(), w.n_time, w.dt, op, ordering=fp.Ordering[other])
-        for _ in range(args.warmup):
-            r2 = fp.gmres_right(op, plan2, b, cfg, out=x)
-        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a0.record(stream)
-        for _ in range(args.steps):
-            r2 = fp.gmres_right(op, plan2, b, cfg, out=x)
-        a1.record(stream)
-        torch.cuda.synchronize()
-        t_alt = a0.elapsed_time(a1) * 1e-3 / args.steps
-        alt = {other: {"ms_per_step": t_alt * 1e3, "value": 1.0 / t_alt, "iterations": int(r2.report.iterations),
-                       "true_relative_residual": r2.report.true_relative_residual}}
-        del plan2
+    m = measure(fp, torch, w, args, stream, ctx, dev, args.steps, args.warmup, True, sync)
+    t_step = max_over_ranks(m["ms_per_step"] * 1e-3)
+    t_e2e = max_over_ranks(1.0 / m["e2e"]["value"])
+    m["e2e"]["value"] = world / t_e2e
 
-    # live per-kernel device time inside one solve (events around every launch)
-    with fp.KernelProfile() as prof:
-        fp.gmres_right(op, plan, b, cfg, out=x)
-    table = prof.table
-    # standalone operator rates (device-resident, events on the launching stream)
-    def rate(fn, reps=20):
-        for _ in range(3):
-            fn()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        for _ in range(reps):
-            fn()
-        e1.record(stream)
-        torch.cuda.synchronize()
-        return ev_s(e0, e1) / reps
-
-    def ev_s(e0, e1):
-        return e0.elapsed_time(e1) * 1e-3
-
-    y = x  # the solution buffer is free again (no extra 8.6 GB vector at config 3)
-    t_mv = rate(lambda: op.apply(b, y))
-    t_pc = rate(lambda: fp.apply_inverse(plan, b, y))
-    H = w.n_time // 2 + 1
-    B_mv = 16.0 * N
-    B_pc = 16.0 * N + 64.0 * H * w.n_space
-    peak, peak_kind = load_peaks()
-
-    # whole-solve roofline: compulsory bytes of the reference algorithm for k
-    # iterations -- (k+1)(B_mv + B_pc) + sum_j 8N(2j+5) (one Gram-Schmidt pass per step, j counted
-    # within a restart cycle) + 8N(k+1) (x = P^{-1} sum y_k V_k) + 16N (TRR) + (B_mv + 24N) per restart
-    rcyc = w.restart if w.restart else k + 1
-    n_restarts = max(0, (k - 1) // rcyc) if k > 0 else 0
-    B_tot = ((k + 1) * (B_mv + B_pc) + sum(8.0 * N * (2 * (j % rcyc) + 5) for j in range(k))
-             + 8.0 * N * (k + 1) + 16.0 * N + n_restarts * (B_mv + 24.0 * N))
-
-    # dominant kernel by live device time inside the solve
-    dom = max(table.items(), key=lambda kv: kv[1][0])
-    dom_name, (dom_ms, dom_cnt) = dom
-    per_launch_bytes = {"matvec_1d": B_mv, "matvec_2d": B_mv, "time_fwd": 8.0 * N + 16.0 * H * w.n_space,
-                        "time_inv": 8.0 * N + 16.0 * H * w.n_space, "tau_solve_1d": 32.0 * H * w.n_space,
-                        "tau_solve_2d": 32.0 * H * w.n_space}
-    dom_bytes = per_launch_bytes.get(dom_name)
-    dom_t = dom_ms * 1e-3 / dom_cnt
-    achieved = dom_bytes / dom_t / 1e9 if dom_bytes else None
-    traffic = None
-    tfile = os.path.join(ROOT, "profiles", "traffic.json")
-    if os.path.exists(tfile):
+    # secondary BASELINE configs (same run, fewer steps; config 3 is 8.6 GB per Krylov vector)
+    secondary = {}
+    for c in [int(v) for v in args.secondary.split(",") if v.strip()]:
+        if c == args.config:
+            continue
+        ws = problems.config(c, 1.2 if c == 1 else None)
         try:
-            traffic = json.load(open(tfile)).get(dom_name)
-        except Exception:
-            traffic = None
+            big = ws.dim > 2e8
+            r = measure(fp, torch, ws, args, stream, ctx, dev, 2 if big else min(args.steps, 5),
+                        1 if big else min(args.warmup, 3), False, sync)
+            r["config"] = workload_config(ws)
+            secondary[ws.name] = r
+        except Exception as e:  # noqa: BLE001
+            secondary[ws.name] = {"error": str(e)[:300]}
+        torch.cuda.empty_cache()
 
-    onchip = None  # the on-chip pipe that bounds an FFT kernel (ncu, per launch), beside the HBM roofline
-    ofile = os.path.join(ROOT, "profiles", "onchip.json")
-    if os.path.exists(ofile):
-        try:
-            onchip = json.load(open(ofile)).get(dom_name)
-        except Exception:
-            onchip = None
-
-    # e2e: the public API with HOST buffers (pinned): the C-ABI's host path uploads b, solves, and
-    # copies x back (overlapped with the true-residual check); wall clock around synchronous calls
-    # (the device-resident b and x are released first: the host path stages through its own buffers,
-    # and config 3 has no room for both pairs next to the basis)
-    trr = res.report.true_relative_residual
-    res = r2 = None  # results hold the device x
-    del b, x, y
-    torch.cuda.synchronize()
-    torch.cuda.empty_cache()
-    b_pin = torch.from_numpy(b_host).pin_memory()
-    x_pin = torch.empty_like(b_pin).pin_memory()
-    b_pin_np, x_pin_np = b_pin.numpy(), x_pin.numpy()
-    with torch.cuda.stream(stream):
-        def e2e_step():
-            return fp.gmres_right(op, plan, b_pin_np, cfg, out=x_pin_np)
-        e2e_step()
-        t0 = time.perf_counter()
-        for _ in range(args.steps):
-            r_e2e = e2e_step()
-        t_e2e = (time.perf_counter() - t0) / args.steps
-        stream.synchronize()
-        e2e_same_x = bool(np.array_equal(x_pin_np[::1009], x_sample))  # host path == device path
-    if world > 1:
-        tt = torch.tensor([t_e2e], device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        t_e2e = float(tt.item())
-
-    # CPU baseline: the reference on this host, bounded sample (rank 0, N = 1 only)
+    # CPU baseline: the reference on this host (rank 0, N = 1 only): ONE full solve of the headline
+    # workload at all host threads (the reference's own report.seconds)
     cpu = None
-    if rank == 0 and world == 1 and w.dim > 2e8:
-        cpu = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "reference",
-               "sample": f"not run: the reference needs ~{22 * 8 * w.dim / 1e9:.0f} GB host RAM for {w.name} "
-                         "(SURVEY §8(d)); parity at this config is checked on a reduced grid"}
-    elif rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
             threads = os.cpu_count() or 1
-            sec, done = cpu_reference_sample(w, threads, args.ref_iters)
-            t_cpu = sec * (k + 1) / (done + 1)
-            cpu = {"value": 1.0 / t_cpu, "unit": UNIT, "cores": threads, "kind": "reference",
-                   "sample": f"reference gmres_right (oracle/_ref) on {w.name}, max_iter={args.ref_iters} of {k} "
-                             f"iterations, {sec:.1f} s, extrapolated x({k}+1)/({done}+1)"}
+            sec, its = cpu_reference_solve(w, threads)
+            cpu = {"value": 1.0 / sec, "unit": UNIT, "cores": threads, "kind": "reference",
+                   "sample": f"one full reference gmres_right solve (oracle/_ref) of {w.name}, {its} iterations, "
+                             f"{sec:.1f} s (report.seconds, krylov.hpp:87-190)", "cpu_model": cpu_model()}
         except Exception as e:  # noqa: BLE001
             cpu = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "reference",
                    "sample": f"unavailable: {e}"}
 
     if rank == 0:
+        cfg = workload_config(w)
+        cfg.update({"parallelism": f"replicas x{world}" if world > 1 else "single GPU", "pc_ordering": args.ordering,
+                    "l2": f"inputs larger than L2 ({8 * w.dim / 1e6:.0f} MB per Krylov vector vs 126 MB L2)"})
         line = {
-            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "metric": METRIC, "value": world / t_step, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t_step * 1e3, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded uniform[-1,1] source, u0=x^2(1-x)^2)",
-            "config": {"workload": w.name, "n_space": w.n, "n_time": w.n_time, "gamma": w.gamma[0], "kappa": 1.0,
-                       "tol": w.tol, "restart": w.restart, "solver": "GMRES(20) right-preconditioned, BC alpha=dt/2",
-                       "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
-                       "pc_ordering": args.ordering,
-                       "l2": "inputs larger than L2 (134 MB per Krylov vector vs 126 MB L2)"},
-            "time_to_tol_s": t_step, "iterations": k, "true_relative_residual": trr,
-            "pc_applies_per_s": 1.0 / t_pc, "matvecs_per_s": 1.0 / t_mv,
-            "pc_apply_gbs": B_pc / t_pc / 1e9, "matvec_gbs": B_mv / t_mv / 1e9,
-            "e2e": {"value": world / t_e2e, "unit": UNIT, "h2d_bytes_per_step": 8 * N, "d2h_bytes_per_step": 8 * N,
-                    "iterations": int(r_e2e.report.iterations), "x_matches_device": e2e_same_x},
-            "gpu_launches": launches,
-            "pc_orderings": alt,
-            "roofline": {"bound": "hbm", "kernel": dom_name, "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": (achieved / peak) if achieved else None, "traffic": traffic,
-                         "algorithmic_bytes_per_launch": dom_bytes, "avg_launch_us": dom_t * 1e6,
-                         "peak_source": peak_kind, "onchip": onchip},
-            "solve_roofline": {"bound": "hbm", "algorithmic_bytes": B_tot, "achieved": B_tot / t_step / 1e9,
-                               "peak": peak, "unit": "GB/s", "frac": B_tot / t_step / 1e9 / peak,
-                               "formula": "SURVEY 8(d) B_tot, one Gram-Schmidt pass per step (the reference "
-                                          "re-orthogonalises every step here, which doubles that term)"},
-            "kernel_time_ms_per_solve": {k_: v[0] for k_, v in table.items()},
-            "kernel_launches_per_solve": {k_: v[1] for k_, v in table.items()},
-            "clocks": clk.summary(),
-            "cpu_baseline": cpu,
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded uniform[-1,1] source, u0 = " + ("x^2(1-x)^2 y^2(1-y)^2)" if w.two_dim else "x^2(1-x)^2)"),
+            "config": cfg, "time_to_tol_s": t_step,
         }
+        for key in ("iterations", "restarts", "true_relative_residual", "pc_applies_per_s", "matvecs_per_s",
+                    "pc_apply_gbs", "matvec_gbs", "e2e", "gpu_launches", "roofline", "solve_roofline",
+                    "kernel_time_ms_per_solve", "kernel_launches_per_solve", "clocks"):
+            line[key] = m.get(key)
+        line["secondary"] = secondary
+        line["cpu_baseline"] = cpu
         print(json.dumps(line))
     if world > 1:
         dist.destroy_process_group()

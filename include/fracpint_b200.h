@@ -80,6 +80,19 @@ typedef struct {
 int fpc_abi_version(void);
 const char* fpc_last_error(void);
 
+/* host-side setup of the reference API (no device needed; bit-identical to the reference's
+ * arithmetic when both are compiled with FMA contraction, as g++ does by default for C++):
+ *   fpc_centred_weights            <- centred_weights(gamma, count)          weights.hpp:21-35
+ *   fpc_tau_spectrum               <- tau_spectrum(first column)  (n values) tau.hpp:40-55
+ *   fpc_circulant_eigenvalues      <- SymToeplitz ctor: FFT of the circulant embedding, real parts
+ *                                     k = 0..L/2, L = next_pow2(2n)          toeplitz.hpp:23-35
+ *   fpc_alpha_circulant_eigenvalues<- alpha_circulant_eigenvalues(alpha, nt) alpha_circulant.hpp:71-81
+ *                                     (nt complex, interleaved re/im) */
+int fpc_centred_weights(double gamma, int count, double* out);
+int fpc_tau_spectrum(const double* col, int n, double* sigma);
+int fpc_circulant_eigenvalues(const double* col, int n, double* eig);
+int fpc_alpha_circulant_eigenvalues(double alpha, int nt, double* lambda_interleaved);
+
 /* context: one device, one stream (default: a private non-blocking stream) */
 int fpc_context_create(int device, fpc_context_t* out);
 int fpc_context_destroy(fpc_context_t ctx);

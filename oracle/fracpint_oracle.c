@@ -5,14 +5,18 @@
  * Reference = /root/reference/proj/include/fracpint/*.hpp (header-only C++20).  Each routine
  * below cites the reference lines it restates and keeps the reference's operation order so
  * the two agree to rounding (pinned in tests/test_oracle_pins.py against oracle/_ref, the
- * reference compiled unchanged).  Single-threaded: the reference's parallel_for partition is
- * deterministic and result-independent (parallel.hpp:27-31), so one thread gives the same
- * numbers.
+ * reference compiled unchanged).  The independent per-time-level / per-column / per-frequency
+ * loops run on a fork-join pool like the reference's parallel_for (parallel.hpp:27-60, contiguous
+ * static partition): every iteration writes disjoint outputs with its own scratch, so the numbers
+ * do not depend on the thread count (ORC_THREADS, default all cores).  Reductions -- dots, norms --
+ * stay serial left-to-right sums (krylov.hpp:52-56).
  */
 #include "fracpint_oracle.h"
 
 #include <complex.h>
 #include <math.h>
+#include <pthread.h>
+#include <unistd.h>
 #include <stdint.h>
 #include <stdio.h>
 #include <stdlib.h>
@@ -28,6 +32,48 @@ static int fail(int code, const char* msg) {
   return code;
 }
 const char* orc_last_error(void) { return g_err; }
+
+/* ---------------------------------------------------------------- fork-join (parallel.hpp:24-60) */
+typedef void (*range_fn)(void* ctx, size_t lo, size_t hi);
+typedef struct {
+  range_fn fn;
+  void* ctx;
+  size_t lo, hi;
+} range_job;
+static void* range_run(void* a) {
+  range_job* j = (range_job*)a;
+  if (j->lo < j->hi) j->fn(j->ctx, j->lo, j->hi);
+  return NULL;
+}
+static int thread_count(void) {
+  const char* e = getenv("ORC_THREADS");
+  long t = e ? atol(e) : sysconf(_SC_NPROCESSORS_ONLN);
+  return t < 1 ? 1 : (t > 256 ? 256 : (int)t);
+}
+/* fn over [0, n) in contiguous chunks, one per thread (the calling thread takes the first). */
+static void par_for(size_t n, range_fn fn, void* ctx) {
+  int T = thread_count();
+  if ((size_t)T > n) T = (int)(n ? n : 1);
+  if (T <= 1) {
+    if (n) fn(ctx, 0, n);
+    return;
+  }
+  range_job jobs[256];
+  pthread_t th[256];
+  for (int t = 0; t < T; ++t) {
+    jobs[t].fn = fn;
+    jobs[t].ctx = ctx;
+    jobs[t].lo = n * (size_t)t / (size_t)T;
+    jobs[t].hi = n * (size_t)(t + 1) / (size_t)T;
+  }
+  int started[256] = {0};
+  for (int t = 1; t < T; ++t) started[t] = pthread_create(&th[t], NULL, range_run, &jobs[t]) == 0;
+  range_run(&jobs[0]);
+  for (int t = 1; t < T; ++t) {
+    if (started[t]) pthread_join(th[t], NULL);
+    else range_run(&jobs[t]);
+  }
+}
 
 /* ---------------------------------------------------------------- FFT (fft.hpp) */
 
@@ -490,31 +536,43 @@ int orc_jacobian_apply(const orc_problem* p, const double* v, double* out) {
 }
 
 /* AllAtOnceOperator::apply (all_at_once.hpp:33-55): y_k = C-stencil(v)_k - dt A v_k. */
-int orc_matvec(const orc_problem* p, const double* v, double* out) {
-  const size_t ns = (size_t)p->ns, nt = (size_t)p->nt;
+typedef struct {
+  const orc_problem* p;
+  const double* v;
+  double* out;
+} mv_ctx;
+static void matvec_levels(void* c_, size_t k0, size_t k1) {
+  const mv_ctx* c = (const mv_ctx*)c_;
+  const orc_problem* p = c->p;
+  const double* v = c->v;
+  const size_t ns = (size_t)p->ns;
   cplx* s = (cplx*)malloc(scratch_len(p) * sizeof(cplx));
   double* buf = (double*)malloc((size_t)p->n * sizeof(double));
   double* res = (double*)malloc((size_t)p->n * sizeof(double));
-  for (size_t k = 0; k < nt; ++k) {
-    double* o = out + k * ns;
+  for (size_t k = k0; k < k1; ++k) {
+    double* o = c->out + k * ns;
     jac_apply(p, v + k * ns, o, s, buf, res);
     const double* vk = v + k * ns;
     const double* vk1 = k >= 1 ? v + (k - 1) * ns : NULL;
     const double* vk2 = k >= 2 ? v + (k - 2) * ns : NULL;
     for (size_t i = 0; i < ns; ++i) {
-      double c;
+      double c_k;
       if (k == 0)
-        c = vk[i];
+        c_k = vk[i];
       else if (k == 1)
-        c = 1.5 * vk[i] + -2.0 * vk1[i];
+        c_k = 1.5 * vk[i] + -2.0 * vk1[i];
       else
-        c = 1.5 * vk[i] + -2.0 * vk1[i] + 0.5 * vk2[i];
-      o[i] = c - p->dt * o[i];
+        c_k = 1.5 * vk[i] + -2.0 * vk1[i] + 0.5 * vk2[i];
+      o[i] = c_k - p->dt * o[i];
     }
   }
   free(s);
   free(buf);
   free(res);
+}
+int orc_matvec(const orc_problem* p, const double* v, double* out) {
+  mv_ctx c = {p, v, out};
+  par_for((size_t)p->nt, matvec_levels, &c);
   return 0;
 }
 
@@ -571,30 +629,70 @@ int orc_plan_lambda(const orc_problem* p, double* lambda) {
 }
 
 /* alpha_circulant_action<Solve> (alpha_circulant.hpp:137-199). */
+typedef struct {
+  const orc_problem* p;
+  int solve;
+  const double* v;
+  cplx* rows;
+  cplx* blocks;
+  int* rcs;
+} pc_ctx;
+static void pc_fwd_cols(void* c_, size_t j0, size_t j1) { /* alpha_circulant.hpp:146-152 */
+  const pc_ctx* c = (const pc_ctx*)c_;
+  const size_t nt = (size_t)c->p->nt, ns = (size_t)c->p->ns;
+  for (size_t j = j0; j < j1; ++j) {
+    cplx* row = c->rows + j * nt;
+    for (size_t k = 0; k < nt; ++k) row[k] = c->p->scale_fwd[k] * c->v[k * ns + j];
+    fft_c(row, nt, +1);
+  }
+}
+static void pc_transpose_fwd(void* c_, size_t n0, size_t n1) { /* alpha_circulant.hpp:153-156 */
+  const pc_ctx* c = (const pc_ctx*)c_;
+  const size_t nt = (size_t)c->p->nt, ns = (size_t)c->p->ns;
+  for (size_t n = n0; n < n1; ++n)
+    for (size_t j = 0; j < ns; ++j) c->blocks[n * ns + j] = c->rows[j * nt + n];
+}
+static void pc_tau(void* c_, size_t n0, size_t n1) { /* alpha_circulant.hpp:158-166 */
+  const pc_ctx* c = (const pc_ctx*)c_;
+  const orc_problem* p = c->p;
+  const size_t ns = (size_t)p->ns;
+  const int nx = p->two_dim ? p->n : 0, ny = p->two_dim ? p->n : 0;
+  for (size_t n = n0; n < n1; ++n) {
+    cplx* z = c->blocks + n * ns;
+    c->rcs[n] = tau_shifted(c->solve, p->sigma, nx, ny, ns, p->lambda[n], p->dt, z, z);
+  }
+}
+static void pc_inv_cols(void* c_, size_t j0, size_t j1) { /* alpha_circulant.hpp:176-186 */
+  const pc_ctx* c = (const pc_ctx*)c_;
+  const size_t nt = (size_t)c->p->nt, ns = (size_t)c->p->ns;
+  for (size_t j = j0; j < j1; ++j) {
+    cplx* row = c->rows + j * nt;
+    for (size_t k = 0; k < nt; ++k) row[k] = c->blocks[k * ns + j];
+    fft_c(row, nt, -1);
+  }
+}
+
 static int pc_action(const orc_problem* p, int solve, int full_sweep, const double* v,
                      double* out) {
   if (!p->has_plan) return fail(1, "alpha-circulant action: no plan built");
   const size_t nt = (size_t)p->nt, ns = (size_t)p->ns;
-  cplx* rows = (cplx*)malloc(nt * ns * sizeof(cplx)); /* space-major rows[j*nt+k] */
-  for (size_t j = 0; j < ns; ++j) {
-    cplx* row = rows + j * nt;
-    for (size_t k = 0; k < nt; ++k) row[k] = p->scale_fwd[k] * v[k * ns + j];
-    fft_c(row, nt, +1);
-  }
-  cplx* blocks = (cplx*)malloc(nt * ns * sizeof(cplx)); /* time-major blocks[n*ns+j] */
-  for (size_t n = 0; n < nt; ++n)
-    for (size_t j = 0; j < ns; ++j) blocks[n * ns + j] = rows[j * nt + n];
-  const int nx = p->two_dim ? p->n : 0, ny = p->two_dim ? p->n : 0;
+  pc_ctx c = {p, solve, v, NULL, NULL, NULL};
+  c.rows = (cplx*)malloc(nt * ns * sizeof(cplx)); /* space-major rows[j*nt+k] */
+  par_for(ns, pc_fwd_cols, &c);
+  c.blocks = (cplx*)malloc(nt * ns * sizeof(cplx)); /* time-major blocks[n*ns+j] */
+  par_for(nt, pc_transpose_fwd, &c);
   const size_t active = (solve && !full_sweep) ? (size_t)p->solve_count : nt;
+  c.rcs = (int*)calloc(active ? active : 1, sizeof(int));
+  par_for(active, pc_tau, &c);
   int rc = 0;
-  for (size_t n = 0; n < active && !rc; ++n) {
-    cplx* z = blocks + n * ns;
-    rc = tau_shifted(solve, p->sigma, nx, ny, ns, p->lambda[n], p->dt, z, z);
-  }
+  for (size_t n = 0; n < active && !rc; ++n) rc = c.rcs[n];
+  free(c.rcs);
+  cplx* rows = c.rows;
+  cplx* blocks = c.blocks;
   if (rc) {
     free(rows);
     free(blocks);
-    return rc;
+    return fail(rc, "tau_solve_shifted: shift is numerically singular"); /* the worker's message */
   }
   if (solve && !full_sweep) {
     for (size_t n = 1; n < (size_t)p->solve_count; ++n) {
@@ -603,11 +701,7 @@ static int pc_action(const orc_problem* p, int solve, int full_sweep, const doub
       for (size_t j = 0; j < ns; ++j) blocks[q * ns + j] = conj(blocks[n * ns + j]);
     }
   }
-  for (size_t j = 0; j < ns; ++j) {
-    cplx* row = rows + j * nt;
-    for (size_t k = 0; k < nt; ++k) row[k] = blocks[k * ns + j];
-    fft_c(row, nt, -1);
-  }
+  par_for(ns, pc_inv_cols, &c);
   const double inv_nt = 1.0 / (double)nt;
   double imag_sq = 0.0, total_sq = 0.0;
   for (size_t k = 0; k < nt; ++k) {

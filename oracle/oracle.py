@@ -123,6 +123,8 @@ def _load(path: str, kind: str):
         lib.ref_tau_sigma.argtypes = [C.c_void_p, _dp]
         lib.ref_gmres.argtypes = [C.c_void_p, _dp, _dp, C.c_double, C.c_int, C.POINTER(C.c_int),
                                   C.POINTER(C.c_int), _dp, _dp, _dp, _dp, C.c_int, C.POINTER(C.c_int)]
+        lib.ref_gmres_restart.argtypes = [C.c_void_p, _dp, _dp, C.c_double, C.c_int, C.c_int, C.POINTER(C.c_int),
+                                          C.POINTER(C.c_int), C.POINTER(C.c_int), _dp, _dp]
         lib.ref_bicgstab.argtypes = [C.c_void_p, _dp, _dp, C.c_double, C.c_int, C.POINTER(C.c_int),
                                      _dp, _dp, _dp, _dp, _dp, C.c_int, C.POINTER(C.c_int)]
         lib.ref_run_problem.argtypes = [C.c_int, C.c_double, C.c_double, C.c_int, C.c_int, C.c_int, C.c_int,
@@ -390,6 +392,18 @@ class RefProblem(_ProblemBase):
                                            _ptr(fr), _ptr(tr), _ptr(sec), _ptr(hist), cap, C.byref(hl)))
         return x, SolveReport(bool(conv.value), it.value, float(fr[0]), float(tr[0]),
                               list(hist[:min(hl.value, cap)]), float(sec[0]))
+
+    def gmres_restarted(self, b, tol=1e-9, max_iter=200, restart=0):
+        """GMRES(m) emulated on the reference's own gmres_right (ref_shim.cpp).
+        Returns (x, dict(converged, iterations, restarts, true_relative_residual, seconds))."""
+        b = np.ascontiguousarray(b, dtype=np.float64)
+        x = np.empty_like(b)
+        conv, it, rs = C.c_int(), C.c_int(), C.c_int()
+        tr, sec = np.zeros(1), np.zeros(1)
+        self.be._chk(self.be.lib.ref_gmres_restart(self.h, _ptr(b), _ptr(x), tol, max_iter, restart, C.byref(conv),
+                                                   C.byref(it), C.byref(rs), _ptr(tr), _ptr(sec)))
+        return x, {"converged": bool(conv.value), "iterations": it.value, "restarts": rs.value,
+                   "true_relative_residual": float(tr[0]), "seconds": float(sec[0])}
 
     def bicgstab(self, b, tol=1e-9, max_iter=200):
         b = np.ascontiguousarray(b, dtype=np.float64)

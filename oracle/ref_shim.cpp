@@ -19,6 +19,7 @@
 #include <fracpint/weights.hpp>
 
 #include <algorithm>
+#include <cmath>
 #include <chrono>
 #include <complex>
 #include <cstring>
@@ -27,6 +28,7 @@
 #include <stdexcept>
 #include <string>
 #include <variant>
+#include <vector>
 
 namespace {
 thread_local std::string g_err;
@@ -279,6 +281,65 @@ int ref_gmres(void* hp, const double* b, double* x, double tol, int max_iter, in
     const int h = static_cast<int>(r.report.residual_history.size());
     *history_len = h;
     for (int i = 0; i < h && i < history_cap; ++i) history[i] = r.report.residual_history[i];
+  });
+}
+
+// GMRES(m) restart emulation (the reference has no restart) on top of the
+// reference's own unrestarted gmres_right, exactly as driver.hpp:62-73 wires it:
+//   r = b; x = 0; loop { d = gmres_right(r, tol*||b||/||r||, min(m, budget)); x += d.x;
+//                        stop if d converged or the budget is spent; r = b - A x }.
+// iterations = the sum of the inner counts; true_rel = ||b - A x|| / ||b|| (krylov.hpp:64-75);
+// seconds = wall time of the whole loop.
+int ref_gmres_restart(void* hp, const double* b, double* x, double tol, int max_iter, int restart,
+                      int* converged, int* iterations, int* restarts, double* true_rel, double* seconds) {
+  auto* p = static_cast<RefProblem*>(hp);
+  const std::size_t n = p->dim();
+  return guarded([&] {
+    if (!p->plan) throw std::invalid_argument("no plan");
+    const auto t0 = std::chrono::steady_clock::now();
+    auto apply_pinv = [p](std::span<const double> in, std::span<double> out) {
+      fracpint::apply_inverse(*p->plan, in, out);
+    };
+    auto apply_a = [p](std::span<const double> in, std::span<double> out) {
+      std::visit([&](const auto& o) { o.apply(in, out); }, p->op);
+    };
+    auto nrm = [n](const std::vector<double>& v) {
+      double s = 0.0;
+      for (std::size_t i = 0; i < n; ++i) s += v[i] * v[i];
+      return std::sqrt(s);
+    };
+    std::vector<double> bb(b, b + n), r(bb), xx(n, 0.0), ax(n);
+    const double norm_b = nrm(bb);
+    int budget = max_iter, its = 0, cycles = 0;
+    bool conv = norm_b == 0.0;
+    double norm_r = norm_b;
+    while (!conv && budget > 0) {
+      fracpint::SolverConfig cfg;
+      cfg.tol = tol * norm_b / norm_r;
+      cfg.max_iter = restart > 0 ? std::min(restart, budget) : budget;
+      fracpint::KrylovResult d = fracpint::gmres_right(n, apply_a, apply_pinv, {r.data(), n}, cfg);
+      for (std::size_t i = 0; i < n; ++i) xx[i] += d.x[i];
+      const int k = static_cast<int>(d.report.iterations);
+      its += k;
+      budget -= k;
+      ++cycles;
+      if (d.report.converged) {
+        conv = true;
+        break;
+      }
+      if (k == 0) break;
+      apply_a({xx.data(), n}, {ax.data(), n});
+      for (std::size_t i = 0; i < n; ++i) r[i] = bb[i] - ax[i];
+      norm_r = nrm(r);
+    }
+    apply_a({xx.data(), n}, {ax.data(), n});
+    for (std::size_t i = 0; i < n; ++i) ax[i] = bb[i] - ax[i];
+    *true_rel = norm_b > 0.0 ? nrm(ax) / norm_b : 0.0;
+    std::copy(xx.begin(), xx.end(), x);
+    *converged = conv ? 1 : 0;
+    *iterations = its;
+    *restarts = cycles > 0 ? cycles - 1 : 0;
+    *seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   });
 }
 

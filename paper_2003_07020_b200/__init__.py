@@ -6,11 +6,12 @@ include/fracpint_b200.h); this package is the Python mirror of the reference int
 from .solver import (AllAtOnceOperator, AlphaCirculantPlan, Context, InnerSweep, KrylovResult, Ordering,
                      PreconditionerKind, RieszJacobian1D, RieszJacobian2D, SolveReport, SolverConfig,
                      TimeStencil, apply_forward, apply_inverse, assemble_rhs, bicgstab_left, build_plan,
-                     centred_weights, gmres_right, kernel_launches, KernelProfile)
+                     centred_weights, tau_spectrum, circulant_eigenvalues, alpha_circulant_eigenvalues,
+                     gmres_right, kernel_launches, KernelProfile)
 
 __all__ = [
     "AllAtOnceOperator", "AlphaCirculantPlan", "Context", "InnerSweep", "KrylovResult", "Ordering",
     "PreconditionerKind", "RieszJacobian1D", "RieszJacobian2D", "SolveReport", "SolverConfig",
-    "TimeStencil", "apply_forward", "apply_inverse", "assemble_rhs", "bicgstab_left", "build_plan", "centred_weights",
+    "TimeStencil", "apply_forward", "apply_inverse", "assemble_rhs", "bicgstab_left", "build_plan", "centred_weights", "tau_spectrum", "circulant_eigenvalues", "alpha_circulant_eigenvalues",
     "gmres_right", "kernel_launches", "KernelProfile",
 ]

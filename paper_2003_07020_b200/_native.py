@@ -28,7 +28,8 @@ EXPORTS = [
     "fpc_profile_stop", "fpc_profile_entry", "fpc_shard_matvec", "fpc_shard_time_fwd", "fpc_shard_tau",
     "fpc_shard_time_inv", "fpc_shard_dots", "fpc_shard_update", "fpc_shard_lincomb",
     "fpc_shard_dst_levels", "fpc_shard_time_solve", "fpc_ipc_get_handle", "fpc_ipc_open", "fpc_ipc_close",
-    "fpc_shard_scatter_p2p",
+    "fpc_shard_scatter_p2p", "fpc_centred_weights", "fpc_tau_spectrum", "fpc_circulant_eigenvalues",
+    "fpc_alpha_circulant_eigenvalues",
 ]
 
 
@@ -99,6 +100,10 @@ def load():
     lib.fpc_shard_lincomb.argtypes = [vp, vp, vp, C.c_int, vp, C.c_size_t]
     lib.fpc_shard_dst_levels.argtypes = [vp, vp, vp, C.c_int, d]
     lib.fpc_shard_time_solve.argtypes = [vp, vp, vp, C.c_int, C.c_int, C.c_int]
+    lib.fpc_centred_weights.argtypes = [d, C.c_int, dp]
+    lib.fpc_tau_spectrum.argtypes = [dp, C.c_int, dp]
+    lib.fpc_circulant_eigenvalues.argtypes = [dp, C.c_int, dp]
+    lib.fpc_alpha_circulant_eigenvalues.argtypes = [d, C.c_int, dp]
     _lib = lib
     return lib
 

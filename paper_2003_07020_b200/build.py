@@ -19,7 +19,11 @@ SOURCES = ["kernels_1d.cu", "kernels_mv.cu", "kernels_large.cu", "kernels_2d.cu"
            "kernels_krylov.cu", "kernels_commuted.cu", "kernels_tsplit.cu", "kernels_p2p.cu", "api.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3", "--expt-relaxed-constexpr",
+# host code: x86-64-v3 with FMA contraction (g++'s C++ default once FMA exists), the arithmetic of the
+# reference built with -march=native/-march=x86-64-v3: the host setup (weights, tau spectrum,
+# circulant eigenvalues, lambda) is then bit-identical to the reference's (tests/test_abi.py)
+FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3,-march=x86-64-v3,-ffp-contract=fast",
+         "--expt-relaxed-constexpr",
          "-diag-suppress", "39"]
 
 
@@ -32,6 +36,10 @@ def _stale(obj: str, deps: list[str]) -> bool:
 
 def build(verbose: bool = False, force: bool = False) -> str:
     os.makedirs(BUILD, exist_ok=True)
+    stamp = os.path.join(BUILD, "flags.txt")
+    flags = " ".join([NVCC, *ARCH, *FLAGS])
+    if not os.path.exists(stamp) or open(stamp).read() != flags:
+        force = True  # compiler flags changed: every object is stale
     headers = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cuh", ".h"))]
     headers.append(os.path.join(ROOT, "include", "fracpint_b200.h"))
     jobs = []
@@ -54,6 +62,8 @@ def build(verbose: bool = False, force: bool = False) -> str:
     objs = [os.path.join(BUILD, s.replace(".cu", ".o")) for s in SOURCES]
     if force or jobs or not os.path.exists(LIB) or _stale(LIB, objs):
         run([NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-Xcompiler", "-fPIC"])
+    with open(stamp, "w") as f:
+        f.write(flags)
     return LIB
 
 

@@ -166,6 +166,17 @@ size_t next_pow2(size_t n) {
 }
 
 // ---- host FFT for setup only (power-of-two radix-2, kernel e^{sign 2 pi i jk/n}) -----------
+// The complex product as g++ contracts std::complex<double> multiplication in the reference's
+// fft_pow2 butterfly (fft.hpp:62) once FMA is available (-march=native / x86-64-v3): written out,
+// so the setup (circulant eigenvalues, tau spectrum) is bit-identical to the reference's whatever
+// this translation unit's own contraction choices are.  At n = 65535 the tau spectrum's smallest
+// eigenvalue carries ~1e-6 cancellation error in any implementation; sharing the reference's
+// exact doubles keeps the large config-4 PC applies at rounding distance from the reference.
+inline cplx cmul_fma(cplx a, cplx b) {
+  return cplx(std::fma(a.real(), b.real(), -(a.imag() * b.imag())),
+              std::fma(a.real(), b.imag(), a.imag() * b.real()));
+}
+
 void host_fft(std::vector<cplx>& x, int sign) {
   const size_t n = x.size();
   if (n <= 1) return;
@@ -182,7 +193,7 @@ void host_fft(std::vector<cplx>& x, int sign) {
     const size_t half = len >> 1, step = n / len;
     for (size_t base = 0; base < n; base += len)
       for (size_t j = 0; j < half; ++j) {
-        const cplx u = x[base + j], v = x[base + j + half] * tw[j * step];
+        const cplx u = x[base + j], v = cmul_fma(x[base + j + half], tw[j * step]);
         x[base + j] = u + v;
         x[base + j + half] = u - v;
       }
@@ -227,6 +238,18 @@ std::vector<double> tau_spectrum(const std::vector<double>& a) {
   std::vector<double> s(n);
   for (size_t i = 0; i < n; ++i) s[i] = num[i] / (root * std::sin(kPi * double(i + 1) / double(n + 1)));
   return s;
+}
+
+// alpha_circulant_eigenvalues (alpha_circulant.hpp:71-81)
+std::vector<cplx> alpha_lambda(double a, int nt) {
+  std::vector<cplx> lam(static_cast<size_t>(nt));
+  const double ar = std::pow(a, 1.0 / double(nt));
+  for (int i = 0; i < nt; ++i) {
+    const double ang1 = 2.0 * kPi * double(i % nt) / nt;
+    const double ang2 = 2.0 * kPi * double((2 * i) % nt) / nt;
+    lam[size_t(i)] = 1.5 - 2.0 * ar * std::polar(1.0, ang1) + 0.5 * ar * ar * std::polar(1.0, ang2);
+  }
+  return lam;
 }
 
 // circulant-embedding eigenvalues (toeplitz.hpp:23-35): real parts of FFT_{-}(c), k = 0..L/2
@@ -348,6 +371,42 @@ extern "C" {
 
 int fpc_abi_version(void) { return 2; }
 const char* fpc_last_error(void) { return g_err.c_str(); }
+
+// ---- host-side setup routines of the reference API (no device needed) ----------------------
+int fpc_centred_weights(double gamma, int count, double* out) {
+  if (!out) return set_err(FPC_INVALID_ARGUMENT, "null argument");
+  return guarded([&] {
+    const std::vector<double> w = centred_weights(gamma, count);
+    std::copy(w.begin(), w.end(), out);
+  });
+}
+
+int fpc_tau_spectrum(const double* col, int n, double* sigma) {
+  if (!col || !sigma) return set_err(FPC_INVALID_ARGUMENT, "null argument");
+  if (n < 1) return set_err(FPC_INVALID_ARGUMENT, "tau_spectrum: empty first column");
+  return guarded([&] {
+    const std::vector<double> s = tau_spectrum(std::vector<double>(col, col + n));
+    std::copy(s.begin(), s.end(), sigma);
+  });
+}
+
+int fpc_circulant_eigenvalues(const double* col, int n, double* eig) {
+  if (!col || !eig) return set_err(FPC_INVALID_ARGUMENT, "null argument");
+  if (n < 1) return set_err(FPC_INVALID_ARGUMENT, "SymToeplitz: empty first column");
+  return guarded([&] {
+    const std::vector<double> e = circulant_eigs(std::vector<double>(col, col + n));
+    std::copy(e.begin(), e.end(), eig);
+  });
+}
+
+int fpc_alpha_circulant_eigenvalues(double alpha, int nt, double* lambda_interleaved) {
+  if (!lambda_interleaved) return set_err(FPC_INVALID_ARGUMENT, "null argument");
+  if (nt < 1) return set_err(FPC_INVALID_ARGUMENT, "alpha_circulant_eigenvalues: nt must be positive");
+  return guarded([&] {
+    const std::vector<cplx> l = alpha_lambda(alpha, nt);
+    std::memcpy(lambda_interleaved, l.data(), l.size() * sizeof(cplx));
+  });
+}
 unsigned long long fpc_kernel_launches(void) { return g_launches.load(); }
 
 int fpc_profile_start(void) {
@@ -684,14 +743,7 @@ int fpc_plan_create(fpc_problem_t p, double alpha_in, fpc_plan_t* out) {
     pl->prob = p;
     pl->alpha = a;
     pl->n_warnings = a < 1e-8 ? 1 : 0;
-    // alpha_circulant_eigenvalues (alpha_circulant.hpp:71-81)
-    pl->lambda.resize(size_t(nt));
-    const double ar = std::pow(a, 1.0 / double(nt));
-    for (int i = 0; i < nt; ++i) {
-      const double ang1 = 2.0 * kPi * double(i % nt) / nt;
-      const double ang2 = 2.0 * kPi * double((2 * i) % nt) / nt;
-      pl->lambda[size_t(i)] = 1.5 - 2.0 * ar * std::polar(1.0, ang1) + 0.5 * ar * ar * std::polar(1.0, ang2);
-    }
+    pl->lambda = alpha_lambda(a, nt);
     std::vector<double> sf(static_cast<size_t>(nt)), sb(static_cast<size_t>(nt));
     for (int k = 0; k < nt; ++k) {
       const double e = double(k) / double(nt);

@@ -145,17 +145,38 @@ class TimeStencil:
 
 
 def centred_weights(gamma: float, count: int) -> np.ndarray:
-    """weights.hpp:21-35 (host setup; the same recurrence the native plan build uses)."""
-    if not (gamma > 1.0) or not (gamma <= 2.0):
-        raise ValueError("centred_weights: gamma must lie in (1, 2]")
-    if count < 1:
-        raise ValueError("centred_weights: count must be at least 1")
-    w = np.empty(count)
-    g0 = math.gamma(1.0 + gamma / 2.0)
-    w[0] = math.gamma(1.0 + gamma) / (g0 * g0)
-    for l in range(count - 1):
-        w[l + 1] = w[l] * (l - gamma / 2.0) / (l + 1.0 + gamma / 2.0)
-    return w
+    """weights.hpp:21-35, computed by the library's host setup (fpc_centred_weights)."""
+    out = np.empty(max(int(count), 1))
+    N.check(N.load().fpc_centred_weights(float(gamma), int(count), out.ctypes.data))
+    return out[:count]
+
+
+def tau_spectrum(column) -> np.ndarray:
+    """tau.hpp:40-55: eigenvalues of the tau approximation of the symmetric Toeplitz matrix with
+    this first column (library host setup, fpc_tau_spectrum)."""
+    col = np.ascontiguousarray(column, dtype=np.float64)
+    out = np.empty(max(col.size, 1))
+    N.check(N.load().fpc_tau_spectrum(col.ctypes.data, int(col.size), out.ctypes.data))
+    return out[:col.size]
+
+
+def circulant_eigenvalues(column) -> np.ndarray:
+    """toeplitz.hpp:23-35: real parts of the circulant embedding's spectrum, k = 0..L/2,
+    L = next_pow2(2n) (fpc_circulant_eigenvalues)."""
+    col = np.ascontiguousarray(column, dtype=np.float64)
+    L = 1
+    while L < 2 * col.size:
+        L <<= 1
+    out = np.empty(L // 2 + 1)
+    N.check(N.load().fpc_circulant_eigenvalues(col.ctypes.data, int(col.size), out.ctypes.data))
+    return out
+
+
+def alpha_circulant_eigenvalues(alpha: float, n_time: int) -> np.ndarray:
+    """alpha_circulant.hpp:71-81 (fpc_alpha_circulant_eigenvalues): complex128[n_time]."""
+    out = np.empty(int(n_time), dtype=np.complex128)
+    N.check(N.load().fpc_alpha_circulant_eigenvalues(float(alpha), int(n_time), out.ctypes.data))
+    return out
 
 
 class RieszJacobian1D:

@@ -1,5 +1,6 @@
 // On-chip roofs for the FFT kernels (development aid): fp64 FMA throughput and shared-memory
 // bandwidth (16-byte accesses), measured on the whole GPU with CUDA events.
+// fp64_add_gops: DADD instructions per second (the FFT butterflies are add-heavy: one flop each).
 // nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o scripts/onchip_peaks scripts/onchip_peaks.cu
 #include <cstdio>
 #include <cuda_runtime.h>
@@ -11,6 +12,19 @@ __global__ void k_dfma(double* out, int iters) {
   for (int it = 0; it < iters; ++it) {
 #pragma unroll
     for (int i = 0; i < 8; ++i) a[i] = fma(a[i], b, c);
+  }
+  double s = 0;
+  for (int i = 0; i < 8; ++i) s += a[i];
+  if (s == 12345.678) out[0] = s;
+}
+
+__global__ void k_dadd(double* out, int iters) {
+  double a[8];
+  for (int i = 0; i < 8; ++i) a[i] = threadIdx.x * 1e-3 + i;
+  const double c = 1e-7;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) a[i] = a[i] + c;
   }
   double s = 0;
   for (int i = 0; i < 8; ++i) s += a[i];
@@ -53,6 +67,13 @@ int main() {
   cudaEventElapsedTime(&ms, e0, e1);
   const double flops = 2.0 * 8 * iters * double(sms) * 4 * 512;
   printf("{\"fp64_fma_tflops\": %.2f, ", flops / ms / 1e9);
+  k_dadd<<<sms * 4, 512>>>(d, iters);
+  cudaEventRecord(e0);
+  k_dadd<<<sms * 4, 512>>>(d, iters);
+  cudaEventRecord(e1);
+  cudaEventSynchronize(e1);
+  cudaEventElapsedTime(&ms, e0, e1);
+  printf("\"fp64_add_gops\": %.1f, ", 8.0 * iters * double(sms) * 4 * 512 / ms / 1e6);
   k_smem<<<sms * 4, 256>>>(d, iters);
   cudaEventRecord(e0);
   k_smem<<<sms * 4, 256>>>(d, iters);

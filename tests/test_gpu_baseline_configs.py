@@ -1,0 +1,149 @@
+"""Parity at the BASELINE.json configs themselves (north star: "GPU solutions matching the CPU
+oracle ... on all five configs"), GPU solve through the C-ABI against the UNMODIFIED reference
+(oracle/_ref, the reference headers compiled by oracle/Makefile; it travels to the GPU box as a
+prebuilt .so) on the same seeded inputs.  Not skippable: a missing oracle/_ref is a failure.
+
+  config 0  1D 1023 x 256, gamma 1.5, GMRES(20), tol 1e-10              full size
+  config 1  1D 8191 x 2048, gamma 1.2 and 1.8, GMRES(20), tol 1e-10     full size
+  config 2  2D 255^2 x 512, gamma 1.3/1.7, GMRES(20), tol 1e-10         full size
+  config 3  2D, gamma 1.5/1.5, GMRES(10), tol 1e-9: its exact parameters on a reduced grid (the full
+            8.6 GB-per-vector case needs ~190 GB of host RAM for the reference),
+            against the restart emulation on the reference's own gmres_right
+  config 4  PC apply + matvec sweep: the corner points 65535 x 256 and 1023 x 8192 (and 8191 x
+            8192) against the reference's apply_inverse / AllAtOnceOperator::apply
+
+Bars (BASELINE north star): iterations equal +-1, ||x - x_ref|| / ||x_ref|| <= 1e-10.  Config 1 at
+gamma 1.8 is below the conditioning floor of that bar for ANY faithful implementation: the C
+oracle (a second CPU restatement of the same algorithm) differs from the reference by ~3e-10 there.
+That case asserts the floor argument instead: ||x_gpu - x_ref|| <= 2 ||x_oracle - x_ref||, the
+same iteration count, and a true residual no worse than the reference's.
+"""
+import os
+
+import numpy as np
+import pytest
+
+import paper_2003_07020_b200 as fp
+from paper_2003_07020_b200 import problems
+
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+
+
+def rel(a, b):
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+@pytest.fixture(scope="module")
+def ref():
+    from oracle import oracle as O
+    assert O.Reference.available(), (
+        "oracle/_ref/libfracpint_ref.so is missing: build it with `make -C oracle` where "
+        "/root/reference exists (it is shipped prebuilt to the GPU box)")
+    r = O.Reference()
+    r.set_threads(os.cpu_count() or 1)
+    return r
+
+
+def gpu_problem(w):
+    if w.two_dim:
+        jac = fp.RieszJacobian2D(w.gamma[0], w.gamma[1], 1.0, 1.0, w.h, w.n)
+    else:
+        jac = fp.RieszJacobian1D(w.gamma[0], 1.0, w.h, w.n)
+    op = fp.AllAtOnceOperator(fp.TimeStencil(w.n_time), jac, w.dt)
+    plan = fp.build_plan(fp.PreconditionerKind.generalized(), w.n_time, w.dt, op)
+    return op, plan
+
+
+def ref_problem(backend, w):
+    if w.two_dim:
+        p = backend.problem_2d(w.gamma[0], w.gamma[1], 1.0, 1.0, w.h, w.n, w.n_time, w.dt)
+    else:
+        p = backend.problem_1d(w.gamma[0], 1.0, w.h, w.n, w.n_time, w.dt)
+    return p.build_plan()
+
+
+def solve_both(ref, w):
+    op, plan = gpu_problem(w)
+    b = problems.rhs(w)
+    res = fp.gmres_right(op, plan, b, fp.SolverConfig(tol=w.tol, max_iter=200, restart=w.restart))
+    pr = ref_problem(ref, w)
+    # the reference has no restart; configs 0-2 converge in fewer than `restart` steps, where
+    # GMRES(20) and the reference's unrestarted gmres_right are the same iteration
+    xr, rr = pr.gmres(b, w.tol, 200)
+    assert rr.iterations < w.restart
+    return res, xr, rr
+
+
+@pytest.mark.parametrize("cfg", [(0, None), (1, 1.2), (2, None)],
+                         ids=["cfg0_1d_1023x256", "cfg1_1d_8191x2048_g1.2", "cfg2_2d_255sq_x512"])
+def test_config_solve_vs_reference(ref, cfg):
+    w = problems.config(cfg[0], cfg[1])
+    res, xr, rr = solve_both(ref, w)
+    print(f"\n{w.name}: iterations gpu {res.report.iterations} ref {rr.iterations}; x vs ref {rel(res.x, xr):.3e}; "
+          f"TRR gpu {res.report.true_relative_residual:.3e} ref {rr.true_relative_residual:.3e}; ref {rr.seconds:.1f} s")
+    assert res.report.converged and rr.converged
+    assert abs(res.report.iterations - rr.iterations) <= 1, (res.report.iterations, rr.iterations)
+    assert rel(res.x, xr) <= 1e-10, rel(res.x, xr)
+    # residual histories agree to well within the straddle of tol (~10x)
+    h_gpu, h_ref = np.array(res.report.residual_history), np.array(rr.residual_history)
+    m = min(len(h_gpu), len(h_ref))
+    assert np.all(np.abs(np.log10(h_gpu[:m] / h_ref[:m])) < 0.05)
+
+
+def test_config1_gamma18_conditioning_floor(ref, oracle):
+    """Config 1, gamma 1.8: the PC apply amplifies rounding by the alpha^{-k/Nt} scalings (up to
+    1/alpha = 4096), so two faithful CPU implementations (the reference and the C oracle) already
+    differ by ~3e-10 in x.  The GPU must sit at that floor: within 2x of the oracle's distance."""
+    w = problems.config(1, 1.8)
+    res, xr, rr = solve_both(ref, w)
+    po = oracle.problem_1d(w.gamma[0], 1.0, w.h, w.n, w.n_time, w.dt).build_plan()
+    xo, ro = po.gmres(problems.rhs(w), w.tol, 200, restart=w.restart)
+    d_gpu, d_orc = rel(res.x, xr), rel(xo, xr)
+    print(f"\n{w.name}: iterations gpu {res.report.iterations} ref {rr.iterations} oracle {ro.iterations}; x: gpu-ref "
+          f"{d_gpu:.3e} oracle-ref {d_orc:.3e} gpu-oracle {rel(res.x, xo):.3e}; TRR gpu "
+          f"{res.report.true_relative_residual:.3e} ref {rr.true_relative_residual:.3e}")
+    assert res.report.converged and rr.converged and ro.converged
+    assert res.report.iterations == rr.iterations == ro.iterations
+    assert d_gpu <= 2.0 * d_orc, (d_gpu, d_orc)
+    assert d_orc > 1e-10  # the floor is real: the 1e-10 bar is below it for a second CPU code too
+    assert res.report.true_relative_residual <= max(rr.true_relative_residual, 1e-9)
+
+
+@pytest.mark.parametrize("n,nt", [(255, 1024), (511, 128)], ids=["255sq_x1024", "511sq_x128"])
+def test_config3_parameters_reduced_grid(ref, n, nt):
+    """Config 3's solver parameters exactly (gamma 1.5/1.5, kappa 1, GMRES(10), tol 1e-9, seeded
+    source and u0 as config 3) on the largest grids the reference finishes in about a minute on the
+    box, against GMRES(10) emulated on the reference's own gmres_right."""
+    w = problems.workload_2d(1.5, 1.5, n + 1, nt, tol=1e-9, restart=10)
+    op, plan = gpu_problem(w)
+    b = problems.rhs(w)
+    res = fp.gmres_right(op, plan, b, fp.SolverConfig(tol=w.tol, max_iter=200, restart=10))
+    xr, rr = ref_problem(ref, w).gmres_restarted(b, w.tol, 200, 10)
+    print(f"\n{w.name} GMRES(10): iterations gpu {res.report.iterations} (restarts {res.report.restarts}) ref "
+          f"{rr['iterations']} (restarts {rr['restarts']}); x vs ref {rel(res.x, xr):.3e}; TRR gpu "
+          f"{res.report.true_relative_residual:.3e} ref {rr['true_relative_residual']:.3e}; ref {rr['seconds']:.1f} s")
+    assert res.report.converged and rr["converged"]
+    assert abs(res.report.iterations - rr["iterations"]) <= 1, (res.report.iterations, rr["iterations"])
+    assert rel(res.x, xr) <= 1e-10, rel(res.x, xr)
+    assert res.report.true_relative_residual <= 1e-8
+
+
+@pytest.mark.parametrize("nx,nt", [(65535, 256), (1023, 8192), (8191, 8192)])
+def test_config4_corner_points(ref, nx, nt):
+    """Config 4 (gamma 1.5, kappa 1, alpha = dt/2): complex128 seeded Gaussian input = a batch of two
+    real vectors (Re, Im) since the operators are real-linear; PC apply and matvec
+    against the reference's apply_inverse / AllAtOnceOperator::apply."""
+    h, dt = 1.0 / (nx + 1), 1.0 / nt
+    op = fp.AllAtOnceOperator(fp.TimeStencil(nt), fp.RieszJacobian1D(1.5, 1.0, h, nx), dt)
+    plan = fp.build_plan(fp.PreconditionerKind.generalized(), nt, dt, op)
+    pr = ref.problem_1d(1.5, 1.0, h, nx, nt, dt).build_plan()
+    g = np.random.default_rng(20260819 + nx * 131 + nt)
+    z = g.standard_normal(nx * nt) + 1j * g.standard_normal(nx * nt)
+    for part in (z.real.copy(), z.imag.copy()):
+        print(f"\ncfg4 {nx}x{nt}: pc vs ref {rel(fp.apply_inverse(plan, part), pr.pc_apply(part)):.3e} "
+              f"matvec vs ref {rel(op.apply(part), pr.matvec(part)):.3e}")
+        # the host setup (tau spectrum, lambda, scalings) is the reference's to the bit
+        # (tests/test_abi.py), so what remains is FFT rounding amplified by the alpha^{-k/Nt}
+        # scalings (1/alpha = 2 Nt): 1e-12, and 1e-11 at Nt = 8192
+        assert rel(fp.apply_inverse(plan, part), pr.pc_apply(part)) <= (1e-11 if nt >= 8192 else 1e-12)
+        assert rel(op.apply(part), pr.matvec(part)) <= 1e-13
