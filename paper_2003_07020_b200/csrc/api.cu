@@ -46,8 +46,7 @@ bool debug_sync() {
   }();
   return on;
 }
-inline void ckl(cudaError_t e, const char* what) {  // kernel launch
-  g_launches.fetch_add(1, std::memory_order_relaxed);
+inline void ckl(cudaError_t e, const char* what) {  // kernel launch (counted by fpc::note_launch)
   ck(e, what);
   if (debug_sync()) ck(cudaDeviceSynchronize(), what);
 }
@@ -366,6 +365,10 @@ void upload(void* dst, const void* src, size_t bytes, cudaStream_t st) {
 }
 
 }  // namespace
+
+namespace fpc {
+void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+}  // namespace fpc
 
 extern "C" {
 

@@ -9,6 +9,10 @@ namespace fpc {
 // t < N, lives at tw_base + N.
 constexpr int kMaxLogTw = 17;
 
+// Kernel-launch counter (fpc_kernel_launches): every launch site of the library calls it once per
+// kernel it enqueues (a launcher may enqueue several, e.g. the 2D matvec's row and column passes).
+void note_launch();
+
 // Shared-memory carveout for a kernel: the smallest supported shared-memory capacity (sm_100: 0, 8,
 // 16, 32, 64, 100, 132, 164, 196, 228 KB per SM) that still holds the CTAs per SM the kernel's
 // register budget allows (threads: <=128 -> 4, <=256 -> 2, else 1), so the rest of the 256 KB
@@ -65,6 +69,12 @@ cudaError_t launch_tau_large(double2* Z, int n_space, int n_rows, const double2*
 cudaError_t launch_matvec_rows(const double* v, double* y, int len, int nrows, int rpt,
                                int sstride, int log_m, const double* eig_scaled,
                                const double2* tw_base, cudaStream_t st, int koff = 0);
+// the same on warp-owned register FFTs (kernels_warp.cu) for log_m = 8; cudaErrorNotSupported
+// otherwise.  Used by launch_matvec_rows unless the environment sets FPC_WARP=0 (A/B).
+cudaError_t launch_matvec_rows_warp(const double* v, double* y, int len, int nrows, int rpt, int sstride,
+                                    int log_m, const double* eig_scaled, const double2* tw_base,
+                                    cudaStream_t st, int koff);
+bool warp_kernels_enabled();
 // in-place orthonormal DST-I of n_rows contiguous complex rows of length n (n + 1 = 2^k)
 cudaError_t launch_dst_rows(double2* Z, int n, int n_rows, const double2* tw_base, cudaStream_t st);
 

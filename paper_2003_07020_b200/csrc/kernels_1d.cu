@@ -586,12 +586,14 @@ cudaError_t launch_matvec_rows(const double* v, double* y, int len, int nrows, i
                                int sstride, int log_m, const double* eig_scaled,
                                const double2* tw_base, cudaStream_t st, int koff) {
   cudaError_t err = cudaSuccess;
+  if (log_m == 8 && warp_kernels_enabled())
+    return launch_matvec_rows_warp(v, y, len, nrows, rpt, sstride, log_m, eig_scaled, tw_base, st, koff);
 #define CALL(LM)                                                                          \
   {                                                                                       \
     using G = Geo<LM, kTotMv, 16>;                                                        \
     if ((err = prep(k_matvec_1d<LM>, MvGeo<LM>::SMEM, Geo<LM, kTotMv, 16>::NT)) != cudaSuccess) return err;        \
     k_matvec_1d<LM><<<(nrows + G::B - 1) / G::B, G::NT, MvGeo<LM>::SMEM, st>>>(           \
-        v, y, len, nrows, rpt, sstride, koff, eig_scaled, tw_base);                       \
+        v, y, len, nrows, rpt, sstride, koff, eig_scaled, tw_base); note_launch();                       \
   }
   FPC_DISPATCH_LOGM(log_m, CALL)
 #undef CALL
@@ -628,7 +630,7 @@ cudaError_t launch_time_fwd(const double* v, double2* Z, int n_space, int n_time
     using G = Geo<LM, tot_t<LM>()>;                                                             \
     if ((err = prep(k_time_fwd<LM>, G::SMEM, G::NT)) != cudaSuccess) return err;                 \
     k_time_fwd<LM><<<(n_space + G::B - 1) / G::B, G::NT, G::SMEM, st>>>(                  \
-        v, Z, n_space, scale_fwd, s_in, tw_base);                                         \
+        v, Z, n_space, scale_fwd, s_in, tw_base); note_launch();                                         \
   }
   FPC_DISPATCH_LOGM(lm, CALL)
 #undef CALL
@@ -645,7 +647,7 @@ cudaError_t launch_time_inv(const double2* Z, double* z, int n_space, int n_time
     using G = Geo<LM, tot_t<LM>()>;                                                               \
     if ((err = prep(k_time_inv<LM>, G::SMEM, G::NT)) != cudaSuccess) return err;                   \
     k_time_inv<LM><<<(n_space + G::B - 1) / G::B, G::NT, G::SMEM, st>>>(Z, z, n_space,       \
-                                                                        scale_bwd, tw_base); \
+                                                                        scale_bwd, tw_base); note_launch(); \
   }
   FPC_DISPATCH_LOGM(lm, CALL)
 #undef CALL
@@ -662,7 +664,7 @@ cudaError_t launch_dst_rows(double2* Z, int n, int n_rows, const double2* tw_bas
     if ((err = prep(k_tau_solve_1d<LM, 0>, TG::SMEM, TG::G::NT)) != cudaSuccess) return err;     \
     const int grid = (n_rows + TG::G::B - 1) / TG::G::B;                                  \
     k_tau_solve_1d<LM, 0><<<grid, TG::G::NT, TG::SMEM, st>>>(Z, n_rows, nullptr, nullptr, \
-                                                                 0.0, tw_base);           \
+                                                                 0.0, tw_base); note_launch();           \
   }
   FPC_DISPATCH_LOGM(lm, CALL)
 #undef CALL
@@ -676,7 +678,7 @@ static cudaError_t tau1d(double2* Z, int n_rows, const double2* lambda, const do
   cudaError_t err = prep(k_tau_solve_1d<LM, MODE>, TG::SMEM, TG::G::NT);
   if (err != cudaSuccess) return err;
   const int grid = (n_rows + TG::G::B - 1) / TG::G::B;
-  k_tau_solve_1d<LM, MODE><<<grid, TG::G::NT, TG::SMEM, st>>>(Z, n_rows, lambda, sigma, dt, tw_base);
+  k_tau_solve_1d<LM, MODE><<<grid, TG::G::NT, TG::SMEM, st>>>(Z, n_rows, lambda, sigma, dt, tw_base); note_launch();
   return cudaGetLastError();
 }
 

@@ -258,7 +258,7 @@ cudaError_t launch_matvec_2d(const double* v, double* y, int n, int n_time, int 
     using G = ColGeo<LM>;                                                                 \
     if ((err = prep2(k_matvec_2d_cols<LM>, G::SMEM_MV, G::NT)) != cudaSuccess) return err;       \
     const int tiles = (n + G::C - 1) / G::C;                                              \
-    k_matvec_2d_cols<LM><<<n_time * tiles, G::NT, G::SMEM_MV, st>>>(v, y, n, eig_x_scaled, tw_base); \
+    k_matvec_2d_cols<LM><<<n_time * tiles, G::NT, G::SMEM_MV, st>>>(v, y, n, eig_x_scaled, tw_base); note_launch(); \
   }
   FPC_DISPATCH_2D(log_m, CALL)
 #undef CALL
@@ -273,7 +273,7 @@ static cudaError_t tau2d_cols(double2* Z, int n, int n_rows, const double2* lamb
   cudaError_t err = prep2(k_tau_2d_cols<LM, MODE>, G::SMEM, G::NT);
   if (err != cudaSuccess) return err;
   const int tiles = (n + G::C - 1) / G::C;
-  k_tau_2d_cols<LM, MODE><<<n_rows * tiles, G::NT, G::SMEM, st>>>(Z, n, lambda, sigma, dt, tw_base);
+  k_tau_2d_cols<LM, MODE><<<n_rows * tiles, G::NT, G::SMEM, st>>>(Z, n, lambda, sigma, dt, tw_base); note_launch();
   return cudaGetLastError();
 }
 

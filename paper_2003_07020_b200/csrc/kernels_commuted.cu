@@ -264,7 +264,7 @@ cudaError_t launch_dst_pairs(const double* v, double* out, int n_space, int n_ti
     using PG = PairGeo<LN>;                                                                   \
     if ((err = prep_c(k_dst_pairs<LN>, PG::SMEM, PG::G::NT)) != cudaSuccess) return err;                 \
     k_dst_pairs<LN><<<(n_pairs + PG::G::B - 1) / PG::G::B, PG::G::NT, PG::SMEM, st>>>(v, out, n_pairs, \
-                                                                                    scale, tw_base); \
+                                                                                    scale, tw_base); note_launch(); \
   }
   FPC_DISPATCH_C(ln, CALL)
 #undef CALL
@@ -285,7 +285,7 @@ cudaError_t launch_time_solve(const double* u, double* z, int n_space, int n_tim
     auto kern = forward ? k_time_solve<LM, 2> : k_time_solve<LM, 1>;                                  \
     if ((err = prep_c(kern, G::SMEM, G::NT)) != cudaSuccess) return err;                                     \
     kern<<<(n_space + G::B - 1) / G::B, G::NT, G::SMEM, st>>>(u, z, n_space, scale_fwd, scale_bwd, s_in, \
-                                                              lambda, sigma, dt, tw_base);            \
+                                                              lambda, sigma, dt, tw_base); note_launch();            \
   }
   FPC_DISPATCH_C(lm, CALL)
 #undef CALL

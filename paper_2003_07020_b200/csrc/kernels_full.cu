@@ -100,7 +100,7 @@ __global__ void __launch_bounds__(FGeo<LOGN>::NT)
 }
 
 cudaError_t launch_mirror_fill(double2* Z, int n_space, int n_time, cudaStream_t st) {
-  k_mirror_fill<<<148 * 4, 256, 0, st>>>(Z, n_space, n_time);
+  k_mirror_fill<<<148 * 4, 256, 0, st>>>(Z, n_space, n_time); note_launch();
   return cudaGetLastError();
 }
 
@@ -114,7 +114,7 @@ cudaError_t launch_time_inv_full(const double2* Z, double* z, int n_space, int n
   {                                                                                        \
     using G = FGeo<LN>;                                                                    \
     if ((err = prep_f(k_time_inv_full<LN>, G::SMEM)) != cudaSuccess) return err;           \
-    k_time_inv_full<LN><<<dots_grid(), G::NT, G::SMEM, st>>>(Z, z, n_space, scale_bwd, tw_base, partial); \
+    k_time_inv_full<LN><<<dots_grid(), G::NT, G::SMEM, st>>>(Z, z, n_space, scale_bwd, tw_base, partial); note_launch(); \
   }
   switch (l) {
     case 2: CALL(2); break;

@@ -104,13 +104,14 @@ cudaError_t launch_dots(const VecSet& vs, int nv, const double* w, size_t n, dou
 #define DOTS(NVV)                                                                             \
   case NVV:                                                                                   \
     if (with_norm)                                                                            \
-      k_dots<NVV, true><<<kDotsGrid, kDotsThreads, 0, st>>>(vs, w, n, partial, stride, col0); \
+      k_dots<NVV, true><<<kDotsGrid, kDotsThreads, 0, st>>>(vs, w, n, partial, stride, col0);  \
     else                                                                                      \
       k_dots<NVV, false><<<kDotsGrid, kDotsThreads, 0, st>>>(vs, w, n, partial, stride, col0); \
+    note_launch();                                                                            \
     break;
   switch (nv) {
     case 0:
-      k_dots<0, true><<<kDotsGrid, kDotsThreads, 0, st>>>(vs, w, n, partial, stride, col0);
+      k_dots<0, true><<<kDotsGrid, kDotsThreads, 0, st>>>(vs, w, n, partial, stride, col0); note_launch();
       break;
     DOTS(1) DOTS(2) DOTS(3) DOTS(4) DOTS(5) DOTS(6) DOTS(7) DOTS(8)
     default:
@@ -151,13 +152,13 @@ __global__ void __launch_bounds__(kDotsThreads)
 cudaError_t launch_reduce(const double* partial, int stride, int count, double* out,
                           bool accumulate, cudaStream_t st) {
   if (count <= 0) return cudaSuccess;
-  k_reduce<<<count, kDotsThreads, 0, st>>>(partial, stride, count, out, accumulate ? 1 : 0, 0);
+  k_reduce<<<count, kDotsThreads, 0, st>>>(partial, stride, count, out, accumulate ? 1 : 0, 0); note_launch();
   return cudaGetLastError();
 }
 
 cudaError_t launch_reduce_dots2(const double* partial, int stride, int nab, double* out, cudaStream_t st) {
   if (nab <= 0 || nab > kDots2B) return cudaErrorInvalidValue;
-  k_reduce<<<2 * nab + 3, kDotsThreads, 0, st>>>(partial, stride, 2 * nab + 3, out, 0, nab);
+  k_reduce<<<2 * nab + 3, kDotsThreads, 0, st>>>(partial, stride, 2 * nab + 3, out, 0, nab); note_launch();
   return cudaGetLastError();
 }
 
@@ -206,7 +207,7 @@ __global__ void __launch_bounds__(kDotsThreads)
 cudaError_t launch_update(const double* const* vptr, const double* scales, const double* coef,
                           int nv, double* w, size_t n, double* partial, cudaStream_t st) {
   if (nv > kMaxVecs) return cudaErrorInvalidValue;
-  k_update<<<kDotsGrid, kDotsThreads, 0, st>>>(vptr, scales, coef, nv, w, n, partial);
+  k_update<<<kDotsGrid, kDotsThreads, 0, st>>>(vptr, scales, coef, nv, w, n, partial); note_launch();
   return cudaGetLastError();
 }
 
@@ -232,7 +233,7 @@ __global__ void __launch_bounds__(kDotsThreads)
 cudaError_t launch_lincomb(const double* const* vptr, const double* scales, const double* coef,
                            int nv, double* u, size_t n, cudaStream_t st) {
   if (nv > kMaxVecs) return cudaErrorInvalidValue;
-  k_lincomb<<<kDotsGrid, kDotsThreads, 0, st>>>(vptr, scales, coef, nv, u, n);
+  k_lincomb<<<kDotsGrid, kDotsThreads, 0, st>>>(vptr, scales, coef, nv, u, n); note_launch();
   return cudaGetLastError();
 }
 
@@ -253,7 +254,7 @@ __global__ void __launch_bounds__(kDotsThreads)
 
 cudaError_t launch_resid_norm(const double* b, const double* y, size_t n, double* partial,
                               cudaStream_t st) {
-  k_resid_norm<<<kDotsGrid, kDotsThreads, 0, st>>>(b, y, n, partial);
+  k_resid_norm<<<kDotsGrid, kDotsThreads, 0, st>>>(b, y, n, partial); note_launch();
   return cudaGetLastError();
 }
 
@@ -263,7 +264,7 @@ __global__ void k_axpy(double a, const double* __restrict__ x, double* __restric
     y[e] += a * x[e];
 }
 cudaError_t launch_axpy(double a, const double* x, double* y, size_t n, cudaStream_t st) {
-  k_axpy<<<kDotsGrid, kDotsThreads, 0, st>>>(a, x, y, n);
+  k_axpy<<<kDotsGrid, kDotsThreads, 0, st>>>(a, x, y, n); note_launch();
   return cudaGetLastError();
 }
 
@@ -273,7 +274,7 @@ __global__ void k_rsub(const double* __restrict__ b, double* __restrict__ y, siz
     y[e] = b[e] - y[e];
 }
 cudaError_t launch_rsub(const double* b, double* y, size_t n, cudaStream_t st) {
-  k_rsub<<<kDotsGrid, kDotsThreads, 0, st>>>(b, y, n);
+  k_rsub<<<kDotsGrid, kDotsThreads, 0, st>>>(b, y, n); note_launch();
   return cudaGetLastError();
 }
 
@@ -343,7 +344,7 @@ cudaError_t launch_update_dots(const VecSetN& vs, int nv, const double* coef, do
                                double* partial, int stride, cudaStream_t st) {
   switch (nv) {
 #define UD(NVV) \
-  case NVV: k_update_dots<NVV><<<kDotsGrid, kDotsThreads, 0, st>>>(vs, coef, w, n, partial, stride); break;
+  case NVV: k_update_dots<NVV><<<kDotsGrid, kDotsThreads, 0, st>>>(vs, coef, w, n, partial, stride); note_launch(); break;
     UD(1) UD(2) UD(3) UD(4) UD(5) UD(6) UD(7) UD(8) UD(9) UD(10) UD(11) UD(12)
     UD(13) UD(14) UD(15) UD(16) UD(17) UD(18) UD(19) UD(20) UD(21) UD(22) UD(23) UD(24)
 #undef UD
@@ -417,18 +418,18 @@ __global__ void __launch_bounds__(kDotsThreads)
 
 cudaError_t launch_bicg_p(const double* r, const double* v, double* p, double beta, double omega,
                           size_t n, bool first, cudaStream_t st) {
-  k_bicg_p<<<kDotsGrid, kDotsThreads, 0, st>>>(r, v, p, beta, omega, n, first ? 1 : 0);
+  k_bicg_p<<<kDotsGrid, kDotsThreads, 0, st>>>(r, v, p, beta, omega, n, first ? 1 : 0); note_launch();
   return cudaGetLastError();
 }
 cudaError_t launch_bicg_s(double* r, double* rt, const double* v, const double* q,
                           const double* rho_denom, size_t n, double* partial, cudaStream_t st) {
-  k_bicg_s<<<kDotsGrid, kDotsThreads, 0, st>>>(r, rt, v, q, rho_denom, n, partial);
+  k_bicg_s<<<kDotsGrid, kDotsThreads, 0, st>>>(r, rt, v, q, rho_denom, n, partial); note_launch();
   return cudaGetLastError();
 }
 cudaError_t launch_bicg_x(double* x, const double* p, double* r, const double* t, double* rt,
                           const double* to, const double* rhat, double alpha, double omega,
                           size_t n, double* partial, cudaStream_t st) {
-  k_bicg_x<<<kDotsGrid, kDotsThreads, 0, st>>>(x, p, r, t, rt, to, rhat, alpha, omega, n, partial);
+  k_bicg_x<<<kDotsGrid, kDotsThreads, 0, st>>>(x, p, r, t, rt, to, rhat, alpha, omega, n, partial); note_launch();
   return cudaGetLastError();
 }
 
@@ -506,13 +507,13 @@ cudaError_t launch_dots2(const VecSet16& vs, int nv, const double* U, const doub
 #define D2(NVV)                                                                                      \
   case NVV:                                                                                          \
     if (extra)                                                                                       \
-      k_dots2<NVV, true><<<kDotsGrid, kDotsThreads, 0, st>>>(vs, U, W, n, partial, stride, col0);    \
+      { k_dots2<NVV, true><<<kDotsGrid, kDotsThreads, 0, st>>>(vs, U, W, n, partial, stride, col0); note_launch(); }    \
     else                                                                                             \
-      k_dots2<NVV, false><<<kDotsGrid, kDotsThreads, 0, st>>>(vs, U, W, n, partial, stride, col0);   \
+      { k_dots2<NVV, false><<<kDotsGrid, kDotsThreads, 0, st>>>(vs, U, W, n, partial, stride, col0); note_launch(); }   \
     break;
   switch (nv) {
     case 0:
-      k_dots2<0, true><<<kDotsGrid, kDotsThreads, 0, st>>>(vs, U, W, n, partial, stride, col0);
+      k_dots2<0, true><<<kDotsGrid, kDotsThreads, 0, st>>>(vs, U, W, n, partial, stride, col0); note_launch();
       break;
     D2(1) D2(2) D2(3) D2(4) D2(5) D2(6) D2(7) D2(8)
     D2(9) D2(10) D2(11) D2(12) D2(13) D2(14) D2(15) D2(16)
@@ -585,13 +586,13 @@ cudaError_t launch_update2(const Update2Args& a, int nv, bool first, bool norm, 
 #define U2(NVV)                                                                                        \
   case NVV:                                                                                            \
     if (first && norm)                                                                                 \
-      k_update2<NVV, true, true><<<kDotsGrid, kDotsThreads, 0, st>>>(a, U, W, n, partial);             \
+      { k_update2<NVV, true, true><<<kDotsGrid, kDotsThreads, 0, st>>>(a, U, W, n, partial); note_launch(); }             \
     else if (first)                                                                                    \
-      k_update2<NVV, true, false><<<kDotsGrid, kDotsThreads, 0, st>>>(a, U, W, n, partial);            \
+      { k_update2<NVV, true, false><<<kDotsGrid, kDotsThreads, 0, st>>>(a, U, W, n, partial); note_launch(); }            \
     else if (norm)                                                                                     \
-      k_update2<NVV, false, true><<<kDotsGrid, kDotsThreads, 0, st>>>(a, U, W, n, partial);            \
+      { k_update2<NVV, false, true><<<kDotsGrid, kDotsThreads, 0, st>>>(a, U, W, n, partial); note_launch(); }            \
     else                                                                                               \
-      k_update2<NVV, false, false><<<kDotsGrid, kDotsThreads, 0, st>>>(a, U, W, n, partial);           \
+      { k_update2<NVV, false, false><<<kDotsGrid, kDotsThreads, 0, st>>>(a, U, W, n, partial); note_launch(); }           \
     break;
   switch (nv) {
     U2(0) U2(1) U2(2) U2(3) U2(4) U2(5) U2(6) U2(7) U2(8) U2(9) U2(10) U2(11) U2(12)

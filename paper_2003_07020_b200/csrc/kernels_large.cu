@@ -306,6 +306,7 @@ cudaError_t launch_cl(K kernel, int C, int nclusters, cudaStream_t st, void** ar
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
+  note_launch();
   return cudaLaunchKernelExC(&cfg, reinterpret_cast<const void*>(kernel), args);
 }
 

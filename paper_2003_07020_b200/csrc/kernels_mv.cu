@@ -268,7 +268,7 @@ static cudaError_t launch_split(const double* v, double* y, int n_space, int n_t
   if (err != cudaSuccess) return err;
   err = cudaFuncSetAttribute(k_matvec_split<LOGM>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   if (err != cudaSuccess) return err;
-  k_matvec_split<LOGM><<<2 * n_time, H / 16, smem, st>>>(v, y, n_space, koff, eig_scaled, tw_base);
+  k_matvec_split<LOGM><<<2 * n_time, H / 16, smem, st>>>(v, y, n_space, koff, eig_scaled, tw_base); note_launch();
   return cudaGetLastError();
 }
 

@@ -92,13 +92,13 @@ cudaError_t launch_p2p_scatter(const double* src, int rows, int cols, int es, bo
   const size_t ntile = size_t(rows) * size_t((cols + kP2PChunk - 1) / kP2PChunk);
   const int grid = int(std::min<size_t>(ntile, size_t(148) * 8));
   if (es == 1 && split_cols)
-    k_p2p_scatter<1, true><<<grid, kP2PThreads, 0, st>>>(src, rows, cols, a, nranks, row_base, col_base);
+    { k_p2p_scatter<1, true><<<grid, kP2PThreads, 0, st>>>(src, rows, cols, a, nranks, row_base, col_base); note_launch(); }
   else if (es == 1)
-    k_p2p_scatter<1, false><<<grid, kP2PThreads, 0, st>>>(src, rows, cols, a, nranks, row_base, col_base);
+    { k_p2p_scatter<1, false><<<grid, kP2PThreads, 0, st>>>(src, rows, cols, a, nranks, row_base, col_base); note_launch(); }
   else if (split_cols)
-    k_p2p_scatter<2, true><<<grid, kP2PThreads, 0, st>>>(src, rows, cols, a, nranks, row_base, col_base);
+    { k_p2p_scatter<2, true><<<grid, kP2PThreads, 0, st>>>(src, rows, cols, a, nranks, row_base, col_base); note_launch(); }
   else
-    k_p2p_scatter<2, false><<<grid, kP2PThreads, 0, st>>>(src, rows, cols, a, nranks, row_base, col_base);
+    { k_p2p_scatter<2, false><<<grid, kP2PThreads, 0, st>>>(src, rows, cols, a, nranks, row_base, col_base); note_launch(); }
   return cudaGetLastError();
 }
 

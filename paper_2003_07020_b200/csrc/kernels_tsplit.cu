@@ -384,7 +384,7 @@ static cudaError_t fwd_split(const double* v, double2* Z, int ns, const double* 
   using G = SGeo<LOGH>;
   cudaError_t e = prep_s(k_time_fwd_split<LOGH>, G::SMEM, G::NT);
   if (e != cudaSuccess) return e;
-  k_time_fwd_split<LOGH><<<2 * ((ns + G::B - 1) / G::B), G::NT, G::SMEM, st>>>(v, Z, ns, sf, s_in, tw);
+  k_time_fwd_split<LOGH><<<2 * ((ns + G::B - 1) / G::B), G::NT, G::SMEM, st>>>(v, Z, ns, sf, s_in, tw); note_launch();
   return cudaGetLastError();
 }
 template <int LOGH>
@@ -393,7 +393,7 @@ static cudaError_t inv_split(const double2* Z, double* z, int ns, const double* 
   using G = SGeo<LOGH>;
   cudaError_t e = prep_s(k_time_inv_split<LOGH>, G::SMEM, G::NT);
   if (e != cudaSuccess) return e;
-  k_time_inv_split<LOGH><<<2 * ((ns + G::B - 1) / G::B), G::NT, G::SMEM, st>>>(Z, z, ns, sb, tw);
+  k_time_inv_split<LOGH><<<2 * ((ns + G::B - 1) / G::B), G::NT, G::SMEM, st>>>(Z, z, ns, sb, tw); note_launch();
   return cudaGetLastError();
 }
 template <int LOGH, int MODE>
@@ -404,7 +404,7 @@ static cudaError_t solve_split(const double* u, double* z, int ns, const double*
   cudaError_t e = prep_s(k_time_solve_split<LOGH, MODE>, G::SMEM, G::NT);
   if (e != cudaSuccess) return e;
   k_time_solve_split<LOGH, MODE><<<2 * ((ns + G::B - 1) / G::B), G::NT, G::SMEM, st>>>(u, z, ns, sf, sb, s_in, lam,
-                                                                                       sigma, dt, tw);
+                                                                                       sigma, dt, tw); note_launch();
   return cudaGetLastError();
 }
 

@@ -1,0 +1,151 @@
+// kernels_warp.cu -- lattice-row kernels on warp-owned register FFTs (warp_fft.cuh), sm_100a.
+//
+// Rows matvec (all_at_once.hpp:33-55 with toeplitz.hpp:41-57 along contiguous rows; the 2D
+// y-direction half of jacobian.hpp:84-87): one row of length ns <= M - 1 per group of R lanes,
+// real packing of the length-L = 2M circulant embedding into an M = R*R point complex transform,
+// so a 255-point row (config 2, L = 512) is one 256-point FFT per direction held in 16 lanes x 16
+// registers.  Per row: three global row reads (v_k and the BDF2 stencil's v_{k-1}, v_{k-2}, all
+// issued up front: 48 loads in flight per lane), forward FFT, the packed pointwise product with
+// the circulant eigenvalues (each bin with its mirror M - k, exchanged through the group's tile),
+// inverse FFT -- which returns each lane exactly the positions it loaded -- and one coalesced row
+// write.  No CTA barrier: a CTA is 8 independent warps.
+#include <cstdlib>
+
+#include "kernels.cuh"
+#include "warp_fft.cuh"
+
+namespace fpc {
+
+namespace {
+
+// Pointwise circulant product on the packed spectrum for bin k of an M-point packed transform
+// (the spectral loop of kernels_1d.cu k_matvec_1d, per bin): own = Z_k, mir = Z_{M-k}; returns the
+// packed inverse-transform input U_k.  eig = eig' (M + 1 values, -dt eig/(2L) pre-folded),
+// twL = tw_L (L = 2M).
+template <int M>
+__device__ __forceinline__ double2 packed_eig_product(double2 own, double2 mir, int k, const double* __restrict__ eig,
+                                                      const double2* __restrict__ twL) {
+  if (k == 0) {
+    const double y0 = __ldg(eig) * (2.0 * (own.x + own.y));
+    const double ym = __ldg(eig + M) * (2.0 * (own.x - own.y));
+    return make_double2(y0 + ym, y0 - ym);
+  }
+  const bool lo = k <= M / 2;
+  const int kk = lo ? k : M - k;
+  const double2 a = lo ? own : mir, bq = lo ? mir : own;
+  const double2 w = __ldg(twL + kk);  // e^{-2 pi i kk/L}
+  const double ek = __ldg(eig + kk), em = __ldg(eig + M - kk);
+  const double2 P = cadd(a, cconj(bq)), Q = csub(a, cconj(bq));
+  const double2 iwQ = mul_si<1>(cmul(w, Q));
+  const double2 Yk = cscale(csub(P, iwQ), ek);
+  const double2 Ym = cscale(cconj(cadd(P, iwQ)), em);
+  const double2 A = cadd(Yk, cconj(Ym)), D = csub(Yk, cconj(Ym));
+  return lo ? cadd(A, mul_si<1>(cmul(D, cconj(w)))) : cadd(cconj(A), mul_si<1>(cmul(cconj(D), w)));
+}
+
+// BDF2 stencil part (time_stencil.hpp:16-26, same association as all_at_once.hpp:44-53)
+__device__ __forceinline__ double bdf2(int k, double x0, double x1, double x2) {
+  if (k == 0) return x0;
+  if (k == 1) return 1.5 * x0 + -2.0 * x1;
+  return 1.5 * x0 + -2.0 * x1 + 0.5 * x2;
+}
+
+constexpr int kWarpsPerCta = 8;
+
+}  // namespace
+
+bool warp_kernels_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("FPC_WARP");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+template <int R>
+__global__ void __launch_bounds__(32 * kWarpsPerCta, 2)
+    k_mv_rows_warp(const double* __restrict__ v, double* __restrict__ y, int ns, int nrows, int rpt,
+                   int sstride, int koff, const double* __restrict__ eig, const double2* __restrict__ twb) {
+  constexpr int M = R * R, L = 2 * M, G = 32 / R, H = R / 2;
+  constexpr int LD = WarpFftTile<R>::LD;
+  extern __shared__ double2 wsm[];
+  const int lane = int(threadIdx.x) & 31;
+  const int t = lane & (R - 1);
+  const int grp = (int(threadIdx.x) >> 5) * G + lane / R;
+  const int row = int(blockIdx.x) * (kWarpsPerCta * G) + grp;
+  const bool valid = row < nrows;
+  const int rr = valid ? row : nrows - 1;  // out-of-range groups compute a duplicate, store nothing
+  const int k = rr / rpt + koff;
+  const double* vr = v + size_t(rr) * ns;
+  double2* xs = wsm + grp * WarpFftTile<R>::SIZE;
+
+  // packed slot m = t + R r holds (x_{2m}, x_{2m+1}); slots with 2m >= ns are the zero padding of
+  // the embedding (all of r >= R/2, since ns <= M - 1)
+  double2 z[R];
+  double x1[2 * H], x2[2 * H];
+#pragma unroll
+  for (int r = 0; r < H; ++r) {
+    const int i0 = 2 * (t + R * r);
+    const bool ok0 = i0 < ns, ok1 = i0 + 1 < ns;
+    z[r] = make_double2(ok0 ? vr[i0] : 0.0, ok1 ? vr[i0 + 1] : 0.0);
+    x1[2 * r] = (ok0 && k >= 1) ? vr[i0 - sstride] : 0.0;
+    x1[2 * r + 1] = (ok1 && k >= 1) ? vr[i0 + 1 - sstride] : 0.0;
+    x2[2 * r] = (ok0 && k >= 2) ? vr[i0 - 2 * size_t(sstride)] : 0.0;
+    x2[2 * r + 1] = (ok1 && k >= 2) ? vr[i0 + 1 - 2 * size_t(sstride)] : 0.0;
+  }
+#pragma unroll
+  for (int r = H; r < R; ++r) z[r] = make_double2(0.0, 0.0);
+  // stencil part, formed now so the two earlier rows' registers are free during the transforms
+  double c[2 * H];
+#pragma unroll
+  for (int r = 0; r < H; ++r) {
+    c[2 * r] = bdf2(k, z[r].x, x1[2 * r], x2[2 * r]);
+    c[2 * r + 1] = bdf2(k, z[r].y, x1[2 * r + 1], x2[2 * r + 1]);
+  }
+
+  warp_fft_sq<R, -1>(z, xs, t, twb);  // lane t now holds Z_{t + R p}
+
+  // spectral product: each bin with its mirror M - k (lane (R - t) mod R, register R-1-p; or
+  // this lane's register (R - p) mod R when t = 0), exchanged through the tile
+#pragma unroll
+  for (int p = 0; p < R; ++p) xs[p * LD + t] = z[p];
+  __syncwarp();
+  const int tm = (R - t) & (R - 1);
+#pragma unroll
+  for (int p = 0; p < R; ++p) {
+    const int pm = t == 0 ? ((R - p) & (R - 1)) : (R - 1 - p);
+    const double2 mir = xs[pm * LD + tm];
+    z[p] = packed_eig_product<M>(z[p], mir, t + R * p, eig, twb + L);
+  }
+  __syncwarp();
+
+  warp_fft_sq<R, 1>(z, xs, t, twb);  // lane t holds the packed inverse at slots t + R r again
+
+  if (valid) {
+    double* yr = y + size_t(row) * ns;
+#pragma unroll
+    for (int r = 0; r < H; ++r) {
+      const int i0 = 2 * (t + R * r);
+      if (i0 < ns) yr[i0] = c[2 * r] + z[r].x;
+      if (i0 + 1 < ns) yr[i0 + 1] = c[2 * r + 1] + z[r].y;
+    }
+  }
+}
+
+// Rows matvec on warp FFTs for M = R*R (R = 16: M = 256, rows of 129..255 points).  Returns
+// cudaErrorNotSupported for other sizes (the caller keeps the CTA-level kernel).
+cudaError_t launch_matvec_rows_warp(const double* v, double* y, int len, int nrows, int rpt, int sstride,
+                                    int log_m, const double* eig_scaled, const double2* tw_base,
+                                    cudaStream_t st, int koff) {
+  if (log_m != 8) return cudaErrorNotSupported;
+  constexpr int R = 16, G = 32 / R;
+  const int rows_per_cta = kWarpsPerCta * G;
+  const size_t smem = size_t(kWarpsPerCta) * G * WarpFftTile<R>::SIZE * sizeof(double2);
+  cudaError_t e = cudaFuncSetAttribute(k_mv_rows_warp<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  if (e != cudaSuccess) return e;
+  k_mv_rows_warp<R><<<(nrows + rows_per_cta - 1) / rows_per_cta, 32 * kWarpsPerCta, smem, st>>>(
+      v, y, len, nrows, rpt, sstride, koff, eig_scaled, tw_base); note_launch();
+  return cudaGetLastError();
+}
+
+}  // namespace fpc
