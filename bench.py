@@ -211,6 +211,16 @@ def run_sharded(args, w, rank, world, local):
                          ordering=fp.Ordering[args.ordering])
     s = ShardedSolver(w.n_time, w.n_space, CudaShardKernels(op, plan), ordering=args.ordering,
                       transport=args.transport)
+    try:
+        _run_sharded_timed(args, w, rank, world, local, s, dev, fp, problems)
+    finally:
+        s.close()
+    dist.destroy_process_group()
+
+
+def _run_sharded_timed(args, w, rank, world, local, s, dev, fp, problems):
+    import torch
+    import torch.distributed as dist
     b_host = problems.rhs(w)
     lo, hi = s.koff * w.n_space, (s.koff + s.nt_loc) * w.n_space
     b_loc_host = np.ascontiguousarray(b_host[lo:hi])
@@ -257,7 +267,6 @@ def run_sharded(args, w, rank, world, local):
             "e2e": {"value": 1.0 / te, "unit": UNIT, "h2d_bytes_per_step": 8 * (hi - lo),
                     "d2h_bytes_per_step": 8 * (hi - lo)},
             "gpu_launches": launches, "clocks": clk.summary(), "cpu_baseline": None}))
-    dist.destroy_process_group()
 
 
 # ------------------------------------------------------------------------------------ config-4 sweep

@@ -22,6 +22,12 @@
  * the call returns when done) or FPC_DEVICE (device pointers on the context's device; the work is
  * stream-ordered on the context stream, 16-byte aligned pointers required).
  *
+ * Threading (the reference's const applies are reentrant, toeplitz.hpp:14-18): every call may come
+ * from any host thread.  Calls on one operator / plan are serialised by the library (they share the
+ * plan's device spectrum scratch and the operator's host staging buffers) and all device work of a
+ * context is ordered on the context's stream, so concurrent calls are safe and run one after the
+ * other.  For concurrent device work use one context (stream) and one plan per worker.
+ *
  * Status codes mirror the reference's exceptions: FPC_INVALID_ARGUMENT <-> std::invalid_argument,
  * FPC_RUNTIME_ERROR <-> std::runtime_error (numerical singularity), FPC_CUDA_ERROR (device failure),
  * FPC_UNSUPPORTED (a size the B200 kernels do not cover; never a silent CPU fallback).
@@ -122,6 +128,8 @@ int fpc_plan_destroy(fpc_plan_t plan);
 int fpc_plan_info(fpc_plan_t plan, double* alpha, double* min_shift_margin, int* solve_count,
                   int* n_warnings);
 int fpc_plan_lambda(fpc_plan_t plan, double* lambda_interleaved);
+/* AlphaCirculantPlan::scale_fwd / scale_bwd (alpha^{+-k/Nt}, n_time values each) */
+int fpc_plan_scales(fpc_plan_t plan, double* scale_fwd, double* scale_bwd);
 /* half-sweep factor ordering of fpc_pc_apply / fpc_pc_forward / the Krylov solvers (the same
  * operator up to rounding; FPC_UNSUPPORTED for 2D or n_space + 1 > 8192 when commuted) */
 int fpc_plan_set_ordering(fpc_plan_t plan, int ordering);
@@ -131,6 +139,18 @@ int fpc_pc_forward(fpc_plan_t plan, const double* v, double* out, int where);
 /* right-preconditioned GMRES on the plan's operator, x0 = 0 */
 int fpc_gmres(fpc_plan_t plan, const double* b, double* x, const fpc_solver_config* cfg,
               fpc_report* report, double* history, int history_cap, int where);
+
+/* gmres_right(n, apply_a, apply_pinv, b, cfg) for arbitrary host callables (krylov.hpp:83-85, the
+ * reference's generic plugin interface): out = op(in) on host arrays of n doubles, return 0 on
+ * success (anything else aborts the solve with FPC_RUNTIME_ERROR).  b and x are host arrays.  The
+ * Krylov basis lives on the context's device (the library's vector kernels run the Gram-Schmidt
+ * with the reference's conditional re-orthogonalisation); each step calls apply_pinv then apply_a
+ * once.  cfg->restart = m > 0: GMRES(m); cfg->sweep is ignored. */
+typedef int (*fpc_apply_fn)(const double* in, double* out, size_t n, void* user);
+int fpc_gmres_callbacks(fpc_context_t ctx, size_t n, fpc_apply_fn apply_a, void* a_user,
+                        fpc_apply_fn apply_pinv, void* p_user, const double* b, double* x,
+                        const fpc_solver_config* cfg, fpc_report* report, double* history,
+                        int history_cap);
 
 /* left-preconditioned BiCGSTAB on the plan's operator, x0 = 0 (cfg->restart is ignored) */
 int fpc_bicgstab(fpc_plan_t plan, const double* b, double* x, const fpc_solver_config* cfg,

@@ -10,6 +10,9 @@
 //   AlphaCirculantPlan, build_plan   alpha_circulant.hpp:52-126 (fpc_plan_create)
 //   apply_inverse / apply_forward    alpha_circulant.hpp:206-215 (fpc_pc_apply / fpc_pc_forward)
 //   SolverConfig/SolveReport/KrylovResult, gmres_right   krylov.hpp:25-42, 83-192 (fpc_gmres)
+//   gmres_right(n, apply_a, apply_pinv, b, cfg) for any host callables  krylov.hpp:83-85
+//                                    (fpc_gmres_callbacks: basis on the device)
+//   TauOperator                      tau.hpp:20-26 (AlphaCirculantPlan::tau)
 // plus SolverConfig::restart (GMRES(m); 0 = the reference's unrestarted GMRES).
 //
 // Two ways to use it:
@@ -26,10 +29,12 @@
 #include <cmath>
 #include <complex>
 #include <cstddef>
+#include <exception>
 #include <memory>
 #include <span>
 #include <stdexcept>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 namespace fracpint::b200 {
@@ -167,10 +172,28 @@ class PreconditionerKind {
 
 enum class InnerSweep { half = FPC_SWEEP_HALF, full = FPC_SWEEP_FULL };
 
+// TauOperator (tau.hpp:20-26): the spectrum of tau(A); 2D: sigma[ix*ny + iy], nx = ny = n.
+struct TauOperator {
+  int n = 0;
+  std::vector<double> sigma;
+  int nx = 0;
+  int ny = 0;
+  bool two_dim() const { return nx > 0; }
+};
+
+// AlphaCirculantPlan (alpha_circulant.hpp:52-67): the reference's fields, filled from the
+// library's plan (the device-resident factors live behind `h`).
 struct AlphaCirculantPlan {
-  int n_time = 0, n_space = 0, solve_count = 0;
-  double dt = 0.0, alpha = 0.0, min_shift_margin = 0.0;
-  std::vector<std::complex<double>> lambda;
+  int n_time = 0;
+  int n_space = 0;
+  double dt = 0.0;
+  double alpha = 0.0;
+  std::vector<std::complex<double>> lambda;  // eigenvalues of C_alpha
+  std::vector<double> scale_fwd;             // alpha^{+k/N_t}
+  std::vector<double> scale_bwd;             // alpha^{-k/N_t}
+  int solve_count = 0;                       // floor(N_t/2)+1
+  TauOperator tau;                           // spectrum of tau(A)
+  double min_shift_margin = 0.0;
   std::vector<std::string> warnings;
   std::shared_ptr<fpc_plan_s> h;
   int mirror_index(int n) const { return n_time - n + 2; }
@@ -193,6 +216,13 @@ AlphaCirculantPlan build_plan(const PreconditionerKind& kind, int n_time, double
   plan.dt = dt;
   plan.lambda.resize(std::size_t(n_time));
   detail::check(fpc_plan_lambda(h, reinterpret_cast<double*>(plan.lambda.data())));
+  plan.scale_fwd.resize(std::size_t(n_time));
+  plan.scale_bwd.resize(std::size_t(n_time));
+  detail::check(fpc_plan_scales(h, plan.scale_fwd.data(), plan.scale_bwd.data()));
+  plan.tau.n = op.n_space();
+  plan.tau.sigma.resize(std::size_t(op.n_space()));
+  detail::check(fpc_problem_tau_sigma(op.handle(), plan.tau.sigma.data()));
+  if constexpr (std::is_same_v<Jacobian, RieszJacobian2D>) plan.tau.nx = plan.tau.ny = op.jacobian().n;
   if (nw)
     plan.warnings.push_back(
         "alpha below 1e-8: the diagonalization scalings span a wide dynamic range and may amplify "
@@ -272,6 +302,51 @@ KrylovResult bicgstab_left(const AllAtOnceOperator<Jacobian>& op, const AlphaCir
   std::vector<double> hist(2 * std::size_t(std::max(cfg.max_iter, 1)) + 2);
   detail::check(fpc_bicgstab(plan.handle(), b.data(), r.x.data(), &c, &rep, hist.data(),
                              int(hist.size()), FPC_HOST));
+  detail::fill_report(r.report, rep, hist);
+  return r;
+}
+
+// gmres_right(n, apply_a, apply_pinv, b, cfg) for ANY host callables with the reference's plugin
+// signature void(std::span<const double>, std::span<double>) (krylov.hpp:83-85): the reference's
+// iteration with the Krylov basis on the context's device (fpc_gmres_callbacks).  An exception
+// thrown by a callable aborts the solve and is rethrown here, as in the reference.
+namespace detail {
+template <class F>
+struct CallableSlot {
+  F* f;
+  std::exception_ptr err;
+  static int call(const double* in, double* out, std::size_t n, void* user) {
+    auto* self = static_cast<CallableSlot*>(user);
+    try {
+      (*self->f)(std::span<const double>(in, n), std::span<double>(out, n));
+      return 0;
+    } catch (...) {
+      self->err = std::current_exception();
+      return 1;
+    }
+  }
+};
+}  // namespace detail
+
+template <class OpA, class OpP>
+KrylovResult gmres_right(std::size_t n, OpA&& apply_a, OpP&& apply_pinv, std::span<const double> b,
+                         const SolverConfig& cfg = {}, Context& ctx = Context::default_context()) {
+  if (b.size() != n) throw std::invalid_argument("gmres_right: size mismatch");
+  using A = std::remove_reference_t<OpA>;
+  using P = std::remove_reference_t<OpP>;
+  detail::CallableSlot<A> sa{&apply_a, nullptr};
+  detail::CallableSlot<P> sp{&apply_pinv, nullptr};
+  KrylovResult r;
+  r.x.assign(n, 0.0);
+  fpc_solver_config c{cfg.tol, cfg.max_iter, cfg.restart, FPC_SWEEP_HALF};
+  fpc_report rep{};
+  std::vector<double> hist(std::size_t(std::max(cfg.max_iter, 1)) + 1);
+  const int rc = fpc_gmres_callbacks(ctx.handle(), n, &detail::CallableSlot<A>::call, &sa,
+                                     &detail::CallableSlot<P>::call, &sp, b.data(), r.x.data(), &c, &rep,
+                                     hist.data(), int(hist.size()));
+  if (sa.err) std::rethrow_exception(sa.err);
+  if (sp.err) std::rethrow_exception(sp.err);
+  detail::check(rc);
   detail::fill_report(r.report, rep, hist);
   return r;
 }

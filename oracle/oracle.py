@@ -65,6 +65,9 @@ class _ORep(C.Structure):
 
 _lib_cache: dict = {}
 
+# int (*)(const double* in, double* out, size_t n, void* user)
+REF_APPLY_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p)
+
 
 def _load(path: str, kind: str):
     if path in _lib_cache:
@@ -123,6 +126,9 @@ def _load(path: str, kind: str):
         lib.ref_tau_sigma.argtypes = [C.c_void_p, _dp]
         lib.ref_gmres.argtypes = [C.c_void_p, _dp, _dp, C.c_double, C.c_int, C.POINTER(C.c_int),
                                   C.POINTER(C.c_int), _dp, _dp, _dp, _dp, C.c_int, C.POINTER(C.c_int)]
+        lib.ref_gmres_callbacks.argtypes = [C.c_size_t, REF_APPLY_FN, C.c_void_p, REF_APPLY_FN, C.c_void_p, _dp, _dp,
+                                            C.c_double, C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int), _dp, _dp,
+                                            C.c_int, C.POINTER(C.c_int)]
         lib.ref_gmres_restart.argtypes = [C.c_void_p, _dp, _dp, C.c_double, C.c_int, C.c_int, C.POINTER(C.c_int),
                                           C.POINTER(C.c_int), C.POINTER(C.c_int), _dp, _dp]
         lib.ref_bicgstab.argtypes = [C.c_void_p, _dp, _dp, C.c_double, C.c_int, C.POINTER(C.c_int),
@@ -353,6 +359,37 @@ class Reference(_Backend):
                                            _ptr(fin)))
         return {"iterations": float(it[0]), "converged": bool(conv.value), "err_inf": float(err[0]),
                 "rhs": rhs, "exact": ex, "final": fin}
+
+    def gmres_callables(self, n, apply_a, apply_pinv, b, tol=1e-9, max_iter=200):
+        """The reference's own gmres_right (krylov.hpp:83-192) driving Python callables
+        apply(v, out) (e.g. the B200 library's operators).  Returns (x, dict(...))."""
+        errors = []
+
+        def wrap(fn):
+            def cb(pin, pout, nn, _u):
+                try:
+                    a = np.ctypeslib.as_array(C.cast(pin, C.POINTER(C.c_double)), shape=(nn,))
+                    o = np.ctypeslib.as_array(C.cast(pout, C.POINTER(C.c_double)), shape=(nn,))
+                    fn(a, o)
+                    return 0
+                except BaseException as e:  # noqa: BLE001
+                    errors.append(e)
+                    return 1
+            return REF_APPLY_FN(cb)
+
+        ca, cp = wrap(apply_a), wrap(apply_pinv)
+        b = np.ascontiguousarray(b, dtype=np.float64)
+        x = np.empty_like(b)
+        conv, it, hl = C.c_int(), C.c_int(), C.c_int()
+        tr = np.zeros(1)
+        hist = np.zeros(max_iter + 1)
+        rc = self.lib.ref_gmres_callbacks(n, ca, None, cp, None, _ptr(b), _ptr(x), tol, max_iter, C.byref(conv),
+                                          C.byref(it), _ptr(tr), _ptr(hist), max_iter + 1, C.byref(hl))
+        if errors:
+            raise errors[0]
+        self._chk(rc)
+        return x, {"converged": bool(conv.value), "iterations": it.value, "true_relative_residual": float(tr[0]),
+                   "residual_history": list(hist[:min(hl.value, max_iter + 1)])}
 
     def problem_1d(self, gamma, kappa, h, n, nt, dt):
         hd = self.lib.ref_problem_1d(gamma, kappa, h, n, nt, dt)

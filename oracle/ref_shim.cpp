@@ -343,4 +343,32 @@ int ref_gmres_restart(void* hp, const double* b, double* x, double tol, int max_
   });
 }
 
+// The reference's own generic gmres_right (krylov.hpp:83-192) driving arbitrary C callbacks
+// (the plugin interface krylov.hpp:83-85): out = op(in), return 0 on success.  Used to drive the
+// B200 library's fpc_matvec / fpc_pc_apply from the unmodified reference Krylov layer.
+typedef int (*ref_apply_fn)(const double* in, double* out, std::size_t n, void* user);
+int ref_gmres_callbacks(std::size_t n, ref_apply_fn a, void* ua, ref_apply_fn pinv, void* up, const double* b,
+                        double* x, double tol, int max_iter, int* converged, int* iterations, double* true_rel,
+                        double* history, int history_cap, int* history_len) {
+  return guarded([&] {
+    fracpint::SolverConfig cfg;
+    cfg.tol = tol;
+    cfg.max_iter = max_iter;
+    auto apply_a = [&](std::span<const double> in, std::span<double> out) {
+      if (a(in.data(), out.data(), in.size(), ua) != 0) throw std::runtime_error("apply_a callback failed");
+    };
+    auto apply_pinv = [&](std::span<const double> in, std::span<double> out) {
+      if (pinv(in.data(), out.data(), in.size(), up) != 0) throw std::runtime_error("apply_pinv callback failed");
+    };
+    fracpint::KrylovResult r = fracpint::gmres_right(n, apply_a, apply_pinv, {b, n}, cfg);
+    std::copy(r.x.begin(), r.x.end(), x);
+    *converged = r.report.converged ? 1 : 0;
+    *iterations = static_cast<int>(r.report.iterations);
+    *true_rel = r.report.true_relative_residual;
+    const int h = static_cast<int>(r.report.residual_history.size());
+    *history_len = h;
+    for (int i = 0; i < h && i < history_cap; ++i) history[i] = r.report.residual_history[i];
+  });
+}
+
 }  // extern "C"

@@ -7,11 +7,11 @@ from .solver import (AllAtOnceOperator, AlphaCirculantPlan, Context, InnerSweep,
                      PreconditionerKind, RieszJacobian1D, RieszJacobian2D, SolveReport, SolverConfig,
                      TimeStencil, apply_forward, apply_inverse, assemble_rhs, bicgstab_left, build_plan,
                      centred_weights, tau_spectrum, circulant_eigenvalues, alpha_circulant_eigenvalues,
-                     gmres_right, kernel_launches, KernelProfile)
+                     gmres_right, gmres_right_callables, kernel_launches, KernelProfile)
 
 __all__ = [
     "AllAtOnceOperator", "AlphaCirculantPlan", "Context", "InnerSweep", "KrylovResult", "Ordering",
     "PreconditionerKind", "RieszJacobian1D", "RieszJacobian2D", "SolveReport", "SolverConfig",
     "TimeStencil", "apply_forward", "apply_inverse", "assemble_rhs", "bicgstab_left", "build_plan", "centred_weights", "tau_spectrum", "circulant_eigenvalues", "alpha_circulant_eigenvalues",
-    "gmres_right", "kernel_launches", "KernelProfile",
+    "gmres_right", "gmres_right_callables", "kernel_launches", "KernelProfile",
 ]

@@ -29,7 +29,7 @@ EXPORTS = [
     "fpc_shard_time_inv", "fpc_shard_dots", "fpc_shard_update", "fpc_shard_lincomb",
     "fpc_shard_dst_levels", "fpc_shard_time_solve", "fpc_ipc_get_handle", "fpc_ipc_open", "fpc_ipc_close",
     "fpc_shard_scatter_p2p", "fpc_centred_weights", "fpc_tau_spectrum", "fpc_circulant_eigenvalues",
-    "fpc_alpha_circulant_eigenvalues",
+    "fpc_alpha_circulant_eigenvalues", "fpc_plan_scales", "fpc_gmres_callbacks",
 ]
 
 
@@ -45,6 +45,9 @@ class ReportC(C.Structure):
 
 
 _lib = None
+
+# int (*)(const double* in, double* out, size_t n, void* user)  -- fpc_apply_fn
+APPLY_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p)
 
 
 def load():
@@ -104,6 +107,9 @@ def load():
     lib.fpc_tau_spectrum.argtypes = [dp, C.c_int, dp]
     lib.fpc_circulant_eigenvalues.argtypes = [dp, C.c_int, dp]
     lib.fpc_alpha_circulant_eigenvalues.argtypes = [d, C.c_int, dp]
+    lib.fpc_plan_scales.argtypes = [vp, dp, dp]
+    lib.fpc_gmres_callbacks.argtypes = [vp, C.c_size_t, APPLY_FN, vp, APPLY_FN, vp, dp, dp,
+                                        C.POINTER(SolverConfigC), C.POINTER(ReportC), dp, C.c_int]
     _lib = lib
     return lib
 

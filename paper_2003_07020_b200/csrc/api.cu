@@ -9,6 +9,7 @@
 #include <algorithm>
 #include <atomic>
 #include <chrono>
+#include <mutex>
 #include <cmath>
 #include <complex>
 #include <cstdio>
@@ -306,6 +307,7 @@ struct DeviceGuard {
 // =================================================================================== problem
 struct fpc_problem_s {
   int refs = 1;
+  std::recursive_mutex mu;  // host calls on one operator (shared staging buffers) are serialised
   fpc_context_s* ctx = nullptr;
   int two_dim = 0;
   int n = 0;   // 1D: n_space; 2D: n per dim
@@ -325,8 +327,10 @@ struct fpc_problem_s {
 
 struct fpc_plan_s {
   fpc_problem_s* prob = nullptr;
+  std::recursive_mutex mu;  // host calls on one plan (shared spectrum scratch, GMRES workspace) are serialised
   double alpha = 0.0;
   std::vector<cplx> lambda;
+  std::vector<double> scale_fwd, scale_bwd;  // alpha^{+-k/Nt} (alpha_circulant.hpp:102-106)
   int solve_count = 0;
   double min_shift_margin = 0.0;
   int n_warnings = 0;
@@ -699,6 +703,7 @@ static void check_dev_aligned(const void* ptr, const char* what) {
 int fpc_matvec(fpc_problem_t p, const double* v, double* out, int where) {
   if (!p) return set_err(FPC_INVALID_ARGUMENT, "null problem");
   return guarded([&] {
+    std::lock_guard<std::recursive_mutex> lk_prob(p->mu);
     check_ptr(v, "fpc_matvec");
     check_ptr(out, "fpc_matvec");
     DeviceGuard g(p->ctx->device);
@@ -781,6 +786,8 @@ int fpc_plan_create(fpc_problem_t p, double alpha_in, fpc_plan_t* out) {
     ck(cudaMemcpy(pl->d_sb, sb.data(), sb.size() * 8, cudaMemcpyHostToDevice), "sb");
     ck(cudaMemcpy(pl->d_lambda, pl->lambda.data(), size_t(nt) * 16, cudaMemcpyHostToDevice), "lambda");
     ck(cudaMemcpy(pl->d_sigma, p->sigma.data(), p->sigma.size() * 8, cudaMemcpyHostToDevice), "sigma");
+    pl->scale_fwd = std::move(sf);
+    pl->scale_bwd = std::move(sb);
     ++p->refs;
     *out = pl;
   });
@@ -807,6 +814,8 @@ int fpc_plan_destroy(fpc_plan_t pl) {
 int fpc_plan_set_ordering(fpc_plan_t pl, int ordering) {
   if (!pl) return set_err(FPC_INVALID_ARGUMENT, "null plan");
   return guarded([&] {
+    std::lock_guard<std::recursive_mutex> lk_plan(pl->mu);
+    std::lock_guard<std::recursive_mutex> lk_prob(pl->prob->mu);
     if (ordering != FPC_ORDER_REFERENCE && ordering != FPC_ORDER_COMMUTED)
       throw InvalidArg{"fpc_plan_set_ordering: bad ordering"};
     const fpc_problem_s* p = pl->prob;
@@ -822,6 +831,13 @@ int fpc_plan_info(fpc_plan_t pl, double* alpha, double* margin, int* solve_count
   if (margin) *margin = pl->min_shift_margin;
   if (solve_count) *solve_count = pl->solve_count;
   if (n_warn) *n_warn = pl->n_warnings;
+  return FPC_OK;
+}
+
+int fpc_plan_scales(fpc_plan_t pl, double* scale_fwd, double* scale_bwd) {
+  if (!pl || !scale_fwd || !scale_bwd) return set_err(FPC_INVALID_ARGUMENT, "null argument");
+  std::copy(pl->scale_fwd.begin(), pl->scale_fwd.end(), scale_fwd);
+  std::copy(pl->scale_bwd.begin(), pl->scale_bwd.end(), scale_bwd);
   return FPC_OK;
 }
 
@@ -894,6 +910,8 @@ static void pc_apply_full_dev(fpc_plan_s* pl, const double* v, double* z, double
 int fpc_pc_apply(fpc_plan_t pl, const double* v, double* out, int sweep, int where) {
   if (!pl) return set_err(FPC_INVALID_ARGUMENT, "null plan");
   return guarded([&] {
+    std::lock_guard<std::recursive_mutex> lk_plan(pl->mu);
+    std::lock_guard<std::recursive_mutex> lk_prob(pl->prob->mu);
     check_ptr(v, "fpc_pc_apply");
     check_ptr(out, "fpc_pc_apply");
     if (sweep != FPC_SWEEP_HALF && sweep != FPC_SWEEP_FULL) throw InvalidArg{"fpc_pc_apply: bad sweep"};
@@ -919,6 +937,8 @@ int fpc_pc_apply(fpc_plan_t pl, const double* v, double* out, int sweep, int whe
 int fpc_pc_forward(fpc_plan_t pl, const double* v, double* out, int where) {
   if (!pl) return set_err(FPC_INVALID_ARGUMENT, "null plan");
   return guarded([&] {
+    std::lock_guard<std::recursive_mutex> lk_plan(pl->mu);
+    std::lock_guard<std::recursive_mutex> lk_prob(pl->prob->mu);
     check_ptr(v, "fpc_pc_forward");
     check_ptr(out, "fpc_pc_forward");
     // apply_forward is the full sweep in the reference (alpha_circulant.hpp:212-215)
@@ -1525,6 +1545,8 @@ int fpc_gmres(fpc_plan_t pl, const double* b, double* x, const fpc_solver_config
               fpc_report* rep, double* history, int history_cap, int where) {
   if (!pl || !rep) return set_err(FPC_INVALID_ARGUMENT, "null argument");
   return guarded([&] {
+    std::lock_guard<std::recursive_mutex> lk_plan(pl->mu);
+    std::lock_guard<std::recursive_mutex> lk_prob(pl->prob->mu);
     check_ptr(b, "fpc_gmres");
     check_ptr(x, "fpc_gmres");
     fpc_solver_config cfg{1e-9, 200, 0, FPC_SWEEP_HALF};
@@ -1532,7 +1554,9 @@ int fpc_gmres(fpc_plan_t pl, const double* b, double* x, const fpc_solver_config
     if (cfg.sweep != FPC_SWEEP_HALF && cfg.sweep != FPC_SWEEP_FULL) throw InvalidArg{"fpc_gmres: bad sweep"};
     pl->sweep_mode = cfg.sweep;
     if (cfg.max_iter < 0) throw InvalidArg{"gmres_right: max_iter must be non-negative"};
-    if (cfg.max_iter > 250) throw Unsupported{"B200 GMRES keeps at most 250 basis vectors"};
+    // basis vectors live at once: one restart cycle (GMRES(m)), or the whole unrestarted solve
+    const int basis_steps = (cfg.restart > 0 && cfg.restart < cfg.max_iter) ? cfg.restart : cfg.max_iter;
+    if (basis_steps > 250) throw Unsupported{"B200 GMRES keeps at most 250 basis vectors per cycle"};
     fpc_problem_s* p = pl->prob;
     DeviceGuard g(p->ctx->device);
     const auto t0 = std::chrono::steady_clock::now();
@@ -1671,6 +1695,8 @@ int fpc_bicgstab(fpc_plan_t pl, const double* b, double* x, const fpc_solver_con
                  fpc_report* rep, double* history, int history_cap, int where) {
   if (!pl || !rep) return set_err(FPC_INVALID_ARGUMENT, "null argument");
   return guarded([&] {
+    std::lock_guard<std::recursive_mutex> lk_plan(pl->mu);
+    std::lock_guard<std::recursive_mutex> lk_prob(pl->prob->mu);
     check_ptr(b, "fpc_bicgstab");
     check_ptr(x, "fpc_bicgstab");
     fpc_solver_config cfg{1e-9, 200, 0, FPC_SWEEP_HALF};
@@ -1716,6 +1742,7 @@ int fpc_bicgstab(fpc_plan_t pl, const double* b, double* x, const fpc_solver_con
 int fpc_shard_matvec(fpc_problem_t p, const double* v, double* y, int nt_local, int k_offset) {
   if (!p) return set_err(FPC_INVALID_ARGUMENT, "null problem");
   return guarded([&] {
+    std::lock_guard<std::recursive_mutex> lk_prob(p->mu);
     check_ptr(v, "fpc_shard_matvec");
     check_ptr(y, "fpc_shard_matvec");
     if (nt_local < 1 || k_offset < 0 || k_offset + nt_local > p->nt)
@@ -1732,6 +1759,8 @@ int fpc_shard_matvec(fpc_problem_t p, const double* v, double* y, int nt_local, 
 int fpc_shard_time_fwd(fpc_plan_t pl, const double* v, double* Z, int ns_local, double s_in) {
   if (!pl) return set_err(FPC_INVALID_ARGUMENT, "null plan");
   return guarded([&] {
+    std::lock_guard<std::recursive_mutex> lk_plan(pl->mu);
+    std::lock_guard<std::recursive_mutex> lk_prob(pl->prob->mu);
     fpc_problem_s* p = pl->prob;
     if (ns_local < 1 || ns_local > p->ns) throw InvalidArg{"fpc_shard_time_fwd: bad column count"};
     DeviceGuard g(p->ctx->device);
@@ -1743,6 +1772,8 @@ int fpc_shard_time_fwd(fpc_plan_t pl, const double* v, double* Z, int ns_local, 
 int fpc_shard_tau(fpc_plan_t pl, double* Z, int row0, int nrows, int forward) {
   if (!pl) return set_err(FPC_INVALID_ARGUMENT, "null plan");
   return guarded([&] {
+    std::lock_guard<std::recursive_mutex> lk_plan(pl->mu);
+    std::lock_guard<std::recursive_mutex> lk_prob(pl->prob->mu);
     fpc_problem_s* p = pl->prob;
     if (row0 < 0 || nrows < 0 || row0 + nrows > pl->solve_count)
       throw InvalidArg{"fpc_shard_tau: bad frequency range"};
@@ -1760,6 +1791,8 @@ int fpc_shard_tau(fpc_plan_t pl, double* Z, int row0, int nrows, int forward) {
 int fpc_shard_time_inv(fpc_plan_t pl, const double* Z, double* z, int ns_local) {
   if (!pl) return set_err(FPC_INVALID_ARGUMENT, "null plan");
   return guarded([&] {
+    std::lock_guard<std::recursive_mutex> lk_plan(pl->mu);
+    std::lock_guard<std::recursive_mutex> lk_prob(pl->prob->mu);
     fpc_problem_s* p = pl->prob;
     if (ns_local < 1 || ns_local > p->ns) throw InvalidArg{"fpc_shard_time_inv: bad column count"};
     DeviceGuard g(p->ctx->device);
@@ -1775,6 +1808,8 @@ static void check_commuted_shard(const fpc_problem_s* p, const char* who) {
 int fpc_shard_dst_levels(fpc_plan_t pl, const double* v, double* out, int nt_local, double s_in) {
   if (!pl || !v || !out) return set_err(FPC_INVALID_ARGUMENT, "null argument");
   return guarded([&] {
+    std::lock_guard<std::recursive_mutex> lk_plan(pl->mu);
+    std::lock_guard<std::recursive_mutex> lk_prob(pl->prob->mu);
     fpc_problem_s* p = pl->prob;
     check_commuted_shard(p, "fpc_shard_dst_levels");
     if (nt_local < 2 || nt_local % 2 || nt_local > p->nt)
@@ -1790,6 +1825,8 @@ int fpc_shard_dst_levels(fpc_plan_t pl, const double* v, double* out, int nt_loc
 int fpc_shard_time_solve(fpc_plan_t pl, const double* u, double* z, int col0, int ns_local, int forward) {
   if (!pl || !u || !z) return set_err(FPC_INVALID_ARGUMENT, "null argument");
   return guarded([&] {
+    std::lock_guard<std::recursive_mutex> lk_plan(pl->mu);
+    std::lock_guard<std::recursive_mutex> lk_prob(pl->prob->mu);
     fpc_problem_s* p = pl->prob;
     check_commuted_shard(p, "fpc_shard_time_solve");
     if (col0 < 0 || ns_local < 1 || col0 + ns_local > p->ns) throw InvalidArg{"fpc_shard_time_solve: bad column range"};
@@ -1914,6 +1951,186 @@ int fpc_shard_lincomb(fpc_context_t c, const double* const* V, const double* coe
     ck(cudaMemcpyAsync(c->dscal + 700, c->hpin + 700, size_t(nv) * sizeof(double), cudaMemcpyHostToDevice, c->stream), "coef");
     LAUNCH("lincomb", c->stream, fpc::launch_lincomb(c->dvptr, c->dscales, c->dscal + 700, nv, u, n, c->stream));
     ck(cudaStreamSynchronize(c->stream), "sync");
+  });
+}
+
+// ---------------------------------------------------------------------------- generic GMRES
+// gmres_right(n, apply_a, apply_pinv, b, cfg) for arbitrary HOST callables (krylov.hpp:83-192):
+// the reference's iteration -- Gram-Schmidt with its conditional re-orthogonalisation (threshold
+// 1/sqrt(2), krylov.hpp:107, 123-130), Givens rotations (133-151), the |g_{j+1}|/||b|| stop test
+// (154-159), the breakdown test (160-165), x = P^{-1}(sum y_k v_k) (180-183) and the fresh TRR
+// (188) -- with the Krylov basis resident on the device and the dots / updates / combinations run
+// by the library's deterministic vector kernels.  Each step stages v_j to the host once, calls
+// apply_pinv then apply_a there (z never leaves the host) and uploads w.  restart = m > 0: the
+// GMRES(m) emulation of SURVEY §8(c) (x0 = 0 per cycle on the residual).
+namespace {
+struct HostPinned {
+  double* p = nullptr;
+  explicit HostPinned(size_t n) { ck(cudaMallocHost(&p, std::max<size_t>(n, 1) * sizeof(double)), "cudaMallocHost"); }
+  ~HostPinned() { if (p) cudaFreeHost(p); }
+};
+struct DevVec {
+  double* p = nullptr;
+  explicit DevVec(size_t n) { p = dalloc<double>(n + 2); }
+  ~DevVec() { if (p) cudaFree(p); }
+  DevVec(DevVec&& o) noexcept : p(o.p) { o.p = nullptr; }
+  DevVec(const DevVec&) = delete;
+};
+void call_op(fpc_apply_fn f, void* user, const double* in, double* out, size_t n, const char* who) {
+  const int rc = f(in, out, n, user);
+  if (rc != 0) throw RuntimeErr{std::string(who) + ": the callable reported failure (status " + std::to_string(rc) + ")"};
+}
+}  // namespace
+
+int fpc_gmres_callbacks(fpc_context_t c, size_t n, fpc_apply_fn apply_a, void* a_user, fpc_apply_fn apply_pinv,
+                        void* p_user, const double* b, double* x, const fpc_solver_config* cfg_in, fpc_report* report,
+                        double* history, int history_cap) {
+  if (!c || !apply_a || !apply_pinv || !b || !x || !cfg_in || !report)
+    return set_err(FPC_INVALID_ARGUMENT, "null argument");
+  return guarded([&] {
+    const fpc_solver_config cfg = *cfg_in;
+    if (n == 0) throw InvalidArg{"gmres_right: empty system"};
+    if (cfg.max_iter < 0) throw InvalidArg{"gmres_right: max_iter must be non-negative"};
+    const int mcyc = (cfg.restart > 0 && cfg.restart < cfg.max_iter) ? cfg.restart : cfg.max_iter;
+    if (mcyc + 1 > 250) throw Unsupported{"gmres_right (callables): at most 249 steps per cycle"};
+    DeviceGuard g(c->device);
+    const auto t0 = std::chrono::steady_clock::now();
+    cudaStream_t st = c->stream;
+    *report = fpc_report{};
+    HostPinned hin(n), hout(n), hz(n);
+    DevVec dr(n), dw(n);
+    std::vector<DevVec> V;
+    V.reserve(size_t(mcyc) + 1);
+    auto h2d = [&](double* d, const double* h) {
+      ck(cudaMemcpyAsync(d, h, n * sizeof(double), cudaMemcpyHostToDevice, st), "H2D");
+    };
+    auto d2h = [&](double* h, const double* d) {
+      ck(cudaMemcpyAsync(h, d, n * sizeof(double), cudaMemcpyDeviceToHost, st), "D2H");
+      ck(cudaStreamSynchronize(st), "sync");
+    };
+    auto check_rc = [](int rc) {
+      if (rc != FPC_OK) throw RuntimeErr{g_err};
+    };
+    auto norm2 = [&](const double* d) {
+      double out = 0.0;
+      check_rc(fpc_shard_dots(c, nullptr, nullptr, 0, d, n, 1, &out));
+      return std::sqrt(out);
+    };
+    std::vector<double> xh(n, 0.0), bh(b, b + n), rh(bh);
+    h2d(dr.p, b);
+    const double norm_b = norm2(dr.p);
+    int hist_len = 0, total = 0, cycles = 0, reorth = 0;
+    bool conv = norm_b == 0.0;
+    double last_rel = conv ? 0.0 : 1.0, norm_r = norm_b;
+    while (!conv && total < cfg.max_iter) {
+      const int budget = std::min(mcyc, cfg.max_iter - total);
+      const double tol_c = cfg.tol * norm_b / norm_r;  // the cycle's tolerance relative to ||r||
+      // v_0 = r / ||r||
+      while (V.size() < size_t(budget) + 1) V.emplace_back(n);
+      {
+        const double* src[1] = {dr.p};
+        const double coef[1] = {1.0 / norm_r};
+        check_rc(fpc_shard_lincomb(c, src, coef, 1, V[0].p, n));
+      }
+      std::vector<std::vector<double>> H;
+      std::vector<double> gc, gs, gg{norm_r};
+      int steps = 0;
+      bool inner_conv = false;
+      for (int j = 0; j < budget; ++j) {
+        d2h(hin.p, V[size_t(j)].p);
+        call_op(apply_pinv, p_user, hin.p, hz.p, n, "apply_pinv");
+        call_op(apply_a, a_user, hz.p, hout.p, n, "apply_a");
+        h2d(dw.p, hout.p);
+        std::vector<const double*> vp(static_cast<size_t>(j) + 1);
+        for (int i = 0; i <= j; ++i) vp[size_t(i)] = V[size_t(i)].p;
+        std::vector<double> ones(size_t(j) + 1, 1.0), hcol(size_t(j) + 2, 0.0), dd(size_t(j) + 2);
+        const double norm_before = norm2(dw.p);
+        // one Gram-Schmidt pass (all projections, then the update), repeated once when the norm
+        // dropped below 1/sqrt(2) of its value before (krylov.hpp:116-131)
+        double norm_w = norm_before;
+        for (int pass = 0; pass < 2; ++pass) {
+          check_rc(fpc_shard_dots(c, vp.data(), ones.data(), j + 1, dw.p, n, 0, dd.data()));
+          double nw2 = 0.0;
+          check_rc(fpc_shard_update(c, vp.data(), dd.data(), j + 1, dw.p, n, &nw2));
+          for (int i = 0; i <= j; ++i) hcol[size_t(i)] += dd[size_t(i)];
+          const double prev = pass == 0 ? norm_before : norm_w;
+          norm_w = std::sqrt(std::max(nw2, 0.0));
+          if (pass == 0 && !(norm_w < 0.70710678118654752 * prev)) break;
+          if (pass == 1) ++reorth;
+        }
+        hcol[size_t(j) + 1] = norm_w;
+        for (int i = 0; i < j; ++i) {  // previous rotations (krylov.hpp:133-140)
+          const double hi = hcol[size_t(i)], hi1 = hcol[size_t(i) + 1];
+          hcol[size_t(i)] = gc[size_t(i)] * hi + gs[size_t(i)] * hi1;
+          hcol[size_t(i) + 1] = -gs[size_t(i)] * hi + gc[size_t(i)] * hi1;
+        }
+        const double hj = hcol[size_t(j)], hj1 = hcol[size_t(j) + 1];
+        const double rad = std::hypot(hj, hj1);
+        const double cs = rad > 0.0 ? hj / rad : 1.0, sn = rad > 0.0 ? hj1 / rad : 0.0;
+        gc.push_back(cs);
+        gs.push_back(sn);
+        hcol[size_t(j)] = rad;
+        hcol[size_t(j) + 1] = 0.0;
+        gg.push_back(-sn * gg[size_t(j)]);
+        gg[size_t(j)] *= cs;
+        H.push_back(hcol);
+        steps = j + 1;
+        const double rel_c = std::abs(gg[size_t(j) + 1]) / norm_r;
+        last_rel = rel_c * norm_r / norm_b;
+        if (history && hist_len < history_cap) history[hist_len] = last_rel;
+        ++hist_len;
+        if (rel_c <= tol_c) {
+          inner_conv = true;
+          break;
+        }
+        if (norm_w <= 1e-14 * std::max(1.0, norm_before)) break;  // breakdown (krylov.hpp:160-165)
+        const double* src[1] = {dw.p};
+        const double coef[1] = {1.0 / norm_w};
+        check_rc(fpc_shard_lincomb(c, src, coef, 1, V[size_t(j) + 1].p, n));
+      }
+      total += steps;
+      ++cycles;
+      if (steps > 0) {  // y by back substitution, u = V y, delta = P^{-1} u (krylov.hpp:175-183)
+        std::vector<double> y(size_t(steps), 0.0);
+        for (int i = steps - 1; i >= 0; --i) {
+          double sacc = gg[size_t(i)];
+          for (int k = i + 1; k < steps; ++k) sacc -= H[size_t(k)][size_t(i)] * y[size_t(k)];
+          y[size_t(i)] = sacc / H[size_t(i)][size_t(i)];
+        }
+        std::vector<const double*> vp(static_cast<size_t>(steps));
+        for (int i = 0; i < steps; ++i) vp[size_t(i)] = V[size_t(i)].p;
+        check_rc(fpc_shard_lincomb(c, vp.data(), y.data(), steps, dw.p, n));
+        d2h(hin.p, dw.p);
+        call_op(apply_pinv, p_user, hin.p, hz.p, n, "apply_pinv");
+        for (size_t i = 0; i < n; ++i) xh[i] += hz.p[i];
+      }
+      if (inner_conv) conv = true;
+      if (conv || steps == 0 || total >= cfg.max_iter) break;
+      // r = b - A x for the next cycle
+      call_op(apply_a, a_user, xh.data(), hout.p, n, "apply_a");
+      for (size_t i = 0; i < n; ++i) rh[i] = bh[i] - hout.p[i];
+      h2d(dr.p, rh.data());
+      norm_r = norm2(dr.p);
+      if (norm_r == 0.0) conv = true;
+    }
+    // fresh true residual (krylov.hpp:188)
+    double trr = 0.0;
+    if (norm_b > 0.0) {
+      call_op(apply_a, a_user, xh.data(), hout.p, n, "apply_a");
+      for (size_t i = 0; i < n; ++i) rh[i] = bh[i] - hout.p[i];
+      h2d(dr.p, rh.data());
+      trr = norm2(dr.p) / norm_b;
+    }
+    std::copy(xh.begin(), xh.end(), x);
+    report->converged = conv ? 1 : 0;
+    report->iterations = total;
+    report->iterations_exact = double(total);
+    report->restarts = cycles > 0 ? cycles - 1 : 0;
+    report->reorthogonalizations = reorth;
+    report->final_relative_residual = last_rel;
+    report->true_relative_residual = trr;
+    report->history_len = hist_len;
+    report->seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   });
 }
 

@@ -183,6 +183,22 @@ __device__ __forceinline__ void cluster_sync_relaxed(Cluster& cluster) {
     cluster.sync();
 }
 
+// Exit barrier of a cluster kernel whose CTAs read each other's shared memory: "every DSMEM read
+// of my partners' buffers has been performed before any partner may retire".  A relaxed arrive
+// does not order a load whose value is never consumed (e.g. a predicated-off store's operand), so
+// these use arrive.release (the memory model's guarantee; it also waits for the CTA's outstanding
+// global stores, ~2% on the split matvec).  FPC_CLUSTER_EXIT_RELAXED=1 restores the relaxed form (A/B).
+#ifndef FPC_CLUSTER_EXIT_RELAXED
+#define FPC_CLUSTER_EXIT_RELAXED 0
+#endif
+template <class Cluster>
+__device__ __forceinline__ void cluster_sync_exit(Cluster& cluster) {
+  if constexpr (FPC_CLUSTER_EXIT_RELAXED)
+    cluster_sync_relaxed(cluster);
+  else
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.aligned;\n" ::: "memory");
+}
+
 // Barrier policies: the whole CTA, or a named barrier over a thread group (warp-specialised
 // kernels running independent transforms in different groups).
 struct CtaSync {

@@ -102,7 +102,7 @@ __global__ void __launch_bounds__(kThr, 1)
       yk[j] = c + t[r].x;
     }
   }
-  cluster_sync_relaxed(cluster);  // partners have read this CTA's buffer (no wait on the y stores)
+  cluster_sync_exit(cluster);  // partners have read this CTA's buffer (no wait on the y stores)
 }
 
 // ------------------------------------------------------------------ matvec, packed residue split
@@ -211,7 +211,7 @@ __global__ void __launch_bounds__(kThr, 1)
       }
     }
   }
-  cluster_sync_relaxed(cluster);  // partners have read this CTA's buffer
+  cluster_sync_exit(cluster);  // partners have read this CTA's buffer
 }
 
 // ---------------------------------------------------------------------------------- tau solve
@@ -264,7 +264,7 @@ __device__ __forceinline__ void dst_cl(double2* row, double2* smem, cg::cluster_
   // row writes visible to the cluster (the next DST's fold reads them); after the last DST only
   // "partners are done with this buffer" is needed
   if constexpr (LAST)
-    cluster_sync_relaxed(cluster);
+    cluster_sync_exit(cluster);
   else
     cluster.sync();
 }

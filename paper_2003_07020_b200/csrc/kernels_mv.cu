@@ -255,7 +255,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((1 << (LOGM - 1)) / 
     }
   }
   FPC_PHM(6);
-  cluster_sync_relaxed(cluster);  // keep both buffers alive until the partner has read them
+  cluster_sync_exit(cluster);  // keep both buffers alive until the partner has read them
 }
 
 template <int LOGM>

@@ -179,7 +179,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(SGeo<LOGH>::NT, SGeo
       Z[size_t(H + n) * ns + p] = zm2;
     }
   }
-  cluster_sync_relaxed(cluster);  // the partner's buffer stays alive until every read of it is done
+  cluster_sync_exit(cluster);  // the partner's buffer stays alive until every read of it is done
 }
 
 // ---------------------------------------------------------------------------------------------

@@ -194,21 +194,31 @@ class P2PTransport:
                     ptrs.append(q)
             self.ptrs[name] = ptrs
         self._flag = torch.zeros(1, dtype=torch.float64, device=kernels.device)
+        self._lib_stream = torch.cuda.ExternalStream(kernels.ctx.stream_handle(), device=kernels.device)
 
     def exchange(self, name, src, rows, cols, es, split_cols, off, stride, row_base, col_base):
         """Scatter src into every rank's `name` buffer; returns this rank's buffer (float64 view)
         once every rank's stores into it are complete (stream order)."""
         self.k.scatter_p2p(src, rows, cols, es, split_cols, self.ptrs[name], off, stride, row_base, col_base)
         if self.G > 1:
-            dist.all_reduce(self._flag, group=self.group)
+            # the barrier must be ordered behind the scatter kernel, i.e. enqueued on the library
+            # context's stream (not whatever torch stream is current)
+            with torch.cuda.stream(self._lib_stream):
+                dist.all_reduce(self._flag, group=self.group)
         ptr, n = self.local[name]
         return self.k.tensor_at(ptr, n)
 
     def close(self):
+        """Unmap the peers' buffers, then -- only after every rank has unmapped this rank's buffers
+        (barrier) -- free the exported ones: freeing an IPC-exported allocation while an importer
+        still maps it is undefined."""
         self.k.synchronize()
         for q in self._opened:
             self.k.ipc_close(q)
         self._opened = []
+        self.k.synchronize()
+        if self.G > 1 and dist.is_initialized():
+            dist.barrier(group=self.group)
         for ptr, _ in self.local.values():
             self.k.free_shared(ptr)
         self.local = {}

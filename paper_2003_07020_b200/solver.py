@@ -467,6 +467,46 @@ def gmres_right(op: AllAtOnceOperator, plan: AlphaCirculantPlan, b, cfg: SolverC
                    op, plan, b, cfg, out)
 
 
+def gmres_right_callables(n: int, apply_a, apply_pinv, b, cfg: SolverConfig | None = None,
+                          ctx: "Context | None" = None) -> KrylovResult:
+    """The reference's generic gmres_right(n, apply_a, apply_pinv, b, cfg) (krylov.hpp:83-85) for any
+    host callables apply(v: np.ndarray, out: np.ndarray) -> None; the Krylov basis and the
+    Gram-Schmidt run on the device (fpc_gmres_callbacks).  A callable's exception is re-raised."""
+    ctx = ctx or Context.default()
+    cfg = cfg or SolverConfig()
+    bh = _host_in(b, n)
+    x = np.empty(n)
+    errors = []
+
+    def wrap(fn):
+        def cb(pin, pout, nn, _user):
+            try:
+                a = np.ctypeslib.as_array(C.cast(pin, C.POINTER(C.c_double)), shape=(nn,))
+                o = np.ctypeslib.as_array(C.cast(pout, C.POINTER(C.c_double)), shape=(nn,))
+                fn(a, o)
+                return 0
+            except BaseException as e:  # noqa: BLE001 -- surfaced below
+                errors.append(e)
+                return 1
+        return N.APPLY_FN(cb)
+
+    ca, cp = wrap(apply_a), wrap(apply_pinv)
+    c = N.SolverConfigC(float(cfg.tol), int(cfg.max_iter), int(cfg.restart), int(cfg.sweep))
+    rep = N.ReportC()
+    cap = max(int(cfg.max_iter), 1) + 1
+    hist = np.zeros(cap)
+    lib = N.load()
+    rc = lib.fpc_gmres_callbacks(ctx.h, n, ca, None, cp, None, C.c_void_p(bh.ctypes.data), C.c_void_p(x.ctypes.data),
+                                 C.byref(c), C.byref(rep), C.c_void_p(hist.ctypes.data), cap)
+    if errors:
+        raise errors[0]
+    N.check(rc)
+    r = SolveReport(bool(rep.converged), float(rep.iterations_exact), list(hist[:min(rep.history_len, cap)]),
+                    rep.final_relative_residual, rep.true_relative_residual, rep.seconds, rep.restarts,
+                    rep.reorthogonalizations)
+    return KrylovResult(x, r)
+
+
 def bicgstab_left(op: AllAtOnceOperator, plan: AlphaCirculantPlan, b, cfg: SolverConfig | None = None,
                   out=None) -> KrylovResult:
     """Left-preconditioned BiCGSTAB on the device (krylov.hpp:204-280), x0 = 0: the recurrence on

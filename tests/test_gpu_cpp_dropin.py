@@ -25,3 +25,24 @@ def test_cpp_dropin_example(tmp_path):
     assert 1 <= float(iters) <= 20
     assert float(trr) <= 1e-9
     assert abs(float(trr_host) - float(trr)) <= 1e-3 * float(trr) + 1e-15
+
+
+def test_cpp_generic_gmres_and_plan_fields(tmp_path):
+    """examples/plugin_gmres.cpp: the generic gmres_right(n, apply_a, apply_pinv, b, cfg) over host
+    callables matches the device-resident solve; AlphaCirculantPlan carries the reference's
+    scale_fwd / scale_bwd / tau fields; a callable's exception propagates."""
+    if not shutil.which("g++"):
+        pytest.skip("no g++")
+    exe = str(tmp_path / "plugin_gmres")
+    lib = os.path.join(ROOT, "paper_2003_07020_b200")
+    subprocess.run(["g++", "-std=c++20", "-O2", "-I" + os.path.join(ROOT, "include"),
+                    os.path.join(ROOT, "examples", "plugin_gmres.cpp"), "-L" + lib, "-lfracpint_b200",
+                    "-Wl,-rpath," + lib, "-o", exe], check=True)
+    out = subprocess.run([exe], capture_output=True, text=True, timeout=120)
+    assert out.returncode == 0, out.stdout + out.stderr
+    it_d, it_g, dx, trr, alpha, sf1, prod, sigma0, solve_count, taun, rethrown = out.stdout.split()
+    assert abs(float(it_d) - float(it_g)) <= 1
+    assert float(dx) <= 1e-10 and float(trr) <= 1e-9
+    assert float(alpha) == 1.0 / 128  # min(0.5, dt/2), dt = 1/64
+    assert abs(float(sf1) - (1.0 / 128) ** (1.0 / 64)) <= 1e-15 and abs(float(prod) - 1.0) <= 1e-15
+    assert float(sigma0) < 0 and int(solve_count) == 33 and int(taun) == 255 and rethrown == "1"
