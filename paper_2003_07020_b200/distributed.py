@@ -194,7 +194,7 @@ class P2PTransport:
                     ptrs.append(q)
             self.ptrs[name] = ptrs
         self._flag = torch.zeros(1, dtype=torch.float64, device=kernels.device)
-        self._lib_stream = torch.cuda.ExternalStream(kernels.ctx.stream_handle(), device=kernels.device)
+        self._lib_stream = torch.cuda.ExternalStream(kernels.ctx.stream_handle, device=kernels.device)
 
     def exchange(self, name, src, rows, cols, es, split_cols, off, stride, row_base, col_base):
         """Scatter src into every rank's `name` buffer; returns this rank's buffer (float64 view)
