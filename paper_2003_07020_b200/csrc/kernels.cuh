@@ -75,6 +75,11 @@ cudaError_t launch_matvec_rows_warp(const double* v, double* y, int len, int nro
                                     int log_m, const double* eig_scaled, const double2* tw_base,
                                     cudaStream_t st, int koff);
 bool warp_kernels_enabled();
+// DST rows of n = 255 on warp-owned transforms (kernels_warp.cu): mode 0 = in-place DST of each row,
+// 1 / 2 = DST, divide / multiply by lambda_row - dt sigma, DST (the 1D tau solve / forward action).
+// cudaErrorNotSupported for other n.
+cudaError_t launch_dst_rows_warp(double2* Z, int n, int n_rows, const double2* lambda, const double* sigma,
+                                 double dt, const double2* tw_base, cudaStream_t st, int mode);
 // in-place orthonormal DST-I of n_rows contiguous complex rows of length n (n + 1 = 2^k)
 cudaError_t launch_dst_rows(double2* Z, int n, int n_rows, const double2* tw_base, cudaStream_t st);
 

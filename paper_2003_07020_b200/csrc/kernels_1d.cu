@@ -657,6 +657,8 @@ cudaError_t launch_time_inv(const double2* Z, double* z, int n_space, int n_time
 // in-place orthonormal DST-I of n_rows contiguous complex rows of length n (n + 1 = 2^k)
 cudaError_t launch_dst_rows(double2* Z, int n, int n_rows, const double2* tw_base, cudaStream_t st) {
   cudaError_t err = cudaSuccess;
+  if (n == 255 && warp_kernels_enabled())
+    return launch_dst_rows_warp(Z, n, n_rows, nullptr, nullptr, 0.0, tw_base, st, 0);
   const int lm = ilog2(n + 1);
 #define CALL(LM)                                                                          \
   {                                                                                       \
@@ -688,6 +690,8 @@ cudaError_t launch_tau_solve_1d(double2* Z, int n_space, int n_rows, const doubl
   cudaError_t err = cudaSuccess;
   const int lm = ilog2(n_space + 1);
   if (lm >= 14) return launch_tau_large(Z, n_space, n_rows, lambda, sigma, dt, tw_base, st, forward);
+  if (n_space == 255 && warp_kernels_enabled())
+    return launch_dst_rows_warp(Z, n_space, n_rows, lambda, sigma, dt, tw_base, st, forward ? 2 : 1);
 #define CALL(LM)                                                                  \
   err = forward ? tau1d<LM, 2>(Z, n_rows, lambda, sigma, dt, tw_base, st)         \
                 : tau1d<LM, 1>(Z, n_rows, lambda, sigma, dt, tw_base, st);

@@ -12,6 +12,7 @@
 #include <cstdlib>
 
 #include "kernels.cuh"
+#include "warp_dst.cuh"
 #include "warp_fft.cuh"
 
 namespace fpc {
@@ -145,6 +146,70 @@ cudaError_t launch_matvec_rows_warp(const double* v, double* y, int len, int nro
   if (e != cudaSuccess) return e;
   k_mv_rows_warp<R><<<(nrows + rows_per_cta - 1) / rows_per_cta, 32 * kWarpsPerCta, smem, st>>>(
       v, y, len, nrows, rpt, sstride, koff, eig_scaled, tw_base); note_launch();
+  return cudaGetLastError();
+}
+
+// DST-I rows of n = 255 complex points on 16-lane groups (warp_dst.cuh), in place: MODE 0 = the
+// row DSTs of the 2D tau solve (tau.hpp:85-86); MODE 1 / 2 = the 1D tau solve / forward action of
+// frequency row r (tau.hpp:98-136): DST, divide (multiply) by lambda_r - dt sigma_i, DST, with the
+// intermediate kept in the group's tile.
+template <int MODE>
+__global__ void __launch_bounds__(32 * kWarpsPerCta, 2)
+    k_dst_rows_warp(double2* __restrict__ Z, int n_rows, const double2* __restrict__ lam,
+                    const double* __restrict__ sigma, double dt, const double2* __restrict__ twb) {
+  constexpr int R = 16, G = 2, NSR = 255;
+  extern __shared__ double2 wsm[];
+  const int lane = int(threadIdx.x) & 31;
+  const int t = lane & (R - 1);
+  const int grp = (int(threadIdx.x) >> 5) * G + lane / R;
+  const int row = int(blockIdx.x) * (kWarpsPerCta * G) + grp;
+  const bool valid = row < n_rows;
+  const int rr = valid ? row : n_rows - 1;
+  double2* zr = Z + size_t(rr) * NSR;
+  double2* xs = wsm + grp * WarpFftTile<R>::SIZE;
+  const double scale = 0.088388347648318440550;  // sqrt(2/256)
+  warp_dst256([&](int j) { return zr[j - 1]; }, xs, t, twb, scale);
+  if constexpr (MODE != 0) {
+    const double2 l = __ldg(lam + rr);
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int i = t + R * r;
+      if (i < NSR) xs[i] = shift_apply<MODE>(xs[i], l.x - dt * __ldg(sigma + i), l.y);
+    }
+    __syncwarp();
+    warp_dst256([&](int j) { return xs[j - 1]; }, xs, t, twb, scale);
+  }
+  if (valid) {
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int i = t + R * r;
+      if (i < NSR) zr[i] = xs[i];
+    }
+  }
+}
+
+cudaError_t launch_dst_rows_warp(double2* Z, int n, int n_rows, const double2* lambda, const double* sigma,
+                                 double dt, const double2* tw_base, cudaStream_t st, int mode) {
+  if (n != 255) return cudaErrorNotSupported;
+  constexpr int R = 16, G = 2;
+  const int rows_per_cta = kWarpsPerCta * G;
+  const size_t smem = size_t(kWarpsPerCta) * G * WarpFftTile<R>::SIZE * sizeof(double2);
+  const unsigned grid = unsigned((n_rows + rows_per_cta - 1) / rows_per_cta);
+#define FPC_DSTW(MODE)                                                                                        \
+  {                                                                                                           \
+    cudaError_t e = cudaFuncSetAttribute(k_dst_rows_warp<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,  \
+                                         int(smem));                                                          \
+    if (e != cudaSuccess) return e;                                                                           \
+    k_dst_rows_warp<MODE><<<grid, 32 * kWarpsPerCta, smem, st>>>(Z, n_rows, lambda, sigma, dt, tw_base);     \
+    note_launch();                                                                                            \
+  }
+  if (mode == 0)
+    FPC_DSTW(0)
+  else if (mode == 1)
+    FPC_DSTW(1)
+  else
+    FPC_DSTW(2)
+#undef FPC_DSTW
   return cudaGetLastError();
 }
 
