@@ -200,6 +200,29 @@ int fpc_shard_scatter_p2p(fpc_context_t ctx, const double* src, int rows, int co
                           double* const* dst, const int* off, const int* stride, int nranks, int row_base,
                           int col_base);
 
+/* Multi-device solve in ONE process: a context over 1..8 devices (peer access
+ * enabled between distinct devices; a device may repeat, which runs the rank schedule on one GPU) and
+ * the frequency-sharded operator on it -- time-sharded Krylov vectors, the BDF2 halo by peer copy,
+ * the PC apply's four transpositions as peer-store kernels, the retained frequencies' tau solves
+ * split across the ranks, Gram-Schmidt partials summed in rank order.  Host buffers hold the whole
+ * time-major vector.  n_time must be divisible by the rank count (>= 2 levels per rank).
+ * alpha <= 0 selects PreconditionerKind::generalized().  Replaces, for a C++ caller of
+ * solve_all_at_once (driver.hpp:49-92), the Python/torchrun ShardedSolver. */
+typedef struct fpc_multi_s* fpc_multi_t;
+typedef struct fpc_sharded_s* fpc_sharded_t;
+int fpc_multi_create(const int* devices, int n_ranks, fpc_multi_t* out);
+int fpc_multi_destroy(fpc_multi_t m);
+int fpc_sharded_create_1d(fpc_multi_t m, double gamma, double kappa, double h, int n_space, int n_time,
+                          double dt, double alpha, fpc_sharded_t* out);
+int fpc_sharded_create_2d(fpc_multi_t m, double gamma_x, double gamma_y, double kappa_x, double kappa_y,
+                          double h, int n_per_dim, int n_time, double dt, double alpha, fpc_sharded_t* out);
+int fpc_sharded_destroy(fpc_sharded_t s);
+int fpc_sharded_info(fpc_sharded_t s, int* n_ranks, int* nt_local);
+int fpc_sharded_matvec(fpc_sharded_t s, const double* v, double* out);
+int fpc_sharded_pc_apply(fpc_sharded_t s, const double* v, double* out);
+int fpc_sharded_gmres(fpc_sharded_t s, const double* b, double* x, const fpc_solver_config* cfg,
+                      fpc_report* report, double* history, int history_cap);
+
 /* instrumentation: number of kernels this library launched in this process */
 unsigned long long fpc_kernel_launches(void);
 /* live per-kernel device time: CUDA events on the launching stream around every launch while

@@ -13,6 +13,7 @@
 //   gmres_right(n, apply_a, apply_pinv, b, cfg) for any host callables  krylov.hpp:83-85
 //                                    (fpc_gmres_callbacks: basis on the device)
 //   TauOperator                      tau.hpp:20-26 (AlphaCirculantPlan::tau)
+//   MultiDevice / ShardedOperator    one process over 1..8 GPUs (fpc_multi_*, fpc_sharded_*)
 // plus SolverConfig::restart (GMRES(m); 0 = the reference's unrestarted GMRES).
 //
 // Two ways to use it:
@@ -350,6 +351,61 @@ KrylovResult gmres_right(std::size_t n, OpA&& apply_a, OpP&& apply_pinv, std::sp
   detail::fill_report(r.report, rep, hist);
   return r;
 }
+
+// ---- one process, 1..8 devices (fpc_multi_* / fpc_sharded_*): the frequency-sharded solve of a C++
+// caller of solve_all_at_once (driver.hpp:49-92) on several GPUs.  A device may repeat.
+class MultiDevice {
+ public:
+  explicit MultiDevice(const std::vector<int>& devices) {
+    fpc_multi_t h = nullptr;
+    detail::check(fpc_multi_create(devices.data(), int(devices.size()), &h));
+    h_.reset(h, [](fpc_multi_t m) { fpc_multi_destroy(m); });
+  }
+  fpc_multi_t handle() const { return h_.get(); }
+
+ private:
+  std::shared_ptr<fpc_multi_s> h_;
+};
+
+template <class Jacobian>
+class ShardedOperator {
+ public:
+  ShardedOperator(MultiDevice& md, TimeStencil stencil, Jacobian jac, double dt,
+                  const PreconditionerKind& kind = PreconditionerKind::generalized())
+      : md_(md), nt_(stencil.n_time), ns_(jac.dim()) {
+    fpc_sharded_t h = nullptr;
+    if constexpr (std::is_same_v<Jacobian, RieszJacobian1D>)
+      detail::check(fpc_sharded_create_1d(md.handle(), jac.gamma, jac.kappa, jac.h, jac.n, nt_, dt,
+                                          kind.alpha_for(dt), &h));
+    else
+      detail::check(fpc_sharded_create_2d(md.handle(), jac.gamma_x, jac.gamma_y, jac.kappa_x, jac.kappa_y, jac.h,
+                                          jac.n, nt_, dt, kind.alpha_for(dt), &h));
+    h_.reset(h, [](fpc_sharded_t p) { fpc_sharded_destroy(p); });
+  }
+  std::size_t dim() const { return std::size_t(nt_) * std::size_t(ns_); }
+  void apply(std::span<const double> v, std::span<double> out) const {
+    detail::check(fpc_sharded_matvec(h_.get(), v.data(), out.data()));
+  }
+  void apply_inverse(std::span<const double> v, std::span<double> out) const {
+    detail::check(fpc_sharded_pc_apply(h_.get(), v.data(), out.data()));
+  }
+  KrylovResult gmres_right(std::span<const double> b, const SolverConfig& cfg = {}) const {
+    if (b.size() != dim()) throw std::invalid_argument("gmres_right: size mismatch");
+    KrylovResult r;
+    r.x.assign(dim(), 0.0);
+    fpc_solver_config c{cfg.tol, cfg.max_iter, cfg.restart, FPC_SWEEP_HALF};
+    fpc_report rep{};
+    std::vector<double> hist(std::size_t(std::max(cfg.max_iter, 1)) + 1);
+    detail::check(fpc_sharded_gmres(h_.get(), b.data(), r.x.data(), &c, &rep, hist.data(), int(hist.size())));
+    detail::fill_report(r.report, rep, hist);
+    return r;
+  }
+
+ private:
+  MultiDevice& md_;
+  int nt_, ns_;
+  std::shared_ptr<fpc_sharded_s> h_;
+};
 
 // Callables for the reference's generic gmres_right(n, apply_a, apply_pinv, b, cfg)
 template <class Jacobian>

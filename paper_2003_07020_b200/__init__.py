@@ -8,10 +8,11 @@ from .solver import (AllAtOnceOperator, AlphaCirculantPlan, Context, InnerSweep,
                      TimeStencil, apply_forward, apply_inverse, assemble_rhs, bicgstab_left, build_plan,
                      centred_weights, tau_spectrum, circulant_eigenvalues, alpha_circulant_eigenvalues,
                      gmres_right, gmres_right_callables, kernel_launches, KernelProfile)
+from .multi import MultiDevice, ShardedProblem
 
 __all__ = [
     "AllAtOnceOperator", "AlphaCirculantPlan", "Context", "InnerSweep", "KrylovResult", "Ordering",
     "PreconditionerKind", "RieszJacobian1D", "RieszJacobian2D", "SolveReport", "SolverConfig",
     "TimeStencil", "apply_forward", "apply_inverse", "assemble_rhs", "bicgstab_left", "build_plan", "centred_weights", "tau_spectrum", "circulant_eigenvalues", "alpha_circulant_eigenvalues",
-    "gmres_right", "gmres_right_callables", "kernel_launches", "KernelProfile",
+    "gmres_right", "gmres_right_callables", "kernel_launches", "KernelProfile", "MultiDevice", "ShardedProblem",
 ]

@@ -30,6 +30,8 @@ EXPORTS = [
     "fpc_shard_dst_levels", "fpc_shard_time_solve", "fpc_ipc_get_handle", "fpc_ipc_open", "fpc_ipc_close",
     "fpc_shard_scatter_p2p", "fpc_centred_weights", "fpc_tau_spectrum", "fpc_circulant_eigenvalues",
     "fpc_alpha_circulant_eigenvalues", "fpc_plan_scales", "fpc_gmres_callbacks",
+    "fpc_multi_create", "fpc_multi_destroy", "fpc_sharded_create_1d", "fpc_sharded_create_2d",
+    "fpc_sharded_destroy", "fpc_sharded_info", "fpc_sharded_matvec", "fpc_sharded_pc_apply", "fpc_sharded_gmres",
 ]
 
 
@@ -110,6 +112,15 @@ def load():
     lib.fpc_plan_scales.argtypes = [vp, dp, dp]
     lib.fpc_gmres_callbacks.argtypes = [vp, C.c_size_t, APPLY_FN, vp, APPLY_FN, vp, dp, dp,
                                         C.POINTER(SolverConfigC), C.POINTER(ReportC), dp, C.c_int]
+    lib.fpc_multi_create.argtypes = [C.POINTER(C.c_int), C.c_int, C.POINTER(C.c_void_p)]
+    lib.fpc_multi_destroy.argtypes = [vp]
+    lib.fpc_sharded_create_1d.argtypes = [vp, d, d, d, C.c_int, C.c_int, d, d, C.POINTER(C.c_void_p)]
+    lib.fpc_sharded_create_2d.argtypes = [vp, d, d, d, d, d, C.c_int, C.c_int, d, d, C.POINTER(C.c_void_p)]
+    lib.fpc_sharded_destroy.argtypes = [vp]
+    lib.fpc_sharded_info.argtypes = [vp, ip, ip]
+    lib.fpc_sharded_matvec.argtypes = [vp, dp, dp]
+    lib.fpc_sharded_pc_apply.argtypes = [vp, dp, dp]
+    lib.fpc_sharded_gmres.argtypes = [vp, dp, dp, C.POINTER(SolverConfigC), C.POINTER(ReportC), dp, C.c_int]
     _lib = lib
     return lib
 

@@ -2135,3 +2135,544 @@ int fpc_gmres_callbacks(fpc_context_t c, size_t n, fpc_apply_fn apply_a, void* a
 }
 
 }  // extern "C"
+
+// ============================================================================ multi-device
+// One process drives 1..8 devices (SURVEY §8(b) "context over 1..8 devices", §8(e)): the solve of
+// the frequency-sharded layout (distributed.py's ShardedSolver, reference ordering) behind the
+// C-ABI.  Krylov vectors are time-sharded (rank r owns time levels [r nt_loc, (r+1) nt_loc), stored
+// after two halo levels); the matvec takes the BDF2 halo from rank r-1 by a peer copy; the PC apply
+// runs the four transpositions time -> space -> frequency -> space -> time as peer-store kernels
+// (kernels_p2p.cu: every element stored straight into its slot of the owner's buffer over NVLink),
+// each ordered by events (every rank's stream waits for every rank's exchange kernel); the tau solves
+// of the retained frequencies (alpha_circulant.hpp:160) are split across the ranks.  The
+// Gram-Schmidt dots are per-rank partials summed in rank order on the host (the Hessenberg
+// recurrence needs them there anyway; deterministic), the updates and combinations are local.
+// Ranks may share a device (devices = {0, 0, ...}): nothing waits on another rank inside a kernel,
+// so one GPU runs the G-rank schedule for testing.
+struct fpc_multi_s {
+  int G = 0;
+  std::vector<int> devices;
+  std::vector<fpc_context_s*> ctx;
+  std::vector<cudaEvent_t> ev;
+};
+
+struct fpc_sharded_s {
+  fpc_multi_s* m = nullptr;
+  int G = 0, nt = 0, ns = 0, n = 0, two_dim = 0, nt_loc = 0, H = 0;
+  std::vector<int> cs, co, hs, ho, ts;  // column split of Ns, frequency split of H, time offsets
+  std::vector<fpc_problem_s*> prob;
+  std::vector<fpc_plan_s*> plan;
+  std::vector<double*> cols, rows, zf, zb, zt, tmp;  // exchange buffers per rank
+  size_t vec_len = 0;                                  // (nt_loc + 2) * ns per rank (halo first)
+};
+
+namespace {
+std::vector<int> split_counts(int n, int G) {
+  std::vector<int> c(size_t(G), n / G);
+  for (int i = 0; i < n % G; ++i) ++c[size_t(i)];
+  return c;
+}
+std::vector<int> offsets_of(const std::vector<int>& c) {
+  std::vector<int> o(c.size() + 1, 0);
+  for (size_t i = 0; i < c.size(); ++i) o[i + 1] = o[i] + c[i];
+  return o;
+}
+void check_rc(int rc) {
+  if (rc != FPC_OK) throw RuntimeErr{g_err};
+}
+
+// every rank's stream waits for everything enqueued so far on every rank's stream
+void multi_barrier(fpc_multi_s* m) {
+  for (int r = 0; r < m->G; ++r) {
+    DeviceGuard g(m->devices[size_t(r)]);
+    ck(cudaEventRecord(m->ev[size_t(r)], m->ctx[size_t(r)]->stream), "cudaEventRecord");
+  }
+  for (int r = 0; r < m->G; ++r) {
+    DeviceGuard g(m->devices[size_t(r)]);
+    for (int q = 0; q < m->G; ++q)
+      if (q != r) ck(cudaStreamWaitEvent(m->ctx[size_t(r)]->stream, m->ev[size_t(q)], 0), "cudaStreamWaitEvent");
+  }
+}
+
+// A sharded vector: one device buffer per rank, the local levels at offset 2 ns (halo first).
+struct SVec {
+  std::vector<double*> p;
+};
+double* loc(const fpc_sharded_s* s, const SVec& v, int r) { return v.p[size_t(r)] + 2 * size_t(s->ns); }
+
+SVec svec_alloc(fpc_sharded_s* s) {
+  SVec v;
+  for (int r = 0; r < s->G; ++r) {
+    DeviceGuard g(s->m->devices[size_t(r)]);
+    v.p.push_back(dalloc<double>(s->vec_len + 2));
+  }
+  return v;
+}
+void svec_free(fpc_sharded_s* s, SVec& v) {
+  for (int r = 0; r < s->G && r < int(v.p.size()); ++r) {
+    DeviceGuard g(s->m->devices[size_t(r)]);
+    cudaFree(v.p[size_t(r)]);
+  }
+  v.p.clear();
+}
+
+void sh_matvec(fpc_sharded_s* s, const SVec& v, SVec& y) {
+  const size_t ns = size_t(s->ns), nl = size_t(s->nt_loc);
+  multi_barrier(s->m);
+  for (int r = 1; r < s->G; ++r) {  // BDF2 halo: the two last levels of rank r-1
+    DeviceGuard g(s->m->devices[size_t(r)]);
+    ck(cudaMemcpyPeerAsync(v.p[size_t(r)], s->m->devices[size_t(r)], loc(s, v, r - 1) + (nl - 2) * ns,
+                           s->m->devices[size_t(r - 1)], 2 * ns * sizeof(double), s->m->ctx[size_t(r)]->stream),
+       "halo copy");
+  }
+  for (int r = 0; r < s->G; ++r)
+    check_rc(fpc_shard_matvec(s->prob[size_t(r)], loc(s, v, r), loc(s, y, r), s->nt_loc, s->ts[size_t(r)]));
+}
+
+void sh_exchange(fpc_sharded_s* s, const std::vector<const double*>& src, int rows, const std::vector<int>& cols,
+                 int es, bool split_cols, const std::vector<double*>& dst, const std::vector<int>& off,
+                 const std::vector<int>& stride, const std::vector<int>& row_base, const std::vector<int>& col_base) {
+  multi_barrier(s->m);
+  for (int r = 0; r < s->G; ++r)
+    check_rc(fpc_shard_scatter_p2p(s->m->ctx[size_t(r)], src[size_t(r)], rows, cols[size_t(r)], es, split_cols ? 1 : 0,
+                                   dst.data(), off.data(), stride.data(), s->G, row_base[size_t(r)], col_base[size_t(r)]));
+  multi_barrier(s->m);
+}
+
+// z = P^{-1} (s_in v), reference ordering (alpha_circulant.hpp:137-199), four peer-store exchanges
+void sh_pc_apply(fpc_sharded_s* s, const SVec& v, SVec& z, double s_in) {
+  const int G = s->G, ns = s->ns;
+  std::vector<const double*> src(static_cast<size_t>(G));
+  std::vector<int> colsz(static_cast<size_t>(G)), rb(static_cast<size_t>(G)), cb(static_cast<size_t>(G), 0);
+  // 1. time -> space: rank r's [nt_loc][ns] levels -> cols[d] [nt][cs_d] rows r nt_loc..
+  for (int r = 0; r < G; ++r) {
+    src[size_t(r)] = loc(s, v, r);
+    colsz[size_t(r)] = ns;
+    rb[size_t(r)] = s->ts[size_t(r)];
+  }
+  std::vector<int> off(s->co.begin(), s->co.end() - 1), stride(s->cs.begin(), s->cs.end());
+  sh_exchange(s, src, s->nt_loc, colsz, 1, true, s->cols, off, stride, rb, cb);
+  // 2. time FFT on my columns -> zf [H][cs_d] complex
+  for (int d = 0; d < G; ++d)
+    check_rc(fpc_shard_time_fwd(s->plan[size_t(d)], s->cols[size_t(d)], s->zf[size_t(d)], s->cs[size_t(d)], s_in));
+  // 3. space -> frequency: zf[d] rows split by ho -> rows[e] [hs_e][ns] at column co[d]
+  for (int d = 0; d < G; ++d) {
+    src[size_t(d)] = s->zf[size_t(d)];
+    colsz[size_t(d)] = s->cs[size_t(d)];
+    rb[size_t(d)] = 0;
+    cb[size_t(d)] = s->co[size_t(d)];
+  }
+  std::vector<int> hoff(s->ho.begin(), s->ho.end() - 1), nsstride(static_cast<size_t>(G), ns);
+  sh_exchange(s, src, s->H, colsz, 2, false, s->rows, hoff, nsstride, rb, cb);
+  // 4. tau solves of my frequencies
+  for (int e = 0; e < G; ++e)
+    check_rc(fpc_shard_tau(s->plan[size_t(e)], s->rows[size_t(e)], s->ho[size_t(e)], s->hs[size_t(e)], 0));
+  // 5. frequency -> space: rows[e] [hs_e][ns] columns split by co -> zb[d] [H][cs_d] at row ho[e]
+  for (int e = 0; e < G; ++e) {
+    src[size_t(e)] = s->rows[size_t(e)];
+    colsz[size_t(e)] = ns;
+    rb[size_t(e)] = s->ho[size_t(e)];
+    cb[size_t(e)] = 0;
+  }
+  // per-source row counts differ (hs_e): exchange rank by rank through the same ordering
+  multi_barrier(s->m);
+  for (int e = 0; e < G; ++e)
+    check_rc(fpc_shard_scatter_p2p(s->m->ctx[size_t(e)], src[size_t(e)], s->hs[size_t(e)], ns, 2, 1, s->zb.data(),
+                                   off.data(), stride.data(), G, rb[size_t(e)], 0));
+  multi_barrier(s->m);
+  // 6. inverse time FFT -> zt [nt][cs_d]
+  for (int d = 0; d < G; ++d)
+    check_rc(fpc_shard_time_inv(s->plan[size_t(d)], s->zb[size_t(d)], s->zt[size_t(d)], s->cs[size_t(d)]));
+  // 7. space -> time: zt[d] rows split by time blocks -> z's local levels of rank r at column co[d]
+  std::vector<double*> zdst(static_cast<size_t>(G));
+  std::vector<int> toff(static_cast<size_t>(G)), tstride(static_cast<size_t>(G), ns);
+  for (int r = 0; r < G; ++r) {
+    zdst[size_t(r)] = loc(s, z, r);
+    toff[size_t(r)] = s->ts[size_t(r)];
+  }
+  for (int d = 0; d < G; ++d) {
+    src[size_t(d)] = s->zt[size_t(d)];
+    colsz[size_t(d)] = s->cs[size_t(d)];
+    rb[size_t(d)] = 0;
+    cb[size_t(d)] = s->co[size_t(d)];
+  }
+  sh_exchange(s, src, s->nt, colsz, 1, false, zdst, toff, tstride, rb, cb);
+}
+
+// per-rank partial dots <V_i, w> (and ||w||^2), summed over ranks in rank order on the host
+std::vector<double> sh_dots(fpc_sharded_s* s, const std::vector<SVec*>& V, const SVec& w, bool with_norm) {
+  const int nv = int(V.size());
+  const size_t n = size_t(s->nt_loc) * size_t(s->ns);
+  const int cnt = nv + (with_norm || nv == 0 ? 1 : 0);
+  for (int r = 0; r < s->G; ++r) {
+    fpc_context_s* c = s->m->ctx[size_t(r)];
+    DeviceGuard g(c->device);
+    GmresState S{nullptr, c, n, c->stream, std::vector<double>(size_t(nv), 1.0), 0};
+    std::vector<const double*> vv;
+    for (auto* x : V) vv.push_back(loc(s, *x, r));
+    dots_into(S, vv, nv, loc(s, w, r), nv == 0 ? true : with_norm, 0);
+    ck(cudaMemcpyAsync(c->hpin, c->dscal, size_t(cnt) * sizeof(double), cudaMemcpyDeviceToHost, c->stream), "D2H");
+  }
+  std::vector<double> out(size_t(cnt), 0.0);
+  for (int r = 0; r < s->G; ++r) {
+    fpc_context_s* c = s->m->ctx[size_t(r)];
+    DeviceGuard g(c->device);
+    ck(cudaStreamSynchronize(c->stream), "sync");
+    for (int i = 0; i < cnt; ++i) out[size_t(i)] += c->hpin[i];
+  }
+  return out;
+}
+
+// w -= sum_i coef_i V_i on every rank; returns ||w||^2
+double sh_update(fpc_sharded_s* s, const std::vector<SVec*>& V, const std::vector<double>& coef, SVec& w) {
+  double tot = 0.0;
+  const size_t n = size_t(s->nt_loc) * size_t(s->ns);
+  std::vector<double> part(static_cast<size_t>(s->G));
+  for (int r = 0; r < s->G; ++r) {
+    std::vector<const double*> vv;
+    for (auto* x : V) vv.push_back(loc(s, *x, r));
+    check_rc(fpc_shard_update(s->m->ctx[size_t(r)], vv.data(), coef.data(), int(V.size()), loc(s, w, r), n,
+                              &part[size_t(r)]));
+  }
+  for (double p : part) tot += p;
+  return tot;
+}
+
+void sh_lincomb(fpc_sharded_s* s, const std::vector<SVec*>& V, const std::vector<double>& coef, SVec& u) {
+  const size_t n = size_t(s->nt_loc) * size_t(s->ns);
+  for (int r = 0; r < s->G; ++r) {
+    std::vector<const double*> vv;
+    for (auto* x : V) vv.push_back(loc(s, *x, r));
+    check_rc(fpc_shard_lincomb(s->m->ctx[size_t(r)], vv.data(), coef.data(), int(V.size()), loc(s, u, r), n));
+  }
+}
+
+void sh_upload(fpc_sharded_s* s, const double* host, SVec& v) {
+  const size_t per = size_t(s->nt_loc) * size_t(s->ns);
+  for (int r = 0; r < s->G; ++r) {
+    fpc_context_s* c = s->m->ctx[size_t(r)];
+    DeviceGuard g(c->device);
+    ck(cudaMemcpyAsync(loc(s, v, r), host + size_t(r) * per, per * sizeof(double), cudaMemcpyHostToDevice, c->stream),
+       "H2D");
+  }
+}
+void sh_download(fpc_sharded_s* s, const SVec& v, double* host) {
+  const size_t per = size_t(s->nt_loc) * size_t(s->ns);
+  for (int r = 0; r < s->G; ++r) {
+    fpc_context_s* c = s->m->ctx[size_t(r)];
+    DeviceGuard g(c->device);
+    ck(cudaMemcpyAsync(host + size_t(r) * per, loc(s, v, r), per * sizeof(double), cudaMemcpyDeviceToHost, c->stream),
+       "D2H");
+  }
+  for (int r = 0; r < s->G; ++r) {
+    DeviceGuard g(s->m->devices[size_t(r)]);
+    ck(cudaStreamSynchronize(s->m->ctx[size_t(r)]->stream), "sync");
+  }
+}
+}  // namespace
+
+extern "C" {
+
+int fpc_multi_create(const int* devices, int n_ranks, fpc_multi_t* out) {
+  if (!devices || !out) return set_err(FPC_INVALID_ARGUMENT, "null argument");
+  return guarded([&] {
+    if (n_ranks < 1 || n_ranks > fpc::kP2PMaxRanks) throw InvalidArg{"fpc_multi_create: 1 <= n_ranks <= 8"};
+    auto* m = new fpc_multi_s();
+    try {
+      m->G = n_ranks;
+      m->devices.assign(devices, devices + n_ranks);
+      for (int r = 0; r < n_ranks; ++r) {
+        fpc_context_t c = nullptr;
+        check_rc(fpc_context_create(devices[r], &c));
+        m->ctx.push_back(c);
+        DeviceGuard g(devices[r]);
+        cudaEvent_t e;
+        ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
+        m->ev.push_back(e);
+      }
+      for (int a = 0; a < n_ranks; ++a)  // peer access between distinct devices (NVLink / NVSwitch)
+        for (int b = 0; b < n_ranks; ++b) {
+          if (devices[a] == devices[b]) continue;
+          int can = 0;
+          ck(cudaDeviceCanAccessPeer(&can, devices[a], devices[b]), "cudaDeviceCanAccessPeer");
+          if (!can) throw Unsupported{"fpc_multi_create: devices without peer access"};
+          DeviceGuard g(devices[a]);
+          const cudaError_t e = cudaDeviceEnablePeerAccess(devices[b], 0);
+          if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+          else ck(e, "cudaDeviceEnablePeerAccess");
+        }
+    } catch (...) {
+      for (auto* c : m->ctx) fpc_context_destroy(c);
+      delete m;
+      throw;
+    }
+    *out = m;
+  });
+}
+
+int fpc_multi_destroy(fpc_multi_t m) {
+  if (!m) return FPC_OK;
+  for (int r = 0; r < m->G; ++r) {
+    DeviceGuard g(m->devices[size_t(r)]);
+    cudaEventDestroy(m->ev[size_t(r)]);
+    fpc_context_destroy(m->ctx[size_t(r)]);
+  }
+  delete m;
+  return FPC_OK;
+}
+
+static int sharded_create(fpc_multi_t m, bool two_dim, double gx, double gy, double kx, double ky, double h, int n,
+                          int n_time, double dt, double alpha, fpc_sharded_t* out) {
+  if (!m || !out) return set_err(FPC_INVALID_ARGUMENT, "null argument");
+  return guarded([&] {
+    auto* s = new fpc_sharded_s();
+    try {
+      s->m = m;
+      s->G = m->G;
+      s->two_dim = two_dim ? 1 : 0;
+      s->n = n;
+      s->nt = n_time;
+      s->ns = two_dim ? n * n : n;
+      s->H = n_time / 2 + 1;
+      if (n_time % s->G) throw InvalidArg{"sharded solve: n_time must be divisible by the number of ranks"};
+      s->nt_loc = n_time / s->G;
+      if (s->G > 1 && s->nt_loc < 2) throw InvalidArg{"sharded solve: at least two time levels per rank"};
+      if (s->ns < s->G || s->H < s->G) throw InvalidArg{"sharded solve: fewer columns or frequencies than ranks"};
+      s->cs = split_counts(s->ns, s->G);
+      s->co = offsets_of(s->cs);
+      s->hs = split_counts(s->H, s->G);
+      s->ho = offsets_of(s->hs);
+      for (int r = 0; r < s->G; ++r) s->ts.push_back(r * s->nt_loc);
+      s->vec_len = size_t(s->nt_loc + 2) * size_t(s->ns);
+      for (int r = 0; r < s->G; ++r) {
+        fpc_problem_t p = nullptr;
+        if (two_dim)
+          check_rc(fpc_problem_create_2d(m->ctx[size_t(r)], gx, gy, kx, ky, h, n, n_time, dt, &p));
+        else
+          check_rc(fpc_problem_create_1d(m->ctx[size_t(r)], gx, kx, h, n, n_time, dt, &p));
+        s->prob.push_back(p);
+        fpc_plan_t pl = nullptr;
+        check_rc(fpc_plan_create(p, alpha, &pl));
+        s->plan.push_back(pl);
+        DeviceGuard g(m->devices[size_t(r)]);
+        const size_t c = size_t(s->cs[size_t(r)]), hr = size_t(s->hs[size_t(r)]);
+        s->cols.push_back(dalloc<double>(size_t(n_time) * c + 2));
+        s->zf.push_back(dalloc<double>(2 * size_t(s->H) * c + 2));
+        s->rows.push_back(dalloc<double>(2 * hr * size_t(s->ns) + 2));
+        s->zb.push_back(dalloc<double>(2 * size_t(s->H) * c + 2));
+        s->zt.push_back(dalloc<double>(size_t(n_time) * c + 2));
+      }
+    } catch (...) {
+      fpc_sharded_destroy(s);
+      throw;
+    }
+    *out = s;
+  });
+}
+
+int fpc_sharded_create_1d(fpc_multi_t m, double gamma, double kappa, double h, int n_space, int n_time, double dt,
+                          double alpha, fpc_sharded_t* out) {
+  return sharded_create(m, false, gamma, 0.0, kappa, 0.0, h, n_space, n_time, dt, alpha, out);
+}
+
+int fpc_sharded_create_2d(fpc_multi_t m, double gx, double gy, double kx, double ky, double h, int n_per_dim,
+                          int n_time, double dt, double alpha, fpc_sharded_t* out) {
+  return sharded_create(m, true, gx, gy, kx, ky, h, n_per_dim, n_time, dt, alpha, out);
+}
+
+int fpc_sharded_destroy(fpc_sharded_t s) {
+  if (!s) return FPC_OK;
+  for (size_t r = 0; r < s->prob.size(); ++r) {
+    DeviceGuard g(s->m->devices[r]);
+    cudaStreamSynchronize(s->m->ctx[r]->stream);
+    for (auto* v : {&s->cols, &s->zf, &s->rows, &s->zb, &s->zt})
+      if (r < v->size()) cudaFree((*v)[r]);
+    if (r < s->plan.size()) fpc_plan_destroy(s->plan[r]);
+    fpc_problem_destroy(s->prob[r]);
+  }
+  delete s;
+  return FPC_OK;
+}
+
+int fpc_sharded_info(fpc_sharded_t s, int* n_ranks, int* nt_local) {
+  if (!s) return set_err(FPC_INVALID_ARGUMENT, "null argument");
+  if (n_ranks) *n_ranks = s->G;
+  if (nt_local) *nt_local = s->nt_loc;
+  return FPC_OK;
+}
+
+int fpc_sharded_matvec(fpc_sharded_t s, const double* v, double* out) {
+  if (!s || !v || !out) return set_err(FPC_INVALID_ARGUMENT, "null argument");
+  return guarded([&] {
+    SVec a = svec_alloc(s), b = svec_alloc(s);
+    try {
+      sh_upload(s, v, a);
+      sh_matvec(s, a, b);
+      sh_download(s, b, out);
+    } catch (...) {
+      svec_free(s, a);
+      svec_free(s, b);
+      throw;
+    }
+    svec_free(s, a);
+    svec_free(s, b);
+  });
+}
+
+int fpc_sharded_pc_apply(fpc_sharded_t s, const double* v, double* out) {
+  if (!s || !v || !out) return set_err(FPC_INVALID_ARGUMENT, "null argument");
+  return guarded([&] {
+    SVec a = svec_alloc(s), b = svec_alloc(s);
+    try {
+      sh_upload(s, v, a);
+      sh_pc_apply(s, a, b, 1.0);
+      sh_download(s, b, out);
+    } catch (...) {
+      svec_free(s, a);
+      svec_free(s, b);
+      throw;
+    }
+    svec_free(s, a);
+    svec_free(s, b);
+  });
+}
+
+// gmres_right on the sharded operator (krylov.hpp:83-192; the reference's Gram-Schmidt with its
+// conditional re-orthogonalisation, as fpc_gmres_callbacks) + GMRES(m) emulation; host b and x.
+int fpc_sharded_gmres(fpc_sharded_t s, const double* b, double* x, const fpc_solver_config* cfg_in, fpc_report* report,
+                      double* history, int history_cap) {
+  if (!s || !b || !x || !cfg_in || !report) return set_err(FPC_INVALID_ARGUMENT, "null argument");
+  return guarded([&] {
+    const fpc_solver_config cfg = *cfg_in;
+    if (cfg.max_iter < 0) throw InvalidArg{"gmres_right: max_iter must be non-negative"};
+    const int mcyc = (cfg.restart > 0 && cfg.restart < cfg.max_iter) ? cfg.restart : cfg.max_iter;
+    if (mcyc + 1 > 250) throw Unsupported{"sharded gmres_right: at most 249 steps per cycle"};
+    const auto t0 = std::chrono::steady_clock::now();
+    *report = fpc_report{};
+    std::vector<SVec> pool;
+    auto fresh = [&]() -> SVec* {
+      pool.push_back(svec_alloc(s));
+      return &pool.back();
+    };
+    pool.reserve(size_t(mcyc) + 8);
+    struct Free {
+      fpc_sharded_s* s;
+      std::vector<SVec>* p;
+      ~Free() {
+        for (auto& v : *p) svec_free(s, v);
+      }
+    } fr{s, &pool};
+    SVec* B = fresh();
+    SVec* X = fresh();
+    SVec* R = fresh();
+    SVec* W = fresh();
+    SVec* Z = fresh();
+    SVec* T = fresh();
+    std::vector<SVec*> V;
+    for (int i = 0; i <= mcyc; ++i) V.push_back(fresh());
+    sh_upload(s, b, *B);
+    const double norm_b = std::sqrt(sh_dots(s, {}, *B, true)[0]);
+    int total = 0, cycles = 0, reorth = 0, hist_len = 0;
+    bool conv = norm_b == 0.0, have_x = false;
+    double last_rel = conv ? 0.0 : 1.0, norm_r = norm_b;
+    SVec* rhs = B;
+    while (!conv && total < cfg.max_iter) {
+      const int budget = std::min(mcyc, cfg.max_iter - total);
+      const double tol_c = cfg.tol * norm_b / norm_r;
+      sh_lincomb(s, {rhs}, {1.0 / norm_r}, *V[0]);
+      std::vector<std::vector<double>> Hc;
+      std::vector<double> gc, gs, gg{norm_r};
+      int steps = 0;
+      bool inner = false;
+      for (int j = 0; j < budget; ++j) {
+        sh_pc_apply(s, *V[size_t(j)], *Z, 1.0);
+        sh_matvec(s, *Z, *W);
+        std::vector<SVec*> Vj(V.begin(), V.begin() + j + 1);
+        std::vector<double> h(size_t(j) + 2, 0.0);
+        const double norm_before = std::sqrt(sh_dots(s, {}, *W, true)[0]);
+        double norm_w = norm_before;
+        for (int pass = 0; pass < 2; ++pass) {  // krylov.hpp:116-131
+          const std::vector<double> d = sh_dots(s, Vj, *W, false);
+          const double nw2 = sh_update(s, Vj, d, *W);
+          for (int i = 0; i <= j; ++i) h[size_t(i)] += d[size_t(i)];
+          const double prev = norm_w;
+          norm_w = std::sqrt(std::max(nw2, 0.0));
+          if (pass == 0 && !(norm_w < 0.70710678118654752 * prev)) break;
+          if (pass == 1) ++reorth;
+        }
+        h[size_t(j) + 1] = norm_w;
+        for (int i = 0; i < j; ++i) {
+          const double hi = h[size_t(i)], hi1 = h[size_t(i) + 1];
+          h[size_t(i)] = gc[size_t(i)] * hi + gs[size_t(i)] * hi1;
+          h[size_t(i) + 1] = -gs[size_t(i)] * hi + gc[size_t(i)] * hi1;
+        }
+        const double rad = std::hypot(h[size_t(j)], h[size_t(j) + 1]);
+        const double c_ = rad > 0.0 ? h[size_t(j)] / rad : 1.0, s_ = rad > 0.0 ? h[size_t(j) + 1] / rad : 0.0;
+        gc.push_back(c_);
+        gs.push_back(s_);
+        h[size_t(j)] = rad;
+        h[size_t(j) + 1] = 0.0;
+        gg.push_back(-s_ * gg[size_t(j)]);
+        gg[size_t(j)] *= c_;
+        Hc.push_back(h);
+        steps = j + 1;
+        const double rel_c = std::abs(gg[size_t(j) + 1]) / norm_r;
+        last_rel = rel_c * norm_r / norm_b;
+        if (history && hist_len < history_cap) history[hist_len] = last_rel;
+        ++hist_len;
+        if (rel_c <= tol_c) {
+          inner = true;
+          break;
+        }
+        if (norm_w <= 1e-14 * std::max(1.0, norm_before)) break;
+        sh_lincomb(s, {W}, {1.0 / norm_w}, *V[size_t(j) + 1]);
+      }
+      total += steps;
+      ++cycles;
+      if (steps > 0) {
+        std::vector<double> y(size_t(steps), 0.0);
+        for (int i = steps - 1; i >= 0; --i) {
+          double acc = gg[size_t(i)];
+          for (int k = i + 1; k < steps; ++k) acc -= Hc[size_t(k)][size_t(i)] * y[size_t(k)];
+          y[size_t(i)] = acc / Hc[size_t(i)][size_t(i)];
+        }
+        std::vector<SVec*> Vs(V.begin(), V.begin() + steps);
+        sh_lincomb(s, Vs, y, *W);
+        sh_pc_apply(s, *W, *Z, 1.0);  // delta = P^{-1} V y (krylov.hpp:180-183)
+        if (have_x) {
+          sh_lincomb(s, {X, Z}, {1.0, 1.0}, *T);
+          std::swap(X, T);
+        } else {
+          sh_lincomb(s, {Z}, {1.0}, *X);
+          have_x = true;
+        }
+      }
+      if (inner) conv = true;
+      if (conv || steps == 0 || total >= cfg.max_iter) break;
+      sh_matvec(s, *X, *W);  // r = b - A x
+      sh_lincomb(s, {B, W}, {1.0, -1.0}, *R);
+      rhs = R;
+      norm_r = std::sqrt(sh_dots(s, {}, *R, true)[0]);
+      if (norm_r == 0.0) conv = true;
+    }
+    double trr = 0.0;
+    if (!have_x) sh_lincomb(s, {B}, {0.0}, *X);
+    if (norm_b > 0.0) {
+      sh_matvec(s, *X, *W);
+      sh_lincomb(s, {B, W}, {1.0, -1.0}, *R);
+      trr = std::sqrt(sh_dots(s, {}, *R, true)[0]) / norm_b;
+    }
+    sh_download(s, *X, x);
+    report->converged = conv ? 1 : 0;
+    report->iterations = total;
+    report->iterations_exact = double(total);
+    report->restarts = cycles > 0 ? cycles - 1 : 0;
+    report->reorthogonalizations = reorth;
+    report->final_relative_residual = last_rel;
+    report->true_relative_residual = trr;
+    report->history_len = hist_len;
+    report->seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  });
+}
+
+}  // extern "C"

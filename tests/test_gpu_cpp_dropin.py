@@ -46,3 +46,21 @@ def test_cpp_generic_gmres_and_plan_fields(tmp_path):
     assert float(alpha) == 1.0 / 128  # min(0.5, dt/2), dt = 1/64
     assert abs(float(sf1) - (1.0 / 128) ** (1.0 / 64)) <= 1e-15 and abs(float(prod) - 1.0) <= 1e-15
     assert float(sigma0) < 0 and int(solve_count) == 33 and int(taun) == 255 and rethrown == "1"
+
+
+def test_cpp_multi_device_example(tmp_path):
+    """examples/multi_gpu_solve.cpp: the sharded solve through the C++ drop-in over 1, 2 and 4 ranks
+    (all on device 0 on this box) equals the single-device solve."""
+    if not shutil.which("g++"):
+        pytest.skip("no g++")
+    exe = str(tmp_path / "multi_gpu_solve")
+    lib = os.path.join(ROOT, "paper_2003_07020_b200")
+    subprocess.run(["g++", "-std=c++20", "-O2", "-I" + os.path.join(ROOT, "include"),
+                    os.path.join(ROOT, "examples", "multi_gpu_solve.cpp"), "-L" + lib, "-lfracpint_b200",
+                    "-Wl,-rpath," + lib, "-o", exe], check=True)
+    for devs in (["0"], ["0", "0"], ["0", "0", "0", "0"]):
+        out = subprocess.run([exe, *devs], capture_output=True, text=True, timeout=120)
+        assert out.returncode == 0, out.stdout + out.stderr
+        ranks, it_s, it_1, dx, trr = out.stdout.split()
+        assert int(ranks) == len(devs) and abs(float(it_s) - float(it_1)) <= 1
+        assert float(dx) <= 1e-10 and float(trr) <= 1e-9
