@@ -281,6 +281,10 @@ def run_sweep(args):
     library stream.  One JSON line per point (not the headline metric)."""
     import torch
     import paper_2003_07020_b200 as fp
+    rank, world, local = dist_env()
+    if world > 1 or args.sweep_sharded:
+        run_sweep_sharded(args, rank, world, local)
+        return
     dev = torch.device("cuda", 0)
     stream = torch.cuda.Stream(device=dev)
     ctx = fp.Context(0, stream)
@@ -356,6 +360,81 @@ def run_sweep(args):
             print(json.dumps(line), flush=True)
             del op, plan, xr, xi, yr, yi
             torch.cuda.empty_cache()
+
+
+def run_sweep_sharded(args, rank, world, local):
+    """Config 4 at N > 1 (torchrun): every (Nx, Nt) point's PC apply and matvec run sharded over the
+    N ranks (distributed.py ShardedSolver: time-sharded vectors, the four all-to-alls around the
+    frequency-sharded tau solves, the BDF2 halo); the same complex128 = (Re, Im) batch of two real
+    vectors per application; time = max over ranks of CUDA events on the rank's stream."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2003_07020_b200 as fp
+    from paper_2003_07020_b200.distributed import CudaShardKernels, ShardedSolver
+    if not dist.is_initialized():
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29533")
+        dist.init_process_group("nccl", rank=rank, world_size=world)
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    ctx = fp.Context(local, torch.cuda.current_stream(dev))
+    peak, peak_kind = load_peaks()
+    nxs = [int(x) for x in args.sweep_nx.split(",")] if args.sweep_nx else SWEEP_NX
+    nts = [int(x) for x in args.sweep_nt.split(",")] if args.sweep_nt else SWEEP_NT
+    for nx in nxs:
+        for nt in nts:
+            if nt % world or nt // world < 2:
+                continue
+            h, dt = 1.0 / (nx + 1), 1.0 / nt
+            op = fp.AllAtOnceOperator(fp.TimeStencil(nt), fp.RieszJacobian1D(1.5, 1.0, h, nx), dt, ctx)
+            plan = fp.build_plan(fp.PreconditionerKind.generalized(), nt, dt, op)
+            s = ShardedSolver(nt, nx, CudaShardKernels(op, plan), transport=args.transport)
+            try:
+                gen = torch.Generator(device=dev)
+                gen.manual_seed(20260819 + nx * 131 + nt + 7919 * rank)
+                nloc = s.nt_loc * nx
+                xr = torch.randn(nloc, dtype=torch.float64, device=dev, generator=gen)
+                xi = torch.randn(nloc, dtype=torch.float64, device=dev, generator=gen)
+
+                def timed(fn, reps):
+                    for _ in range(args.warmup):
+                        fn()
+                    dist.barrier()
+                    torch.cuda.synchronize()
+                    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    e0.record()
+                    for _ in range(reps):
+                        fn()
+                    e1.record()
+                    torch.cuda.synchronize()
+                    t = torch.tensor([e0.elapsed_time(e1) * 1e-3 / reps], device=dev)
+                    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+                    return float(t.item())
+
+                t_pc = timed(lambda: (s.pc_apply(xr), s.pc_apply(xi)), args.sweep_reps)
+                t_mv = timed(lambda: (s.matvec(xr), s.matvec(xi)), args.sweep_reps)
+            finally:
+                s.close()
+            N = nx * nt
+            H = nt // 2 + 1
+            B_pc = 2 * (16.0 * N + 64.0 * H * nx)
+            B_mv = 2 * 16.0 * N
+            if rank == 0:
+                print(json.dumps({
+                    "metric": "config-4 sweep: BC PC applies/s and matvecs/s (complex128 input)", "n_gpus": world,
+                    "scaling": "strong",
+                    "config": {"workload": "cfg4_sweep", "n_space": nx, "n_time": nt, "gamma": 1.5,
+                               "reps": args.sweep_reps, "input": "complex128 Gaussian = (Re, Im) real batch of 2",
+                               "parallelism": f"time-sharded x{world} ({args.transport} exchanges)"},
+                    "pc_applies_per_s": 1.0 / t_pc, "matvecs_per_s": 1.0 / t_mv,
+                    "pc_apply_gbs": B_pc / t_pc / 1e9, "matvec_gbs": B_mv / t_mv / 1e9,
+                    "pc_apply_hbm_frac_per_gpu": B_pc / t_pc / 1e9 / peak / world,
+                    "matvec_hbm_frac_per_gpu": B_mv / t_mv / 1e9 / peak / world,
+                    "peak_gbs": peak, "peak_source": peak_kind}), flush=True)
+            del op, plan, s
+            torch.cuda.empty_cache()
+    dist.destroy_process_group()
 
 
 # ------------------------------------------------------------------------------------ our arm
@@ -556,6 +635,8 @@ def main():
     ap.add_argument("--sweep-nx", default="", help="comma list (default 1023..65535)")
     ap.add_argument("--sweep-nt", default="", help="comma list (default 256..8192)")
     ap.add_argument("--sweep-reps", type=int, default=50)
+    ap.add_argument("--sweep-sharded", action="store_true",
+                    help="config 4 through the sharded (torchrun) path even at N = 1")
     ap.add_argument("--sweep-cpu-max", type=float, default=4e6, help="largest N timed on the CPU reference")
     args = ap.parse_args()
     if args.sweep:

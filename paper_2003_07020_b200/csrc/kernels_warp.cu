@@ -11,6 +11,7 @@
 // write.  No CTA barrier: a CTA is 8 independent warps.
 #include <cstdlib>
 
+#include "bulk_copy.cuh"
 #include "kernels.cuh"
 #include "warp_dst.cuh"
 #include "warp_fft.cuh"
@@ -166,7 +167,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta, 2)
   const bool valid = row < n_rows;
   const int rr = valid ? row : n_rows - 1;
   double2* zr = Z + size_t(rr) * NSR;
-  double2* xs = wsm + grp * WarpFftTile<R>::SIZE;
+  double2* xs = wsm + grp * kDstTileSize;
   const double scale = 0.088388347648318440550;  // sqrt(2/256)
   warp_dst256([&](int j) { return zr[j - 1]; }, xs, t, twb, scale);
   if constexpr (MODE != 0) {
@@ -174,16 +175,16 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta, 2)
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       const int i = t + R * r;
-      if (i < NSR) xs[i] = shift_apply<MODE>(xs[i], l.x - dt * __ldg(sigma + i), l.y);
+      if (i < NSR) xs[dst_slot(i)] = shift_apply<MODE>(xs[dst_slot(i)], l.x - dt * __ldg(sigma + i), l.y);
     }
     __syncwarp();
-    warp_dst256([&](int j) { return xs[j - 1]; }, xs, t, twb, scale);
+    warp_dst256([&](int j) { return xs[dst_slot(j - 1)]; }, xs, t, twb, scale);
   }
   if (valid) {
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       const int i = t + R * r;
-      if (i < NSR) zr[i] = xs[i];
+      if (i < NSR) zr[i] = xs[dst_slot(i)];
     }
   }
 }
@@ -193,7 +194,7 @@ cudaError_t launch_dst_rows_warp(double2* Z, int n, int n_rows, const double2* l
   if (n != 255) return cudaErrorNotSupported;
   constexpr int R = 16, G = 2;
   const int rows_per_cta = kWarpsPerCta * G;
-  const size_t smem = size_t(kWarpsPerCta) * G * WarpFftTile<R>::SIZE * sizeof(double2);
+  const size_t smem = size_t(kWarpsPerCta) * G * kDstTileSize * sizeof(double2);
   const unsigned grid = unsigned((n_rows + rows_per_cta - 1) / rows_per_cta);
 #define FPC_DSTW(MODE)                                                                                        \
   {                                                                                                           \

@@ -50,9 +50,16 @@ __device__ __forceinline__ void warp_fft_8x16(double2 (&v)[8], double2* __restri
   Dft<8, S>::run(v);
 }
 
+// Output slot of DST index i in the group's tile: i + i/8, so the stride-2 and stride-4 scatter
+// of the assembly and the unit-stride read-back are all free of 16-byte bank conflicts.  The tile
+// needs kDstTileSize >= dst_slot(254) + 1 double2.
+__device__ __forceinline__ int dst_slot(int i) { return i + (i >> 3); }
+constexpr int kDstTileSize = 288;
+
 // DST of one row: f(j) returns f_j (j = 1..255, complex).  On return the group's tile holds
-// DST(f)_i * scale at tile slot i (i = 0..254, natural order); the caller reads it back after a
-// __syncwarp (slot t + 16 r is lane t's r-th coalesced output).
+// DST(f)_i * scale at tile slot dst_slot(i) (i = 0..254); the caller reads it back after a
+// __syncwarp (index t + 16 r is lane t's r-th coalesced output).  A tile-backed source may use the
+// same layout (f(j) = xs[dst_slot(j - 1)]): every f is read before the first transpose.
 template <class Src>
 __device__ __forceinline__ void warp_dst256(Src f, double2* __restrict__ xs, int t, const double2* __restrict__ twb,
                                             double scale) {
@@ -110,12 +117,12 @@ __device__ __forceinline__ void warp_dst256(Src f, double2* __restrict__ xs, int
 #pragma unroll
   for (int p = 0; p < 8; ++p) {
     const int k = t + 16 * p;
-    if (k >= 1) xs[2 * k - 1] = cscale(ev[p], scale);
+    if (k >= 1) xs[dst_slot(2 * k - 1)] = cscale(ev[p], scale);
     const int m = k;
     if (m < M / 2)
-      xs[4 * m] = cscale(V[p], scale);
+      xs[dst_slot(4 * m)] = cscale(V[p], scale);
     else
-      xs[510 - 4 * m] = cscale(V[p], -scale);
+      xs[dst_slot(510 - 4 * m)] = cscale(V[p], -scale);
   }
   __syncwarp();
 }
