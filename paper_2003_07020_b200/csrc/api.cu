@@ -9,6 +9,7 @@
 #include <algorithm>
 #include <atomic>
 #include <chrono>
+#include <cstdint>
 #include <mutex>
 #include <cmath>
 #include <complex>
@@ -177,7 +178,7 @@ inline cplx cmul_fma(cplx a, cplx b) {
               std::fma(a.real(), b.imag(), a.imag() * b.real()));
 }
 
-void host_fft(std::vector<cplx>& x, int sign) {
+void host_fft_pow2(std::vector<cplx>& x, int sign) {
   const size_t n = x.size();
   if (n <= 1) return;
   for (size_t i = 1, j = 0; i < n; ++i) {
@@ -200,7 +201,48 @@ void host_fft(std::vector<cplx>& x, int sign) {
   }
 }
 
-// orthonormal DST-I of real data (dst.hpp:21-43), n+1 must be a power of two
+// Bluestein chirp (fft.hpp:74-77) of an arbitrary length n and kernel sign
+std::vector<cplx> bluestein_chirp(size_t n, int sign) {
+  const double dir = sign >= 0 ? 1.0 : -1.0;
+  std::vector<cplx> chirp(n);
+  for (size_t m = 0; m < n; ++m) {
+    const uint64_t sq = (uint64_t(m) * m) % (2 * n);
+    chirp[m] = std::polar(1.0, dir * kPi * double(sq) / double(n));
+  }
+  return chirp;
+}
+// its convolution filter FFT_L^-(b), b_m = conj(chirp_|m|) circularly (fft.hpp:78-83)
+std::vector<cplx> bluestein_filter(const std::vector<cplx>& chirp, size_t L) {
+  const size_t n = chirp.size();
+  std::vector<cplx> b(L);
+  b[0] = std::conj(chirp[0]);
+  for (size_t m = 1; m < n; ++m) b[m] = b[L - m] = std::conj(chirp[m]);
+  host_fft_pow2(b, -1);
+  return b;
+}
+// fft_bluestein (fft.hpp:71-89), products written as the reference's contracted ones (cmul_fma)
+void host_fft_bluestein(std::vector<cplx>& x, int sign) {
+  const size_t n = x.size(), L = next_pow2(2 * n - 1);
+  const std::vector<cplx> chirp = bluestein_chirp(n, sign);
+  std::vector<cplx> a(L);
+  for (size_t j = 0; j < n; ++j) a[j] = cmul_fma(x[j], chirp[j]);
+  const std::vector<cplx> b = bluestein_filter(chirp, L);
+  host_fft_pow2(a, -1);
+  for (size_t j = 0; j < L; ++j) a[j] = cmul_fma(a[j], b[j]);
+  host_fft_pow2(a, 1);
+  const double inv_L = 1.0 / double(L);
+  for (size_t k = 0; k < n; ++k) x[k] = cmul_fma(chirp[k], a[k]) * inv_L;
+}
+// fft_inplace (fft.hpp:95-101)
+void host_fft(std::vector<cplx>& x, int sign) {
+  if (x.size() <= 1) return;
+  if (ilog2_exact(x.size()) >= 0)
+    host_fft_pow2(x, sign);
+  else
+    host_fft_bluestein(x, sign);
+}
+
+// orthonormal DST-I of real data (dst.hpp:21-43), any n
 std::vector<double> host_dst1(const std::vector<double>& x) {
   const size_t n = x.size(), L = 2 * (n + 1);
   std::vector<cplx> v(L);
@@ -318,6 +360,7 @@ struct fpc_problem_s {
   std::vector<double> colx, coly;  // 1D: colx = scaled Jacobian column; 2D: unscaled weights
   std::vector<double> sigma;       // jac.tau() spectrum (jacobian.hpp:45, 96-98)
   int log_m = 0;                   // Toeplitz packed FFT size M = L/2
+  int generic = 0;                 // a size outside the power-of-two kernels: PC apply on kernels_generic.cu
   double* d_eig = nullptr;         // 1D: -dt*eig/(2L); 2D: y-axis factor
   double* d_eig_x = nullptr;       // 2D: x-axis factor
   double* d_in = nullptr;          // staging for host-pointer calls
@@ -341,6 +384,10 @@ struct fpc_plan_s {
   double2* d_Z = nullptr;  // half spectrum scratch (H x ns complex)
   double2* d_Zf = nullptr; // full spectrum (Nt x ns complex), InnerSweep::full only
   int sweep_mode = FPC_SWEEP_HALF;
+  // generic (Bluestein) path: chirps and filter spectra of the time transforms (signs +1 / -1) and
+  // of the DST odd-extension transform; the full spectrum and the odd-extension scratch
+  double2 *d_ctf = nullptr, *d_btf = nullptr, *d_cti = nullptr, *d_bti = nullptr, *d_cds = nullptr, *d_bds = nullptr;
+  double2 *d_U = nullptr, *d_D = nullptr;
   int ordering = FPC_ORDER_REFERENCE;  // FPC_ORDER_COMMUTED: DST-first (kernels_commuted.cu)
   // GMRES workspace (grown on demand, reused across solves)
   std::vector<double*> basis;
@@ -355,13 +402,22 @@ struct fpc_plan_s {
 
 namespace {
 
-void check_sizes_1d(int n_space, int n_time) {
-  if (ilog2_exact(size_t(n_time)) < 0 || n_time < 4)
-    throw Unsupported{"B200 path needs n_time to be a power of two >= 4"};
-  if (n_time > 16384) throw Unsupported{"B200 path supports n_time <= 16384"};
-  if (ilog2_exact(size_t(n_space) + 1) < 0 || n_space < 3)
-    throw Unsupported{"B200 path needs n_space + 1 to be a power of two >= 4 (DST-I length)"};
-  if (n_space + 1 > 65536) throw Unsupported{"B200 path supports n_space + 1 <= 65536"};
+// Sizes of the power-of-two kernels (fast path) and of the Bluestein path (kernels_generic.cu):
+// the latter covers any n_time <= 4096 and any DST length n <= 2047 (transforms of length 2(n+1)
+// up to 4096, i.e. convolutions of length <= 8192 in one CTA's shared memory).
+bool pow2_sizes_1d(int n_space, int n_time) {
+  return ilog2_exact(size_t(n_time)) >= 0 && n_time >= 4 && n_time <= 16384 &&
+         ilog2_exact(size_t(n_space) + 1) >= 0 && n_space >= 3 && n_space + 1 <= 65536;
+}
+bool generic_sizes(int n_dst, int n_time) {
+  return n_time >= 3 && n_time <= 4096 && n_dst >= 1 && n_dst <= 2047;
+}
+// returns 1 when the problem takes the generic (Bluestein) PC path
+int check_sizes_1d(int n_space, int n_time) {
+  if (pow2_sizes_1d(n_space, n_time)) return 0;
+  if (generic_sizes(n_space, n_time) && n_space <= 65535) return 1;
+  throw Unsupported{"B200 path: n_time must be a power of two in [4, 16384] and n_space + 1 a power of two "
+                    "<= 65536, or (any size) n_time <= 4096 and n_space <= 2047"};
 }
 
 void upload(void* dst, const void* src, size_t bytes, cudaStream_t st) {
@@ -559,9 +615,10 @@ int fpc_problem_create_1d(fpc_context_t c, double gamma, double kappa, double h,
     std::vector<double> w = centred_weights(gamma, n_space);
     if (n_time < 3) throw InvalidArg{"TimeStencil: need at least 3 time levels"};
     if (!(dt > 0.0)) throw InvalidArg{"AllAtOnceOperator: dt must be positive"};
-    check_sizes_1d(n_space, n_time);
+    const int generic = check_sizes_1d(n_space, n_time);
     DeviceGuard g(c->device);
     fpc_problem_s* p = new_problem(c, n_time, dt);
+    p->generic = generic;
     p->n = p->ns = n_space;
     const double scale = -kappa / std::pow(h, gamma);
     for (double& x : w) x *= scale;
@@ -602,12 +659,14 @@ int fpc_problem_create_2d(fpc_context_t c, double gx, double gy, double kx, doub
     std::vector<double> wx = centred_weights(gx, n), wy = centred_weights(gy, n);
     if (n_time < 3) throw InvalidArg{"TimeStencil: need at least 3 time levels"};
     if (!(dt > 0.0)) throw InvalidArg{"AllAtOnceOperator: dt must be positive"};
-    if (ilog2_exact(size_t(n_time)) < 0 || n_time < 4 || n_time > 16384)
-      throw Unsupported{"B200 path needs n_time to be a power of two in [4, 16384]"};
-    if (ilog2_exact(size_t(n) + 1) < 0 || n < 3 || n + 1 > 4096)
-      throw Unsupported{"B200 2D path needs n_per_dim + 1 to be a power of two in [4, 4096]"};
+    const bool pow2 = ilog2_exact(size_t(n_time)) >= 0 && n_time >= 4 && n_time <= 16384 &&
+                      ilog2_exact(size_t(n) + 1) >= 0 && n >= 3 && n + 1 <= 4096;
+    if (!pow2 && !(generic_sizes(n, n_time) && n >= 2))
+      throw Unsupported{"B200 2D path: n_time a power of two in [4, 16384] and n_per_dim + 1 a power of two "
+                        "in [4, 4096], or (any size) n_time <= 4096 and 2 <= n_per_dim <= 2047"};
     DeviceGuard g(c->device);
     fpc_problem_s* p = new_problem(c, n_time, dt);
+    p->generic = pow2 ? 0 : 1;
     p->two_dim = 1;
     p->n = n;
     p->ns = n * n;
@@ -788,6 +847,24 @@ int fpc_plan_create(fpc_problem_t p, double alpha_in, fpc_plan_t* out) {
     ck(cudaMemcpy(pl->d_sigma, p->sigma.data(), p->sigma.size() * 8, cudaMemcpyHostToDevice), "sigma");
     pl->scale_fwd = std::move(sf);
     pl->scale_bwd = std::move(sb);
+    if (p->generic) {
+      auto upload_c = [](const std::vector<cplx>& h) {
+        double2* d = dalloc<double2>(h.size());
+        ck(cudaMemcpy(d, h.data(), h.size() * sizeof(double2), cudaMemcpyHostToDevice), "chirp");
+        return d;
+      };
+      const size_t nt_ = size_t(nt), P = 2 * (size_t(p->n) + 1);
+      const auto ctf = bluestein_chirp(nt_, 1), cti = bluestein_chirp(nt_, -1), cds = bluestein_chirp(P, -1);
+      pl->d_ctf = upload_c(ctf);
+      pl->d_btf = upload_c(bluestein_filter(ctf, next_pow2(2 * nt_ - 1)));
+      pl->d_cti = upload_c(cti);
+      pl->d_bti = upload_c(bluestein_filter(cti, next_pow2(2 * nt_ - 1)));
+      pl->d_cds = upload_c(cds);
+      pl->d_bds = upload_c(bluestein_filter(cds, next_pow2(2 * P - 1)));
+      pl->d_U = dalloc<double2>(nt_ * size_t(p->ns));
+      const size_t seqs = p->two_dim ? nt_ * size_t(p->n) : nt_;  // full sweep: every frequency
+      pl->d_D = dalloc<double2>(seqs * P);
+    }
     ++p->refs;
     *out = pl;
   });
@@ -803,7 +880,9 @@ int fpc_plan_destroy(fpc_plan_t pl) {
     for (double* b : pl->zbasis) cudaFree(b);
     for (void* q : {(void*)pl->d_sf, (void*)pl->d_sb, (void*)pl->d_lambda, (void*)pl->d_sigma,
                     (void*)pl->d_Z, (void*)pl->d_z, (void*)pl->d_u, (void*)pl->d_r, (void*)pl->d_x,
-                    (void*)pl->d_d, (void*)pl->d_b, (void*)pl->d_Zf})
+                    (void*)pl->d_d, (void*)pl->d_b, (void*)pl->d_Zf, (void*)pl->d_ctf, (void*)pl->d_btf,
+                    (void*)pl->d_cti, (void*)pl->d_bti, (void*)pl->d_cds, (void*)pl->d_bds, (void*)pl->d_U,
+                    (void*)pl->d_D})
       cudaFree(q);
   }
   delete pl;
@@ -819,8 +898,8 @@ int fpc_plan_set_ordering(fpc_plan_t pl, int ordering) {
     if (ordering != FPC_ORDER_REFERENCE && ordering != FPC_ORDER_COMMUTED)
       throw InvalidArg{"fpc_plan_set_ordering: bad ordering"};
     const fpc_problem_s* p = pl->prob;
-    if (ordering == FPC_ORDER_COMMUTED && (p->two_dim || p->ns + 1 > 8192))
-      throw Unsupported{"commuted ordering: 1D with n_space + 1 <= 8192 only"};
+    if (ordering == FPC_ORDER_COMMUTED && (p->two_dim || p->ns + 1 > 8192 || p->generic))
+      throw Unsupported{"commuted ordering: 1D with power-of-two sizes and n_space + 1 <= 8192 only"};
     pl->ordering = ordering;
   });
 }
@@ -852,8 +931,62 @@ int fpc_plan_lambda(fpc_plan_t pl, double* out) {
 // the reference runs it as a full sweep, which for real v equals the Hermitian half sweep).
 static void pc_apply_full_dev(fpc_plan_s* pl, const double* v, double* z, double s_in, bool forward);
 
+// Generic sizes (kernels_generic.cu): the reference ordering on a full [Nt][Ns] complex spectrum
+// with Bluestein transforms -- time FFT (fft_inplace(+1), alpha_circulant.hpp:146-152), the tau
+// solves as dst_lattice / divide / dst_lattice (tau.hpp:79-119; 2D rows then columns), the
+// conjugate mirror for the half sweep (167-175), inverse time FFT and real output (176-198),
+// with the imaginary-residue guard for the full sweep.  apply_forward is the full sweep.
+static void pc_apply_generic(fpc_plan_s* pl, const double* v, double* z, double s_in, bool forward) {
+  fpc_problem_s* p = pl->prob;
+  fpc_context_s* c = p->ctx;
+  cudaStream_t st = c->stream;
+  const int nt = p->nt, ns = p->ns, n = p->n, H = nt / 2 + 1;
+  const bool full = forward || pl->sweep_mode == FPC_SWEEP_FULL;
+  const long long act = full ? nt : H;
+  const int mode = forward ? 2 : 1;
+  LAUNCH("gen_time", st, fpc::launch_gen_time_in(v, pl->d_U, ns, nt, pl->d_sf, s_in, st));
+  LAUNCH("gen_time", st, fpc::launch_bluestein(pl->d_U, nt, ns, ns, 0, 1, ns, pl->d_ctf, pl->d_btf, c->tw, st, 1));
+  if (!p->two_dim) {
+    LAUNCH("gen_tau", st, fpc::launch_gen_dst(pl->d_U, pl->d_D, n, act, 1, ns, 0, 1, pl->d_cds, pl->d_bds, c->tw, mode,
+                                              1, ns, pl->d_lambda, pl->d_sigma, p->dt, st));
+    LAUNCH("gen_tau", st, fpc::launch_gen_dst(pl->d_U, pl->d_D, n, act, 1, ns, 0, 1, pl->d_cds, pl->d_bds, c->tw, 0,
+                                              1, ns, pl->d_lambda, pl->d_sigma, p->dt, st));
+  } else {
+    const long long nn = (long long)n * n, cnt = act * n;
+    auto rows = [&](int md) {  // DST over iy of every (frequency, ix) row
+      LAUNCH("gen_tau", st, fpc::launch_gen_dst(pl->d_U, pl->d_D, n, cnt, 1, n, 0, 1, pl->d_cds, pl->d_bds, c->tw, md,
+                                                n, nn, pl->d_lambda, pl->d_sigma, p->dt, st));
+    };
+    auto cols = [&](int md) {  // DST over ix of every (frequency, iy) column
+      LAUNCH("gen_tau", st, fpc::launch_gen_dst(pl->d_U, pl->d_D, n, cnt, n, nn, 1, n, pl->d_cds, pl->d_bds, c->tw, md,
+                                                n, nn, pl->d_lambda, pl->d_sigma, p->dt, st));
+    };
+    rows(0);
+    cols(mode);
+    rows(0);
+    cols(0);
+  }
+  if (!full) LAUNCH("gen_time", st, fpc::launch_gen_mirror(pl->d_U, nt, ns, H, st));
+  LAUNCH("gen_time", st, fpc::launch_bluestein(pl->d_U, nt, ns, ns, 0, 1, ns, pl->d_cti, pl->d_bti, c->tw, st, -1));
+  if (!full) {
+    LAUNCH("gen_time", st, fpc::launch_gen_time_out(pl->d_U, z, ns, nt, pl->d_sb, st));
+    return;
+  }
+  LAUNCH("gen_time", st, fpc::launch_gen_time_out_guard(pl->d_U, z, ns, nt, pl->d_sb, c->partial, st));
+  LAUNCH("reduce", st, fpc::launch_reduce(c->partial, 2, 2, c->dscal + 960, false, st));
+  ck(cudaMemcpyAsync(c->hpin + 960, c->dscal + 960, 2 * sizeof(double), cudaMemcpyDeviceToHost, st), "D2H");
+  ck(cudaStreamSynchronize(st), "sync");
+  const double im2 = c->hpin[960], tot2 = c->hpin[961];
+  if (tot2 > 0.0 && std::sqrt(im2) > 1e-10 * std::sqrt(tot2))
+    throw RuntimeErr{"alpha-circulant action: imaginary residue exceeds 1e-10 of the output norm"};
+}
+
 static void pc_apply_dev(fpc_plan_s* pl, const double* v, double* z, double s_in,
                          bool forward = false) {
+  if (pl->prob->generic) {
+    pc_apply_generic(pl, v, z, s_in, forward);
+    return;
+  }
   if (pl->sweep_mode == FPC_SWEEP_FULL) {
     pc_apply_full_dev(pl, v, z, s_in, forward);
     return;
@@ -1762,6 +1895,7 @@ int fpc_shard_time_fwd(fpc_plan_t pl, const double* v, double* Z, int ns_local, 
     std::lock_guard<std::recursive_mutex> lk_plan(pl->mu);
     std::lock_guard<std::recursive_mutex> lk_prob(pl->prob->mu);
     fpc_problem_s* p = pl->prob;
+    if (p->generic) throw Unsupported{"fpc_shard_time_fwd: power-of-two sizes only (the sharded path)"};
     if (ns_local < 1 || ns_local > p->ns) throw InvalidArg{"fpc_shard_time_fwd: bad column count"};
     DeviceGuard g(p->ctx->device);
     cudaStream_t st = p->ctx->stream;
@@ -1775,6 +1909,7 @@ int fpc_shard_tau(fpc_plan_t pl, double* Z, int row0, int nrows, int forward) {
     std::lock_guard<std::recursive_mutex> lk_plan(pl->mu);
     std::lock_guard<std::recursive_mutex> lk_prob(pl->prob->mu);
     fpc_problem_s* p = pl->prob;
+    if (p->generic) throw Unsupported{"fpc_shard_tau: power-of-two sizes only (the sharded path)"};
     if (row0 < 0 || nrows < 0 || row0 + nrows > pl->solve_count)
       throw InvalidArg{"fpc_shard_tau: bad frequency range"};
     if (nrows == 0) return;
@@ -1794,6 +1929,7 @@ int fpc_shard_time_inv(fpc_plan_t pl, const double* Z, double* z, int ns_local) 
     std::lock_guard<std::recursive_mutex> lk_plan(pl->mu);
     std::lock_guard<std::recursive_mutex> lk_prob(pl->prob->mu);
     fpc_problem_s* p = pl->prob;
+    if (p->generic) throw Unsupported{"fpc_shard_time_inv: power-of-two sizes only (the sharded path)"};
     if (ns_local < 1 || ns_local > p->ns) throw InvalidArg{"fpc_shard_time_inv: bad column count"};
     DeviceGuard g(p->ctx->device);
     cudaStream_t st = p->ctx->stream;
@@ -2451,6 +2587,7 @@ static int sharded_create(fpc_multi_t m, bool two_dim, double gx, double gy, dou
         else
           check_rc(fpc_problem_create_1d(m->ctx[size_t(r)], gx, kx, h, n, n_time, dt, &p));
         s->prob.push_back(p);
+        if (p->generic) throw Unsupported{"sharded solve: power-of-two sizes only"};
         fpc_plan_t pl = nullptr;
         check_rc(fpc_plan_create(p, alpha, &pl));
         s->plan.push_back(pl);

@@ -91,6 +91,28 @@ cudaError_t launch_tau_solve_2d(double2* Z, int n, int n_rows, const double2* la
                                 const double* sigma, double dt, const double2* tw_base,
                                 cudaStream_t st, bool forward = false);
 
+// ---- generic sizes (kernels_generic.cu): Bluestein transforms along a strided batch ---------
+// sequence s (s < count) element j sits at data + (s / inner) * outer_stride + (s % inner) *
+// inner_stride + j * es; chirp / bhat as fft.hpp:71-89 (host-built); len <= 4096.
+// (sign = the transform's kernel sign; a power-of-two len runs the plain transform, no chirp)
+cudaError_t launch_bluestein(double2* data, int len, long long count, long long inner, long long outer_stride,
+                             long long inner_stride, long long es, const double2* chirp, const double2* bhat,
+                             const double2* tw_base, cudaStream_t st, int sign);
+cudaError_t launch_gen_time_in(const double* v, double2* U, int ns, int nt, const double* sf, double s_in,
+                               cudaStream_t st);
+cudaError_t launch_gen_time_out(const double2* U, double* z, int ns, int nt, const double* sb, cudaStream_t st);
+// + the imaginary-residue partials (dots_grid() blocks x {Im^2, |.|^2}) for InnerSweep::full
+cudaError_t launch_gen_time_out_guard(const double2* U, double* z, int ns, int nt, const double* sb, double* partial,
+                                      cudaStream_t st);
+cudaError_t launch_gen_mirror(double2* U, int nt, int ns, int h, cudaStream_t st);
+// DST-I (odd extension, length-2(n+1) Bluestein transform, extraction) of `count` strided
+// sequences of n complex values in place; mode 1 / 2 divides / multiplies the DST output by
+// lambda_f - dt sigma (f = s / per_freq, sigma at the element's offset minus f * plane).
+cudaError_t launch_gen_dst(double2* U, double2* D, int n, long long count, long long inner, long long outer_stride,
+                           long long inner_stride, long long es, const double2* chirp, const double2* bhat,
+                           const double2* tw_base, int mode, long long per_freq, long long plane, const double2* lam,
+                           const double* sigma, double dt, cudaStream_t st);
+
 // ---- Krylov vector kernels (krylov.hpp:52-62, 116-131, 166-167, 180-182) -------------------
 struct VecSet {
   const double* v[8];

@@ -152,8 +152,11 @@ def test_gmres_host_buffers_match_device(pinned):
 
 
 def test_unsupported_sizes_fail_loudly():
+    # beyond both the power-of-two kernels and the Bluestein path (n_time <= 4096, n_space <= 2047)
     with pytest.raises(NotImplementedError):
-        fp.AllAtOnceOperator(fp.TimeStencil(6), fp.RieszJacobian1D(1.5, 1.0, 0.1, 9), 0.1)
+        fp.AllAtOnceOperator(fp.TimeStencil(6), fp.RieszJacobian1D(1.5, 1.0, 1e-4, 9999), 1 / 6)
+    with pytest.raises(NotImplementedError):
+        fp.AllAtOnceOperator(fp.TimeStencil(5000), fp.RieszJacobian1D(1.5, 1.0, 0.1, 9), 1 / 5000)
     with pytest.raises(ValueError):
         fp.AllAtOnceOperator(fp.TimeStencil(8), fp.RieszJacobian1D(1.5, -1.0, 0.1, 7), 0.1)
 
