@@ -388,6 +388,7 @@ struct fpc_plan_s {
   // of the DST odd-extension transform; the full spectrum and the odd-extension scratch
   double2 *d_ctf = nullptr, *d_btf = nullptr, *d_cti = nullptr, *d_bti = nullptr, *d_cds = nullptr, *d_bds = nullptr;
   double2 *d_U = nullptr, *d_D = nullptr;
+  double2* d_P = nullptr;  // commuted ordering beyond 1D n_space + 1 <= 8192: time-level pairs as complex levels
   int ordering = FPC_ORDER_REFERENCE;  // FPC_ORDER_COMMUTED: DST-first (kernels_commuted.cu)
   // GMRES workspace (grown on demand, reused across solves)
   std::vector<double*> basis;
@@ -882,7 +883,7 @@ int fpc_plan_destroy(fpc_plan_t pl) {
                     (void*)pl->d_Z, (void*)pl->d_z, (void*)pl->d_u, (void*)pl->d_r, (void*)pl->d_x,
                     (void*)pl->d_d, (void*)pl->d_b, (void*)pl->d_Zf, (void*)pl->d_ctf, (void*)pl->d_btf,
                     (void*)pl->d_cti, (void*)pl->d_bti, (void*)pl->d_cds, (void*)pl->d_bds, (void*)pl->d_U,
-                    (void*)pl->d_D})
+                    (void*)pl->d_D, (void*)pl->d_P})
       cudaFree(q);
   }
   delete pl;
@@ -898,8 +899,8 @@ int fpc_plan_set_ordering(fpc_plan_t pl, int ordering) {
     if (ordering != FPC_ORDER_REFERENCE && ordering != FPC_ORDER_COMMUTED)
       throw InvalidArg{"fpc_plan_set_ordering: bad ordering"};
     const fpc_problem_s* p = pl->prob;
-    if (ordering == FPC_ORDER_COMMUTED && (p->two_dim || p->ns + 1 > 8192 || p->generic))
-      throw Unsupported{"commuted ordering: 1D with power-of-two sizes and n_space + 1 <= 8192 only"};
+    if (ordering == FPC_ORDER_COMMUTED && p->generic)
+      throw Unsupported{"commuted ordering: power-of-two sizes only"};
     pl->ordering = ordering;
   });
 }
@@ -981,6 +982,28 @@ static void pc_apply_generic(fpc_plan_s* pl, const double* v, double* z, double 
     throw RuntimeErr{"alpha-circulant action: imaginary residue exceeds 1e-10 of the output norm"};
 }
 
+// out = S (s_in v) for nlev (even) time levels: the spatial DST-I of every level (commuted ordering,
+// SURVEY §8(f)1; dst.hpp:21-43 per level, tau.hpp:79-96 rows then columns in 2D).  1D with
+// n_space + 1 <= 8192: the fused pair kernel; otherwise levels (2j, 2j+1) packed as one complex
+// level, the complex row DSTs (1D: cluster kernels; 2D: rows then columns), unpacked.
+static void dst_levels_dev(fpc_plan_s* pl, const double* v, double* out, int nlev, double s_in) {
+  fpc_problem_s* p = pl->prob;
+  cudaStream_t st = p->ctx->stream;
+  if (!p->two_dim && p->ns + 1 <= 8192) {
+    LAUNCH("dst_pairs", st, fpc::launch_dst_pairs(v, out, p->ns, nlev, s_in, p->ctx->tw, st));
+    return;
+  }
+  if (!pl->d_P) pl->d_P = dalloc<double2>(size_t(p->nt / 2) * size_t(p->ns) + 1);
+  LAUNCH("dst_pairs", st, fpc::launch_pack_pairs(v, pl->d_P, p->ns, nlev, s_in, st));
+  if (!p->two_dim) {
+    LAUNCH("dst_pairs", st, fpc::launch_dst_large(pl->d_P, p->ns, nlev / 2, p->ctx->tw, st));
+  } else {
+    LAUNCH("dst_pairs", st, fpc::launch_dst_rows(pl->d_P, p->n, (nlev / 2) * p->n, p->ctx->tw, st));
+    LAUNCH("dst_pairs", st, fpc::launch_dst_cols_2d(pl->d_P, p->n, nlev / 2, p->ctx->tw, st));
+  }
+  LAUNCH("dst_pairs", st, fpc::launch_unpack_pairs(pl->d_P, out, p->ns, nlev, st));
+}
+
 static void pc_apply_dev(fpc_plan_s* pl, const double* v, double* z, double s_in,
                          bool forward = false) {
   if (pl->prob->generic) {
@@ -996,11 +1019,11 @@ static void pc_apply_dev(fpc_plan_s* pl, const double* v, double* z, double s_in
   if (pl->ordering == FPC_ORDER_COMMUTED) {
     // S per time level -> per-column time solve -> S per time level
     double* U = reinterpret_cast<double*>(pl->d_Z);
-    LAUNCH("dst_pairs", st, fpc::launch_dst_pairs(v, U, p->ns, p->nt, s_in, p->ctx->tw, st));
+    dst_levels_dev(pl, v, U, p->nt, s_in);
     LAUNCH("time_solve", st,
            fpc::launch_time_solve(U, U, p->ns, p->nt, pl->d_sf, pl->d_sb, 1.0, pl->d_lambda, pl->d_sigma, p->dt,
                                   p->ctx->tw, st, forward));
-    LAUNCH("dst_pairs", st, fpc::launch_dst_pairs(U, z, p->ns, p->nt, 1.0, p->ctx->tw, st));
+    dst_levels_dev(pl, U, z, p->nt, 1.0);
     return;
   }
   LAUNCH("time_fwd", st, fpc::launch_time_fwd(v, pl->d_Z, p->ns, p->nt, pl->d_sf, s_in, p->ctx->tw, st));
@@ -1938,7 +1961,7 @@ int fpc_shard_time_inv(fpc_plan_t pl, const double* Z, double* z, int ns_local) 
 }
 
 static void check_commuted_shard(const fpc_problem_s* p, const char* who) {
-  if (p->two_dim || p->ns + 1 > 8192) throw Unsupported{std::string(who) + ": 1D with n_space + 1 <= 8192 only"};
+  if (p->generic) throw Unsupported{std::string(who) + ": power-of-two sizes only"};
 }
 
 int fpc_shard_dst_levels(fpc_plan_t pl, const double* v, double* out, int nt_local, double s_in) {
@@ -1953,8 +1976,8 @@ int fpc_shard_dst_levels(fpc_plan_t pl, const double* v, double* out, int nt_loc
     if (v == out) throw InvalidArg{"fpc_shard_dst_levels: input and output must be disjoint"};
     DeviceGuard g(p->ctx->device);
     cudaStream_t st = p->ctx->stream;
-    // any pairing of levels into complex rows is valid: (k, k + nt_local/2) of the local block
-    LAUNCH("dst_pairs", st, fpc::launch_dst_pairs(v, out, p->ns, nt_local, s_in, p->ctx->tw, st));
+    // any pairing of levels into complex rows is valid (the transform is per level)
+    dst_levels_dev(pl, v, out, nt_local, s_in);
   });
 }
 

@@ -91,6 +91,14 @@ cudaError_t launch_tau_solve_2d(double2* Z, int n, int n_rows, const double2* la
                                 const double* sigma, double dt, const double2* tw_base,
                                 cudaStream_t st, bool forward = false);
 
+// ---- commuted ordering beyond kernels_commuted.cu's 1D n_space + 1 <= 8192 -------------------
+// time-level pairs as complex levels (kernels_2d.cu), one DST per complex row for n_space + 1 =
+// 16384..65536 (kernels_large.cu), one DST along the columns of n_planes 2D planes (kernels_2d.cu)
+cudaError_t launch_pack_pairs(const double* v, double2* U, int ns, int n_levels, double s, cudaStream_t st);
+cudaError_t launch_unpack_pairs(const double2* U, double* v, int ns, int n_levels, cudaStream_t st);
+cudaError_t launch_dst_large(double2* Z, int n_space, int n_rows, const double2* tw_base, cudaStream_t st);
+cudaError_t launch_dst_cols_2d(double2* Z, int n, int n_planes, const double2* tw_base, cudaStream_t st);
+
 // ---- generic sizes (kernels_generic.cu): Bluestein transforms along a strided batch ---------
 // sequence s (s < count) element j sits at data + (s / inner) * outer_stride + (s % inner) *
 // inner_stride + j * es; chirp / bhat as fft.hpp:71-89 (host-built); len <= 4096.

@@ -6,6 +6,8 @@
 // Lattice p = ix*n + iy (x slow, problems.hpp:164-165).  A CTA owns C consecutive iy columns of one
 // time block (matvec) or one frequency row (tau): each lattice row ix contributes C contiguous
 // values (coalesced), and each column becomes one smem FFT buffer.
+#include <algorithm>
+
 #include "dst_block.cuh"
 #include "fft_block.cuh"
 #include "kernels.cuh"
@@ -161,7 +163,7 @@ __global__ void __launch_bounds__(ColGeo<LOGM>::NT, (ColGeo<LOGM>::NT <= 256 ? 2
 // (lambda_r - dt sigma[ix*n + iy]), DST over ix again.  Rows (iy) are done before and after by
 // launch_dst_rows.
 // ------------------------------------------------------------------------------------------
-template <int LOGM, int MODE>  // MODE 1: solve (divide), 2: forward action (multiply)
+template <int LOGM, int MODE>  // MODE 1: solve (divide), 2: forward action (multiply), 0: one DST only
 __global__ void __launch_bounds__(ColGeo<LOGM>::NT, (ColGeo<LOGM>::NT <= 256 ? 2 : 1))
     k_tau_2d_cols(double2* __restrict__ Z, int n, const double2* __restrict__ lam,
                   const double* __restrict__ sigma, double dt, const double2* __restrict__ twb) {
@@ -198,6 +200,16 @@ __global__ void __launch_bounds__(ColGeo<LOGM>::NT, (ColGeo<LOGM>::NT <= 256 ? 2
     }
   }
   __syncthreads();
+  if constexpr (MODE == 0) {  // the column DST of the 2D lattice transform (commuted ordering)
+    block_dst<LOGM, BS, BH, 0>(smem, hbuf, twb, scale);
+    for (int e = threadIdx.x; e < C * NSR; e += NT) {
+      const int c = e % C, ix = e / C;
+      const int iy = iy0 + c;
+      if (iy >= NSR) continue;
+      Zr[size_t(ix) * NSR + iy] = smem[c * BS + pad16(ix)];
+    }
+    return;
+  }
   block_dst<LOGM, BS, BH, 1>(smem, hbuf, twb, scale);
   const double2 l = __ldg(lam + r);
   for (int e0 = threadIdx.x; e0 < C * NSR; e0 += U * NT) {
@@ -227,6 +239,38 @@ __global__ void __launch_bounds__(ColGeo<LOGM>::NT, (ColGeo<LOGM>::NT <= 256 ? 2
     if (iy >= NSR) continue;
     Zr[size_t(ix) * NSR + iy] = smem[c * BS + pad16(ix)];
   }
+}
+
+// ------------------------------------------------------------------------------------------
+// time levels (2j, 2j+1) as one complex level: U[j][p] = s (v[2j][p] + i v[2j+1][p]), and back.
+// The spatial transforms are real-linear, so a complex transform of the pair is the pair of real
+// transforms (the commuted ordering's DST per time level).
+__global__ void k_pack_pairs(const double* __restrict__ v, double2* __restrict__ U, int ns, size_t npairs_ns,
+                             double s) {
+  for (size_t e = size_t(blockIdx.x) * blockDim.x + threadIdx.x; e < npairs_ns; e += size_t(gridDim.x) * blockDim.x) {
+    const size_t j = e / size_t(ns), p = e - j * size_t(ns);
+    U[e] = make_double2(s * v[(2 * j) * size_t(ns) + p], s * v[(2 * j + 1) * size_t(ns) + p]);
+  }
+}
+__global__ void k_unpack_pairs(const double2* __restrict__ U, double* __restrict__ v, int ns, size_t npairs_ns) {
+  for (size_t e = size_t(blockIdx.x) * blockDim.x + threadIdx.x; e < npairs_ns; e += size_t(gridDim.x) * blockDim.x) {
+    const size_t j = e / size_t(ns), p = e - j * size_t(ns);
+    const double2 u = U[e];
+    v[(2 * j) * size_t(ns) + p] = u.x;
+    v[(2 * j + 1) * size_t(ns) + p] = u.y;
+  }
+}
+cudaError_t launch_pack_pairs(const double* v, double2* U, int ns, int n_levels, double s, cudaStream_t st) {
+  const size_t n = size_t(n_levels / 2) * size_t(ns);
+  k_pack_pairs<<<unsigned(std::min<size_t>((n + 255) / 256, 148 * 16)), 256, 0, st>>>(v, U, ns, n, s);
+  note_launch();
+  return cudaGetLastError();
+}
+cudaError_t launch_unpack_pairs(const double2* U, double* v, int ns, int n_levels, cudaStream_t st) {
+  const size_t n = size_t(n_levels / 2) * size_t(ns);
+  k_unpack_pairs<<<unsigned(std::min<size_t>((n + 255) / 256, 148 * 16)), 256, 0, st>>>(U, v, ns, n);
+  note_launch();
+  return cudaGetLastError();
 }
 
 // ------------------------------------------------------------------------------------------
@@ -274,6 +318,17 @@ static cudaError_t tau2d_cols(double2* Z, int n, int n_rows, const double2* lamb
   if (err != cudaSuccess) return err;
   const int tiles = (n + G::C - 1) / G::C;
   k_tau_2d_cols<LM, MODE><<<n_rows * tiles, G::NT, G::SMEM, st>>>(Z, n, lambda, sigma, dt, tw_base); note_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t launch_dst_cols_2d(double2* Z, int n, int n_planes, const double2* tw_base, cudaStream_t st) {
+  cudaError_t err = cudaSuccess;
+  const int lm = ilog2i(n + 1);
+#define CALL(LM)                                                                            \
+  err = tau2d_cols<LM, 0>(Z, n, n_planes, nullptr, nullptr, 0.0, tw_base, st);             \
+  if (err != cudaSuccess) return err;
+  FPC_DISPATCH_2D(lm, CALL)
+#undef CALL
   return cudaGetLastError();
 }
 

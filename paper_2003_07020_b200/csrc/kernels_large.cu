@@ -284,6 +284,19 @@ __global__ void __launch_bounds__(kThr, 1)
   dst_cl<C, 0, true>(row, smem, cluster, q, twb, l, sigma, dt);
 }
 
+// one DST-I per row (the commuted ordering's per-level DST at n_space + 1 >= 16384)
+template <int C>
+__global__ void __launch_bounds__(kThr, 1)
+    k_dst_cl(double2* __restrict__ Z, int ns, const double2* __restrict__ lam, const double* __restrict__ sigma,
+             double dt, const double2* __restrict__ twb) {
+  extern __shared__ double2 smem[];
+  cg::cluster_group cluster = cg::this_cluster();
+  const int q = int(cluster.block_rank());
+  double2* row = Z + size_t(blockIdx.x / C) * ns;
+  cluster_sync_relaxed(cluster);  // every CTA of the cluster is running before its shared memory is written
+  dst_cl<C, 0, true>(row, smem, cluster, q, twb, make_double2(1.0, 0.0), sigma, dt);
+}
+
 template <class K>
 cudaError_t launch_cl(K kernel, int C, int nclusters, cudaStream_t st, void** args) {
   cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
@@ -352,6 +365,20 @@ cudaError_t launch_tau_large(double2* Z, int n_space, int n_rows, const double2*
       return cudaErrorInvalidValue;
   }
 #undef TAU_CASE
+}
+
+cudaError_t launch_dst_large(double2* Z, int n_space, int n_rows, const double2* tw_base, cudaStream_t st) {
+  const int C = 2 * (n_space + 1) / kS;
+  const double2* lam = nullptr;
+  const double* sigma = nullptr;
+  double dt = 0.0;
+  void* args[] = {(void*)&Z, (void*)&n_space, (void*)&lam, (void*)&sigma, (void*)&dt, (void*)&tw_base};
+  switch (C) {
+    case 4: return launch_cl(k_dst_cl<4>, 4, n_rows, st, args);
+    case 8: return launch_cl(k_dst_cl<8>, 8, n_rows, st, args);
+    case 16: return launch_cl(k_dst_cl<16>, 16, n_rows, st, args);
+    default: return cudaErrorInvalidValue;
+  }
 }
 
 }  // namespace fpc

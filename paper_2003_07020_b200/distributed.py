@@ -10,7 +10,7 @@ Layouts (G ranks, N = Nt*Ns, H = Nt/2 + 1):
       all-to-all time -> space columns; time FFT (local columns); all-to-all space -> frequency rows;
       tau solves (local rows, alpha_circulant.hpp:160 -- the independent PinT work);
       all-to-all back to space; inverse time FFT; all-to-all back to time.
-  * PC apply, commuted ordering (ordering="commuted", 1D): DST of every local time
+  * PC apply, commuted ordering (ordering="commuted", 1D and 2D): DST of every local time
     level; all-to-all time -> space columns; per-column time solve (FFT, divide, inverse FFT);
     all-to-all back to time; DST of every local time level -- two all-to-alls instead of four,
     real-valued in flight, rounding-level difference from the reference ordering.

@@ -58,7 +58,8 @@ def _worker(rank, world, port, case, out_dir):
 
 @pytest.mark.parametrize("case", [(False, (1.5,), 31, 16, 0), (False, (1.3,), 63, 8, 5),
                                   (True, (1.3, 1.7), 7, 8, 0),
-                                  (False, (1.5,), 31, 16, 0, "commuted"), (False, (1.7,), 15, 32, 5, "commuted")])
+                                  (False, (1.5,), 31, 16, 0, "commuted"), (False, (1.7,), 15, 32, 5, "commuted"),
+                                  (True, (1.3, 1.7), 7, 8, 0, "commuted")])
 def test_sharded_solve_matches_oracle(tmp_path, oracle, case):
     world = 2
     mp.spawn(_worker, args=(world, free_port(), case, str(tmp_path)), nprocs=world, join=True)

@@ -10,7 +10,8 @@ from paper_2003_07020_b200 import problems
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("two_dim,ordering", [(False, "reference"), (True, "reference"), (False, "commuted")])
+@pytest.mark.parametrize("two_dim,ordering", [(False, "reference"), (True, "reference"), (False, "commuted"),
+                                             (True, "commuted")])
 def test_sharded_world1_matches_single_gpu(oracle, two_dim, ordering):
     torch = pytest.importorskip("torch")
     from paper_2003_07020_b200.distributed import CudaShardKernels, ShardedSolver
