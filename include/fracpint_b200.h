@@ -176,6 +176,12 @@ int fpc_shard_dots(fpc_context_t ctx, const double* const* V, const double* scal
                    const double* w, size_t n, int with_norm, double* out_host);
 int fpc_shard_update(fpc_context_t ctx, const double* const* V, const double* coef, int nv,
                      double* w, size_t n, double* norm2_host);
+/* the same two with the results left in device memory (stream-ordered, no host synchronisation):
+ * the sharded solver all-reduces them on the device and reads the sum once per reduction */
+int fpc_shard_dots_dev(fpc_context_t ctx, const double* const* V, const double* scales, int nv,
+                       const double* w, size_t n, int with_norm, double* out_dev);
+int fpc_shard_update_dev(fpc_context_t ctx, const double* const* V, const double* coef, int nv,
+                         double* w, size_t n, double* norm2_dev);
 int fpc_shard_lincomb(fpc_context_t ctx, const double* const* V, const double* coef, int nv,
                       double* u, size_t n);
 int fpc_shard_dst_levels(fpc_plan_t plan, const double* v, double* out, int nt_local, double s_in);

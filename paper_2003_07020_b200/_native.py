@@ -32,6 +32,7 @@ EXPORTS = [
     "fpc_alpha_circulant_eigenvalues", "fpc_plan_scales", "fpc_gmres_callbacks",
     "fpc_multi_create", "fpc_multi_destroy", "fpc_sharded_create_1d", "fpc_sharded_create_2d",
     "fpc_sharded_destroy", "fpc_sharded_info", "fpc_sharded_matvec", "fpc_sharded_pc_apply", "fpc_sharded_gmres",
+    "fpc_shard_dots_dev", "fpc_shard_update_dev",
 ]
 
 
@@ -112,6 +113,8 @@ def load():
     lib.fpc_plan_scales.argtypes = [vp, dp, dp]
     lib.fpc_gmres_callbacks.argtypes = [vp, C.c_size_t, APPLY_FN, vp, APPLY_FN, vp, dp, dp,
                                         C.POINTER(SolverConfigC), C.POINTER(ReportC), dp, C.c_int]
+    lib.fpc_shard_dots_dev.argtypes = [vp, vp, vp, C.c_int, vp, C.c_size_t, C.c_int, vp]
+    lib.fpc_shard_update_dev.argtypes = [vp, vp, vp, C.c_int, vp, C.c_size_t, vp]
     lib.fpc_multi_create.argtypes = [C.POINTER(C.c_int), C.c_int, C.POINTER(C.c_void_p)]
     lib.fpc_multi_destroy.argtypes = [vp]
     lib.fpc_sharded_create_1d.argtypes = [vp, d, d, d, C.c_int, C.c_int, d, d, C.POINTER(C.c_void_p)]

@@ -2072,6 +2072,49 @@ int fpc_shard_scatter_p2p(fpc_context_t c, const double* src, int rows, int cols
   });
 }
 
+// The same dots left on the device: out_dev[0..cnt) (device pointer), stream-ordered, no host sync
+// -- the sharded solver all-reduces them in place with NCCL and reads the sum once.
+int fpc_shard_dots_dev(fpc_context_t c, const double* const* V, const double* scales, int nv, const double* w,
+                       size_t n, int with_norm, double* out_dev) {
+  if (!c || !out_dev) return set_err(FPC_INVALID_ARGUMENT, "null argument");
+  return guarded([&] {
+    if (nv < 0 || nv > 250) throw InvalidArg{"fpc_shard_dots_dev: 0 <= nv <= 250"};
+    for (int i = 0; i < nv; ++i) check_dev_aligned(V[i], "fpc_shard_dots_dev");
+    check_dev_aligned(w, "fpc_shard_dots_dev");
+    DeviceGuard g(c->device);
+    GmresState S{nullptr, c, n, c->stream, std::vector<double>(scales, scales + nv), 0};
+    std::vector<const double*> vv(V, V + nv);
+    dots_into(S, vv, nv, w, nv == 0 ? true : with_norm != 0, 0);
+    const int cnt = nv + ((with_norm || nv == 0) ? 1 : 0);
+    ck(cudaMemcpyAsync(out_dev, c->dscal, size_t(cnt) * sizeof(double), cudaMemcpyDeviceToDevice, c->stream), "D2D");
+  });
+}
+
+// w <- w - sum_i coef_i V_i with ||w||^2 left at norm2_dev (device pointer), no host sync
+int fpc_shard_update_dev(fpc_context_t c, const double* const* V, const double* coef, int nv, double* w, size_t n,
+                         double* norm2_dev) {
+  if (!c || !norm2_dev) return set_err(FPC_INVALID_ARGUMENT, "null argument");
+  return guarded([&] {
+    if (nv < 0 || nv > 250) throw InvalidArg{"fpc_shard_update_dev: 0 <= nv <= 250"};
+    for (int i = 0; i < nv; ++i) check_dev_aligned(V[i], "fpc_shard_update_dev");
+    check_dev_aligned(w, "fpc_shard_update_dev");
+    DeviceGuard g(c->device);
+    std::vector<double> ones(size_t(nv), 1.0);
+    // the coefficient and pointer tables go through pinned staging (hpin), so the copies are
+    // genuinely asynchronous: wait for the previous user of that staging area first
+    ck(cudaStreamSynchronize(c->stream), "sync");
+    std::memcpy(c->hpin + 700, coef, size_t(nv) * sizeof(double));
+    std::memcpy(c->hpin + 1300, ones.data(), size_t(nv) * sizeof(double));
+    ck(cudaMemcpyAsync(c->dvptr, V, size_t(nv) * sizeof(double*), cudaMemcpyHostToDevice, c->stream), "vptr");
+    ck(cudaMemcpyAsync(c->dscales, c->hpin + 1300, size_t(nv) * sizeof(double), cudaMemcpyHostToDevice, c->stream),
+       "scales");
+    ck(cudaMemcpyAsync(c->dscal + 700, c->hpin + 700, size_t(nv) * sizeof(double), cudaMemcpyHostToDevice, c->stream),
+       "coef");
+    LAUNCH("update", c->stream, fpc::launch_update(c->dvptr, c->dscales, c->dscal + 700, nv, w, n, c->partial, c->stream));
+    LAUNCH("reduce", c->stream, fpc::launch_reduce(c->partial, 1, 1, norm2_dev, false, c->stream));
+  });
+}
+
 // w <- w - sum_i coef_i * V_i (coef on the host, scales already folded in); returns ||w||^2.
 int fpc_shard_update(fpc_context_t c, const double* const* V, const double* coef, int nv, double* w,
                      size_t n, double* norm2_host) {

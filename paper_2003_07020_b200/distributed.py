@@ -112,6 +112,22 @@ class CudaShardKernels:
                                         self._p(w), w.numel(), int(with_norm), C.c_void_p(out.ctypes.data)))
         return out[:len(V) + (1 if with_norm or not V else 0)]
 
+    # device-resident variants: the partial sums stay on the GPU for an in-place NCCL all-reduce
+    def dots_dev(self, V, scales, w, with_norm):
+        cnt = len(V) + (1 if with_norm or not V else 0)
+        out = torch.empty(max(cnt, 1), dtype=torch.float64, device=self.device)
+        sc = np.ascontiguousarray(scales, dtype=np.float64)
+        N.check(self.lib.fpc_shard_dots_dev(self.ctx.h, self._ptrs(V), C.c_void_p(sc.ctypes.data), len(V),
+                                            self._p(w), w.numel(), int(with_norm), self._p(out)))
+        return out[:cnt]
+
+    def update_dev(self, V, coef, w):
+        c = np.ascontiguousarray(coef, dtype=np.float64)
+        out = torch.empty(1, dtype=torch.float64, device=self.device)
+        N.check(self.lib.fpc_shard_update_dev(self.ctx.h, self._ptrs(V), C.c_void_p(c.ctypes.data), len(V),
+                                              self._p(w), w.numel(), self._p(out)))
+        return out
+
     def update(self, V, coef, w):
         c = np.ascontiguousarray(coef, dtype=np.float64)
         out = np.zeros(1)
@@ -251,6 +267,10 @@ class ShardedSolver:
         self.hs = split_counts(self.H, self.G)
         self.ho = offsets(self.hs)
         self.koff = self.rank * self.nt_loc
+        # CUDA kernels: Gram-Schmidt partials reduced on the device (one host read per reduction)
+        self._dev_reduce = hasattr(kernels, "dots_dev")
+        if self._dev_reduce:
+            self._lib_stream = torch.cuda.ExternalStream(kernels.ctx.stream_handle, device=kernels.device)
         self.p2p = None
         if transport == "p2p":
             r = self.rank
@@ -302,18 +322,44 @@ class ShardedSolver:
         dist.all_reduce(t, group=self.group)
         return t.cpu().numpy()
 
+    def _allreduce_dev(self, t):
+        """In-place all-reduce of device partials, enqueued on the library stream behind the kernels
+        that produced them; one host read of the sum."""
+        if self.G > 1:
+            with torch.cuda.stream(self._lib_stream):
+                dist.all_reduce(t, group=self.group)
+        return t.cpu().numpy()
+
+    def _dots(self, V, sc, w, with_norm):
+        if self._dev_reduce:
+            return self._allreduce_dev(self.k.dots_dev(V, sc, w, with_norm))
+        return self._allreduce(self.k.dots(V, sc, w, with_norm))
+
+    def _update(self, V, coef, w):
+        if self._dev_reduce:
+            return float(self._allreduce_dev(self.k.update_dev(V, coef, w))[0])
+        return float(self._allreduce(np.array([self.k.update(V, coef, w)]))[0])
+
+    def _peer(self, group_rank):
+        return dist.get_global_rank(self.group, group_rank) if self.group is not None else group_rank
+
     # ------------------------------------------------------------------ operators
     def matvec(self, v_loc):
         ns, G, r = self.ns, self.G, self.rank
         halo = None
         if G > 1:
-            tail = v_loc[(self.nt_loc - 2) * ns:].contiguous() if self.nt_loc >= 2 else None
-            if tail is None:
+            if self.nt_loc < 2:
                 raise ValueError("ShardedSolver: need at least two time blocks per rank")
-            gathered = [torch.empty_like(tail) for _ in range(G)]
-            dist.all_gather(gathered, tail, group=self.group)
+            # the BDF2 halo (the last two levels of rank r-1) point to point: send to r+1, receive from r-1
+            tail = v_loc[(self.nt_loc - 2) * ns:].contiguous()
+            ops = []
+            if r + 1 < G:
+                ops.append(dist.P2POp(dist.isend, tail, self._peer(r + 1), group=self.group))
             if r > 0:
-                halo = gathered[r - 1]
+                halo = torch.empty_like(tail)
+                ops.append(dist.P2POp(dist.irecv, halo, self._peer(r - 1), group=self.group))
+            for req in dist.batch_isend_irecv(ops):
+                req.wait()
         if halo is not None:
             buf = torch.cat([halo, v_loc])
             return self.k.matvec(buf, self.nt_loc, self.koff, True)
@@ -379,7 +425,7 @@ class ShardedSolver:
 
     # ------------------------------------------------------------------ GMRES
     def _norm(self, w):
-        return math.sqrt(float(self._allreduce(self.k.dots([], [], w, True))[0]))
+        return math.sqrt(float(self._dots([], [], w, True)[0]))
 
     def _inner(self, b, tol, max_iter, rep):
         """One unrestarted gmres_right (x0 = 0) on rhs b; returns x, steps, converged."""
@@ -393,15 +439,15 @@ class ShardedSolver:
             z = self.pc_apply(V[j], sc[j])
             w = self.matvec(z)
             nv = j + 1
-            d = self._allreduce(self.k.dots(V, sc, w, True))
+            d = self._dots(V, sc, w, True)
             h = list(d[:nv]) + [0.0]
             norm_before = math.sqrt(d[nv])
-            nw2 = self._allreduce(np.array([self.k.update(V, [h[i] * sc[i] for i in range(nv)], w)]))[0]
+            nw2 = self._update(V, [h[i] * sc[i] for i in range(nv)], w)
             norm_w = math.sqrt(nw2)
             if norm_w < 0.70710678118654752 * norm_before:  # krylov.hpp:123-130
                 rep.reorthogonalizations += 1
-                c2 = self._allreduce(self.k.dots(V, sc, w, False))
-                nw2 = self._allreduce(np.array([self.k.update(V, [c2[i] * sc[i] for i in range(nv)], w)]))[0]
+                c2 = self._dots(V, sc, w, False)
+                nw2 = self._update(V, [c2[i] * sc[i] for i in range(nv)], w)
                 for i in range(nv):
                     h[i] += c2[i]
                 norm_w = math.sqrt(nw2)
