@@ -75,6 +75,9 @@ cudaError_t launch_matvec_rows_warp(const double* v, double* y, int len, int nro
                                     int log_m, const double* eig_scaled, const double2* tw_base,
                                     cudaStream_t st, int koff);
 bool warp_kernels_enabled();
+// the 2D matvec's x-direction column pass on warp-owned transforms for log_m = 8 (n <= 255)
+cudaError_t launch_matvec_cols_warp(const double* v, double* y, int n, int n_time, int log_m, const double* eig_x,
+                                    const double2* tw_base, cudaStream_t st);
 // DST rows of n = 255 on warp-owned transforms (kernels_warp.cu): mode 0 = in-place DST of each row,
 // 1 / 2 = DST, divide / multiply by lambda_row - dt sigma, DST (the 1D tau solve / forward action).
 // cudaErrorNotSupported for other n.

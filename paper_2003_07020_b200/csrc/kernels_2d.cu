@@ -297,6 +297,8 @@ cudaError_t launch_matvec_2d(const double* v, double* y, int n, int n_time, int 
   cudaError_t err =
       launch_matvec_rows(v, y, n, n_time * n, n, n * n, log_m, eig_y_scaled, tw_base, st, koff);
   if (err != cudaSuccess) return err;
+  if (log_m == 8 && warp_kernels_enabled())
+    return launch_matvec_cols_warp(v, y, n, n_time, log_m, eig_x_scaled, tw_base, st);
 #define CALL(LM)                                                                          \
   {                                                                                       \
     using G = ColGeo<LM>;                                                                 \

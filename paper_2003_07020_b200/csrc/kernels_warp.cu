@@ -214,4 +214,171 @@ cudaError_t launch_dst_rows_warp(double2* Z, int n, int n_rows, const double2* l
   return cudaGetLastError();
 }
 
+// ------------------------------------------------------------------------------------------
+// 2D matvec, x-direction half (jacobian.hpp:88-93): y[k][ix][iy] += (dt sx / 2L) (T_x v[k][.][iy])[ix]
+// for n <= 255 (M = 256).  A CTA owns 16 columns iy of one time level: the [256][16] tile is
+// loaded cooperatively (128-byte row segments, coalesced) into shared memory, each 16-lane group
+// transforms one column straight from the tile (no CTA barrier inside the transforms), writes the
+// result back into its tile column, and the CTA adds the tile to y row by row (coalesced).
+constexpr int kColTile = 16;         // columns per CTA = groups per CTA
+constexpr int kColPitch = 17;        // tile row pitch in doubles: the groups' column reads hit 16 bank pairs
+__global__ void __launch_bounds__(32 * kWarpsPerCta, 2)
+    k_mv_cols_warp(const double* __restrict__ v, double* __restrict__ y, int n, const double* __restrict__ eig,
+                   const double2* __restrict__ twb) {
+  constexpr int R = 16, M = R * R, L = 2 * M, H = R / 2, G = 2;
+  constexpr int LD = WarpFftTile<R>::LD;
+  constexpr int NTHR = 32 * kWarpsPerCta;
+  extern __shared__ double2 wsm[];
+  double* tile = reinterpret_cast<double*>(wsm + kWarpsPerCta * G * WarpFftTile<R>::SIZE);  // [M][kColPitch]
+  const int tiles = (n + kColTile - 1) / kColTile;
+  const int k = int(blockIdx.x) / tiles;
+  const int iy0 = (int(blockIdx.x) - k * tiles) * kColTile;
+  const size_t base = size_t(k) * size_t(n) * size_t(n);
+  const int ncol = min(kColTile, n - iy0);
+  // 1. tile load: element (ix, c) = v[k][ix][iy0 + c], rows ix >= n zero (16 loads in flight per thread)
+  constexpr int UL = M * kColTile / NTHR;  // 16
+  double x[UL];
+#pragma unroll
+  for (int u = 0; u < UL; ++u) {
+    const int e = int(threadIdx.x) + u * NTHR;
+    const int ix = e / kColTile, c = e % kColTile;
+    x[u] = (ix < n && c < ncol) ? v[base + size_t(ix) * n + iy0 + c] : 0.0;
+  }
+#pragma unroll
+  for (int u = 0; u < UL; ++u) {
+    const int e = int(threadIdx.x) + u * NTHR;
+    tile[(e / kColTile) * kColPitch + e % kColTile] = x[u];
+  }
+  __syncthreads();
+  // 2. one column per group: packed slot m = t + R r holds (x_{2m}, x_{2m+1}) of the column
+  const int lane = int(threadIdx.x) & 31;
+  const int t = lane & (R - 1);
+  const int grp = (int(threadIdx.x) >> 5) * G + lane / R;  // = the tile column
+  double2* xs = wsm + grp * WarpFftTile<R>::SIZE;
+  double2 z[R];
+#pragma unroll
+  for (int r = 0; r < H; ++r) {
+    const int m = t + R * r;
+    z[r] = make_double2(tile[(2 * m) * kColPitch + grp], tile[(2 * m + 1) * kColPitch + grp]);
+  }
+#pragma unroll
+  for (int r = H; r < R; ++r) z[r] = make_double2(0.0, 0.0);
+  warp_fft_sq<R, -1>(z, xs, t, twb);
+#pragma unroll
+  for (int p = 0; p < R; ++p) xs[p * LD + t] = z[p];
+  __syncwarp();
+  const int tm = (R - t) & (R - 1);
+#pragma unroll
+  for (int p = 0; p < R; ++p) {
+    const int pm = t == 0 ? ((R - p) & (R - 1)) : (R - 1 - p);
+    z[p] = packed_eig_product<M>(z[p], xs[pm * LD + tm], t + R * p, eig, twb + L);
+  }
+  __syncwarp();
+  warp_fft_sq<R, 1>(z, xs, t, twb);
+#pragma unroll
+  for (int r = 0; r < H; ++r) {
+    const int m = t + R * r;
+    tile[(2 * m) * kColPitch + grp] = z[r].x;
+    tile[(2 * m + 1) * kColPitch + grp] = z[r].y;
+  }
+  __syncthreads();
+  // 3. y += tile, row segments of ncol doubles (coalesced read-modify-write)
+  double yo[UL];
+#pragma unroll
+  for (int u = 0; u < UL; ++u) {
+    const int e = int(threadIdx.x) + u * NTHR;
+    const int ix = e / kColTile, c = e % kColTile;
+    yo[u] = (ix < n && c < ncol) ? y[base + size_t(ix) * n + iy0 + c] : 0.0;
+  }
+#pragma unroll
+  for (int u = 0; u < UL; ++u) {
+    const int e = int(threadIdx.x) + u * NTHR;
+    const int ix = e / kColTile, c = e % kColTile;
+    if (ix < n && c < ncol) y[base + size_t(ix) * n + iy0 + c] = yo[u] + tile[ix * kColPitch + c];
+  }
+}
+
+// The same column pass without the shared tile: each group loads its column straight into
+// registers (a warp's two groups read 16 B per row; a CTA's 8 warps cover 128-byte row segments, so
+// the L2 sectors are shared within the CTA) and adds its result to y directly -- warps never wait
+// on each other.  FPC_COLS_TILE=1 selects the tiled kernel above (A/B).
+__global__ void __launch_bounds__(32 * kWarpsPerCta, 2)
+    k_mv_cols_direct(const double* __restrict__ v, double* __restrict__ y, int n, const double* __restrict__ eig,
+                     const double2* __restrict__ twb) {
+  constexpr int R = 16, M = R * R, L = 2 * M, H = R / 2, G = 2;
+  constexpr int LD = WarpFftTile<R>::LD;
+  extern __shared__ double2 wsm[];
+  const int tiles = (n + kColTile - 1) / kColTile;
+  const int k = int(blockIdx.x) / tiles;
+  const int lane = int(threadIdx.x) & 31;
+  const int t = lane & (R - 1);
+  const int grp = (int(threadIdx.x) >> 5) * G + lane / R;
+  const int iy = (int(blockIdx.x) - k * tiles) * kColTile + grp;
+  const bool valid = iy < n;
+  const double* vc = v + size_t(k) * size_t(n) * size_t(n) + (valid ? iy : 0);
+  double2* xs = wsm + grp * WarpFftTile<R>::SIZE;
+  double2 z[R];
+#pragma unroll
+  for (int r = 0; r < H; ++r) {
+    const int i0 = 2 * (t + R * r);
+    z[r] = make_double2(i0 < n ? vc[size_t(i0) * n] : 0.0, i0 + 1 < n ? vc[size_t(i0 + 1) * n] : 0.0);
+  }
+#pragma unroll
+  for (int r = H; r < R; ++r) z[r] = make_double2(0.0, 0.0);
+  warp_fft_sq<R, -1>(z, xs, t, twb);
+#pragma unroll
+  for (int p = 0; p < R; ++p) xs[p * LD + t] = z[p];
+  __syncwarp();
+  const int tm = (R - t) & (R - 1);
+#pragma unroll
+  for (int p = 0; p < R; ++p) {
+    const int pm = t == 0 ? ((R - p) & (R - 1)) : (R - 1 - p);
+    z[p] = packed_eig_product<M>(z[p], xs[pm * LD + tm], t + R * p, eig, twb + L);
+  }
+  __syncwarp();
+  warp_fft_sq<R, 1>(z, xs, t, twb);
+  if (valid) {
+    double* yc = y + size_t(k) * size_t(n) * size_t(n) + iy;
+    double yo[2 * H];
+#pragma unroll
+    for (int r = 0; r < H; ++r) {
+      const int i0 = 2 * (t + R * r);
+      yo[2 * r] = i0 < n ? yc[size_t(i0) * n] : 0.0;
+      yo[2 * r + 1] = i0 + 1 < n ? yc[size_t(i0 + 1) * n] : 0.0;
+    }
+#pragma unroll
+    for (int r = 0; r < H; ++r) {
+      const int i0 = 2 * (t + R * r);
+      if (i0 < n) yc[size_t(i0) * n] = yo[2 * r] + z[r].x;
+      if (i0 + 1 < n) yc[size_t(i0 + 1) * n] = yo[2 * r + 1] + z[r].y;
+    }
+  }
+}
+
+cudaError_t launch_matvec_cols_warp(const double* v, double* y, int n, int n_time, int log_m, const double* eig_x,
+                                    const double2* tw_base, cudaStream_t st) {
+  if (log_m != 8) return cudaErrorNotSupported;
+  constexpr int R = 16, G = 2, M = 256;
+  const int tiles = (n + kColTile - 1) / kColTile;
+  static const bool tiled = [] {
+    const char* e = std::getenv("FPC_COLS_TILE");
+    return e && e[0] == '1';
+  }();
+  if (!tiled) {
+    const size_t smem = size_t(kWarpsPerCta) * G * WarpFftTile<R>::SIZE * sizeof(double2);
+    cudaError_t e = cudaFuncSetAttribute(k_mv_cols_direct, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    if (e != cudaSuccess) return e;
+    k_mv_cols_direct<<<unsigned(n_time) * unsigned(tiles), 32 * kWarpsPerCta, smem, st>>>(v, y, n, eig_x, tw_base);
+    note_launch();
+    return cudaGetLastError();
+  }
+  const size_t smem = size_t(kWarpsPerCta) * G * WarpFftTile<R>::SIZE * sizeof(double2) +
+                      size_t(M) * kColPitch * sizeof(double);
+  cudaError_t e = cudaFuncSetAttribute(k_mv_cols_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  if (e != cudaSuccess) return e;
+  k_mv_cols_warp<<<unsigned(n_time) * unsigned(tiles), 32 * kWarpsPerCta, smem, st>>>(v, y, n, eig_x, tw_base);
+  note_launch();
+  return cudaGetLastError();
+}
+
 }  // namespace fpc
