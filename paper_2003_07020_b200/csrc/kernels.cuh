@@ -75,6 +75,9 @@ cudaError_t launch_matvec_rows_warp(const double* v, double* y, int len, int nro
                                     int log_m, const double* eig_scaled, const double2* tw_base,
                                     cudaStream_t st, int koff);
 bool warp_kernels_enabled();
+// the 2D tau solve's column pass (DST, shift, DST along ix) on warp-owned transforms for n = 255
+cudaError_t launch_tau_cols_warp(double2* Z, int n, int n_planes, const double2* lambda, const double* sigma,
+                                 double dt, const double2* tw_base, cudaStream_t st, bool forward);
 // the 2D matvec's x-direction column pass on warp-owned transforms for log_m = 8 (n <= 255)
 cudaError_t launch_matvec_cols_warp(const double* v, double* y, int n, int n_time, int log_m, const double* eig_x,
                                     const double2* tw_base, cudaStream_t st);

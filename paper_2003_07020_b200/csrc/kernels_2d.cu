@@ -341,6 +341,11 @@ cudaError_t launch_tau_solve_2d(double2* Z, int n, int n_rows, const double2* la
   cudaError_t err = launch_dst_rows(Z, n, n_rows * n, tw_base, st);
   if (err != cudaSuccess) return err;
   const int lm = ilog2i(n + 1);
+  if (n == 255 && warp_kernels_enabled()) {
+    if ((err = launch_tau_cols_warp(Z, n, n_rows, lambda, sigma, dt, tw_base, st, forward)) != cudaSuccess)
+      return err;
+    return launch_dst_rows(Z, n, n_rows * n, tw_base, st);
+  }
 #define CALL(LM)                                                                            \
   err = forward ? tau2d_cols<LM, 2>(Z, n, n_rows, lambda, sigma, dt, tw_base, st)           \
                 : tau2d_cols<LM, 1>(Z, n, n_rows, lambda, sigma, dt, tw_base, st);          \

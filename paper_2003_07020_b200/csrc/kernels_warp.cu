@@ -381,4 +381,66 @@ cudaError_t launch_matvec_cols_warp(const double* v, double* y, int n, int n_tim
   return cudaGetLastError();
 }
 
+// 2D tau solve, column pass (tau.hpp:79-119 along ix): for frequency plane r and column iy, DST over
+// ix, divide (MODE 1) / multiply (MODE 2) by lambda_r - dt sigma[ix n + iy], DST over ix, in place.
+// One 16-lane group per column, loads straight from global memory (a warp's two groups read
+// adjacent 16-byte elements of each row; a CTA's 16 groups cover 256-byte row segments), the
+// intermediate kept in the group's tile.  n = 255.
+template <int MODE>
+__global__ void __launch_bounds__(32 * kWarpsPerCta, 2)
+    k_tau_cols_warp(double2* __restrict__ Z, int n_planes, const double2* __restrict__ lam,
+                    const double* __restrict__ sigma, double dt, const double2* __restrict__ twb) {
+  constexpr int R = 16, G = 2, NSR = 255, NG = kWarpsPerCta * G;
+  extern __shared__ double2 wsm[];
+  constexpr int tiles = (NSR + NG - 1) / NG;
+  const int rp = int(blockIdx.x) / tiles;
+  const int lane = int(threadIdx.x) & 31;
+  const int t = lane & (R - 1);
+  const int grp = (int(threadIdx.x) >> 5) * G + lane / R;
+  const int iy = (int(blockIdx.x) - rp * tiles) * NG + grp;
+  const bool valid = iy < NSR;
+  double2* zc = Z + size_t(rp) * NSR * NSR + (valid ? iy : 0);
+  double2* xs = wsm + grp * kDstTileSize;
+  const double scale = 0.088388347648318440550;  // sqrt(2/256)
+  warp_dst256([&](int j) { return zc[size_t(j - 1) * NSR]; }, xs, t, twb, scale);
+  const double2 l = __ldg(lam + rp);
+  const double* sg = sigma + (valid ? iy : 0);
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int i = t + R * r;
+    if (i < NSR) xs[dst_slot(i)] = shift_apply<MODE>(xs[dst_slot(i)], l.x - dt * __ldg(sg + size_t(i) * NSR), l.y);
+  }
+  __syncwarp();
+  warp_dst256([&](int j) { return xs[dst_slot(j - 1)]; }, xs, t, twb, scale);
+  if (valid) {
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int i = t + R * r;
+      if (i < NSR) zc[size_t(i) * NSR] = xs[dst_slot(i)];
+    }
+  }
+}
+
+cudaError_t launch_tau_cols_warp(double2* Z, int n, int n_planes, const double2* lambda, const double* sigma,
+                                 double dt, const double2* tw_base, cudaStream_t st, bool forward) {
+  if (n != 255) return cudaErrorNotSupported;
+  constexpr int NG = kWarpsPerCta * 2;
+  const size_t smem = size_t(NG) * kDstTileSize * sizeof(double2);
+  const unsigned grid = unsigned(n_planes) * unsigned((255 + NG - 1) / NG);
+  cudaError_t e = cudaSuccess;
+  if (forward) {
+    if ((e = cudaFuncSetAttribute(k_tau_cols_warp<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem))) !=
+        cudaSuccess)
+      return e;
+    k_tau_cols_warp<2><<<grid, 32 * kWarpsPerCta, smem, st>>>(Z, n_planes, lambda, sigma, dt, tw_base);
+  } else {
+    if ((e = cudaFuncSetAttribute(k_tau_cols_warp<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem))) !=
+        cudaSuccess)
+      return e;
+    k_tau_cols_warp<1><<<grid, 32 * kWarpsPerCta, smem, st>>>(Z, n_planes, lambda, sigma, dt, tw_base);
+  }
+  note_launch();
+  return cudaGetLastError();
+}
+
 }  // namespace fpc
