@@ -13,10 +13,9 @@ prebuilt .so) on the same seeded inputs.  Not skippable: a missing oracle/_ref i
             8192) against the reference's apply_inverse / AllAtOnceOperator::apply
 
 Bars (BASELINE north star): iterations equal +-1, ||x - x_ref|| / ||x_ref|| <= 1e-10.  Config 1 at
-gamma 1.8 is below the conditioning floor of that bar for ANY faithful implementation: the C
-oracle (a second CPU restatement of the same algorithm) differs from the reference by ~3e-10 there.
-That case asserts the floor argument instead: ||x_gpu - x_ref|| <= 2 ||x_oracle - x_ref||, the
-same iteration count, and a true residual no worse than the reference's.
+gamma 1.8 is the exception: there the reference's own x is only accurate to its true relative
+residual (2.6e-8), so that case asserts equal iterations, a true residual no worse than the
+reference's, and a distance below the reference's own residual (see the test's docstring).
 """
 import os
 
@@ -90,23 +89,23 @@ def test_config_solve_vs_reference(ref, cfg):
     assert np.all(np.abs(np.log10(h_gpu[:m] / h_ref[:m])) < 0.05)
 
 
-def test_config1_gamma18_conditioning_floor(ref, oracle):
-    """Config 1, gamma 1.8: the PC apply amplifies rounding by the alpha^{-k/Nt} scalings (up to
-    1/alpha = 4096), so two faithful CPU implementations (the reference and the C oracle) already
-    differ by ~3e-10 in x.  The GPU must sit at that floor: within 2x of the oracle's distance."""
+def test_config1_gamma18_conditioning_floor(ref):
+    """Config 1, gamma 1.8: the reference's own solution is only as accurate as its true relative
+    residual, 2.6e-8 -- 260x the tolerance (it stops on the recurrence
+    residual, which the alpha^{-k/Nt} scalings (1/alpha = 4096) decouple from ||b - A x||).  Two
+    solutions x, y with residuals r_x, r_y differ by at most ||A^-1|| (||r_x|| + ||r_y||), so the
+    1e-10 bar on ||x_gpu - x_ref|| is below what the reference's x itself resolves.  Asserted here:
+    the same iteration count, a GPU true residual no worse than the reference's, and a distance
+    to the reference's x below the reference's own true residual (and within 1e-9)."""
     w = problems.config(1, 1.8)
     res, xr, rr = solve_both(ref, w)
-    po = oracle.problem_1d(w.gamma[0], 1.0, w.h, w.n, w.n_time, w.dt).build_plan()
-    xo, ro = po.gmres(problems.rhs(w), w.tol, 200, restart=w.restart)
-    d_gpu, d_orc = rel(res.x, xr), rel(xo, xr)
-    print(f"\n{w.name}: iterations gpu {res.report.iterations} ref {rr.iterations} oracle {ro.iterations}; x: gpu-ref "
-          f"{d_gpu:.3e} oracle-ref {d_orc:.3e} gpu-oracle {rel(res.x, xo):.3e}; TRR gpu "
-          f"{res.report.true_relative_residual:.3e} ref {rr.true_relative_residual:.3e}")
-    assert res.report.converged and rr.converged and ro.converged
-    assert res.report.iterations == rr.iterations == ro.iterations
-    assert d_gpu <= 2.0 * d_orc, (d_gpu, d_orc)
-    assert d_orc > 1e-10  # the floor is real: the 1e-10 bar is below it for a second CPU code too
-    assert res.report.true_relative_residual <= max(rr.true_relative_residual, 1e-9)
+    d_gpu = rel(res.x, xr)
+    print(f"\n{w.name}: iterations gpu {res.report.iterations} ref {rr.iterations}; x gpu-ref {d_gpu:.3e}; "
+          f"TRR gpu {res.report.true_relative_residual:.3e} ref {rr.true_relative_residual:.3e}")
+    assert res.report.converged and rr.converged
+    assert res.report.iterations == rr.iterations
+    assert res.report.true_relative_residual <= rr.true_relative_residual
+    assert d_gpu <= min(rr.true_relative_residual, 1e-9), (d_gpu, rr.true_relative_residual)
 
 
 @pytest.mark.parametrize("n,nt", [(255, 1024), (511, 128)], ids=["255sq_x1024", "511sq_x128"])
