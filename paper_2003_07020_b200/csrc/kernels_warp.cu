@@ -45,6 +45,60 @@ __device__ __forceinline__ double2 packed_eig_product(double2 own, double2 mir, 
   return lo ? cadd(A, mul_si<1>(cmul(D, cconj(w)))) : cadd(cconj(A), mul_si<1>(cmul(cconj(D), w)));
 }
 
+// The packed circulant product of a whole group spectrum with each mirror pair (k, M - k) formed
+// once: lane t computes the pairs of its bins k = t + 16 p, p < 8 (k < M/2), keeps U_k and stores
+// U_{M-k} into the tile slot of bin M - k -- a slot only this lane reads (its mirror operand,
+// read just before) -- then reads its bins p >= 8 back; bin M/2 (lane 0, p = 8) pairs with itself.
+// Same per-pair arithmetic as k_matvec_1d's spectral loop (kernels_1d.cu).
+template <int R>
+__device__ __forceinline__ void warp_packed_product(double2 (&z)[R], double2* __restrict__ xs, int t,
+                                                    const double* __restrict__ eig, const double2* __restrict__ twL) {
+  constexpr int M = R * R, LD = WarpFftTile<R>::LD, H = R / 2;
+#pragma unroll
+  for (int p = 0; p < R; ++p) xs[p * LD + t] = z[p];
+  __syncwarp();
+  const int tm = (R - t) & (R - 1);
+  const double2 mid = z[H];  // lane 0: bin M/2
+#pragma unroll
+  for (int p = 0; p < H; ++p) {
+    const int k = t + R * p;
+    const double2 a = z[p];
+    if (k == 0) {
+      const double y0 = __ldg(eig) * (2.0 * (a.x + a.y));
+      const double ym = __ldg(eig + M) * (2.0 * (a.x - a.y));
+      z[p] = make_double2(y0 + ym, y0 - ym);
+      continue;
+    }
+    const int pm = t == 0 ? ((R - p) & (R - 1)) : (R - 1 - p);
+    double2* slot = xs + pm * LD + tm;
+    const double2 bq = *slot;
+    const double2 w = __ldg(twL + k);  // e^{-2 pi i k/L}
+    const double ek = __ldg(eig + k), em = __ldg(eig + M - k);
+    const double2 P = cadd(a, cconj(bq)), Q = csub(a, cconj(bq));
+    const double2 iwQ = mul_si<1>(cmul(w, Q));
+    const double2 Yk = cscale(csub(P, iwQ), ek);
+    const double2 Ym = cscale(cconj(cadd(P, iwQ)), em);
+    const double2 A = cadd(Yk, cconj(Ym)), D = csub(Yk, cconj(Ym));
+    z[p] = cadd(A, mul_si<1>(cmul(D, cconj(w))));
+    *slot = cadd(cconj(A), mul_si<1>(cmul(cconj(D), w)));
+  }
+  if (t == 0) {  // the self pair k = M/2
+    const double2 w = __ldg(twL + M / 2);
+    const double ek = __ldg(eig + M / 2);
+    const double2 P = cadd(mid, cconj(mid)), Q = csub(mid, cconj(mid));
+    const double2 iwQ = mul_si<1>(cmul(w, Q));
+    const double2 Yk = cscale(csub(P, iwQ), ek);
+    const double2 Ym = cscale(cconj(cadd(P, iwQ)), ek);
+    const double2 A = cadd(Yk, cconj(Ym)), D = csub(Yk, cconj(Ym));
+    z[H] = cadd(A, mul_si<1>(cmul(D, cconj(w))));
+  }
+  __syncwarp();
+#pragma unroll
+  for (int p = H; p < R; ++p)
+    if (!(t == 0 && p == H)) z[p] = xs[p * LD + t];
+  __syncwarp();
+}
+
 // BDF2 stencil part (time_stencil.hpp:16-26, same association as all_at_once.hpp:44-53)
 __device__ __forceinline__ double bdf2(int k, double x0, double x1, double x2) {
   if (k == 0) return x0;
@@ -105,23 +159,10 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta, 2)
     c[2 * r + 1] = bdf2(k, z[r].y, x1[2 * r + 1], x2[2 * r + 1]);
   }
 
-  warp_fft_sq<R, -1>(z, xs, t, twb);  // lane t now holds Z_{t + R p}
-
-  // spectral product: each bin with its mirror M - k (lane (R - t) mod R, register R-1-p; or
-  // this lane's register (R - p) mod R when t = 0), exchanged through the tile
-#pragma unroll
-  for (int p = 0; p < R; ++p) xs[p * LD + t] = z[p];
-  __syncwarp();
-  const int tm = (R - t) & (R - 1);
-#pragma unroll
-  for (int p = 0; p < R; ++p) {
-    const int pm = t == 0 ? ((R - p) & (R - 1)) : (R - 1 - p);
-    const double2 mir = xs[pm * LD + tm];
-    z[p] = packed_eig_product<M>(z[p], mir, t + R * p, eig, twb + L);
-  }
-  __syncwarp();
-
-  warp_fft_sq<R, 1>(z, xs, t, twb);  // lane t holds the packed inverse at slots t + R r again
+  // the zero-padded upper half in, the truncated lower half out (pruned first / last passes)
+  warp_fft_sq<R, -1, true, false>(z, xs, t, twb);  // lane t now holds Z_{t + R p}
+  warp_packed_product<R>(z, xs, t, eig, twb + L);   // each mirror pair (k, M - k) once
+  warp_fft_sq<R, 1, false, true>(z, xs, t, twb);   // lane t holds the packed inverse at slots t + R r < M/2
 
   if (valid) {
     double* yr = y + size_t(row) * ns;
@@ -325,18 +366,9 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta, 2)
   }
 #pragma unroll
   for (int r = H; r < R; ++r) z[r] = make_double2(0.0, 0.0);
-  warp_fft_sq<R, -1>(z, xs, t, twb);
-#pragma unroll
-  for (int p = 0; p < R; ++p) xs[p * LD + t] = z[p];
-  __syncwarp();
-  const int tm = (R - t) & (R - 1);
-#pragma unroll
-  for (int p = 0; p < R; ++p) {
-    const int pm = t == 0 ? ((R - p) & (R - 1)) : (R - 1 - p);
-    z[p] = packed_eig_product<M>(z[p], xs[pm * LD + tm], t + R * p, eig, twb + L);
-  }
-  __syncwarp();
-  warp_fft_sq<R, 1>(z, xs, t, twb);
+  warp_fft_sq<R, -1, true, false>(z, xs, t, twb);
+  warp_packed_product<R>(z, xs, t, eig, twb + L);
+  warp_fft_sq<R, 1, false, true>(z, xs, t, twb);
   if (valid) {
     double* yc = y + size_t(k) * size_t(n) * size_t(n) + iy;
     double yo[2 * H];

@@ -31,15 +31,67 @@ struct WarpFftTile {
   static constexpr int SIZE = R * LD;  // double2 per group
 };
 
+// v *= w^{S r} with w = e^{2 pi i/16}, r < 8 (the constants of Dft<16>)
+template <int S>
+__device__ __forceinline__ double2 rot16(double2 x, int r) {
+  if (r == 0) return x;
+  if (r == 4) return mul_si<S>(x);
+  const double c = kC16[r], sn = S * kC16[(r + 12) & 15];
+  return make_double2(fma(x.x, c, -x.y * sn), fma(x.x, sn, x.y * c));
+}
+
+// DFT_16 of v[0..7] with v[8..15] = 0 (the zero-padded half of a packed circulant embedding):
+// X_{2q} = DFT_8(v)_q, X_{2q+1} = DFT_8(v_r w^r)_q -- a quarter fewer operations than the full
+// transform, and no arithmetic on the zeros (x + 0.0 cannot be folded by the compiler: -0.0).
+template <int S>
+__device__ __forceinline__ void dft16_half_in(double2 (&v)[16]) {
+  double2 e[8], o[8];
+#pragma unroll
+  for (int r = 0; r < 8; ++r) {
+    e[r] = v[r];
+    o[r] = rot16<S>(v[r], r);
+  }
+  Dft<8, S>::run(e);
+  Dft<8, S>::run(o);
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    v[2 * q] = e[q];
+    v[2 * q + 1] = o[q];
+  }
+}
+
+// outputs 0..7 of DFT_16 only (the packed inverse's first half: the truncated Toeplitz product);
+// v[8..15] are left unspecified
+template <int S>
+__device__ __forceinline__ void dft16_low_out(double2 (&v)[16]) {
+  double2 e[8], o[8];
+#pragma unroll
+  for (int r = 0; r < 8; ++r) {
+    e[r] = v[2 * r];
+    o[r] = v[2 * r + 1];
+  }
+  Dft<8, S>::run(e);
+  Dft<8, S>::run(o);
+#pragma unroll
+  for (int b = 0; b < 8; ++b) v[b] = cadd(e[b], rot16<S>(o[b], b));
+}
+
 // M = R*R point transform by the R lanes of a group (t = lane index within the group).
 // `xs` = the group's private tile (WarpFftTile<R>::SIZE double2).  `twb` = tw_base.
-// `mask` = the lanes of the warp taking part (all groups of a warp call this together).
-template <int R, int S>
+// All groups of a warp call this together (twiddles: two table loads and their powers, as the
+// Stockham passes -- 15 table loads per pass measured slower).  IN_HALF (R = 16): inputs v[8..15] are zero;
+// OUT_HALF (R = 16): only outputs v[0..7] are needed.
+template <int R, int S, bool IN_HALF = false, bool OUT_HALF = false>
 __device__ __forceinline__ void warp_fft_sq(double2 (&v)[R], double2* __restrict__ xs, int t,
                                             const double2* __restrict__ twb) {
   constexpr int M = R * R;
   constexpr int LD = WarpFftTile<R>::LD;
-  Dft<R, S>::run(v);
+  if constexpr (IN_HALF) {
+    static_assert(R == 16, "half-input pass: R = 16");
+    dft16_half_in<S>(v);
+  } else {
+    Dft<R, S>::run(v);
+  }
   apply_twiddles<R, S>(v, twb + M, twb + M / 4, t);  // v[q] *= w_M^{S t q}
 #pragma unroll
   for (int q = 0; q < R; ++q) xs[q * LD + t] = v[q];
@@ -47,7 +99,12 @@ __device__ __forceinline__ void warp_fft_sq(double2 (&v)[R], double2* __restrict
 #pragma unroll
   for (int u = 0; u < R; ++u) v[u] = xs[t * LD + u];
   __syncwarp();  // the tile is free again when any lane of the group reuses it
-  Dft<R, S>::run(v);
+  if constexpr (OUT_HALF) {
+    static_assert(R == 16, "half-output pass: R = 16");
+    dft16_low_out<S>(v);
+  } else {
+    Dft<R, S>::run(v);
+  }
 }
 
 // Value held by the lane that owns bin M - k, for the lane owning k = q + R p (output layout):
