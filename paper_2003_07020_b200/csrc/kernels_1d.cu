@@ -109,9 +109,9 @@ constexpr int kTotMv = 4096;
 // (B200 config 2, M = 256: 2D matvec 1182 -> 932 us).  FPC_MV_CST_SMEM = 0 / 1 forces either.
 template <int LOGM>
 constexpr bool mv_cst_parked() { return FPC_MV_CST_SMEM == 1 || (FPC_MV_CST_SMEM == 2 && LOGM >= 10); }
-template <int LOGM>
+template <int LOGM, int TOT = kTotMv>
 struct MvGeo {
-  using G = Geo<LOGM, kTotMv, 16>;
+  using G = Geo<LOGM, TOT, 16>;
   static constexpr size_t SMEM = G::SMEM + (mv_cst_parked<LOGM>() ? size_t(G::B) * G::M * sizeof(double) : 0);
 };
 
@@ -125,8 +125,8 @@ __device__ __forceinline__ int div_small(int e, int d, float inv_d) {
   return q;
 }
 
-template <int LOGM>
-__global__ void __launch_bounds__(Geo<LOGM, kTotMv, 16>::NT, minb(Geo<LOGM, kTotMv, 16>::NT))
+template <int LOGM, int TOT = kTotMv>
+__global__ void __launch_bounds__(Geo<LOGM, TOT, 16>::NT, minb(Geo<LOGM, TOT, 16>::NT))
     k_matvec_1d(const double* __restrict__ v, double* __restrict__ y, int ns, int nrows, int rpt,
                 int sstride, int koff, const double* __restrict__ eig,
                 const double2* __restrict__ twb) {
@@ -135,7 +135,7 @@ __global__ void __launch_bounds__(Geo<LOGM, kTotMv, 16>::NT, minb(Geo<LOGM, kTot
   // sstride and 2*sstride earlier.  1D: rows = time blocks (rpt = 1, sstride = ns);
   // 2D: rows = lattice rows ix of every time block (rpt = n, sstride = n^2), the y-direction
   // half of jacobian.hpp:84-87.
-  using G = Geo<LOGM, kTotMv, 16>;
+  using G = Geo<LOGM, TOT, 16>;
   constexpr int M = G::M, B = G::B, L = 2 * M, BS = G::BS, NT = G::NT;
   constexpr int U = 4;
   extern __shared__ double2 smem[];
@@ -296,11 +296,11 @@ __global__ void __launch_bounds__(Geo<LOGM, kTotMv, 16>::NT, minb(Geo<LOGM, kTot
 template <int LOGM>
 constexpr int tot_t() { return LOGM >= 10 ? 8192 : 4096; }
 
-template <int LOGM>
-__global__ void __launch_bounds__(Geo<LOGM, tot_t<LOGM>()>::NT, minb(Geo<LOGM, tot_t<LOGM>()>::NT))
+template <int LOGM, int TOT = tot_t<LOGM>()>
+__global__ void __launch_bounds__(Geo<LOGM, TOT>::NT, minb(Geo<LOGM, TOT>::NT))
     k_time_fwd(const double* __restrict__ v, double2* __restrict__ Z, int ns,
                const double* __restrict__ sf, double s_in, const double2* __restrict__ twb) {
-  using G = Geo<LOGM, tot_t<LOGM>()>;
+  using G = Geo<LOGM, TOT>;
   constexpr int M = G::M, B = G::B, NTIME = 2 * M, BS = G::BS, NT = G::NT;
 #ifndef FPC_TF_U
 #define FPC_TF_U 16
@@ -373,11 +373,11 @@ __global__ void __launch_bounds__(Geo<LOGM, tot_t<LOGM>()>::NT, minb(Geo<LOGM, t
 // K4: inverse time FFT (alpha_circulant.hpp:167-198) from the half spectrum; the mirror
 // Z_{Nt-n} = conj(Z_n) (alpha_circulant.hpp:167-175) is folded into the real-output packing.
 // =====================================================================================
-template <int LOGM>
-__global__ void __launch_bounds__(Geo<LOGM, tot_t<LOGM>()>::NT, minb(Geo<LOGM, tot_t<LOGM>()>::NT))
+template <int LOGM, int TOT = tot_t<LOGM>()>
+__global__ void __launch_bounds__(Geo<LOGM, TOT>::NT, minb(Geo<LOGM, TOT>::NT))
     k_time_inv(const double2* __restrict__ Z, double* __restrict__ z, int ns,
                const double* __restrict__ sb, const double2* __restrict__ twb) {
-  using G = Geo<LOGM, tot_t<LOGM>()>;
+  using G = Geo<LOGM, TOT>;
   constexpr int M = G::M, B = G::B, NTIME = 2 * M, BS = G::BS, NT = G::NT;
   constexpr int U = 8;
   constexpr int TASKS = B * (M / 2 + 1);
@@ -441,25 +441,25 @@ __global__ void __launch_bounds__(Geo<LOGM, tot_t<LOGM>()>::NT, minb(Geo<LOGM, t
 // =====================================================================================
 constexpr int kTotTau = 4096;
 
-template <int LOGM>
+template <int LOGM, int TOT = (LOGM >= 13 ? (1 << LOGM) : kTotTau)>
 struct TauGeo {
   static constexpr int EE = (1 << LOGM) < 16 ? (1 << LOGM) : 16;
-  using G = Geo<LOGM, (LOGM >= 13 ? (1 << LOGM) : kTotTau), EE>;
+  using G = Geo<LOGM, TOT, EE>;
   static constexpr int BH = G::B > 1 ? skewed(G::M / 2) : padded(G::M / 2);
   static constexpr size_t SMEM = G::SMEM + size_t(G::B) * BH * sizeof(double2);
 };
 
-template <int LOGM, int MODE>  // 0: DST rows only; 1: DST-divide-DST (solve); 2: DST-multiply-DST
-__global__ void __launch_bounds__(TauGeo<LOGM>::G::NT, minb(TauGeo<LOGM>::G::NT))
+template <int LOGM, int MODE, int TOT = (LOGM >= 13 ? (1 << LOGM) : kTotTau)>  // MODE 0: DST rows only; 1: DST-divide-DST (solve); 2: DST-multiply-DST
+__global__ void __launch_bounds__(TauGeo<LOGM, TOT>::G::NT, minb(TauGeo<LOGM, TOT>::G::NT))
     k_tau_solve_1d(double2* __restrict__ Z, int n_rows, const double2* __restrict__ lam,
                    const double* __restrict__ sigma, double dt, const double2* __restrict__ twb) {
-  using G = typename TauGeo<LOGM>::G;
+  using G = typename TauGeo<LOGM, TOT>::G;
   constexpr int M = G::M, B = G::B, BS = G::BS, NT = G::NT, E = G::E;
   constexpr int NSR = M - 1;  // row length (n_space)
   constexpr int U = 4;
   extern __shared__ double2 smem[];
   double2* hbuf = smem + B * BS;  // DCT-III scratch rows (dst_block.cuh)
-  constexpr int BH = TauGeo<LOGM>::BH;
+  constexpr int BH = TauGeo<LOGM, TOT>::BH;
   const int r0 = blockIdx.x * B;
   const int nb = min(B, n_rows - r0);
   const double scale = sqrt(2.0 / double(M));
@@ -582,6 +582,16 @@ static cudaError_t prep(K kernel, size_t smem, int threads = 1024) {
     default: return cudaErrorInvalidValue; \
   }
 
+// Small grids (config 0, the small config-4 points): the tuned tiles hold several rows / columns per
+// CTA, which leaves most of the 148 SMs idle when there are only a few hundred rows (config 0: 64
+// matvec CTAs, 33 tau CTAs, 32 time-FFT CTAs).  When the default tiling gives fewer than two waves,
+// the same kernels run with 512-slot tiles (B = max(1, 512 / M): 1-4 rows or columns per CTA).
+constexpr int kSmallGrid = 2 * 148;
+template <int LM>
+constexpr int small_tot() { return (1 << LM) >= 512 ? (1 << LM) : 512; }
+template <int LM, int TOT>
+constexpr bool is_smaller() { return small_tot<LM>() < TOT; }
+
 cudaError_t launch_matvec_rows(const double* v, double* y, int len, int nrows, int rpt,
                                int sstride, int log_m, const double* eig_scaled,
                                const double2* tw_base, cudaStream_t st, int koff) {
@@ -591,6 +601,17 @@ cudaError_t launch_matvec_rows(const double* v, double* y, int len, int nrows, i
 #define CALL(LM)                                                                          \
   {                                                                                       \
     using G = Geo<LM, kTotMv, 16>;                                                        \
+    if constexpr (is_smaller<LM, kTotMv>()) {                                             \
+      if ((nrows + G::B - 1) / G::B < kSmallGrid) {                                       \
+        constexpr int T = small_tot<LM>();                                                \
+        using GS = Geo<LM, T, 16>;                                                        \
+        if ((err = prep(k_matvec_1d<LM, T>, MvGeo<LM, T>::SMEM, GS::NT)) != cudaSuccess) return err; \
+        k_matvec_1d<LM, T><<<(nrows + GS::B - 1) / GS::B, GS::NT, MvGeo<LM, T>::SMEM, st>>>( \
+            v, y, len, nrows, rpt, sstride, koff, eig_scaled, tw_base);                   \
+        note_launch();                                                                    \
+        return cudaGetLastError();                                                        \
+      }                                                                                   \
+    }                                                                                     \
     if ((err = prep(k_matvec_1d<LM>, MvGeo<LM>::SMEM, Geo<LM, kTotMv, 16>::NT)) != cudaSuccess) return err;        \
     k_matvec_1d<LM><<<(nrows + G::B - 1) / G::B, G::NT, MvGeo<LM>::SMEM, st>>>(           \
         v, y, len, nrows, rpt, sstride, koff, eig_scaled, tw_base); note_launch();                       \
@@ -628,6 +649,17 @@ cudaError_t launch_time_fwd(const double* v, double2* Z, int n_space, int n_time
 #define CALL(LM)                                                                          \
   {                                                                                       \
     using G = Geo<LM, tot_t<LM>()>;                                                             \
+    if constexpr (is_smaller<LM, tot_t<LM>()>()) {                                        \
+      if ((n_space + G::B - 1) / G::B < kSmallGrid) {                                     \
+        constexpr int T = small_tot<LM>();                                                \
+        using GS = Geo<LM, T>;                                                            \
+        if ((err = prep(k_time_fwd<LM, T>, GS::SMEM, GS::NT)) != cudaSuccess) return err; \
+        k_time_fwd<LM, T><<<(n_space + GS::B - 1) / GS::B, GS::NT, GS::SMEM, st>>>(       \
+            v, Z, n_space, scale_fwd, s_in, tw_base);                                     \
+        note_launch();                                                                    \
+        return cudaGetLastError();                                                        \
+      }                                                                                   \
+    }                                                                                     \
     if ((err = prep(k_time_fwd<LM>, G::SMEM, G::NT)) != cudaSuccess) return err;                 \
     k_time_fwd<LM><<<(n_space + G::B - 1) / G::B, G::NT, G::SMEM, st>>>(                  \
         v, Z, n_space, scale_fwd, s_in, tw_base); note_launch();                                         \
@@ -645,6 +677,17 @@ cudaError_t launch_time_inv(const double2* Z, double* z, int n_space, int n_time
 #define CALL(LM)                                                                            \
   {                                                                                         \
     using G = Geo<LM, tot_t<LM>()>;                                                               \
+    if constexpr (is_smaller<LM, tot_t<LM>()>()) {                                          \
+      if ((n_space + G::B - 1) / G::B < kSmallGrid) {                                       \
+        constexpr int T = small_tot<LM>();                                                  \
+        using GS = Geo<LM, T>;                                                              \
+        if ((err = prep(k_time_inv<LM, T>, GS::SMEM, GS::NT)) != cudaSuccess) return err;   \
+        k_time_inv<LM, T><<<(n_space + GS::B - 1) / GS::B, GS::NT, GS::SMEM, st>>>(Z, z, n_space, \
+                                                                                 scale_bwd, tw_base); \
+        note_launch();                                                                      \
+        return cudaGetLastError();                                                          \
+      }                                                                                     \
+    }                                                                                       \
     if ((err = prep(k_time_inv<LM>, G::SMEM, G::NT)) != cudaSuccess) return err;                   \
     k_time_inv<LM><<<(n_space + G::B - 1) / G::B, G::NT, G::SMEM, st>>>(Z, z, n_space,       \
                                                                         scale_bwd, tw_base); note_launch(); \
@@ -677,6 +720,19 @@ template <int LM, int MODE>
 static cudaError_t tau1d(double2* Z, int n_rows, const double2* lambda, const double* sigma,
                          double dt, const double2* tw_base, cudaStream_t st) {
   using TG = TauGeo<LM>;
+  constexpr int TD = (LM >= 13 ? (1 << LM) : kTotTau);
+  if constexpr (is_smaller<LM, TD>()) {
+    if ((n_rows + TG::G::B - 1) / TG::G::B < kSmallGrid) {
+      constexpr int T = small_tot<LM>();
+      using TS = TauGeo<LM, T>;
+      cudaError_t err = prep(k_tau_solve_1d<LM, MODE, T>, TS::SMEM, TS::G::NT);
+      if (err != cudaSuccess) return err;
+      k_tau_solve_1d<LM, MODE, T><<<(n_rows + TS::G::B - 1) / TS::G::B, TS::G::NT, TS::SMEM, st>>>(
+          Z, n_rows, lambda, sigma, dt, tw_base);
+      note_launch();
+      return cudaGetLastError();
+    }
+  }
   cudaError_t err = prep(k_tau_solve_1d<LM, MODE>, TG::SMEM, TG::G::NT);
   if (err != cudaSuccess) return err;
   const int grid = (n_rows + TG::G::B - 1) / TG::G::B;
