@@ -115,7 +115,36 @@ def _dev_in(x, n: int):
     return x
 
 
-def _call_vec(fn, handle, n, v, out, *extra):
+class _TorchOrder:
+    """Device-tensor calls run on the library context's stream; order them after the work torch
+    has queued on its current stream (the inputs' producers) and make torch's stream wait for the
+    call (the outputs' consumers).  Two events, no host synchronisation; nothing when the context
+    already runs on torch's current stream."""
+
+    def __init__(self, ctx):
+        self.ctx = ctx
+
+    def __enter__(self):
+        import torch
+        self.cur = torch.cuda.current_stream()
+        self.same = int(self.cur.cuda_stream) == int(self.ctx.stream_handle)
+        if not self.same:
+            self.lib_stream = torch.cuda.ExternalStream(self.ctx.stream_handle)
+            ev = torch.cuda.Event()
+            ev.record(self.cur)
+            self.lib_stream.wait_event(ev)
+        return self
+
+    def __exit__(self, *exc):
+        if not self.same:
+            import torch
+            ev = torch.cuda.Event()
+            ev.record(self.lib_stream)
+            self.cur.wait_event(ev)
+        return False
+
+
+def _call_vec(fn, handle, n, v, out, *extra, ctx=None):
     """Run fn(handle, in, out, *extra, where) for numpy or torch-CUDA arguments."""
     if _is_torch(v):
         import torch
@@ -123,7 +152,11 @@ def _call_vec(fn, handle, n, v, out, *extra):
         if out is None:
             out = torch.empty_like(vin)
         _dev_in(out, n)
-        N.check(fn(handle, C.c_void_p(vin.data_ptr()), C.c_void_p(out.data_ptr()), *extra, N.FPC_DEVICE))
+        if ctx is None:
+            N.check(fn(handle, C.c_void_p(vin.data_ptr()), C.c_void_p(out.data_ptr()), *extra, N.FPC_DEVICE))
+        else:
+            with _TorchOrder(ctx):
+                N.check(fn(handle, C.c_void_p(vin.data_ptr()), C.c_void_p(out.data_ptr()), *extra, N.FPC_DEVICE))
         return out
     vin = _host_in(v, n)
     res = np.empty(n) if out is None else out
@@ -265,7 +298,7 @@ class AllAtOnceOperator:
         return s
 
     def apply(self, v, out=None):
-        return _call_vec(self.lib.fpc_matvec, self.h, self.dim(), v, out)
+        return _call_vec(self.lib.fpc_matvec, self.h, self.dim(), v, out, ctx=self.ctx)
 
     def __del__(self):
         try:
@@ -390,13 +423,13 @@ def build_plan(kind: PreconditionerKind, n_time: int, dt: float, op,
 def apply_inverse(plan: AlphaCirculantPlan, v, out=None, sweep: InnerSweep = InnerSweep.half):
     """out = P^{-1} v (alpha_circulant.hpp:206-209)."""
     n = plan.n_time * plan.n_space
-    return _call_vec(plan.lib.fpc_pc_apply, plan.h, n, v, out, int(sweep))
+    return _call_vec(plan.lib.fpc_pc_apply, plan.h, n, v, out, int(sweep), ctx=plan.op.ctx)
 
 
 def apply_forward(plan: AlphaCirculantPlan, v, out=None):
     """out = P v (alpha_circulant.hpp:212-215)."""
     n = plan.n_time * plan.n_space
-    return _call_vec(plan.lib.fpc_pc_forward, plan.h, n, v, out)
+    return _call_vec(plan.lib.fpc_pc_forward, plan.h, n, v, out, ctx=plan.op.ctx)
 
 
 # ---------------------------------------------------------------------------------- Krylov
@@ -441,8 +474,9 @@ def _krylov(fn, name, op, plan, b, cfg, out):
         import torch
         bin_ = _dev_in(b, n)
         x = torch.empty_like(bin_) if out is None else _dev_in(out, n)
-        N.check(fn(plan.h, C.c_void_p(bin_.data_ptr()), C.c_void_p(x.data_ptr()), C.byref(c),
-                   C.byref(rep), C.c_void_p(hist.ctypes.data), cap, N.FPC_DEVICE))
+        with _TorchOrder(op.ctx):
+            N.check(fn(plan.h, C.c_void_p(bin_.data_ptr()), C.c_void_p(x.data_ptr()), C.byref(c),
+                       C.byref(rep), C.c_void_p(hist.ctypes.data), cap, N.FPC_DEVICE))
     else:
         bin_ = _host_in(b, n)
         x = np.empty(n) if out is None else out

@@ -146,3 +146,40 @@ def test_config4_corner_points(ref, nx, nt):
         # scalings (1/alpha = 2 Nt): 1e-12, and 1e-11 at Nt = 8192
         assert rel(fp.apply_inverse(plan, part), pr.pc_apply(part)) <= (1e-11 if nt >= 8192 else 1e-12)
         assert rel(op.apply(part), pr.matvec(part)) <= 1e-13
+
+
+@pytest.mark.parametrize("cfg", [(1, 1.2), (2, None), (3, None)], ids=["cfg1", "cfg2", "cfg3"])
+def test_full_size_properties(cfg):
+    """Size-independent properties at the BASELINE sizes themselves (config 3: 8.6 GB vectors, which
+    no CPU oracle here can hold): real-linearity of the matvec and of P^{-1}, the round trip
+    P (P^{-1} v) = v (test_pint.cpp:188-201), and P^{-1} of a PC image, all device-resident."""
+    torch = pytest.importorskip("torch")
+    w = problems.config(cfg[0], cfg[1])
+    op, plan = gpu_problem(w)
+    n = w.dim
+    g = torch.Generator(device="cuda")
+    g.manual_seed(20260819 + cfg[0])
+    u = torch.rand(n, dtype=torch.float64, device="cuda", generator=g) * 2 - 1
+    v = torch.rand(n, dtype=torch.float64, device="cuda", generator=g) * 2 - 1
+    a, b = 0.75, -1.25
+    nrm = lambda t: float(torch.linalg.vector_norm(t))
+    # linearity of A
+    s = a * u + b * v
+    As = op.apply(s)
+    Au, Av = op.apply(u), op.apply(v)
+    lin = nrm(As - (a * Au + b * Av)) / nrm(As)
+    del As, Au, Av
+    # linearity of P^{-1} and the round trip
+    Ps = fp.apply_inverse(plan, s)
+    Pu = fp.apply_inverse(plan, u)
+    Pv = fp.apply_inverse(plan, v)
+    lin_p = nrm(Ps - (a * Pu + b * Pv)) / nrm(Ps)
+    del Pu, Pv, Ps
+    z = fp.apply_inverse(plan, u)
+    back = fp.apply_forward(plan, z)
+    rt = nrm(back - u) / nrm(u)
+    op.ctx.synchronize()
+    print(f"\n{w.name}: A linearity {lin:.2e}, P^-1 linearity {lin_p:.2e}, P P^-1 u - u {rt:.2e}")
+    assert lin <= 1e-13 and lin_p <= 1e-12
+    # the round trip loses what the alpha^{-k/Nt} scalings amplify (1/alpha = 2 Nt)
+    assert rt <= 1e-13 * 2 * w.n_time
