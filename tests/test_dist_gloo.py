@@ -61,7 +61,18 @@ def _worker(rank, world, port, case, out_dir):
                                   (False, (1.5,), 31, 16, 0, "commuted"), (False, (1.7,), 15, 32, 5, "commuted"),
                                   (True, (1.3, 1.7), 7, 8, 0, "commuted")])
 def test_sharded_solve_matches_oracle(tmp_path, oracle, case):
-    world = 2
+    _run_and_check(tmp_path, oracle, case, 2)
+
+
+@pytest.mark.parametrize("case", [(False, (1.5,), 31, 16, 0), (True, (1.3, 1.7), 7, 8, 0, "commuted"),
+                                  (False, (1.7,), 15, 32, 5, "commuted")])
+def test_sharded_solve_world4(tmp_path, oracle, case):
+    """World size 4: uneven column / frequency splits (31 columns, 9 retained frequencies over 4
+    ranks), the halo chain through three ranks."""
+    _run_and_check(tmp_path, oracle, case, 4)
+
+
+def _run_and_check(tmp_path, oracle, case, world):
     mp.spawn(_worker, args=(world, free_port(), case, str(tmp_path)), nprocs=world, join=True)
     parts = [np.load(tmp_path / f"r{r}.npz") for r in range(world)]
     two_dim, g, n, nt, restart = case[:5]
