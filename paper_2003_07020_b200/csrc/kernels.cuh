@@ -47,6 +47,14 @@ cudaError_t launch_time_fwd(const double* v, double2* Z, int n_space, int n_time
 // K4: z[k][p] = Re( scale_bwd[k]/Nt * sum_n Z_n e^{-2 pi i kn/Nt} ), Z_{Nt-n} = conj(Z_n).
 cudaError_t launch_time_inv(const double2* Z, double* z, int n_space, int n_time,
                             const double* scale_bwd, const double2* tw_base, cudaStream_t st);
+// K2 / K4 for n_time = 128..512 on persistent CTAs fed by TMA (kernels_time_tma.cu): used when the
+// grid has at least two waves of column tiles and the input is 16-byte aligned; FPC_TIME_TMA=0
+// keeps the register-staged kernels (A/B).
+bool time_tma_supported(int n_space, int n_time, const void* in, bool inverse);
+cudaError_t launch_time_fwd_tma(const double* v, double2* Z, int n_space, int n_time, const double* scale_fwd,
+                                double s_in, const double2* tw_base, cudaStream_t st);
+cudaError_t launch_time_inv_tma(const double2* Z, double* z, int n_space, int n_time, const double* scale_bwd,
+                                const double2* tw_base, cudaStream_t st);
 // InnerSweep::full (kernels_full.cu): mirror-fill rows Nt/2+1..Nt-1 of a full [Nt][ns] spectrum,
 // and the complex inverse time FFT with the imaginary-residue partials (partial[blk*2 + {0,1}] =
 // {sum Im^2, sum |.|^2}, dots_grid() CTAs).

@@ -108,6 +108,40 @@ __device__ __forceinline__ double bdf2(int k, double x0, double x1, double x2) {
 
 constexpr int kWarpsPerCta = 8;
 
+// Row data read once (no reuse inside the SM): L2-only loads keep the L1 for the twiddle and
+// eigenvalue tables.  FPC_WARP_CG=0 restores plain loads (A/B).
+#ifndef FPC_WARP_CG
+#define FPC_WARP_CG 1
+#endif
+__device__ __forceinline__ double ld_once(const double* p) {
+#if FPC_WARP_CG
+  return __ldcg(p);
+#else
+  return *p;
+#endif
+}
+__device__ __forceinline__ double2 ld_once(const double2* p) {
+#if FPC_WARP_CG
+  return __ldcg(p);
+#else
+  return *p;
+#endif
+}
+
+// Shared-memory carveout of the warp kernels (two 256-thread CTAs per SM): FPC_WARP_CARVE = percent,
+// "auto" = the smallest capacity that holds two CTAs (kernels.cuh carveout_pct), unset = driver default.
+cudaError_t set_warp_carveout(const void* kernel, size_t smem) {
+  static const int mode = [] {
+    const char* e = std::getenv("FPC_WARP_CARVE");
+    if (!e || !e[0]) return -1;
+    if (e[0] == 'a') return -2;
+    return std::atoi(e);
+  }();
+  if (mode == -1) return cudaSuccess;
+  const int pct = mode == -2 ? carveout_pct(smem, 32 * kWarpsPerCta) : mode;
+  return cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
+}
+
 }  // namespace
 
 bool warp_kernels_enabled() {
@@ -143,11 +177,11 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta, 2)
   for (int r = 0; r < H; ++r) {
     const int i0 = 2 * (t + R * r);
     const bool ok0 = i0 < ns, ok1 = i0 + 1 < ns;
-    z[r] = make_double2(ok0 ? vr[i0] : 0.0, ok1 ? vr[i0 + 1] : 0.0);
-    x1[2 * r] = (ok0 && k >= 1) ? vr[i0 - sstride] : 0.0;
-    x1[2 * r + 1] = (ok1 && k >= 1) ? vr[i0 + 1 - sstride] : 0.0;
-    x2[2 * r] = (ok0 && k >= 2) ? vr[i0 - 2 * size_t(sstride)] : 0.0;
-    x2[2 * r + 1] = (ok1 && k >= 2) ? vr[i0 + 1 - 2 * size_t(sstride)] : 0.0;
+    z[r] = make_double2(ok0 ? ld_once(vr + i0) : 0.0, ok1 ? ld_once(vr + i0 + 1) : 0.0);
+    x1[2 * r] = (ok0 && k >= 1) ? ld_once(vr + (i0 - sstride)) : 0.0;
+    x1[2 * r + 1] = (ok1 && k >= 1) ? ld_once(vr + (i0 + 1 - sstride)) : 0.0;
+    x2[2 * r] = (ok0 && k >= 2) ? ld_once(vr + i0 - 2 * size_t(sstride)) : 0.0;
+    x2[2 * r + 1] = (ok1 && k >= 2) ? ld_once(vr + i0 + 1 - 2 * size_t(sstride)) : 0.0;
   }
 #pragma unroll
   for (int r = H; r < R; ++r) z[r] = make_double2(0.0, 0.0);
@@ -186,6 +220,7 @@ cudaError_t launch_matvec_rows_warp(const double* v, double* y, int len, int nro
   const size_t smem = size_t(kWarpsPerCta) * G * WarpFftTile<R>::SIZE * sizeof(double2);
   cudaError_t e = cudaFuncSetAttribute(k_mv_rows_warp<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   if (e != cudaSuccess) return e;
+  if ((e = set_warp_carveout((const void*)k_mv_rows_warp<R>, smem)) != cudaSuccess) return e;
   k_mv_rows_warp<R><<<(nrows + rows_per_cta - 1) / rows_per_cta, 32 * kWarpsPerCta, smem, st>>>(
       v, y, len, nrows, rpt, sstride, koff, eig_scaled, tw_base); note_launch();
   return cudaGetLastError();
@@ -242,6 +277,7 @@ cudaError_t launch_dst_rows_warp(double2* Z, int n, int n_rows, const double2* l
     cudaError_t e = cudaFuncSetAttribute(k_dst_rows_warp<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,  \
                                          int(smem));                                                          \
     if (e != cudaSuccess) return e;                                                                           \
+    if ((e = set_warp_carveout((const void*)k_dst_rows_warp<MODE>, smem)) != cudaSuccess) return e;           \
     k_dst_rows_warp<MODE><<<grid, 32 * kWarpsPerCta, smem, st>>>(Z, n_rows, lambda, sigma, dt, tw_base);     \
     note_launch();                                                                                            \
   }
@@ -400,6 +436,7 @@ cudaError_t launch_matvec_cols_warp(const double* v, double* y, int n, int n_tim
     const size_t smem = size_t(kWarpsPerCta) * G * WarpFftTile<R>::SIZE * sizeof(double2);
     cudaError_t e = cudaFuncSetAttribute(k_mv_cols_direct, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     if (e != cudaSuccess) return e;
+    if ((e = set_warp_carveout((const void*)k_mv_cols_direct, smem)) != cudaSuccess) return e;
     k_mv_cols_direct<<<unsigned(n_time) * unsigned(tiles), 32 * kWarpsPerCta, smem, st>>>(v, y, n, eig_x, tw_base);
     note_launch();
     return cudaGetLastError();
@@ -464,11 +501,13 @@ cudaError_t launch_tau_cols_warp(double2* Z, int n, int n_planes, const double2*
     if ((e = cudaFuncSetAttribute(k_tau_cols_warp<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem))) !=
         cudaSuccess)
       return e;
+    if ((e = set_warp_carveout((const void*)k_tau_cols_warp<2>, smem)) != cudaSuccess) return e;
     k_tau_cols_warp<2><<<grid, 32 * kWarpsPerCta, smem, st>>>(Z, n_planes, lambda, sigma, dt, tw_base);
   } else {
     if ((e = cudaFuncSetAttribute(k_tau_cols_warp<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem))) !=
         cudaSuccess)
       return e;
+    if ((e = set_warp_carveout((const void*)k_tau_cols_warp<1>, smem)) != cudaSuccess) return e;
     k_tau_cols_warp<1><<<grid, 32 * kWarpsPerCta, smem, st>>>(Z, n_planes, lambda, sigma, dt, tw_base);
   }
   note_launch();
