@@ -48,6 +48,9 @@ int ilog2i(int n) {
 }
 
 constexpr int kTot2 = 4096;
+#ifndef FPC_COLS_RED
+#define FPC_COLS_RED 1
+#endif
 
 template <int LOGM>
 struct ColGeo {
@@ -137,6 +140,17 @@ __global__ void __launch_bounds__(ColGeo<LOGM>::NT, (ColGeo<LOGM>::NT <= 256 ? 2
   }
   __syncthreads();
   block_fft<LOGM, 1, BS, E>(smem, twb + M, C);
+#if FPC_COLS_RED
+  // y += x-direction term as reductions performed at the L2 (RED.ADD.F64, no return value): every
+  // element receives exactly one add -- the same double as load-add-store -- without the strided
+  // read of y or the wait for it (B200 config 2: matvec 667 -> 592 us; kernels_warp.cu)
+  for (int e = threadIdx.x; e < C * n; e += NT) {
+    const int c = e % C, ix = e / C;
+    const int iy = iy0 + c;
+    if (iy < n) atomicAdd(y + base + size_t(ix) * n + iy, comp2(smem, c * BS + pad16(ix >> 1), ix & 1));
+  }
+  return;
+#endif
   // y += x-direction term: the read-modify-write batched 8 deep (latency bound otherwise)
   constexpr int UE = 8;
   for (int e0 = threadIdx.x; e0 < C * n; e0 += UE * NT) {

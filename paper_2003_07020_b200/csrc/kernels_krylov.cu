@@ -23,9 +23,16 @@ int carveout_pct(size_t dyn_smem, int threads) {
   const int by_smem = int((228u * 1024u) / per_cta);
   const int ctas = by_smem < by_regs ? (by_smem > 0 ? by_smem : 1) : by_regs;
   const size_t need = size_t(ctas) * per_cta;
+  // The driver takes the smallest capacity >= pct% of 228 KB: rounding the percentage UP overshoots
+  // the capacity aimed at (164 KB -> 72% = 164.2 KB -> 196 KB), so round it down (71% = 161.9 KB ->
+  // 164 KB).  FPC_CARVE_ROUND=up restores the round-1 behaviour (A/B).
+  static const bool round_up = [] {
+    const char* e = std::getenv("FPC_CARVE_ROUND");
+    return e && e[0] == 'u';
+  }();
   static const int caps[] = {0, 8, 16, 32, 64, 100, 132, 164, 196, 228};
   for (int c : caps)
-    if (size_t(c) * 1024 >= need) return (c * 100 + 227) / 228;
+    if (size_t(c) * 1024 >= need) return round_up ? (c * 100 + 227) / 228 : (c * 100) / 228;
   return 100;
 }
 

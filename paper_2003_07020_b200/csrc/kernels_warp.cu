@@ -113,6 +113,9 @@ constexpr int kWarpsPerCta = 8;
 #ifndef FPC_WARP_CG
 #define FPC_WARP_CG 1
 #endif
+#ifndef FPC_COLS_RED
+#define FPC_COLS_RED 1
+#endif
 __device__ __forceinline__ double ld_once(const double* p) {
 #if FPC_WARP_CG
   return __ldcg(p);
@@ -407,6 +410,17 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta, 2)
   warp_fft_sq<R, 1, false, true>(z, xs, t, twb);
   if (valid) {
     double* yc = y + size_t(k) * size_t(n) * size_t(n) + iy;
+#if FPC_COLS_RED
+    // y += result as reductions performed at the L2 (RED.ADD.F64, no return value): every element
+    // receives exactly one add, so the sum is the same double as load-add-store, without the
+    // strided read of y, its registers or the wait for it at the end of the task
+#pragma unroll
+    for (int r = 0; r < H; ++r) {
+      const int i0 = 2 * (t + R * r);
+      if (i0 < n) atomicAdd(yc + size_t(i0) * n, z[r].x);
+      if (i0 + 1 < n) atomicAdd(yc + size_t(i0 + 1) * n, z[r].y);
+    }
+#else
     double yo[2 * H];
 #pragma unroll
     for (int r = 0; r < H; ++r) {
@@ -420,6 +434,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta, 2)
       if (i0 < n) yc[size_t(i0) * n] = yo[2 * r] + z[r].x;
       if (i0 + 1 < n) yc[size_t(i0 + 1) * n] = yo[2 * r + 1] + z[r].y;
     }
+#endif
   }
 }
 
@@ -471,9 +486,9 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta, 2)
   double2* zc = Z + size_t(rp) * NSR * NSR + (valid ? iy : 0);
   double2* xs = wsm + grp * kDstTileSize;
   const double scale = 0.088388347648318440550;  // sqrt(2/256)
+  const double* sg = sigma + (valid ? iy : 0);
   warp_dst256([&](int j) { return zc[size_t(j - 1) * NSR]; }, xs, t, twb, scale);
   const double2 l = __ldg(lam + rp);
-  const double* sg = sigma + (valid ? iy : 0);
 #pragma unroll
   for (int r = 0; r < R; ++r) {
     const int i = t + R * r;

@@ -19,7 +19,8 @@ for c in cfgs:
     jac = (fp.RieszJacobian2D(w.gamma[0], w.gamma[1], 1.0, 1.0, w.h, w.n) if w.two_dim
            else fp.RieszJacobian1D(w.gamma[0], 1.0, w.h, w.n))
     op = fp.AllAtOnceOperator(fp.TimeStencil(w.n_time), jac, w.dt, ctx)
-    plan = fp.build_plan(fp.PreconditionerKind.generalized(), w.n_time, w.dt, op)
+    order = fp.Ordering.commuted if "commuted" in sys.argv else fp.Ordering.reference
+    plan = fp.build_plan(fp.PreconditionerKind.generalized(), w.n_time, w.dt, op, ordering=order)
     cfg = fp.SolverConfig(tol=w.tol, max_iter=200, restart=w.restart)
     with torch.cuda.stream(stream):
         b = torch.from_numpy(problems.rhs(w)).cuda()
