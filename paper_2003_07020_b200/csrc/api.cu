@@ -840,12 +840,21 @@ int fpc_plan_create(fpc_problem_t p, double alpha_in, fpc_plan_t* out) {
     pl->d_sf = dalloc<double>(size_t(nt));
     pl->d_sb = dalloc<double>(size_t(nt));
     pl->d_lambda = dalloc<double2>(size_t(nt));  // all Nt: the full sweep solves every frequency
-    pl->d_sigma = dalloc<double>(p->sigma.size());
+    // 2D: the transposed table sigma[iy][ix] follows the natural one (the column pass of the tau
+    // solve reads sigma along ix for a fixed iy: contiguous in the transposed copy)
+    pl->d_sigma = dalloc<double>(p->sigma.size() * (p->two_dim ? 2 : 1));
     pl->d_Z = dalloc<double2>(size_t(pl->solve_count) * size_t(p->ns));
     ck(cudaMemcpy(pl->d_sf, sf.data(), sf.size() * 8, cudaMemcpyHostToDevice), "sf");
     ck(cudaMemcpy(pl->d_sb, sb.data(), sb.size() * 8, cudaMemcpyHostToDevice), "sb");
     ck(cudaMemcpy(pl->d_lambda, pl->lambda.data(), size_t(nt) * 16, cudaMemcpyHostToDevice), "lambda");
     ck(cudaMemcpy(pl->d_sigma, p->sigma.data(), p->sigma.size() * 8, cudaMemcpyHostToDevice), "sigma");
+    if (p->two_dim) {
+      const size_t n = size_t(p->n);
+      std::vector<double> st(p->sigma.size());
+      for (size_t ix = 0; ix < n; ++ix)
+        for (size_t iy = 0; iy < n; ++iy) st[iy * n + ix] = p->sigma[ix * n + iy];
+      ck(cudaMemcpy(pl->d_sigma + p->sigma.size(), st.data(), st.size() * 8, cudaMemcpyHostToDevice), "sigmaT");
+    }
     pl->scale_fwd = std::move(sf);
     pl->scale_bwd = std::move(sb);
     if (p->generic) {

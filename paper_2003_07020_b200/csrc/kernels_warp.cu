@@ -50,10 +50,75 @@ __device__ __forceinline__ double2 packed_eig_product(double2 own, double2 mir, 
 // U_{M-k} into the tile slot of bin M - k -- a slot only this lane reads (its mirror operand,
 // read just before) -- then reads its bins p >= 8 back; bin M/2 (lane 0, p = 8) pairs with itself.
 // Same per-pair arithmetic as k_matvec_1d's spectral loop (kernels_1d.cu).
+#ifndef FPC_MV_SHFL
+#define FPC_MV_SHFL 1
+#endif
+// The same with the mirror operands and the partners' results exchanged by width-16 shuffles instead
+// of the tile (B200: a double2 through the tile is a 4-wavefront store plus a 4-wavefront load on the
+// L1/shared pipe these kernels are bound on; the DST's mirror exchange gained 3% this way).
+__device__ __forceinline__ void warp_packed_product_shfl(double2 (&z)[16], int t, const double* __restrict__ eig,
+                                                         const double2* __restrict__ twL) {
+  constexpr int R = 16, M = 256, H = 8;
+  const int src = (R - t) & (R - 1);
+  const double2 mid = z[H];  // lane 0: bin M/2
+  double2 um[H];             // U_{M-k} of this lane's pairs k = t + 16 p, p < 8
+#pragma unroll
+  for (int p = 0; p < H; ++p) {
+    const int k = t + R * p;
+    const double2 a = z[p];
+    // Z_{M-k}: lane (16 - t) mod 16, register 15 - p (t != 0); this lane's register 16 - p (t = 0)
+    double2 bq;
+    bq.x = __shfl_sync(0xffffffffu, z[R - 1 - p].x, src, R);
+    bq.y = __shfl_sync(0xffffffffu, z[R - 1 - p].y, src, R);
+    if (t == 0) bq = z[(R - p) & (R - 1)];
+    if (k == 0) {
+      const double y0 = __ldg(eig) * (2.0 * (a.x + a.y));
+      const double ym = __ldg(eig + M) * (2.0 * (a.x - a.y));
+      z[p] = make_double2(y0 + ym, y0 - ym);
+      um[p] = make_double2(0.0, 0.0);
+      continue;
+    }
+    const double2 w = __ldg(twL + k);  // e^{-2 pi i k/L}
+    const double ek = __ldg(eig + k), em = __ldg(eig + M - k);
+    const double2 P = cadd(a, cconj(bq)), Q = csub(a, cconj(bq));
+    const double2 iwQ = mul_si<1>(cmul(w, Q));
+    const double2 Yk = cscale(csub(P, iwQ), ek);
+    const double2 Ym = cscale(cconj(cadd(P, iwQ)), em);
+    const double2 A = cadd(Yk, cconj(Ym)), D = csub(Yk, cconj(Ym));
+    z[p] = cadd(A, mul_si<1>(cmul(D, cconj(w))));
+    um[p] = cadd(cconj(A), mul_si<1>(cmul(cconj(D), w)));
+  }
+  double2 zmid = mid;
+  if (t == 0) {  // the self pair k = M/2
+    const double2 w = __ldg(twL + M / 2);
+    const double ek = __ldg(eig + M / 2);
+    const double2 P = cadd(mid, cconj(mid)), Q = csub(mid, cconj(mid));
+    const double2 iwQ = mul_si<1>(cmul(w, Q));
+    const double2 Yk = cscale(csub(P, iwQ), ek);
+    const double2 Ym = cscale(cconj(cadd(P, iwQ)), ek);
+    const double2 A = cadd(Yk, cconj(Ym)), D = csub(Yk, cconj(Ym));
+    zmid = cadd(A, mul_si<1>(cmul(D, cconj(w))));
+  }
+  // bin k' = t + 16 p' (p' >= 8) = M - k with k = (16 - t) + 16 (15 - p'): lane 16 - t, pair 15 - p'
+  // (t != 0); lane 0: k' = 16 p' = M - 16 (16 - p'): its own pair 16 - p' (p' >= 9), p' = 8 the self pair
+#pragma unroll
+  for (int pp = H; pp < R; ++pp) {
+    double2 u;
+    u.x = __shfl_sync(0xffffffffu, um[R - 1 - pp].x, src, R);
+    u.y = __shfl_sync(0xffffffffu, um[R - 1 - pp].y, src, R);
+    if (t == 0) u = pp == H ? zmid : um[(R - pp) & (H - 1)];
+    z[pp] = u;
+  }
+}
+
 template <int R>
 __device__ __forceinline__ void warp_packed_product(double2 (&z)[R], double2* __restrict__ xs, int t,
                                                     const double* __restrict__ eig, const double2* __restrict__ twL) {
   constexpr int M = R * R, LD = WarpFftTile<R>::LD, H = R / 2;
+  if constexpr (R == 16 && FPC_MV_SHFL) {
+    warp_packed_product_shfl(z, t, eig, twL);
+    return;
+  }
 #pragma unroll
   for (int p = 0; p < R; ++p) xs[p * LD + t] = z[p];
   __syncwarp();
@@ -467,6 +532,7 @@ cudaError_t launch_matvec_cols_warp(const double* v, double* y, int n, int n_tim
 
 // 2D tau solve, column pass (tau.hpp:79-119 along ix): for frequency plane r and column iy, DST over
 // ix, divide (MODE 1) / multiply (MODE 2) by lambda_r - dt sigma[ix n + iy], DST over ix, in place.
+// sigma = the plan's table [ix][iy] followed by its transpose [iy][ix] (read here: contiguous in ix).
 // One 16-lane group per column, loads straight from global memory (a warp's two groups read
 // adjacent 16-byte elements of each row; a CTA's 16 groups cover 256-byte row segments), the
 // intermediate kept in the group's tile.  n = 255.
@@ -486,13 +552,13 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta, 2)
   double2* zc = Z + size_t(rp) * NSR * NSR + (valid ? iy : 0);
   double2* xs = wsm + grp * kDstTileSize;
   const double scale = 0.088388347648318440550;  // sqrt(2/256)
-  const double* sg = sigma + (valid ? iy : 0);
+  const double* sg = sigma + size_t(NSR) * NSR + size_t(valid ? iy : 0) * NSR;  // transposed table: row iy
   warp_dst256([&](int j) { return zc[size_t(j - 1) * NSR]; }, xs, t, twb, scale);
   const double2 l = __ldg(lam + rp);
 #pragma unroll
   for (int r = 0; r < R; ++r) {
     const int i = t + R * r;
-    if (i < NSR) xs[dst_slot(i)] = shift_apply<MODE>(xs[dst_slot(i)], l.x - dt * __ldg(sg + size_t(i) * NSR), l.y);
+    if (i < NSR) xs[dst_slot(i)] = shift_apply<MODE>(xs[dst_slot(i)], l.x - dt * __ldg(sg + i), l.y);
   }
   __syncwarp();
   warp_dst256([&](int j) { return xs[dst_slot(j - 1)]; }, xs, t, twb, scale);

@@ -16,6 +16,10 @@
 #pragma once
 #include "warp_fft.cuh"
 
+#ifndef FPC_DST_SHFL
+#define FPC_DST_SHFL 1
+#endif
+
 namespace fpc {
 
 // 128-point transform by 16 lanes, 8 values each: lane t holds x[t + 16 r] (r < 8) on entry and
@@ -98,11 +102,22 @@ __device__ __forceinline__ void warp_dst256(Src f, double2* __restrict__ xs, int
   warp_fft_sq<16, 1>(y, xs, t, twb);  // lane t: Y_{t + 16 p}
   // even outputs F_{2k} = -(i/2)(Y_k - Y_{N-k}), k = t + 16 p (p < 8, k >= 1): the mirror N - k sits
   // in lane (16 - t) mod 16, register 15 - p (t != 0), or this lane's register 16 - p (t = 0)
+  double2 ev[8];
+#if FPC_DST_SHFL
+  {
+    double2 ym[8];
+    ym[0] = warp_fft_mirror<16, 0>(y, t); ym[1] = warp_fft_mirror<16, 1>(y, t);
+    ym[2] = warp_fft_mirror<16, 2>(y, t); ym[3] = warp_fft_mirror<16, 3>(y, t);
+    ym[4] = warp_fft_mirror<16, 4>(y, t); ym[5] = warp_fft_mirror<16, 5>(y, t);
+    ym[6] = warp_fft_mirror<16, 6>(y, t); ym[7] = warp_fft_mirror<16, 7>(y, t);
+#pragma unroll
+    for (int p = 0; p < 8; ++p) ev[p] = make_double2(0.5 * (y[p].y - ym[p].y), -0.5 * (y[p].x - ym[p].x));
+  }
+#else
   constexpr int LD = WarpFftTile<16>::LD;
 #pragma unroll
   for (int p = 0; p < 16; ++p) xs[p * LD + t] = y[p];
   __syncwarp();
-  double2 ev[8];
   const int tm = (16 - t) & 15;
 #pragma unroll
   for (int p = 0; p < 8; ++p) {
@@ -111,6 +126,7 @@ __device__ __forceinline__ void warp_dst256(Src f, double2* __restrict__ xs, int
     ev[p] = make_double2(0.5 * (y[p].y - ym.y), -0.5 * (y[p].x - ym.x));
   }
   __syncwarp();
+#endif
   warp_fft_8x16<1>(V, xs, t, twb);  // lane t: v_{t + 16 p}
   // assemble DST(f)_i = scale F_{i+1} in natural order: F_{2k} -> i = 2k - 1; v_m -> i = 4m (m < 64)
   // or -v_m -> i = 510 - 4m (m >= 64)
