@@ -523,6 +523,10 @@ def measure(fp, torch, w, args, stream, ctx, dev, steps, warmup, full, sync=None
                              "formula": "SURVEY 8(d) B_tot, one Gram-Schmidt pass per step (the reference "
                                         "re-orthogonalises every step here, which doubles that term)"}
     if not full:
+        with fp.KernelProfile() as prof:  # live per-kernel device time inside one more solve
+            fp.gmres_right(op, plan, b, cfg, out=x)
+        out["kernel_time_ms_per_solve"] = {k_: v[0] for k_, v in prof.table.items()}
+        out["kernel_launches_per_solve"] = {k_: v[1] for k_, v in prof.table.items()}
         del b, x, res, op, plan
         torch.cuda.synchronize()
         torch.cuda.empty_cache()

@@ -171,7 +171,21 @@ __device__ __forceinline__ double bdf2(int k, double x0, double x1, double x2) {
   return 1.5 * x0 + -2.0 * x1 + 0.5 * x2;
 }
 
-constexpr int kWarpsPerCta = 8;
+#ifndef FPC_COL_WARPS
+#define FPC_COL_WARPS 4  // B200 config 2: matvec columns 4 warps (8 columns) per CTA, tau columns 8 (16 columns)
+#endif
+#ifndef FPC_TAU_COL_WARPS
+#define FPC_TAU_COL_WARPS 8
+#endif
+constexpr int kTauColWarps = FPC_TAU_COL_WARPS;
+constexpr int kWarpsPerCta = FPC_COL_WARPS;  // column kernels: a CTA covers 2 * kWarpsPerCta adjacent columns
+// Row kernels (contiguous rows: nothing shared between a CTA's warps): smaller CTAs, the same 16
+// warps per SM -- the warps of a CTA start together and so wait on their row loads together; more,
+// smaller CTAs spread those phases (FPC_ROW_WARPS: build knob).
+#ifndef FPC_ROW_WARPS
+#define FPC_ROW_WARPS 4
+#endif
+constexpr int kRowWarps = FPC_ROW_WARPS;
 
 // Row data read once (no reuse inside the SM): L2-only loads keep the L1 for the twiddle and
 // eigenvalue tables.  FPC_WARP_CG=0 restores plain loads (A/B).
@@ -221,7 +235,7 @@ bool warp_kernels_enabled() {
 }
 
 template <int R>
-__global__ void __launch_bounds__(32 * kWarpsPerCta, 2)
+__global__ void __launch_bounds__(32 * kRowWarps, 16 / kRowWarps)
     k_mv_rows_warp(const double* __restrict__ v, double* __restrict__ y, int ns, int nrows, int rpt,
                    int sstride, int koff, const double* __restrict__ eig, const double2* __restrict__ twb) {
   constexpr int M = R * R, L = 2 * M, G = 32 / R, H = R / 2;
@@ -230,7 +244,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta, 2)
   const int lane = int(threadIdx.x) & 31;
   const int t = lane & (R - 1);
   const int grp = (int(threadIdx.x) >> 5) * G + lane / R;
-  const int row = int(blockIdx.x) * (kWarpsPerCta * G) + grp;
+  const int row = int(blockIdx.x) * (kRowWarps * G) + grp;
   const bool valid = row < nrows;
   const int rr = valid ? row : nrows - 1;  // out-of-range groups compute a duplicate, store nothing
   const int k = rr / rpt + koff;
@@ -284,12 +298,12 @@ cudaError_t launch_matvec_rows_warp(const double* v, double* y, int len, int nro
                                     cudaStream_t st, int koff) {
   if (log_m != 8) return cudaErrorNotSupported;
   constexpr int R = 16, G = 32 / R;
-  const int rows_per_cta = kWarpsPerCta * G;
-  const size_t smem = size_t(kWarpsPerCta) * G * WarpFftTile<R>::SIZE * sizeof(double2);
+  const int rows_per_cta = kRowWarps * G;
+  const size_t smem = size_t(kRowWarps) * G * WarpFftTile<R>::SIZE * sizeof(double2);
   cudaError_t e = cudaFuncSetAttribute(k_mv_rows_warp<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   if (e != cudaSuccess) return e;
   if ((e = set_warp_carveout((const void*)k_mv_rows_warp<R>, smem)) != cudaSuccess) return e;
-  k_mv_rows_warp<R><<<(nrows + rows_per_cta - 1) / rows_per_cta, 32 * kWarpsPerCta, smem, st>>>(
+  k_mv_rows_warp<R><<<(nrows + rows_per_cta - 1) / rows_per_cta, 32 * kRowWarps, smem, st>>>(
       v, y, len, nrows, rpt, sstride, koff, eig_scaled, tw_base); note_launch();
   return cudaGetLastError();
 }
@@ -299,7 +313,7 @@ cudaError_t launch_matvec_rows_warp(const double* v, double* y, int len, int nro
 // frequency row r (tau.hpp:98-136): DST, divide (multiply) by lambda_r - dt sigma_i, DST, with the
 // intermediate kept in the group's tile.
 template <int MODE>
-__global__ void __launch_bounds__(32 * kWarpsPerCta, 2)
+__global__ void __launch_bounds__(32 * kRowWarps, 16 / kRowWarps)
     k_dst_rows_warp(double2* __restrict__ Z, int n_rows, const double2* __restrict__ lam,
                     const double* __restrict__ sigma, double dt, const double2* __restrict__ twb) {
   constexpr int R = 16, G = 2, NSR = 255;
@@ -307,7 +321,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta, 2)
   const int lane = int(threadIdx.x) & 31;
   const int t = lane & (R - 1);
   const int grp = (int(threadIdx.x) >> 5) * G + lane / R;
-  const int row = int(blockIdx.x) * (kWarpsPerCta * G) + grp;
+  const int row = int(blockIdx.x) * (kRowWarps * G) + grp;
   const bool valid = row < n_rows;
   const int rr = valid ? row : n_rows - 1;
   double2* zr = Z + size_t(rr) * NSR;
@@ -337,8 +351,8 @@ cudaError_t launch_dst_rows_warp(double2* Z, int n, int n_rows, const double2* l
                                  double dt, const double2* tw_base, cudaStream_t st, int mode) {
   if (n != 255) return cudaErrorNotSupported;
   constexpr int R = 16, G = 2;
-  const int rows_per_cta = kWarpsPerCta * G;
-  const size_t smem = size_t(kWarpsPerCta) * G * kDstTileSize * sizeof(double2);
+  const int rows_per_cta = kRowWarps * G;
+  const size_t smem = size_t(kRowWarps) * G * kDstTileSize * sizeof(double2);
   const unsigned grid = unsigned((n_rows + rows_per_cta - 1) / rows_per_cta);
 #define FPC_DSTW(MODE)                                                                                        \
   {                                                                                                           \
@@ -346,7 +360,7 @@ cudaError_t launch_dst_rows_warp(double2* Z, int n, int n_rows, const double2* l
                                          int(smem));                                                          \
     if (e != cudaSuccess) return e;                                                                           \
     if ((e = set_warp_carveout((const void*)k_dst_rows_warp<MODE>, smem)) != cudaSuccess) return e;           \
-    k_dst_rows_warp<MODE><<<grid, 32 * kWarpsPerCta, smem, st>>>(Z, n_rows, lambda, sigma, dt, tw_base);     \
+    k_dst_rows_warp<MODE><<<grid, 32 * kRowWarps, smem, st>>>(Z, n_rows, lambda, sigma, dt, tw_base);     \
     note_launch();                                                                                            \
   }
   if (mode == 0)
@@ -365,9 +379,9 @@ cudaError_t launch_dst_rows_warp(double2* Z, int n, int n_rows, const double2* l
 // loaded cooperatively (128-byte row segments, coalesced) into shared memory, each 16-lane group
 // transforms one column straight from the tile (no CTA barrier inside the transforms), writes the
 // result back into its tile column, and the CTA adds the tile to y row by row (coalesced).
-constexpr int kColTile = 16;         // columns per CTA = groups per CTA
+constexpr int kColTile = 2 * kWarpsPerCta;  // columns per CTA = groups per CTA
 constexpr int kColPitch = 17;        // tile row pitch in doubles: the groups' column reads hit 16 bank pairs
-__global__ void __launch_bounds__(32 * kWarpsPerCta, 2)
+__global__ void __launch_bounds__(32 * kWarpsPerCta, 16 / kWarpsPerCta)
     k_mv_cols_warp(const double* __restrict__ v, double* __restrict__ y, int n, const double* __restrict__ eig,
                    const double2* __restrict__ twb) {
   constexpr int R = 16, M = R * R, L = 2 * M, H = R / 2, G = 2;
@@ -447,7 +461,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta, 2)
 // registers (a warp's two groups read 16 B per row; a CTA's 8 warps cover 128-byte row segments, so
 // the L2 sectors are shared within the CTA) and adds its result to y directly -- warps never wait
 // on each other.  FPC_COLS_TILE=1 selects the tiled kernel above (A/B).
-__global__ void __launch_bounds__(32 * kWarpsPerCta, 2)
+__global__ void __launch_bounds__(32 * kWarpsPerCta, 16 / kWarpsPerCta)
     k_mv_cols_direct(const double* __restrict__ v, double* __restrict__ y, int n, const double* __restrict__ eig,
                      const double2* __restrict__ twb) {
   constexpr int R = 16, M = R * R, L = 2 * M, H = R / 2, G = 2;
@@ -537,10 +551,10 @@ cudaError_t launch_matvec_cols_warp(const double* v, double* y, int n, int n_tim
 // adjacent 16-byte elements of each row; a CTA's 16 groups cover 256-byte row segments), the
 // intermediate kept in the group's tile.  n = 255.
 template <int MODE>
-__global__ void __launch_bounds__(32 * kWarpsPerCta, 2)
+__global__ void __launch_bounds__(32 * kTauColWarps, 16 / kTauColWarps)
     k_tau_cols_warp(double2* __restrict__ Z, int n_planes, const double2* __restrict__ lam,
                     const double* __restrict__ sigma, double dt, const double2* __restrict__ twb) {
-  constexpr int R = 16, G = 2, NSR = 255, NG = kWarpsPerCta * G;
+  constexpr int R = 16, G = 2, NSR = 255, NG = kTauColWarps * G;
   extern __shared__ double2 wsm[];
   constexpr int tiles = (NSR + NG - 1) / NG;
   const int rp = int(blockIdx.x) / tiles;
@@ -574,7 +588,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta, 2)
 cudaError_t launch_tau_cols_warp(double2* Z, int n, int n_planes, const double2* lambda, const double* sigma,
                                  double dt, const double2* tw_base, cudaStream_t st, bool forward) {
   if (n != 255) return cudaErrorNotSupported;
-  constexpr int NG = kWarpsPerCta * 2;
+  constexpr int NG = kTauColWarps * 2;
   const size_t smem = size_t(NG) * kDstTileSize * sizeof(double2);
   const unsigned grid = unsigned(n_planes) * unsigned((255 + NG - 1) / NG);
   cudaError_t e = cudaSuccess;
@@ -583,13 +597,13 @@ cudaError_t launch_tau_cols_warp(double2* Z, int n, int n_planes, const double2*
         cudaSuccess)
       return e;
     if ((e = set_warp_carveout((const void*)k_tau_cols_warp<2>, smem)) != cudaSuccess) return e;
-    k_tau_cols_warp<2><<<grid, 32 * kWarpsPerCta, smem, st>>>(Z, n_planes, lambda, sigma, dt, tw_base);
+    k_tau_cols_warp<2><<<grid, 32 * kTauColWarps, smem, st>>>(Z, n_planes, lambda, sigma, dt, tw_base);
   } else {
     if ((e = cudaFuncSetAttribute(k_tau_cols_warp<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem))) !=
         cudaSuccess)
       return e;
     if ((e = set_warp_carveout((const void*)k_tau_cols_warp<1>, smem)) != cudaSuccess) return e;
-    k_tau_cols_warp<1><<<grid, 32 * kWarpsPerCta, smem, st>>>(Z, n_planes, lambda, sigma, dt, tw_base);
+    k_tau_cols_warp<1><<<grid, 32 * kTauColWarps, smem, st>>>(Z, n_planes, lambda, sigma, dt, tw_base);
   }
   note_launch();
   return cudaGetLastError();
