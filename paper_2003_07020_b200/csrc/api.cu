@@ -1398,6 +1398,16 @@ static void gmres_inner_lagged(fpc_plan_s* pl, const double* b, double* x, doubl
   // V[i]: buffer of basis vector i (V[0] = b, read only); v_i = sc[i] * V[i] once final
   std::vector<double*> V{const_cast<double*>(b)};
   std::vector<double> sc{1.0 / norm_b};
+  // Implicit re-orthogonalisation (default): the stored vectors V[k] are never rewritten; the
+  // orthonormal basis is v_k = sum_{i<=k} Sc[k][i] V[i], with the lagged second Gram-Schmidt pass
+  // of vector k entering Sc[k] instead of a U <- U - V a sweep (same vectors, two basis passes less
+  // per step: no read and no write of U in Q2).  Dots against the stored vectors are mapped to the
+  // orthonormal basis by Sc^T, update coefficients back by Sc.  FPC_GS_IMPLICIT=0: rewrite U.
+  static const bool implicit = [] {
+    const char* e = std::getenv("FPC_GS_IMPLICIT");
+    return !(e && e[0] == '0');
+  }();
+  std::vector<std::vector<double>> Sc{{1.0 / norm_b}};
   std::vector<std::vector<double>> R;   // raw Hessenberg columns (final, except the newest)
   std::vector<std::vector<double>> T;   // T[j][i]: Z_j = sum_i T[j][i] z~_i
   std::vector<double> gc, gs, g{norm_b}, g_pre, nb_before;
@@ -1467,7 +1477,7 @@ static void gmres_inner_lagged(fpc_plan_s* pl, const double* b, double* x, doubl
         fpc::VecSet16 vs{};
         for (int i = 0; i < cnt; ++i) {
           vs.v[i] = V[size_t(g0 + i)];
-          vs.s[i] = sc[size_t(g0 + i)];
+          vs.s[i] = implicit ? 1.0 : sc[size_t(g0 + i)];
         }
         LAUNCH("dots2", st, fpc::launch_dots2(vs, cnt, U, W, n, c->partial, stride, g0, g0 == 0, st));
       }
@@ -1478,8 +1488,18 @@ static void gmres_inner_lagged(fpc_plan_s* pl, const double* b, double* x, doubl
       std::vector<double> a(static_cast<size_t>(j)), bb(static_cast<size_t>(j));
       double aa = 0.0, ab = 0.0;
       for (int i = 0; i < j; ++i) {
-        a[size_t(i)] = c->hpin[i];
-        bb[size_t(i)] = c->hpin[fpc::kDots2B + i];
+        if (implicit) {  // <v_i, .> = sum_l Sc[i][l] <V[l], .>
+          double sa = 0.0, sb = 0.0;
+          for (int l = 0; l <= i; ++l) {
+            sa += Sc[size_t(i)][size_t(l)] * c->hpin[l];
+            sb += Sc[size_t(i)][size_t(l)] * c->hpin[fpc::kDots2B + l];
+          }
+          a[size_t(i)] = sa;
+          bb[size_t(i)] = sb;
+        } else {
+          a[size_t(i)] = c->hpin[i];
+          bb[size_t(i)] = c->hpin[fpc::kDots2B + i];
+        }
         aa += a[size_t(i)] * a[size_t(i)];
         ab += a[size_t(i)] * bb[size_t(i)];
       }
@@ -1500,6 +1520,13 @@ static void gmres_inner_lagged(fpc_plan_s* pl, const double* b, double* x, doubl
       }
       if (rho <= 1e-14 * std::max(1.0, nb_before[size_t(j) - 1])) break;  // krylov.hpp:160-165
       sc.push_back(1.0 / rho);
+      if (implicit) {  // v_j = (V[j] - sum_l a_l v_l)/rho
+        std::vector<double> sj(size_t(j) + 1, 0.0);
+        for (int l = 0; l < j; ++l)
+          for (int i = 0; i <= l; ++i) sj[size_t(i)] -= a[size_t(l)] * Sc[size_t(l)][size_t(i)] / rho;
+        sj[size_t(j)] = 1.0 / rho;
+        Sc.push_back(sj);
+      }
       // T column j: Z_j = (nu z~_j - sum_l a_l Z_l)/rho
       std::vector<double> tj(size_t(j) + 1, 0.0);
       tj[size_t(j)] = nu / rho;
@@ -1515,6 +1542,12 @@ static void gmres_inner_lagged(fpc_plan_s* pl, const double* b, double* x, doubl
       // Q2: U <- U - V a (= rho v_j);  W <- cw W + cu U + V cd (= the next candidate)
       const double t = gg[size_t(j)] / rho + col[size_t(j)];
       const double cw = nu / rho, cu = -t / rho;
+      // coefficient of v_k in the W update; implicit: mapped onto the stored vectors, cds = Sc cdt
+      std::vector<double> cdt(static_cast<size_t>(j)), cds(static_cast<size_t>(j), 0.0);
+      for (int k = 0; k < j; ++k) cdt[size_t(k)] = -gg[size_t(k)] / rho - col[size_t(k)] + t * a[size_t(k)] / rho;
+      if (implicit)
+        for (int k = 0; k < j; ++k)
+          for (int i = 0; i <= k; ++i) cds[size_t(i)] += Sc[size_t(k)][size_t(i)] * cdt[size_t(k)];
       for (int g0 = 0; g0 < j || g0 == 0; g0 += fpc::kMaxUpd2) {
         const int cnt = std::min(fpc::kMaxUpd2, j - g0);
         fpc::Update2Args ua{};
@@ -1523,11 +1556,11 @@ static void gmres_inner_lagged(fpc_plan_s* pl, const double* b, double* x, doubl
         for (int i = 0; i < cnt; ++i) {
           const int k = g0 + i;
           ua.v[i] = V[size_t(k)];
-          ua.ca[i] = a[size_t(k)] * sc[size_t(k)];
-          ua.cd[i] = (-gg[size_t(k)] / rho - col[size_t(k)] + t * a[size_t(k)] / rho) * sc[size_t(k)];
+          ua.ca[i] = implicit ? 0.0 : a[size_t(k)] * sc[size_t(k)];
+          ua.cd[i] = implicit ? cds[size_t(k)] : cdt[size_t(k)] * sc[size_t(k)];
         }
         const bool last = g0 + cnt >= j;
-        LAUNCH("update2", st, fpc::launch_update2(ua, cnt, g0 == 0, last, U, W, n, c->partial, st));
+        LAUNCH("update2", st, fpc::launch_update2(ua, cnt, g0 == 0, last, U, W, n, c->partial, st, implicit));
         if (last) break;
       }
       LAUNCH("reduce", st, fpc::launch_reduce(c->partial, 1, 1, c->dscal + 512, false, st));
@@ -1574,6 +1607,12 @@ static void gmres_inner_lagged(fpc_plan_s* pl, const double* b, double* x, doubl
       coef[size_t(i)] = y[size_t(i)];
       scales[size_t(i)] = sc[size_t(i)];
       ptr[size_t(i)] = V[size_t(i)];
+    }
+    if (implicit) {  // V y = V~ (Sc y)
+      std::fill(coef.begin(), coef.end(), 0.0);
+      std::fill(scales.begin(), scales.end(), 1.0);
+      for (int k = 0; k < steps; ++k)
+        for (int i = 0; i <= k; ++i) coef[size_t(i)] += Sc[size_t(k)][size_t(i)] * y[size_t(k)];
     }
   }
   ck(cudaMemcpyAsync(c->dvptr, ptr.data(), ptr.size() * sizeof(double*), cudaMemcpyHostToDevice, st), "vptr");

@@ -193,8 +193,9 @@ struct Update2Args {
   double cu, cw;
 };
 // U <- U - sum ca_i v_i; W <- (first ? cw W + cu U_old : W) + sum cd_i v_i; norm: partial = ||W||^2
+// keep_u: U is read (first group: the cu term) but not updated or written
 cudaError_t launch_update2(const Update2Args& a, int nv, bool first, bool norm, double* U, double* W,
-                           size_t n, double* partial, cudaStream_t st);
+                           size_t n, double* partial, cudaStream_t st, bool keep_u = false);
 
 // ---- commuted preconditioner ordering (kernels_commuted.cu), 1D --------------
 // out = S v per time level, levels (k, k + Nt/2) paired in one complex row; scale s_in

@@ -100,6 +100,9 @@ __device__ __forceinline__ double& comp(double2* s, int slot_padded, int c) {
 // =====================================================================================
 constexpr int kTotMv = 4096;
 
+#ifndef FPC_MV_PARKED_DEEP
+#define FPC_MV_PARKED_DEEP 1
+#endif
 #ifndef FPC_MV_CST_SMEM
 #define FPC_MV_CST_SMEM 2
 #endif
@@ -175,7 +178,53 @@ __global__ void __launch_bounds__(Geo<LOGM, TOT, 16>::NT, minb(Geo<LOGM, TOT, 16
       else if ((ns & 1) && m == s0 - 1) comp(smem, b * BS + pad16(m), 1) = 0.0;
     }
   }
-  for (int e0 = threadIdx.x; e0 < (kParked ? B * L : 0); e0 += U * NT) {
+#if FPC_MV_PARKED_DEEP
+  if (kParked) {
+    // the nb rows are one contiguous stretch of nb*ns doubles: only the real elements are visited
+    // (not the zero-padded half of the embedding), 3 x UP loads in flight per thread -- the phase is
+    // one DRAM round trip per batch (B200 config 3: four batches of 12 loads -> two of 24)
+    constexpr int UP = 8;
+    const int nreal = nb * ns;
+    const double* src = v + size_t(k0) * ns;
+    for (int e0 = threadIdx.x; e0 < nreal; e0 += UP * NT) {
+      double x0[UP], x1[UP], x2[UP];
+#pragma unroll
+      for (int u = 0; u < UP; ++u) {
+        const int e = e0 + u * NT;
+        const bool ok = e < nreal;
+        const int b = div_small(ok ? e : 0, ns, inv_ns);
+        const int k = div_small(k0 + b, rpt, inv_rpt) + koff;
+        x0[u] = ok ? src[e] : 0.0;
+        x1[u] = (ok && k >= 1) ? src[ptrdiff_t(e) - sstride] : 0.0;
+        x2[u] = (ok && k >= 2) ? src[ptrdiff_t(e) - 2 * ptrdiff_t(sstride)] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < UP; ++u) {
+        const int e = e0 + u * NT;
+        if (e < nreal) {
+          const int b = div_small(e, ns, inv_ns), idx = e - b * ns;
+          const int k = div_small(k0 + b, rpt, inv_rpt) + koff;
+          comp(smem, b * BS + pad16(idx >> 1), idx & 1) = x0[u];
+          double c;
+          if (k == 0)
+            c = x0[u];
+          else if (k == 1)
+            c = 1.5 * x0[u] + -2.0 * x1[u];
+          else
+            c = 1.5 * x0[u] + -2.0 * x1[u] + 0.5 * x2[u];
+          cst[b * M + idx] = c;
+        }
+      }
+    }
+    const int s0 = (ns + 1) >> 1;
+    for (int t = threadIdx.x; t < B * M; t += NT) {
+      const int b = t / M, m = t - b * M;
+      if (b >= nb || m >= s0) smem[b * BS + pad16(m)] = make_double2(0.0, 0.0);
+      else if ((ns & 1) && m == s0 - 1) comp(smem, b * BS + pad16(m), 1) = 0.0;
+    }
+  }
+#endif
+  for (int e0 = threadIdx.x; e0 < ((kParked && !FPC_MV_PARKED_DEEP) ? B * L : 0); e0 += U * NT) {
     double x0[U], x1[U], x2[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {

@@ -534,7 +534,10 @@ cudaError_t launch_dots2(const VecSet16& vs, int nv, const double* U, const doub
 // U <- U - sum_i ca_i v_i ; W <- cw W + cu U_old + sum_i cd_i v_i  (coefficients already carry the
 // basis scales); NORM: partial[blk] = ||W_new||^2.  FIRST: the cw/cu terms are applied (a later
 // group of basis vectors only adds its sums in place).
-template <int NV, bool FIRST, bool NORM>
+// KEEPU: U is left as stored (the re-orthogonalisation of the previous vector is carried in the
+// host's basis-transformation matrix instead, api.cu gmres_inner_lagged): no U update, no U write,
+// and no U read at all in the later groups.
+template <int NV, bool FIRST, bool NORM, bool KEEPU>
 __global__ void __launch_bounds__(kDotsThreads)
     k_update2(Update2Args a, double* __restrict__ U, double* __restrict__ W, size_t n,
               double* __restrict__ partial) {
@@ -544,7 +547,9 @@ __global__ void __launch_bounds__(kDotsThreads)
   double2* w2 = reinterpret_cast<double2*>(W);
   for (size_t e = size_t(blockIdx.x) * kDotsThreads + threadIdx.x; e < n2;
        e += size_t(kDotsGrid) * kDotsThreads) {
-    const double2 uv = u2[e], wv = w2[e];
+    const double2 wv = w2[e];
+    double2 uv = make_double2(0.0, 0.0);
+    if (FIRST || !KEEPU) uv = u2[e];
     double2 nu = uv, nw;
     if (FIRST) {
       nw.x = fma(a.cw, wv.x, a.cu * uv.x);
@@ -555,12 +560,14 @@ __global__ void __launch_bounds__(kDotsThreads)
 #pragma unroll
     for (int i = 0; i < NV; ++i) {
       const double2 x = reinterpret_cast<const double2*>(a.v[i])[e];
-      nu.x = fma(-a.ca[i], x.x, nu.x);
-      nu.y = fma(-a.ca[i], x.y, nu.y);
+      if (!KEEPU) {
+        nu.x = fma(-a.ca[i], x.x, nu.x);
+        nu.y = fma(-a.ca[i], x.y, nu.y);
+      }
       nw.x = fma(a.cd[i], x.x, nw.x);
       nw.y = fma(a.cd[i], x.y, nw.y);
     }
-    u2[e] = nu;
+    if (!KEEPU) u2[e] = nu;
     w2[e] = nw;
     if (NORM) {
       acc[0] = fma(nw.x, nw.x, acc[0]);
@@ -576,7 +583,7 @@ __global__ void __launch_bounds__(kDotsThreads)
       nu = fma(-a.ca[i], x, nu);
       nw = fma(a.cd[i], x, nw);
     }
-    U[n - 1] = nu;
+    if (!KEEPU) U[n - 1] = nu;
     W[n - 1] = nw;
     if (NORM) acc[0] = fma(nw, nw, acc[0]);
   }
@@ -589,17 +596,25 @@ __global__ void __launch_bounds__(kDotsThreads)
 }
 
 cudaError_t launch_update2(const Update2Args& a, int nv, bool first, bool norm, double* U, double* W,
-                           size_t n, double* partial, cudaStream_t st) {
+                           size_t n, double* partial, cudaStream_t st, bool keep_u) {
+#define U2K(NVV, F, NRM)                                                                               \
+  {                                                                                                    \
+    if (keep_u)                                                                                        \
+      k_update2<NVV, F, NRM, true><<<kDotsGrid, kDotsThreads, 0, st>>>(a, U, W, n, partial);           \
+    else                                                                                               \
+      k_update2<NVV, F, NRM, false><<<kDotsGrid, kDotsThreads, 0, st>>>(a, U, W, n, partial);          \
+    note_launch();                                                                                     \
+  }
 #define U2(NVV)                                                                                        \
   case NVV:                                                                                            \
     if (first && norm)                                                                                 \
-      { k_update2<NVV, true, true><<<kDotsGrid, kDotsThreads, 0, st>>>(a, U, W, n, partial); note_launch(); }             \
+      U2K(NVV, true, true)                                                                             \
     else if (first)                                                                                    \
-      { k_update2<NVV, true, false><<<kDotsGrid, kDotsThreads, 0, st>>>(a, U, W, n, partial); note_launch(); }            \
+      U2K(NVV, true, false)                                                                            \
     else if (norm)                                                                                     \
-      { k_update2<NVV, false, true><<<kDotsGrid, kDotsThreads, 0, st>>>(a, U, W, n, partial); note_launch(); }            \
+      U2K(NVV, false, true)                                                                            \
     else                                                                                               \
-      { k_update2<NVV, false, false><<<kDotsGrid, kDotsThreads, 0, st>>>(a, U, W, n, partial); note_launch(); }           \
+      U2K(NVV, false, false)                                                                           \
     break;
   switch (nv) {
     U2(0) U2(1) U2(2) U2(3) U2(4) U2(5) U2(6) U2(7) U2(8) U2(9) U2(10) U2(11) U2(12)
@@ -607,6 +622,7 @@ cudaError_t launch_update2(const Update2Args& a, int nv, bool first, bool norm, 
     default:
       return cudaErrorInvalidValue;
   }
+#undef U2K
 #undef U2
   return cudaGetLastError();
 }
