@@ -48,12 +48,19 @@ struct TmaGeo {
   static constexpr int B = 2048 / M;
   static constexpr int NT = B * M / 16;
   static constexpr int BS = skewed_t(M);
-  static constexpr int RB = M / 2 + 1;  // rows per box of the inverse's spectrum tile
+  // a TMA box has at most 256 rows: the forward tile is NBF boxes of RF time-level pairs per parity,
+  // the inverse's spectrum tile (M + 1 rows) NBI boxes of RB rows (RB B a multiple of 8, so every
+  // box lands 128-byte aligned; rows past M are zero filled)
+  static constexpr int RF = M < 256 ? M : 256, NBF = M / RF;
+  static constexpr int NBI = (M + 1 + 255) / 256;
+  static constexpr int RBQ = B >= 8 ? 1 : 8 / B;
+  static constexpr int RB = ((M + 1 + NBI - 1) / NBI + RBQ - 1) / RBQ * RBQ;
+  static constexpr bool TABLE = LOGM <= 8;  // scale_bwd / Nt in shared memory (no room at M = 512)
   static constexpr size_t FFT = size_t(B) * BS * sizeof(double2);
   static constexpr size_t STAGE_EVEN = size_t(M) * B * sizeof(double);
   static constexpr size_t STAGE_FWD = STAGE_EVEN + size_t(M) * (B + 2) * sizeof(double);
-  static constexpr size_t STAGE_INV = size_t(2 * RB) * B * sizeof(double2);
-  static constexpr size_t TAB = size_t(NTIME) * sizeof(double);
+  static constexpr size_t STAGE_INV = size_t(NBI * RB) * B * sizeof(double2);
+  static constexpr size_t TAB = TABLE ? size_t(NTIME) * sizeof(double) : 0;
   static constexpr size_t SMEM_FWD = STAGE_FWD + FFT + 16;
   static constexpr size_t SMEM_INV = STAGE_INV + FFT + TAB + 16;
 };
@@ -95,8 +102,12 @@ __global__ void __launch_bounds__(TmaGeo<LOGM>::NT, kCtasPerSm)
   __syncthreads();
   auto fetch = [&](int tile) {  // one thread: both boxes of the tile, one barrier phase
     mbar_arrive_expect_tx(bar, uint32_t(M * (B + po) * sizeof(double)));
-    tma_load_2d(stage, &map_even, tile * B, 0, bar);
-    tma_load_2d(base + G::STAGE_EVEN, &map_odd, ns - off + tile * B, 0, bar);
+#pragma unroll
+    for (int bi = 0; bi < G::NBF; ++bi) {
+      tma_load_2d(stage + bi * G::RF * B, &map_even, tile * B, bi * G::RF, bar);
+      tma_load_2d(base + G::STAGE_EVEN + size_t(bi) * G::RF * po * sizeof(double), &map_odd, ns - off + tile * B,
+                  bi * G::RF, bar);
+    }
   };
   int tile = int(blockIdx.x);
   uint32_t phase = 0;
@@ -191,12 +202,14 @@ __global__ void __launch_bounds__(TmaGeo<LOGM>::NT, kCtasPerSm)
     mbar_fence_init();
   }
   const double inv_nt = 1.0 / double(NTIME);
-  for (int i = tid; i < NTIME; i += NT) sbs[i] = __ldg(sb + i) * inv_nt;
+  if constexpr (G::TABLE)
+    for (int i = tid; i < NTIME; i += NT) sbs[i] = __ldg(sb + i) * inv_nt;
   __syncthreads();
   auto fetch = [&](int tile) {
     mbar_arrive_expect_tx(bar, uint32_t(G::STAGE_INV));
-    tma_load_2d(stage, &tmap, 2 * tile * B, 0, bar);
-    tma_load_2d(stage + RB * B, &tmap, 2 * tile * B, RB, bar);  // rows past n_time/2 are zero filled
+#pragma unroll
+    for (int bi = 0; bi < G::NBI; ++bi)  // rows past n_time/2 are zero filled
+      tma_load_2d(stage + bi * RB * B, &tmap, 2 * tile * B, bi * RB, bar);
   };
   int tile = int(blockIdx.x);
   uint32_t phase = 0;
@@ -255,7 +268,7 @@ __global__ void __launch_bounds__(TmaGeo<LOGM>::NT, kCtasPerSm)
       for (int i = 0; i < ITER; ++i) {
         const int kk = tid / B + i * STEP;
         const double val = reinterpret_cast<const double*>(s + pad16(kk >> 1))[kk & 1];
-        z[size_t(kk) * ns + p] = sbs[kk] * val;
+        z[size_t(kk) * ns + p] = (G::TABLE ? sbs[kk] : __ldg(sb + kk) * inv_nt) * val;
       }
     }
     __syncthreads();
@@ -323,7 +336,12 @@ cudaError_t prep_tma(K kernel, size_t smem) {
 }  // namespace
 
 bool time_tma_supported(int n_space, int n_time, const void* in, bool inverse) {
-  if (!tma_enabled(inverse) || (n_time != 128 && n_time != 256 && n_time != 512)) return false;
+  static const bool t1024 = [] {  // n_time = 1024: the 2-CTA split kernels unless FPC_TIME_TMA_1024=1 (A/B)
+    const char* e = std::getenv("FPC_TIME_TMA_1024");
+    return e && e[0] == '1';
+  }();
+  if (!tma_enabled(inverse) || (n_time != 128 && n_time != 256 && n_time != 512 && !(n_time == 1024 && t1024)))
+    return false;
   if (reinterpret_cast<uintptr_t>(in) & 15) return false;
   const int b = 2048 / (n_time / 2);
   return (n_space + b - 1) / b >= 2 * sm_count() && encode_fn() != nullptr;
@@ -335,8 +353,8 @@ cudaError_t launch_time_fwd_tma(const double* v, double2* Z, int n_space, int n_
 #define CALL(LM)                                                                                         \
   {                                                                                                      \
     using G = TmaGeo<LM>;                                                                                \
-    if (!make_map(&map, v, n_space, G::M, G::B, G::M) ||                                                 \
-        !make_map(&map_odd, v, n_space, G::M, G::B + 2 * (n_space & 1), G::M))                           \
+    if (!make_map(&map, v, n_space, G::M, G::B, G::RF) ||                                                \
+        !make_map(&map_odd, v, n_space, G::M, G::B + 2 * (n_space & 1), G::RF))                          \
       return cudaErrorInvalidValue;                                                                      \
     const int tiles = (n_space + G::B - 1) / G::B;                                                       \
     const int grid = tiles < kCtasPerSm * sm_count() ? tiles : kCtasPerSm * sm_count();                  \
@@ -346,7 +364,7 @@ cudaError_t launch_time_fwd_tma(const double* v, double2* Z, int n_space, int n_
                                                          tw_base);                                       \
     note_launch();                                                                                       \
   }
-  if (n_time == 512) CALL(8) else if (n_time == 256) CALL(7) else if (n_time == 128) CALL(6) else return cudaErrorNotSupported;
+  if (n_time == 1024) CALL(9) else if (n_time == 512) CALL(8) else if (n_time == 256) CALL(7) else if (n_time == 128) CALL(6) else return cudaErrorNotSupported;
 #undef CALL
   return cudaGetLastError();
 }
@@ -365,7 +383,7 @@ cudaError_t launch_time_inv_tma(const double2* Z, double* z, int n_space, int n_
     k_time_inv_tma<LM><<<grid, G::NT, G::SMEM_INV, st>>>(map, z, n_space, tiles, scale_bwd, tw_base); \
     note_launch();                                                                                   \
   }
-  if (n_time == 512) CALL(8) else if (n_time == 256) CALL(7) else if (n_time == 128) CALL(6) else return cudaErrorNotSupported;
+  if (n_time == 1024) CALL(9) else if (n_time == 512) CALL(8) else if (n_time == 256) CALL(7) else if (n_time == 128) CALL(6) else return cudaErrorNotSupported;
 #undef CALL
   return cudaGetLastError();
 }
