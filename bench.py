@@ -586,6 +586,11 @@ def measure(fp, torch, w, args, stream, ctx, dev, steps, warmup, full, sync=None
                         "peak_tflops": ocp["fp64_fma_tflops"], "frac": f / dom_t / 1e12 / ocp["fp64_fma_tflops"],
                         "formula": "SURVEY 8(d) F_mv (reference algorithm: two complex FFTs of length L per "
                                    "Toeplitz product)", "peak_source": "profiles/onchip_peaks.json (measured)"}
+    if onchip and onchip.get("kernels"):  # ncu pipe utilisation of the category's kernels, time weighted
+        ks = list(onchip["kernels"].values())
+        tw = sum(k_["us_ncu"] for k_ in ks) or 1.0
+        roof["fp64_pipe_frac"] = sum(k_["us_ncu"] * k_["fp64_pipe_pct"] for k_ in ks) / tw / 100.0
+        roof["l1_data_pipe_frac"] = sum(k_["us_ncu"] * k_["l1tex_pct"] for k_ in ks) / tw / 100.0
     out["roofline"] = roof
     out["kernel_time_ms_per_solve"] = {k_: v[0] for k_, v in table.items()}
     out["kernel_launches_per_solve"] = {k_: v[1] for k_, v in table.items()}
