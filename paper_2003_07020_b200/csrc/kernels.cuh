@@ -15,7 +15,7 @@ void note_launch();
 
 // Shared-memory carveout for a kernel: the smallest supported shared-memory capacity (sm_100: 0, 8,
 // 16, 32, 64, 100, 132, 164, 196, 228 KB per SM) that still holds the CTAs per SM the kernel's
-// register budget allows (threads: <=128 -> 4, <=256 -> 2, else 1), so the rest of the 256 KB
+// register budget allows (threads: <=64 -> 8, <=128 -> 4, <=256 -> 2, else 1), so the rest of the 256 KB
 // L1/shared array stays L1 for the twiddle and eigenvalue tables.  FPC_CARVEOUT=max restores
 // the maximum shared-memory carveout.
 int carveout_pct(size_t dyn_smem, int threads);

@@ -700,7 +700,7 @@ cudaError_t launch_time_fwd(const double* v, double2* Z, int n_space, int n_time
 #define CALL(LM)                                                                          \
   {                                                                                       \
     using G = Geo<LM, tot_t<LM>()>;                                                             \
-    if constexpr (is_smaller<LM, tot_t<LM>()>()) {                                        \
+    if constexpr (is_smaller<LM, tot_t<LM>()>() && LM <= 10) {  /* n_time >= 4096: one-column tiles (8-byte row segments) lose */                                        \
       if ((n_space + G::B - 1) / G::B < kSmallGrid) {                                     \
         constexpr int T = small_tot<LM>();                                                \
         using GS = Geo<LM, T>;                                                            \
@@ -729,7 +729,7 @@ cudaError_t launch_time_inv(const double2* Z, double* z, int n_space, int n_time
 #define CALL(LM)                                                                            \
   {                                                                                         \
     using G = Geo<LM, tot_t<LM>()>;                                                               \
-    if constexpr (is_smaller<LM, tot_t<LM>()>()) {                                          \
+    if constexpr (is_smaller<LM, tot_t<LM>()>() && LM <= 10) {  /* n_time >= 4096: one-column tiles (8-byte row segments) lose */                                          \
       if ((n_space + G::B - 1) / G::B < kSmallGrid) {                                       \
         constexpr int T = small_tot<LM>();                                                  \
         using GS = Geo<LM, T>;                                                              \

@@ -18,7 +18,8 @@ int carveout_pct(size_t dyn_smem, int threads) {
     return e && std::string(e) == "max";
   }();
   if (maxed) return 100;
-  const int by_regs = threads <= 128 ? 4 : threads <= 256 ? 2 : 1;
+  // CTAs per SM at ~128 registers per thread (16 warps): 64-thread CTAs of the small-grid tilings fit 8
+  const int by_regs = threads <= 64 ? 8 : threads <= 128 ? 4 : threads <= 256 ? 2 : 1;
   const size_t per_cta = dyn_smem + 2048;  // + static shared memory and the 1 KB system reserve
   const int by_smem = int((228u * 1024u) / per_cta);
   const int ctas = by_smem < by_regs ? (by_smem > 0 ? by_smem : 1) : by_regs;
