@@ -333,7 +333,9 @@ def run_sweep(args):
                 op.apply(xr, yr)
                 op.apply(xi, yi)
 
-            with ClockSampler(0) as clk:
+            # torch's current stream = the library stream: the API's cross-stream ordering events
+            # (two per call) are not needed and are skipped
+            with ClockSampler(0) as clk, torch.cuda.stream(stream):
                 t_pc = timed(pc, args.sweep_reps)
                 t_mv = timed(mv, args.sweep_reps)
             H = nt // 2 + 1

@@ -636,6 +636,9 @@ static cudaError_t prep(K kernel, size_t smem, int threads = 1024) {
 // matvec CTAs, 33 tau CTAs, 32 time-FFT CTAs).  When the default tiling gives fewer than two waves,
 // the same kernels run with 512-slot tiles (B = max(1, 512 / M): 1-4 rows or columns per CTA).
 constexpr int kSmallGrid = 2 * 148;
+// rows matvec: the 64-thread tiling wins at 128 default CTAs (1023 x 512: 27K -> 30K matvecs/s) and
+// loses at 256 (1023 x 1024: 20K -> 17K)
+constexpr int kSmallGridMv = 200;
 template <int LM>
 constexpr int small_tot() { return (1 << LM) >= 512 ? (1 << LM) : 512; }
 template <int LM, int TOT>
@@ -651,7 +654,7 @@ cudaError_t launch_matvec_rows(const double* v, double* y, int len, int nrows, i
   {                                                                                       \
     using G = Geo<LM, kTotMv, 16>;                                                        \
     if constexpr (is_smaller<LM, kTotMv>()) {                                             \
-      if ((nrows + G::B - 1) / G::B < kSmallGrid) {                                       \
+      if ((nrows + G::B - 1) / G::B < kSmallGridMv) {                                     \
         constexpr int T = small_tot<LM>();                                                \
         using GS = Geo<LM, T, 16>;                                                        \
         if ((err = prep(k_matvec_1d<LM, T>, MvGeo<LM, T>::SMEM, GS::NT)) != cudaSuccess) return err; \
