@@ -83,6 +83,17 @@ cudaError_t launch_matvec_rows_warp(const double* v, double* y, int len, int nro
                                     int log_m, const double* eig_scaled, const double2* tw_base,
                                     cudaStream_t st, int koff);
 bool warp_kernels_enabled();
+// the same for M = 1024 (rows / columns of 513..1023 points: config 3's n = 1023) on one warp per
+// transform, 32 lanes x 32 registers (kernels_warp32.cu).  FPC_W32=0 keeps the CTA-level kernels (A/B).
+bool warp32_kernels_enabled();
+cudaError_t launch_matvec_rows_w32(const double* v, double* y, int len, int nrows, int rpt, int sstride,
+                                   const double* eig_scaled, const double2* tw_base, cudaStream_t st, int koff);
+cudaError_t launch_dst_rows_w32(double2* Z, int n, int n_rows, const double2* lambda, const double* sigma,
+                                double dt, const double2* tw_base, cudaStream_t st, int mode);
+cudaError_t launch_tau_cols_w32(double2* Z, int n, int n_planes, const double2* lambda, const double* sigma,
+                                double dt, const double2* tw_base, cudaStream_t st, bool forward);
+cudaError_t launch_matvec_cols_w32(const double* v, double* y, int n, int n_time, const double* eig_x,
+                                   const double2* tw_base, cudaStream_t st);
 // the 2D tau solve's column pass (DST, shift, DST along ix) on warp-owned transforms for n = 255
 cudaError_t launch_tau_cols_warp(double2* Z, int n, int n_planes, const double2* lambda, const double* sigma,
                                  double dt, const double2* tw_base, cudaStream_t st, bool forward);

@@ -313,6 +313,8 @@ cudaError_t launch_matvec_2d(const double* v, double* y, int n, int n_time, int 
   if (err != cudaSuccess) return err;
   if (log_m == 8 && warp_kernels_enabled())
     return launch_matvec_cols_warp(v, y, n, n_time, log_m, eig_x_scaled, tw_base, st);
+  if (log_m == 10 && warp32_kernels_enabled())
+    return launch_matvec_cols_w32(v, y, n, n_time, eig_x_scaled, tw_base, st);
 #define CALL(LM)                                                                          \
   {                                                                                       \
     using G = ColGeo<LM>;                                                                 \
@@ -357,6 +359,11 @@ cudaError_t launch_tau_solve_2d(double2* Z, int n, int n_rows, const double2* la
   const int lm = ilog2i(n + 1);
   if (n == 255 && warp_kernels_enabled()) {
     if ((err = launch_tau_cols_warp(Z, n, n_rows, lambda, sigma, dt, tw_base, st, forward)) != cudaSuccess)
+      return err;
+    return launch_dst_rows(Z, n, n_rows * n, tw_base, st);
+  }
+  if (n == 1023 && warp32_kernels_enabled()) {
+    if ((err = launch_tau_cols_w32(Z, n, n_rows, lambda, sigma, dt, tw_base, st, forward)) != cudaSuccess)
       return err;
     return launch_dst_rows(Z, n, n_rows * n, tw_base, st);
   }
