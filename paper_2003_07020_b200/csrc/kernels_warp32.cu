@@ -16,6 +16,19 @@ namespace fpc {
 namespace {
 
 constexpr int kW32Warps = 4;  // warps per CTA; two CTAs per SM (255 registers per thread)
+// column kernels: warps (= adjacent columns) per CTA, 8 warps per SM either way (build knobs, A/B on
+// 1023^2 x 64): the matvec columns (8-byte elements) gain from 64-byte row segments with 8 columns
+// (844 -> 750 us), the tau columns (16-byte elements, 64-byte segments already) lose the overlap of
+// two CTAs' staging phases (1.41 -> 1.47 ms per tau solve)
+#ifndef FPC_W32_MV_COLW
+#define FPC_W32_MV_COLW 8
+#endif
+#ifndef FPC_W32_TAU_COLW
+#define FPC_W32_TAU_COLW 4
+#endif
+constexpr int kW32MvColWarps = FPC_W32_MV_COLW, kW32TauColWarps = FPC_W32_TAU_COLW;
+static_assert((kW32MvColWarps == 4 || kW32MvColWarps == 8) && (kW32TauColWarps == 4 || kW32TauColWarps == 8),
+              "column kernels: 4 or 8 columns per CTA");
 
 __device__ __forceinline__ double bdf2_w32(int k, double x0, double x1, double x2) {
   if (k == 0) return x0;
@@ -38,11 +51,11 @@ __device__ __forceinline__ void cp_async16(void* smem_dst, const void* src, bool
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
-cudaError_t prep_w32(const void* kernel, size_t smem) {
+cudaError_t prep_w32(const void* kernel, size_t smem, int warps = kW32Warps) {
   cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   if (e != cudaSuccess) return e;
   return cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
-                              carveout_pct(smem, 32 * kW32Warps));
+                              carveout_pct(smem, 32 * warps));
 }
 
 }  // namespace
@@ -128,16 +141,16 @@ cudaError_t launch_matvec_rows_w32(const double* v, double* y, int len, int nrow
 // of 32 different rows) and writes column c into warp c's tile; the results go back the same way and
 // are added to y as L2 reductions (RED.ADD.F64: each element receives exactly one add, so the sum
 // is the same double as load-add-store).
-__global__ void __launch_bounds__(32 * kW32Warps, 2)
+__global__ void __launch_bounds__(32 * kW32MvColWarps, 8 / kW32MvColWarps)
     k_mv_cols_w32(const double* __restrict__ v, double* __restrict__ y, int n, const double* __restrict__ eig,
                   const double2* __restrict__ twb) {
-  constexpr int R = 32, M = 1024, L = 2 * M, H = 16, C = kW32Warps, NT = 32 * kW32Warps;
+  constexpr int R = 32, M = 1024, L = 2 * M, H = 16, C = kW32MvColWarps, NT = 32 * kW32MvColWarps;
   constexpr int CP = 2 * kW32Tile;  // doubles per warp tile (2112)
   // staged column of warp c: element ix = 2 m + h (packed slot m = tt + 32 r) at (2 r + h) * SH + tt,
   // shifted by c * SC: a lane's reads are unit stride over tt, and a staging instruction (4 columns x 8
   // rows = 4 m x 2 h per column) spreads over all 16 bank pairs (m: 0..3, h: +4, c: +8 mod 16)
-  constexpr int SH = 36, SC = 8;
-  static_assert(31 * SH + 32 + 3 * SC <= CP, "staged column fits the tile");
+  constexpr int SH = 36, SC = C == 4 ? 8 : 2;
+  static_assert(31 * SH + 32 + (C - 1) * SC <= CP, "staged column fits the tile");
   extern __shared__ double2 wsm[];
   double* tiles = reinterpret_cast<double*>(wsm);
   const int ntile = (n + C - 1) / C;
@@ -196,11 +209,11 @@ __global__ void __launch_bounds__(32 * kW32Warps, 2)
 
 cudaError_t launch_matvec_cols_w32(const double* v, double* y, int n, int n_time, const double* eig_x,
                                    const double2* tw_base, cudaStream_t st) {
-  const size_t smem = size_t(kW32Warps) * kW32Tile * sizeof(double2);
-  cudaError_t e = prep_w32((const void*)k_mv_cols_w32, smem);
+  const size_t smem = size_t(kW32MvColWarps) * kW32Tile * sizeof(double2);
+  cudaError_t e = prep_w32((const void*)k_mv_cols_w32, smem, kW32MvColWarps);
   if (e != cudaSuccess) return e;
-  const unsigned grid = unsigned(n_time) * unsigned((n + kW32Warps - 1) / kW32Warps);
-  k_mv_cols_w32<<<grid, 32 * kW32Warps, smem, st>>>(v, y, n, eig_x, tw_base);
+  const unsigned grid = unsigned(n_time) * unsigned((n + kW32MvColWarps - 1) / kW32MvColWarps);
+  k_mv_cols_w32<<<grid, 32 * kW32MvColWarps, smem, st>>>(v, y, n, eig_x, tw_base);
   note_launch();
   return cudaGetLastError();
 }
@@ -273,10 +286,10 @@ cudaError_t launch_dst_rows_w32(double2* Z, int n, int n_rows, const double2* la
 // quarter warp hit 8 different 16-byte banks.  sigma = the plan's table [ix][iy] followed by its
 // transpose [iy][ix] (read here: contiguous in ix).
 template <int MODE>
-__global__ void __launch_bounds__(32 * kW32Warps, 2)
+__global__ void __launch_bounds__(32 * kW32TauColWarps, 8 / kW32TauColWarps)
     k_tau_cols_w32(double2* __restrict__ Z, const double2* __restrict__ lam, const double* __restrict__ sigma,
                    double dt, const double2* __restrict__ twb) {
-  constexpr int NSR = 1023, C = kW32Warps, NT = 32 * kW32Warps, RS = NT / C;
+  constexpr int NSR = 1023, C = kW32TauColWarps, NT = 32 * kW32TauColWarps, RS = NT / C, SK = 8 / C;
   extern __shared__ double2 wsm[];
   constexpr int ntile = (NSR + C - 1) / C;
   const int rp = int(blockIdx.x) / ntile;
@@ -288,14 +301,14 @@ __global__ void __launch_bounds__(32 * kW32Warps, 2)
   const int c = int(threadIdx.x) % C, ix0 = int(threadIdx.x) / C;
   const bool okc = c < ncol;
   {
-    double2* dst = wsm + c * kDst32Tile + 2 * c;
+    double2* dst = wsm + c * kDst32Tile + SK * c;
     const double2* zc = zb + (okc ? c : 0);
 #pragma unroll 8
     for (int ix = ix0; ix < NSR; ix += RS) cp_async16(dst + dst32_slot(ix), zc + size_t(ix) * NSR, okc);
     cp_async_wait_all();
   }
   __syncthreads();
-  double2* xs = wsm + w * kDst32Tile + 2 * w;
+  double2* xs = wsm + w * kDst32Tile + SK * w;
   const double scale = 0.044194173824159220275;  // sqrt(2/1024)
   // DST, shift, DST: one copy of the transform code (the unrolled DST is ~10K instructions)
 #pragma unroll 1
@@ -319,7 +332,7 @@ __global__ void __launch_bounds__(32 * kW32Warps, 2)
   }
   __syncthreads();
   if (okc) {
-    const double2* src = wsm + c * kDst32Tile + 2 * c;
+    const double2* src = wsm + c * kDst32Tile + SK * c;
 #pragma unroll 8
     for (int ix = ix0; ix < NSR; ix += RS) zb[size_t(ix) * NSR + c] = src[dst32_slot(ix)];
   }
@@ -328,15 +341,15 @@ __global__ void __launch_bounds__(32 * kW32Warps, 2)
 cudaError_t launch_tau_cols_w32(double2* Z, int n, int n_planes, const double2* lambda, const double* sigma,
                                 double dt, const double2* tw_base, cudaStream_t st, bool forward) {
   if (n != 1023) return cudaErrorNotSupported;
-  const size_t smem = size_t(kW32Warps) * kDst32Tile * sizeof(double2);
-  const unsigned grid = unsigned(n_planes) * unsigned((1023 + kW32Warps - 1) / kW32Warps);
+  const size_t smem = size_t(kW32TauColWarps) * kDst32Tile * sizeof(double2);
+  const unsigned grid = unsigned(n_planes) * unsigned((1023 + kW32TauColWarps - 1) / kW32TauColWarps);
   cudaError_t e = cudaSuccess;
   if (forward) {
-    if ((e = prep_w32((const void*)k_tau_cols_w32<2>, smem)) != cudaSuccess) return e;
-    k_tau_cols_w32<2><<<grid, 32 * kW32Warps, smem, st>>>(Z, lambda, sigma, dt, tw_base);
+    if ((e = prep_w32((const void*)k_tau_cols_w32<2>, smem, kW32TauColWarps)) != cudaSuccess) return e;
+    k_tau_cols_w32<2><<<grid, 32 * kW32TauColWarps, smem, st>>>(Z, lambda, sigma, dt, tw_base);
   } else {
-    if ((e = prep_w32((const void*)k_tau_cols_w32<1>, smem)) != cudaSuccess) return e;
-    k_tau_cols_w32<1><<<grid, 32 * kW32Warps, smem, st>>>(Z, lambda, sigma, dt, tw_base);
+    if ((e = prep_w32((const void*)k_tau_cols_w32<1>, smem, kW32TauColWarps)) != cudaSuccess) return e;
+    k_tau_cols_w32<1><<<grid, 32 * kW32TauColWarps, smem, st>>>(Z, lambda, sigma, dt, tw_base);
   }
   note_launch();
   return cudaGetLastError();
