@@ -86,6 +86,7 @@ bool warp_kernels_enabled();
 // the same for M = 1024 (rows / columns of 513..1023 points: config 3's n = 1023) on one warp per
 // transform, 32 lanes x 32 registers (kernels_warp32.cu).  FPC_W32=0 keeps the CTA-level kernels (A/B).
 bool warp32_kernels_enabled();
+int warp32_min_rows();
 cudaError_t launch_matvec_rows_w32(const double* v, double* y, int len, int nrows, int rpt, int sstride,
                                    const double* eig_scaled, const double2* tw_base, cudaStream_t st, int koff);
 cudaError_t launch_dst_rows_w32(double2* Z, int n, int n_rows, const double2* lambda, const double* sigma,

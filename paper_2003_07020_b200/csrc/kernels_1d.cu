@@ -651,7 +651,7 @@ cudaError_t launch_matvec_rows(const double* v, double* y, int len, int nrows, i
   if (log_m == 8 && warp_kernels_enabled())
     return launch_matvec_rows_warp(v, y, len, nrows, rpt, sstride, log_m, eig_scaled, tw_base, st, koff);
   // one warp per row needs a full wave of warps (8 per SM) to pay; smaller grids keep the CTA kernel
-  if (log_m == 10 && nrows >= 8 * 148 && warp32_kernels_enabled())
+  if (log_m == 10 && nrows >= warp32_min_rows() && warp32_kernels_enabled())
     return launch_matvec_rows_w32(v, y, len, nrows, rpt, sstride, eig_scaled, tw_base, st, koff);
 #define CALL(LM)                                                                          \
   {                                                                                       \
@@ -760,7 +760,7 @@ cudaError_t launch_dst_rows(double2* Z, int n, int n_rows, const double2* tw_bas
   cudaError_t err = cudaSuccess;
   if (n == 255 && warp_kernels_enabled())
     return launch_dst_rows_warp(Z, n, n_rows, nullptr, nullptr, 0.0, tw_base, st, 0);
-  if (n == 1023 && n_rows >= 8 * 148 && warp32_kernels_enabled())
+  if (n == 1023 && n_rows >= warp32_min_rows() && warp32_kernels_enabled())
     return launch_dst_rows_w32(Z, n, n_rows, nullptr, nullptr, 0.0, tw_base, st, 0);
   const int lm = ilog2(n + 1);
 #define CALL(LM)                                                                          \
@@ -808,7 +808,7 @@ cudaError_t launch_tau_solve_1d(double2* Z, int n_space, int n_rows, const doubl
   if (lm >= 14) return launch_tau_large(Z, n_space, n_rows, lambda, sigma, dt, tw_base, st, forward);
   if (n_space == 255 && warp_kernels_enabled())
     return launch_dst_rows_warp(Z, n_space, n_rows, lambda, sigma, dt, tw_base, st, forward ? 2 : 1);
-  if (n_space == 1023 && n_rows >= 8 * 148 && warp32_kernels_enabled())
+  if (n_space == 1023 && n_rows >= warp32_min_rows() && warp32_kernels_enabled())
     return launch_dst_rows_w32(Z, n_space, n_rows, lambda, sigma, dt, tw_base, st, forward ? 2 : 1);
 #define CALL(LM)                                                                  \
   err = forward ? tau1d<LM, 2>(Z, n_rows, lambda, sigma, dt, tw_base, st)         \

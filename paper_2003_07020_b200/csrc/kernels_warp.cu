@@ -585,13 +585,109 @@ __global__ void __launch_bounds__(32 * kTauColWarps, 16 / kTauColWarps)
   }
 }
 
+// Ampere-style asynchronous copies (LDGSTS) for staging column tiles: a thread issues its whole
+// share of the tile, then waits once.  bytes = 0 writes zeros without reading src.
+__device__ __forceinline__ void cp_async16_z(void* smem_dst, const void* src, bool ok) {
+  const unsigned d = unsigned(__cvta_generic_to_shared(smem_dst));
+  const int bytes = ok ? 16 : 0;
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(src), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void cp_async8_z(void* smem_dst, const void* src, bool ok) {
+  const unsigned d = unsigned(__cvta_generic_to_shared(smem_dst));
+  const int bytes = ok ? 8 : 0;
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(d), "l"(src), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all_() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+// The tau column pass with the CTA's 16 columns staged through the groups' own tiles: the CTA copies
+// row segments of 16 complex values (256 bytes: two rows per warp instruction, against one element
+// of 16 different rows per instruction in the direct kernel -- on the L1 data pipe these kernels
+// are bound on, a strided access costs a wavefront per row touched) straight into the DST's slot
+// layout, each group transforms from and into its tile, and the CTA writes the tile back the same
+// way.  Tile c is shifted by c mod 8 slots so the 8 columns of a quarter warp hit 8 different banks.
+constexpr int kDstTileStage = kDstTileSize + 16;  // 304 double2: a multiple of 8, + the shift
+template <int MODE>
+__global__ void __launch_bounds__(32 * kTauColWarps, 16 / kTauColWarps)
+    k_tau_cols_staged(double2* __restrict__ Z, int n_planes, const double2* __restrict__ lam,
+                      const double* __restrict__ sigma, double dt, const double2* __restrict__ twb) {
+  constexpr int R = 16, G = 2, NSR = 255, NG = kTauColWarps * G, NT = 32 * kTauColWarps, RS = NT / NG;
+  extern __shared__ double2 wsm[];
+  constexpr int tiles = (NSR + NG - 1) / NG;
+  const int rp = int(blockIdx.x) / tiles;
+  const int iy0 = (int(blockIdx.x) - rp * tiles) * NG;
+  const int ncol = min(NG, NSR - iy0);
+  double2* zb = Z + size_t(rp) * NSR * NSR + iy0;
+  const int c = int(threadIdx.x) % NG, ix0 = int(threadIdx.x) / NG;
+  const bool okc = c < ncol;
+  {
+    double2* dst = wsm + c * kDstTileStage + (c & 7);
+    const double2* zc = zb + (okc ? c : 0);
+#pragma unroll
+    for (int u = 0; u < (NSR + RS - 1) / RS; ++u) {
+      const int ix = ix0 + u * RS;
+      if (ix < NSR) cp_async16_z(dst + dst_slot(ix), zc + size_t(ix) * NSR, okc);
+    }
+    cp_async_wait_all_();
+  }
+  __syncthreads();
+  const int lane = int(threadIdx.x) & 31;
+  const int t = lane & (R - 1);
+  const int grp = (int(threadIdx.x) >> 5) * G + lane / R;
+  double2* xs = wsm + grp * kDstTileStage + (grp & 7);
+  const double scale = 0.088388347648318440550;  // sqrt(2/256)
+  const double* sg = sigma + size_t(NSR) * NSR + size_t(min(iy0 + grp, NSR - 1)) * NSR;  // transposed table
+  warp_dst256([&](int j) { return xs[dst_slot(j - 1)]; }, xs, t, twb, scale);
+  const double2 l = __ldg(lam + rp);
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int i = t + R * r;
+    if (i < NSR) xs[dst_slot(i)] = shift_apply<MODE>(xs[dst_slot(i)], l.x - dt * __ldg(sg + i), l.y);
+  }
+  __syncwarp();
+  warp_dst256([&](int j) { return xs[dst_slot(j - 1)]; }, xs, t, twb, scale);
+  __syncthreads();
+  if (okc) {
+    const double2* src = wsm + c * kDstTileStage + (c & 7);
+#pragma unroll
+    for (int u = 0; u < (NSR + RS - 1) / RS; ++u) {
+      const int ix = ix0 + u * RS;
+      if (ix < NSR) zb[size_t(ix) * NSR + c] = src[dst_slot(ix)];
+    }
+  }
+}
+
 cudaError_t launch_tau_cols_warp(double2* Z, int n, int n_planes, const double2* lambda, const double* sigma,
                                  double dt, const double2* tw_base, cudaStream_t st, bool forward) {
   if (n != 255) return cudaErrorNotSupported;
   constexpr int NG = kTauColWarps * 2;
-  const size_t smem = size_t(NG) * kDstTileSize * sizeof(double2);
   const unsigned grid = unsigned(n_planes) * unsigned((255 + NG - 1) / NG);
   cudaError_t e = cudaSuccess;
+  // FPC_TAU_COLS_STAGED=1: the staged kernel (A/B).  Measured at config 2: 0.551 ms per tau solve
+  // against 0.532 direct -- at n = 255 the two CTA barriers cost more than the saved wavefronts
+  // (the n = 1023 kernels, one element of 32 rows per direct instruction, do gain: kernels_warp32.cu)
+  static const bool staged = [] {
+    const char* v = std::getenv("FPC_TAU_COLS_STAGED");
+    return v && v[0] == '1';
+  }();
+  if (staged) {
+    const size_t smem = size_t(NG) * kDstTileStage * sizeof(double2);
+    if (forward) {
+      if ((e = cudaFuncSetAttribute(k_tau_cols_staged<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem))) !=
+          cudaSuccess)
+        return e;
+      if ((e = set_warp_carveout((const void*)k_tau_cols_staged<2>, smem)) != cudaSuccess) return e;
+      k_tau_cols_staged<2><<<grid, 32 * kTauColWarps, smem, st>>>(Z, n_planes, lambda, sigma, dt, tw_base);
+    } else {
+      if ((e = cudaFuncSetAttribute(k_tau_cols_staged<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem))) !=
+          cudaSuccess)
+        return e;
+      if ((e = set_warp_carveout((const void*)k_tau_cols_staged<1>, smem)) != cudaSuccess) return e;
+      k_tau_cols_staged<1><<<grid, 32 * kTauColWarps, smem, st>>>(Z, n_planes, lambda, sigma, dt, tw_base);
+    }
+    note_launch();
+    return cudaGetLastError();
+  }
+  const size_t smem = size_t(NG) * kDstTileSize * sizeof(double2);
   if (forward) {
     if ((e = cudaFuncSetAttribute(k_tau_cols_warp<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem))) !=
         cudaSuccess)

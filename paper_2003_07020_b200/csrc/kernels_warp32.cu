@@ -68,6 +68,17 @@ bool warp32_kernels_enabled() {
   return on;
 }
 
+// Smallest row count the row kernels take (one warp per row: below a wave of 8 warps per SM the
+// CTA-level kernels, which spread a row over a CTA, keep more SMs busy; measured on 1D 1023 x n_time:
+// ahead from ~1000 rows, behind at 513).  FPC_W32_MIN_ROWS overrides.
+int warp32_min_rows() {
+  static const int v = [] {
+    const char* e = std::getenv("FPC_W32_MIN_ROWS");
+    return (e && e[0]) ? std::atoi(e) : 1000;
+  }();
+  return v;
+}
+
 // One row of ns <= 1023 reals per warp.  The BDF2 stencil part of the row (three rows of v) is
 // formed first and parked in shared memory (one double per (lane, slot): conflict free) so that the
 // 128 data registers of the transforms are all that is live across them.

@@ -108,11 +108,14 @@ def test_config1_gamma18_conditioning_floor(ref):
     assert d_gpu <= min(rr.true_relative_residual, 1e-9), (d_gpu, rr.true_relative_residual)
 
 
-@pytest.mark.parametrize("n,nt", [(255, 1024), (511, 128)], ids=["255sq_x1024", "511sq_x128"])
+@pytest.mark.parametrize("n,nt", [(255, 1024), (511, 128), (1023, 16)],
+                         ids=["255sq_x1024", "511sq_x128", "1023sq_x16"])
 def test_config3_parameters_reduced_grid(ref, n, nt):
     """Config 3's solver parameters exactly (gamma 1.5/1.5, kappa 1, GMRES(10), tol 1e-9, seeded
     source and u0 as config 3) on the largest grids the reference finishes in about a minute on the
-    box, against GMRES(10) emulated on the reference's own gmres_right."""
+    box, against GMRES(10) emulated on the reference's own gmres_right.  1023^2 x 16
+    is config 3's own lattice (the one-warp-per-row 1024-point kernels, kernels_warp32.cu) on a
+    short time axis."""
     w = problems.workload_2d(1.5, 1.5, n + 1, nt, tol=1e-9, restart=10)
     op, plan = gpu_problem(w)
     b = problems.rhs(w)
