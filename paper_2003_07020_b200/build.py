@@ -16,7 +16,7 @@ ROOT = os.path.dirname(HERE)
 BUILD = os.path.join(ROOT, "build", "fpc")
 LIB = os.path.join(HERE, "libfracpint_b200.so")
 SOURCES = ["kernels_1d.cu", "kernels_mv.cu", "kernels_large.cu", "kernels_2d.cu", "kernels_full.cu",
-           "kernels_krylov.cu", "kernels_commuted.cu", "kernels_tsplit.cu", "kernels_p2p.cu", "kernels_warp.cu", "kernels_warp32.cu", "kernels_generic.cu", "kernels_time_tma.cu",
+           "kernels_krylov.cu", "kernels_commuted.cu", "kernels_tsplit.cu", "kernels_p2p.cu", "kernels_warp.cu", "kernels_warp32.cu", "kernels_generic.cu", "kernels_time_tma.cu", "kernels_time_warp.cu",
            "api.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

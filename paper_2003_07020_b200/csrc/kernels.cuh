@@ -51,6 +51,12 @@ cudaError_t launch_time_inv(const double2* Z, double* z, int n_space, int n_time
 // grid has at least two waves of column tiles and the input is 16-byte aligned; FPC_TIME_TMA=0
 // keeps the register-staged kernels (A/B).
 bool time_tma_supported(int n_space, int n_time, const void* in, bool inverse);
+// n_time = 1024 on warp-owned 512-point transforms, one column per warp (kernels_time_warp.cu)
+bool time_warp_supported(int n_space, int n_time);
+cudaError_t launch_time_fwd_warp(const double* v, double2* Z, int n_space, int n_time, const double* scale_fwd,
+                                 double s_in, const double2* tw_base, cudaStream_t st);
+cudaError_t launch_time_inv_warp(const double2* Z, double* z, int n_space, int n_time, const double* scale_bwd,
+                                 const double2* tw_base, cudaStream_t st);
 cudaError_t launch_time_fwd_tma(const double* v, double2* Z, int n_space, int n_time, const double* scale_fwd,
                                 double s_in, const double2* tw_base, cudaStream_t st);
 cudaError_t launch_time_inv_tma(const double2* Z, double* z, int n_space, int n_time, const double* scale_bwd,

@@ -698,6 +698,8 @@ cudaError_t launch_time_fwd(const double* v, double2* Z, int n_space, int n_time
                             const double* scale_fwd, double s_in, const double2* tw_base,
                             cudaStream_t st) {
   cudaError_t err = cudaSuccess;
+  if (time_warp_supported(n_space, n_time))
+    return launch_time_fwd_warp(v, Z, n_space, n_time, scale_fwd, s_in, tw_base, st);
   if (time_tma_supported(n_space, n_time, v, false))
     return launch_time_fwd_tma(v, Z, n_space, n_time, scale_fwd, s_in, tw_base, st);
   if (time_split_supported(n_time))
@@ -729,6 +731,8 @@ cudaError_t launch_time_fwd(const double* v, double2* Z, int n_space, int n_time
 cudaError_t launch_time_inv(const double2* Z, double* z, int n_space, int n_time,
                             const double* scale_bwd, const double2* tw_base, cudaStream_t st) {
   cudaError_t err = cudaSuccess;
+  if (time_warp_supported(n_space, n_time))
+    return launch_time_inv_warp(Z, z, n_space, n_time, scale_bwd, tw_base, st);
   if (time_tma_supported(n_space, n_time, Z, true)) return launch_time_inv_tma(Z, z, n_space, n_time, scale_bwd, tw_base, st);
   if (time_split_supported(n_time)) return launch_time_inv_split(Z, z, n_space, n_time, scale_bwd, tw_base, st);
   const int lm = ilog2(n_time) - 1;
