@@ -20,11 +20,14 @@ namespace fpc {
 
 namespace {
 
-constexpr int kTwCols = 8;      // columns (= warps) per CTA
+#ifndef FPC_TW_COLS
+#define FPC_TW_COLS 8
+#endif
+constexpr int kTwCols = FPC_TW_COLS;  // columns (= warps) per CTA: 8 (two CTAs per SM) or 16 (one)
 constexpr int kTwBuf = 8592;    // bytes per warp buffer: >= the 16 x 33 tile (8448) and the 513-row
                                 // spectrum (8208); = 16 mod 128, so the 8 buffers' equal offsets
                                 // fall in 8 different 16-byte banks
-constexpr int kTwSkew = 16;     // extra bytes per column for the 8-byte phases (4 rows x 8 columns of
+constexpr int kTwSkew = kTwCols == 8 ? 16 : 0;  // extra bytes per column for the 8-byte phases (4 rows x 8 columns of
                                 // a warp instruction then cover all sixteen 8-byte banks twice)
 static_assert(kTwBuf % 16 == 0 && kTwBuf % 128 == 16, "buffer stride");
 static_assert(16 * kW32LD * 16 <= kTwBuf && (kTwCols - 1) * kTwSkew + 8192 <= kTwBuf && 513 * 16 <= kTwBuf, "buffer");
@@ -48,7 +51,7 @@ __device__ __forceinline__ void cpa_wait() { asm volatile("cp.async.wait_all;" :
 //   Z_n = (1/2) [ (X_n + conj X_{M-n}) - i e^{+2 pi i n/Nt} (X_n - conj X_{M-n}) ],  Z_M = Re X_0 - Im X_0
 // (the per-bin arithmetic of k_time_fwd, kernels_1d.cu; every lane forms its own 16 bins, the mirror
 // X_{M-n} of bin n = t + 32 p coming from lane 32 - t, register 15 - p).
-__global__ void __launch_bounds__(32 * kTwCols, 2)
+__global__ void __launch_bounds__(32 * kTwCols, 16 / kTwCols)
     k_time_fwd_w512(const double* __restrict__ v, double2* __restrict__ Z, int ns, const double* __restrict__ sf,
                     double s_in, const double2* __restrict__ twb) {
   constexpr int M = 512, NTIME = 1024, C = kTwCols, RS = 32;
@@ -113,7 +116,7 @@ __global__ void __launch_bounds__(32 * kTwCols, 2)
 // K4: z[k][p] = (scale_bwd[k] / Nt) sum_n Z_n e^{-2 pi i kn/Nt} over the Hermitian extension of the
 // half spectrum Z_0..Z_M: s_m = (Z_m + conj Z_{M-m}) + i e^{-2 pi i m/Nt} (Z_m - conj Z_{M-m})
 // (m = 0: (Z_0 + Z_M) + i (Z_0 - Z_M), as k_time_inv), c = FFT_M^-(s), z_{2m} = Re c_m, z_{2m+1} = Im c_m.
-__global__ void __launch_bounds__(32 * kTwCols, 2)
+__global__ void __launch_bounds__(32 * kTwCols, 16 / kTwCols)
     k_time_inv_w512(const double2* __restrict__ Z, double* __restrict__ z, int ns, const double* __restrict__ sb,
                     const double2* __restrict__ twb) {
   constexpr int M = 512, NTIME = 1024, C = kTwCols, RS = 32;

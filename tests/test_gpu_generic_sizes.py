@@ -16,9 +16,13 @@ def rel(a, b):
     return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
 
 
+# (1.5, 777, 1200): 1200 rows of 777 points run the matvec on the one-warp-per-row kernels
+# (kernels_warp32.cu) with a ragged zero-padded row; (.., 603, 3) in 2D: their column pass with a
+# partial last tile (603 = 8 * 75 + 3)
 CASES_1D = [(1.5, 100, 10), (1.3, 1000, 7), (1.7, 2047, 3), (1.5, 500, 64), (1.8, 255, 12), (1.2, 6, 5),
+            (1.5, 777, 1200),
             (1.5, 5000, 16)]  # the last: Ns > 2047 with Nt a power of two -> NotImplementedError
-CASES_2D = [(1.3, 1.7, 20, 6), (1.5, 1.5, 50, 16), (1.4, 1.2, 31, 12)]
+CASES_2D = [(1.3, 1.7, 20, 6), (1.5, 1.5, 50, 16), (1.4, 1.2, 31, 12), (1.6, 1.3, 603, 3)]
 
 
 def prob_1d(gamma, ns, nt):
