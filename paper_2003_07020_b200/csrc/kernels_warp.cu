@@ -606,11 +606,15 @@ __device__ __forceinline__ void cp_async_wait_all_() { asm volatile("cp.async.wa
 // layout, each group transforms from and into its tile, and the CTA writes the tile back the same
 // way.  Tile c is shifted by c mod 8 slots so the 8 columns of a quarter warp hit 8 different banks.
 constexpr int kDstTileStage = kDstTileSize + 16;  // 304 double2: a multiple of 8, + the shift
+#ifndef FPC_TAU_STAGED_WARPS
+#define FPC_TAU_STAGED_WARPS 4
+#endif
+constexpr int kTauStWarps = FPC_TAU_STAGED_WARPS;  // 8 columns per CTA (128-byte row segments), four CTAs per SM
 template <int MODE>
-__global__ void __launch_bounds__(32 * kTauColWarps, 16 / kTauColWarps)
+__global__ void __launch_bounds__(32 * kTauStWarps, 16 / kTauStWarps)
     k_tau_cols_staged(double2* __restrict__ Z, int n_planes, const double2* __restrict__ lam,
                       const double* __restrict__ sigma, double dt, const double2* __restrict__ twb) {
-  constexpr int R = 16, G = 2, NSR = 255, NG = kTauColWarps * G, NT = 32 * kTauColWarps, RS = NT / NG;
+  constexpr int R = 16, G = 2, NSR = 255, NG = kTauStWarps * G, NT = 32 * kTauStWarps, RS = NT / NG;
   extern __shared__ double2 wsm[];
   constexpr int tiles = (NSR + NG - 1) / NG;
   const int rp = int(blockIdx.x) / tiles;
@@ -662,27 +666,30 @@ cudaError_t launch_tau_cols_warp(double2* Z, int n, int n_planes, const double2*
   constexpr int NG = kTauColWarps * 2;
   const unsigned grid = unsigned(n_planes) * unsigned((255 + NG - 1) / NG);
   cudaError_t e = cudaSuccess;
-  // FPC_TAU_COLS_STAGED=1: the staged kernel (A/B).  Measured at config 2: 0.551 ms per tau solve
-  // against 0.532 direct -- at n = 255 the two CTA barriers cost more than the saved wavefronts
-  // (the n = 1023 kernels, one element of 32 rows per direct instruction, do gain: kernels_warp32.cu)
+  // FPC_TAU_COLS_STAGED=1: the staged kernel (A/B).  Measured at config 2: 0.551 ms per tau solve in
+  // 8-warp CTAs, 0.525 in 4-warp CTAs, against 0.528-0.532 direct -- at n = 255 the CTA barriers cost
+  // what the saved wavefronts gain (the n = 1023 kernels, one element of 32 rows per direct
+  // instruction, do gain: kernels_warp32.cu)
   static const bool staged = [] {
     const char* v = std::getenv("FPC_TAU_COLS_STAGED");
     return v && v[0] == '1';
   }();
   if (staged) {
-    const size_t smem = size_t(NG) * kDstTileStage * sizeof(double2);
+    constexpr int NGS = kTauStWarps * 2;
+    const size_t smem = size_t(NGS) * kDstTileStage * sizeof(double2);
+    const unsigned grid = unsigned(n_planes) * unsigned((255 + NGS - 1) / NGS);
     if (forward) {
       if ((e = cudaFuncSetAttribute(k_tau_cols_staged<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem))) !=
           cudaSuccess)
         return e;
       if ((e = set_warp_carveout((const void*)k_tau_cols_staged<2>, smem)) != cudaSuccess) return e;
-      k_tau_cols_staged<2><<<grid, 32 * kTauColWarps, smem, st>>>(Z, n_planes, lambda, sigma, dt, tw_base);
+      k_tau_cols_staged<2><<<grid, 32 * kTauStWarps, smem, st>>>(Z, n_planes, lambda, sigma, dt, tw_base);
     } else {
       if ((e = cudaFuncSetAttribute(k_tau_cols_staged<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem))) !=
           cudaSuccess)
         return e;
       if ((e = set_warp_carveout((const void*)k_tau_cols_staged<1>, smem)) != cudaSuccess) return e;
-      k_tau_cols_staged<1><<<grid, 32 * kTauColWarps, smem, st>>>(Z, n_planes, lambda, sigma, dt, tw_base);
+      k_tau_cols_staged<1><<<grid, 32 * kTauStWarps, smem, st>>>(Z, n_planes, lambda, sigma, dt, tw_base);
     }
     note_launch();
     return cudaGetLastError();

@@ -31,7 +31,11 @@ def build(G, two_dim, n, nt):
 
 @pytest.mark.parametrize("G,two_dim,n,nt", [(1, False, 255, 64), (2, False, 255, 64), (4, False, 1023, 256),
                                             (8, False, 127, 32),
-                                            (2, True, 31, 16), (4, True, 63, 32)])
+                                            (2, True, 31, 16), (4, True, 63, 32),
+                                            # the one-warp-per-transform kernels on shards: n = 1023 rows /
+                                            # columns (kernels_warp32.cu), n_time = 1024 on 4096-column
+                                            # blocks (kernels_time_warp.cu)
+                                            (2, True, 1023, 8), (2, False, 1023, 4096), (2, False, 8191, 1024)])
 def test_sharded_operators_match_single_device(G, two_dim, n, nt):
     w, md, sp, op, plan = build(G, two_dim, n, nt)
     v = np.random.default_rng(G * 7 + n).uniform(-1, 1, op.dim())
