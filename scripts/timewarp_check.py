@@ -9,7 +9,7 @@ from oracle import oracle as O
 
 rel = lambda a, b: np.linalg.norm(a - b) / np.linalg.norm(b)
 orc = O.Oracle()
-nt = 1024
+nt = int(sys.argv[1]) if len(sys.argv) > 1 else 1024
 for (g, n) in [(1.5, 8191), (1.2, 4095), (1.8, 2371 * 2 + 1)]:
     if (n + 1) & n:
         continue
