@@ -48,4 +48,21 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
       : "memory");
 }
 
+// Per-thread asynchronous copies (cp.async, SASS LDGSTS) for staging column tiles: a thread issues
+// its whole share of a tile, then waits once (cp_async_wait_all), so everything it copies is in flight
+// together instead of a register-limited batch.  ok = false writes zeros (rows / columns past the
+// edge) without reading src; src must still be a valid address.
+__device__ __forceinline__ void cp_async8_zfill(void* smem_dst, const void* src, bool ok) {
+  const int bytes = ok ? 8 : 0;
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(smem_u32(smem_dst)), "l"(src), "r"(bytes)
+               : "memory");
+}
+// dst and src 16-byte aligned
+__device__ __forceinline__ void cp_async16_zfill(void* smem_dst, const void* src, bool ok) {
+  const int bytes = ok ? 16 : 0;
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(smem_dst)), "l"(src), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
 }  // namespace fpc

@@ -13,6 +13,7 @@
 // then the transpose tile, then the output area.
 #include <cstdlib>
 
+#include "bulk_copy.cuh"
 #include "kernels.cuh"
 #include "warp_dst32.cuh"
 
@@ -31,18 +32,6 @@ constexpr int kTwSkew = kTwCols == 8 ? 16 : 0;  // extra bytes per column for th
                                 // a warp instruction then cover all sixteen 8-byte banks twice)
 static_assert(kTwBuf % 16 == 0 && kTwBuf % 128 == 16, "buffer stride");
 static_assert(16 * kW32LD * 16 <= kTwBuf && (kTwCols - 1) * kTwSkew + 8192 <= kTwBuf && 513 * 16 <= kTwBuf, "buffer");
-
-__device__ __forceinline__ void cpa8(void* smem_dst, const void* src, bool ok) {
-  const unsigned d = unsigned(__cvta_generic_to_shared(smem_dst));
-  const int bytes = ok ? 8 : 0;
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(d), "l"(src), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void cpa16(void* smem_dst, const void* src, bool ok) {
-  const unsigned d = unsigned(__cvta_generic_to_shared(smem_dst));
-  const int bytes = ok ? 16 : 0;
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(src), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void cpa_wait() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
 }  // namespace
 
@@ -65,8 +54,8 @@ __global__ void __launch_bounds__(32 * kTwCols, 16 / kTwCols)
     double* dst = reinterpret_cast<double*>(tsm + c * kTwBuf + c * kTwSkew);
     const double* src = v + p0 + (okc ? c : 0);
 #pragma unroll 8
-    for (int k = k0; k < NTIME; k += RS) cpa8(dst + k, src + size_t(k) * ns, okc);
-    cpa_wait();
+    for (int k = k0; k < NTIME; k += RS) cp_async8_zfill(dst + k, src + size_t(k) * ns, okc);
+    cp_async_wait_all();
   }
   __syncthreads();
   const int w = tid >> 5, t = tid & 31;
@@ -130,8 +119,8 @@ __global__ void __launch_bounds__(32 * kTwCols, 16 / kTwCols)
     double2* dst = reinterpret_cast<double2*>(tsm + c * kTwBuf);
     const double2* src = Z + p0 + (okc ? c : 0);
 #pragma unroll 8
-    for (int n = k0; n <= M; n += RS) cpa16(dst + n, src + size_t(n) * ns, okc);
-    cpa_wait();
+    for (int n = k0; n <= M; n += RS) cp_async16_zfill(dst + n, src + size_t(n) * ns, okc);
+    cp_async_wait_all();
   }
   __syncthreads();
   const int w = tid >> 5, t = tid & 31;

@@ -585,20 +585,6 @@ __global__ void __launch_bounds__(32 * kTauColWarps, 16 / kTauColWarps)
   }
 }
 
-// Ampere-style asynchronous copies (LDGSTS) for staging column tiles: a thread issues its whole
-// share of the tile, then waits once.  bytes = 0 writes zeros without reading src.
-__device__ __forceinline__ void cp_async16_z(void* smem_dst, const void* src, bool ok) {
-  const unsigned d = unsigned(__cvta_generic_to_shared(smem_dst));
-  const int bytes = ok ? 16 : 0;
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(src), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void cp_async8_z(void* smem_dst, const void* src, bool ok) {
-  const unsigned d = unsigned(__cvta_generic_to_shared(smem_dst));
-  const int bytes = ok ? 8 : 0;
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(d), "l"(src), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void cp_async_wait_all_() { asm volatile("cp.async.wait_all;" ::: "memory"); }
-
 // The tau column pass with the CTA's 16 columns staged through the groups' own tiles: the CTA copies
 // row segments of 16 complex values (256 bytes: two rows per warp instruction, against one element
 // of 16 different rows per instruction in the direct kernel -- on the L1 data pipe these kernels
@@ -629,9 +615,9 @@ __global__ void __launch_bounds__(32 * kTauStWarps, 16 / kTauStWarps)
 #pragma unroll
     for (int u = 0; u < (NSR + RS - 1) / RS; ++u) {
       const int ix = ix0 + u * RS;
-      if (ix < NSR) cp_async16_z(dst + dst_slot(ix), zc + size_t(ix) * NSR, okc);
+      if (ix < NSR) cp_async16_zfill(dst + dst_slot(ix), zc + size_t(ix) * NSR, okc);
     }
-    cp_async_wait_all_();
+    cp_async_wait_all();
   }
   __syncthreads();
   const int lane = int(threadIdx.x) & 31;

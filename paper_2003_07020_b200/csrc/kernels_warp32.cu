@@ -7,6 +7,7 @@
 // y-direction half of jacobian.hpp:84-87) and the x-direction column pass (jacobian.hpp:88-93).
 #include <cstdlib>
 
+#include "bulk_copy.cuh"
 #include "kernels.cuh"
 #include "warp_dst32.cuh"
 #include "warp_fft32.cuh"
@@ -35,21 +36,6 @@ __device__ __forceinline__ double bdf2_w32(int k, double x0, double x1, double x
   if (k == 1) return 1.5 * x0 + -2.0 * x1;
   return 1.5 * x0 + -2.0 * x1 + 0.5 * x2;
 }
-
-// Ampere-style asynchronous copies (LDGSTS): a staging phase issues all its copies, then waits once,
-// so every thread has its whole share of the tile in flight instead of a register-limited batch.
-// bytes = 0 writes zeros (out-of-range rows / columns) without reading src.
-__device__ __forceinline__ void cp_async8(void* smem_dst, const void* src, bool ok) {
-  const unsigned d = unsigned(__cvta_generic_to_shared(smem_dst));
-  const int bytes = ok ? 8 : 0;
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(d), "l"(src), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void cp_async16(void* smem_dst, const void* src, bool ok) {
-  const unsigned d = unsigned(__cvta_generic_to_shared(smem_dst));
-  const int bytes = ok ? 16 : 0;
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(src), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
 cudaError_t prep_w32(const void* kernel, size_t smem, int warps = kW32Warps) {
   cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
@@ -146,20 +132,21 @@ cudaError_t launch_matvec_rows_w32(const double* v, double* y, int len, int nrow
 }
 
 // x-direction column pass of the 2D matvec for n <= 1023: y[k][ix][iy] += (T_x v[k][.][iy])[ix].
-// A CTA owns kW32Warps adjacent columns of one time level, one per warp.  The column tile is staged
-// through the warps' own transpose tiles (free before the first transform and after the last): the
-// CTA reads row segments of kW32Warps doubles (8 rows per warp instruction instead of one element
-// of 32 different rows) and writes column c into warp c's tile; the results go back the same way and
-// are added to y as L2 reductions (RED.ADD.F64: each element receives exactly one add, so the sum
-// is the same double as load-add-store).
+// A CTA owns C = kW32MvColWarps adjacent columns of one time level, one per warp.  The column tile is
+// staged through the warps' own transpose tiles (free before the first transform and after the
+// last): the CTA copies row segments of C doubles (32 / C rows per warp instruction, instead of one
+// element of 32 different rows) and column c lands in warp c's tile; the results go back the same way
+// and are added to y as L2 reductions (RED.ADD.F64: each element receives exactly one add, so the
+// sum is the same double as load-add-store).
 __global__ void __launch_bounds__(32 * kW32MvColWarps, 8 / kW32MvColWarps)
     k_mv_cols_w32(const double* __restrict__ v, double* __restrict__ y, int n, const double* __restrict__ eig,
                   const double2* __restrict__ twb) {
   constexpr int R = 32, M = 1024, L = 2 * M, H = 16, C = kW32MvColWarps, NT = 32 * kW32MvColWarps;
   constexpr int CP = 2 * kW32Tile;  // doubles per warp tile (2112)
   // staged column of warp c: element ix = 2 m + h (packed slot m = tt + 32 r) at (2 r + h) * SH + tt,
-  // shifted by c * SC: a lane's reads are unit stride over tt, and a staging instruction (4 columns x 8
-  // rows = 4 m x 2 h per column) spreads over all 16 bank pairs (m: 0..3, h: +4, c: +8 mod 16)
+  // shifted by c * SC: a lane's reads are unit stride over tt, and a staging instruction spreads over
+  // all sixteen 8-byte banks twice (C = 4: 8 rows = 4 m x 2 h per column, m: 0..3, h: +4, c: +8 mod 16;
+  // C = 8: 4 rows = 2 m x 2 h per column, c: +2 mod 16)
   constexpr int SH = 36, SC = C == 4 ? 8 : 2;
   static_assert(31 * SH + 32 + (C - 1) * SC <= CP, "staged column fits the tile");
   extern __shared__ double2 wsm[];
@@ -171,7 +158,7 @@ __global__ void __launch_bounds__(32 * kW32MvColWarps, 8 / kW32MvColWarps)
   const int ncol = min(C, n - iy0);
   const int t = int(threadIdx.x) & 31;
   const int w = int(threadIdx.x) >> 5;
-  // 1. stage: element e = ix * C + c; thread handles e = tid + u NT: c = tid % C fixed, ix = tid / C + u (NT / C)
+  // 1. stage: thread tid copies column c = tid % C of rows ix = tid / C + u (NT / C)
   {
     const int c = int(threadIdx.x) % C, ix0 = int(threadIdx.x) / C;
     constexpr int RS = NT / C;  // rows per sweep (32)
@@ -182,7 +169,7 @@ __global__ void __launch_bounds__(32 * kW32MvColWarps, 8 / kW32MvColWarps)
     for (int ix = ix0; ix < M; ix += RS) {
       const bool ok = okc && ix < n;
       const int m = ix >> 1, h = ix & 1;
-      cp_async8(dst + ((m >> 5) * 2 + h) * SH + (m & 31), vb + size_t(ok ? ix : 0) * n, ok);
+      cp_async8_zfill(dst + ((m >> 5) * 2 + h) * SH + (m & 31), vb + size_t(ok ? ix : 0) * n, ok);
     }
     cp_async_wait_all();
   }
@@ -315,7 +302,7 @@ __global__ void __launch_bounds__(32 * kW32TauColWarps, 8 / kW32TauColWarps)
     double2* dst = wsm + c * kDst32Tile + SK * c;
     const double2* zc = zb + (okc ? c : 0);
 #pragma unroll 8
-    for (int ix = ix0; ix < NSR; ix += RS) cp_async16(dst + dst32_slot(ix), zc + size_t(ix) * NSR, okc);
+    for (int ix = ix0; ix < NSR; ix += RS) cp_async16_zfill(dst + dst32_slot(ix), zc + size_t(ix) * NSR, okc);
     cp_async_wait_all();
   }
   __syncthreads();
