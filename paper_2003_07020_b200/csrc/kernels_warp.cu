@@ -183,7 +183,7 @@ constexpr int kWarpsPerCta = FPC_COL_WARPS;  // column kernels: a CTA covers 2 *
 // warps per SM -- the warps of a CTA start together and so wait on their row loads together; more,
 // smaller CTAs spread those phases (FPC_ROW_WARPS: build knob).
 #ifndef FPC_ROW_WARPS
-#define FPC_ROW_WARPS 4
+#define FPC_ROW_WARPS 1  // config 2: matvec 518 (4 warps) -> 511 (2) -> 500 us (1), tau solve 527 -> 524 us
 #endif
 constexpr int kRowWarps = FPC_ROW_WARPS;
 

@@ -16,7 +16,17 @@ namespace fpc {
 
 namespace {
 
-constexpr int kW32Warps = 4;  // warps per CTA; two CTAs per SM (255 registers per thread)
+#ifndef FPC_W32_ROWW
+#define FPC_W32_ROWW 4
+#endif
+constexpr int kW32Warps = FPC_W32_ROWW;  // matvec rows: warps per CTA; 8 warps per SM (255 registers per thread)
+// DST rows: one warp per CTA -- a 4-warp CTA's slots stay empty until its slowest warp is done (tau
+// solve at 1023^2 x 64: 1.40 ms in 4-warp CTAs, 1.24 in 2-warp, 1.21 in 1-warp; the matvec rows, with
+// their three row loads up front, measured the other way: 1.495 / 1.507 / 1.558 ms)
+#ifndef FPC_W32_DSTW
+#define FPC_W32_DSTW 1
+#endif
+constexpr int kW32DstWarps = FPC_W32_DSTW;
 // column kernels: warps (= adjacent columns) per CTA, 8 warps per SM either way (build knobs, A/B on
 // 1023^2 x 64): the matvec columns (8-byte elements) gain from 64-byte row segments with 8 columns
 // (844 -> 750 us), the tau columns (16-byte elements, 64-byte segments already) lose the overlap of
@@ -28,8 +38,9 @@ constexpr int kW32Warps = 4;  // warps per CTA; two CTAs per SM (255 registers p
 #define FPC_W32_TAU_COLW 4
 #endif
 constexpr int kW32MvColWarps = FPC_W32_MV_COLW, kW32TauColWarps = FPC_W32_TAU_COLW;
-static_assert((kW32MvColWarps == 4 || kW32MvColWarps == 8) && (kW32TauColWarps == 4 || kW32TauColWarps == 8),
-              "column kernels: 4 or 8 columns per CTA");
+static_assert((kW32MvColWarps == 4 || kW32MvColWarps == 8) &&
+                  (kW32TauColWarps == 2 || kW32TauColWarps == 4 || kW32TauColWarps == 8),
+              "column kernels: 4 or 8 (tau: 2, 4 or 8) columns per CTA");
 
 __device__ __forceinline__ double bdf2_w32(int k, double x0, double x1, double x2) {
   if (k == 0) return x0;
@@ -37,11 +48,21 @@ __device__ __forceinline__ double bdf2_w32(int k, double x0, double x1, double x
   return 1.5 * x0 + -2.0 * x1 + 0.5 * x2;
 }
 
+// Shared-memory carveout for 8 warps per SM in CTAs of `warps` warps: the smallest capacity that
+// holds them (dynamic + the 1 KB system reserve per CTA), the rest of the 256 KB array stays L1 for
+// the twiddle / eigenvalue tables.  The driver takes the smallest capacity >= pct% of 228 KB, so the
+// percentage is rounded down (kernels_krylov.cu carveout_pct).
 cudaError_t prep_w32(const void* kernel, size_t smem, int warps = kW32Warps) {
   cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   if (e != cudaSuccess) return e;
-  return cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
-                              carveout_pct(smem, 32 * warps));
+  const size_t need = size_t(8 / warps) * (smem + 1024);
+  int pct = 100;
+  for (int c : {8, 16, 32, 64, 100, 132, 164, 196, 228})
+    if (size_t(c) * 1024 >= need) {
+      pct = (c * 100) / 228;
+      break;
+    }
+  return cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
 }
 
 }  // namespace
@@ -68,7 +89,7 @@ int warp32_min_rows() {
 // One row of ns <= 1023 reals per warp.  The BDF2 stencil part of the row (three rows of v) is
 // formed first and parked in shared memory (one double per (lane, slot): conflict free) so that the
 // 128 data registers of the transforms are all that is live across them.
-__global__ void __launch_bounds__(32 * kW32Warps, 2)
+__global__ void __launch_bounds__(32 * kW32Warps, 8 / kW32Warps)
     k_mv_rows_w32(const double* __restrict__ v, double* __restrict__ y, int ns, int nrows, int rpt, int sstride,
                   int koff, const double* __restrict__ eig, const double2* __restrict__ twb) {
   constexpr int R = 32, M = 1024, L = 2 * M, H = 16;
@@ -221,14 +242,14 @@ cudaError_t launch_matvec_cols_w32(const double* v, double* y, int n, int n_time
 // (tau.hpp:98-136): DST, divide (multiply) by lambda_r - dt sigma_i, DST, the intermediate kept in
 // the warp's tile.
 template <int MODE>
-__global__ void __launch_bounds__(32 * kW32Warps, 2)
+__global__ void __launch_bounds__(32 * kW32DstWarps, 8 / kW32DstWarps)
     k_dst_rows_w32(double2* __restrict__ Z, int n_rows, const double2* __restrict__ lam,
                    const double* __restrict__ sigma, double dt, const double2* __restrict__ twb) {
   constexpr int NSR = 1023;
   extern __shared__ double2 wsm[];
   const int t = int(threadIdx.x) & 31;
   const int w = int(threadIdx.x) >> 5;
-  const int row = int(blockIdx.x) * kW32Warps + w;
+  const int row = int(blockIdx.x) * kW32DstWarps + w;
   if (row >= n_rows) return;
   double2* zr = Z + size_t(row) * NSR;
   double2* xs = wsm + w * kDst32Tile;
@@ -257,13 +278,13 @@ __global__ void __launch_bounds__(32 * kW32Warps, 2)
 cudaError_t launch_dst_rows_w32(double2* Z, int n, int n_rows, const double2* lambda, const double* sigma,
                                 double dt, const double2* tw_base, cudaStream_t st, int mode) {
   if (n != 1023) return cudaErrorNotSupported;
-  const size_t smem = size_t(kW32Warps) * kDst32Tile * sizeof(double2);
-  const unsigned grid = unsigned((n_rows + kW32Warps - 1) / kW32Warps);
+  const size_t smem = size_t(kW32DstWarps) * kDst32Tile * sizeof(double2);
+  const unsigned grid = unsigned((n_rows + kW32DstWarps - 1) / kW32DstWarps);
   cudaError_t e = cudaSuccess;
 #define FPC_DSTW32(MODE)                                                                               \
   {                                                                                                    \
-    if ((e = prep_w32((const void*)k_dst_rows_w32<MODE>, smem)) != cudaSuccess) return e;              \
-    k_dst_rows_w32<MODE><<<grid, 32 * kW32Warps, smem, st>>>(Z, n_rows, lambda, sigma, dt, tw_base);   \
+    if ((e = prep_w32((const void*)k_dst_rows_w32<MODE>, smem, kW32DstWarps)) != cudaSuccess) return e;              \
+    k_dst_rows_w32<MODE><<<grid, 32 * kW32DstWarps, smem, st>>>(Z, n_rows, lambda, sigma, dt, tw_base);   \
     note_launch();                                                                                     \
   }
   if (mode == 0)
