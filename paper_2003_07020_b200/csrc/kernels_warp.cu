@@ -172,12 +172,20 @@ __device__ __forceinline__ double bdf2(int k, double x0, double x1, double x2) {
 }
 
 #ifndef FPC_COL_WARPS
-#define FPC_COL_WARPS 4  // B200 config 2: matvec columns 4 warps (8 columns) per CTA, tau columns 8 (16 columns)
+#define FPC_COL_WARPS 4  // B200 config 2: matvec columns 4 warps (8 columns) per CTA, tau columns 4 (8 columns)
 #endif
 #ifndef FPC_TAU_COL_WARPS
-#define FPC_TAU_COL_WARPS 8
+#define FPC_TAU_COL_WARPS 4  // with FPC_TAU_COL_OCC 12 (170 registers, no spills): config-2 tau solve 505 -> 496 us
 #endif
 constexpr int kTauColWarps = FPC_TAU_COL_WARPS;
+#ifndef FPC_TAU_COL_OCC
+#define FPC_TAU_COL_OCC 12
+#endif
+constexpr int kTauColOcc = FPC_TAU_COL_OCC;
+#ifndef FPC_COL_OCC
+#define FPC_COL_OCC 16
+#endif
+constexpr int kColOcc = FPC_COL_OCC;
 constexpr int kWarpsPerCta = FPC_COL_WARPS;  // column kernels: a CTA covers 2 * kWarpsPerCta adjacent columns
 // Row kernels (contiguous rows: nothing shared between a CTA's warps): smaller CTAs, the same 16
 // warps per SM -- the warps of a CTA start together and so wait on their row loads together; more,
@@ -186,6 +194,14 @@ constexpr int kWarpsPerCta = FPC_COL_WARPS;  // column kernels: a CTA covers 2 *
 #define FPC_ROW_WARPS 1  // config 2: matvec 518 (4 warps) -> 511 (2) -> 500 us (1), tau solve 527 -> 524 us
 #endif
 constexpr int kRowWarps = FPC_ROW_WARPS;
+#ifndef FPC_ROW_OCC
+#define FPC_ROW_OCC 16  // resident warps per SM the row kernels are compiled for (register cap 65536 / 32 / occ)
+#endif
+constexpr int kRowOcc = FPC_ROW_OCC;
+#ifndef FPC_DST_ROW_OCC
+#define FPC_DST_ROW_OCC 12  // config 2: tau solve 527 (16 warps per SM, 128 registers, 16-192 B of spills) -> 506 us (12 or 10 warps); 8: 527
+#endif
+constexpr int kDstRowOcc = FPC_DST_ROW_OCC;
 
 // Row data read once (no reuse inside the SM): L2-only loads keep the L1 for the twiddle and
 // eigenvalue tables.  FPC_WARP_CG=0 restores plain loads (A/B).
@@ -235,7 +251,7 @@ bool warp_kernels_enabled() {
 }
 
 template <int R>
-__global__ void __launch_bounds__(32 * kRowWarps, 16 / kRowWarps)
+__global__ void __launch_bounds__(32 * kRowWarps, kRowOcc / kRowWarps)
     k_mv_rows_warp(const double* __restrict__ v, double* __restrict__ y, int ns, int nrows, int rpt,
                    int sstride, int koff, const double* __restrict__ eig, const double2* __restrict__ twb) {
   constexpr int M = R * R, L = 2 * M, G = 32 / R, H = R / 2;
@@ -313,7 +329,7 @@ cudaError_t launch_matvec_rows_warp(const double* v, double* y, int len, int nro
 // frequency row r (tau.hpp:98-136): DST, divide (multiply) by lambda_r - dt sigma_i, DST, with the
 // intermediate kept in the group's tile.
 template <int MODE>
-__global__ void __launch_bounds__(32 * kRowWarps, 16 / kRowWarps)
+__global__ void __launch_bounds__(32 * kRowWarps, kDstRowOcc / kRowWarps)
     k_dst_rows_warp(double2* __restrict__ Z, int n_rows, const double2* __restrict__ lam,
                     const double* __restrict__ sigma, double dt, const double2* __restrict__ twb) {
   constexpr int R = 16, G = 2, NSR = 255;
@@ -381,7 +397,7 @@ cudaError_t launch_dst_rows_warp(double2* Z, int n, int n_rows, const double2* l
 // result back into its tile column, and the CTA adds the tile to y row by row (coalesced).
 constexpr int kColTile = 2 * kWarpsPerCta;  // columns per CTA = groups per CTA
 constexpr int kColPitch = 17;        // tile row pitch in doubles: the groups' column reads hit 16 bank pairs
-__global__ void __launch_bounds__(32 * kWarpsPerCta, 16 / kWarpsPerCta)
+__global__ void __launch_bounds__(32 * kWarpsPerCta, kColOcc / kWarpsPerCta)
     k_mv_cols_warp(const double* __restrict__ v, double* __restrict__ y, int n, const double* __restrict__ eig,
                    const double2* __restrict__ twb) {
   constexpr int R = 16, M = R * R, L = 2 * M, H = R / 2, G = 2;
@@ -461,7 +477,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta, 16 / kWarpsPerCta)
 // registers (a warp's two groups read 16 B per row; a CTA's 8 warps cover 128-byte row segments, so
 // the L2 sectors are shared within the CTA) and adds its result to y directly -- warps never wait
 // on each other.  FPC_COLS_TILE=1 selects the tiled kernel above (A/B).
-__global__ void __launch_bounds__(32 * kWarpsPerCta, 16 / kWarpsPerCta)
+__global__ void __launch_bounds__(32 * kWarpsPerCta, kColOcc / kWarpsPerCta)
     k_mv_cols_direct(const double* __restrict__ v, double* __restrict__ y, int n, const double* __restrict__ eig,
                      const double2* __restrict__ twb) {
   constexpr int R = 16, M = R * R, L = 2 * M, H = R / 2, G = 2;
@@ -551,7 +567,7 @@ cudaError_t launch_matvec_cols_warp(const double* v, double* y, int n, int n_tim
 // adjacent 16-byte elements of each row; a CTA's 16 groups cover 256-byte row segments), the
 // intermediate kept in the group's tile.  n = 255.
 template <int MODE>
-__global__ void __launch_bounds__(32 * kTauColWarps, 16 / kTauColWarps)
+__global__ void __launch_bounds__(32 * kTauColWarps, kTauColOcc / kTauColWarps)
     k_tau_cols_warp(double2* __restrict__ Z, int n_planes, const double2* __restrict__ lam,
                     const double* __restrict__ sigma, double dt, const double2* __restrict__ twb) {
   constexpr int R = 16, G = 2, NSR = 255, NG = kTauColWarps * G;
