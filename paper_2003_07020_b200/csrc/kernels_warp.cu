@@ -613,7 +613,7 @@ constexpr int kDstTileStage = kDstTileSize + 16;  // 304 double2: a multiple of 
 #endif
 constexpr int kTauStWarps = FPC_TAU_STAGED_WARPS;  // 8 columns per CTA (128-byte row segments), four CTAs per SM
 template <int MODE>
-__global__ void __launch_bounds__(32 * kTauStWarps, 16 / kTauStWarps)
+__global__ void __launch_bounds__(32 * kTauStWarps, kTauColOcc / kTauStWarps)
     k_tau_cols_staged(double2* __restrict__ Z, int n_planes, const double2* __restrict__ lam,
                       const double* __restrict__ sigma, double dt, const double2* __restrict__ twb) {
   constexpr int R = 16, G = 2, NSR = 255, NG = kTauStWarps * G, NT = 32 * kTauStWarps, RS = NT / NG;
