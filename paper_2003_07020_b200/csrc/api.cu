@@ -382,6 +382,7 @@ struct fpc_plan_s {
   double2* d_lambda = nullptr;
   double* d_sigma = nullptr;
   double2* d_Z = nullptr;  // half spectrum scratch (H x ns complex)
+  double2* d_ZT = nullptr; // 2D n = 255: the transposed spectrum of the tau solve's row passes (allocated on first use)
   double2* d_Zf = nullptr; // full spectrum (Nt x ns complex), InnerSweep::full only
   int sweep_mode = FPC_SWEEP_HALF;
   // generic (Bluestein) path: chirps and filter spectra of the time transforms (signs +1 / -1) and
@@ -889,7 +890,7 @@ int fpc_plan_destroy(fpc_plan_t pl) {
     for (double* b : pl->basis) cudaFree(b);
     for (double* b : pl->zbasis) cudaFree(b);
     for (void* q : {(void*)pl->d_sf, (void*)pl->d_sb, (void*)pl->d_lambda, (void*)pl->d_sigma,
-                    (void*)pl->d_Z, (void*)pl->d_z, (void*)pl->d_u, (void*)pl->d_r, (void*)pl->d_x,
+                    (void*)pl->d_Z, (void*)pl->d_ZT, (void*)pl->d_z, (void*)pl->d_u, (void*)pl->d_r, (void*)pl->d_x,
                     (void*)pl->d_d, (void*)pl->d_b, (void*)pl->d_Zf, (void*)pl->d_ctf, (void*)pl->d_btf,
                     (void*)pl->d_cti, (void*)pl->d_bti, (void*)pl->d_cds, (void*)pl->d_bds, (void*)pl->d_U,
                     (void*)pl->d_D, (void*)pl->d_P})
@@ -1040,10 +1041,12 @@ static void pc_apply_dev(fpc_plan_s* pl, const double* v, double* z, double s_in
     LAUNCH("tau_solve_1d", st,
            fpc::launch_tau_solve_1d(pl->d_Z, p->ns, pl->solve_count, pl->d_lambda, pl->d_sigma, p->dt,
                                     p->ctx->tw, st, forward));
-  else
+  else {
+    if (p->n == 255 && !pl->d_ZT) pl->d_ZT = dalloc<double2>(size_t(pl->solve_count) * size_t(p->ns));
     LAUNCH("tau_solve_2d", st,
            fpc::launch_tau_solve_2d(pl->d_Z, p->n, pl->solve_count, pl->d_lambda, pl->d_sigma, p->dt,
-                                    p->ctx->tw, st, forward));
+                                    p->ctx->tw, st, forward, pl->d_ZT));
+  }
   LAUNCH("time_inv", st, fpc::launch_time_inv(pl->d_Z, z, p->ns, p->nt, pl->d_sb, p->ctx->tw, st));
 }
 

@@ -119,9 +119,13 @@ cudaError_t launch_dst_rows(double2* Z, int n, int n_rows, const double2* tw_bas
 cudaError_t launch_matvec_2d(const double* v, double* y, int n, int n_time, int log_m,
                              const double* eig_y_scaled, const double* eig_x_scaled,
                              const double2* tw_base, cudaStream_t st, int koff = 0);
+// scratch (optional, n_rows * n * n complex): with it the n = 255 solve runs without strided loads
+// (two row passes with transposed stores through scratch, kernels_warp.cu k_dst_rows_T)
 cudaError_t launch_tau_solve_2d(double2* Z, int n, int n_rows, const double2* lambda,
                                 const double* sigma, double dt, const double2* tw_base,
-                                cudaStream_t st, bool forward = false);
+                                cudaStream_t st, bool forward = false, double2* scratch = nullptr);
+cudaError_t launch_dst_rows_T(const double2* in, double2* out, int n, int n_planes, const double2* lambda,
+                              const double* sigma, double dt, const double2* tw_base, cudaStream_t st, int mode);
 
 // ---- commuted ordering beyond kernels_commuted.cu's 1D n_space + 1 <= 8192 -------------------
 // time-level pairs as complex levels (kernels_2d.cu), one DST per complex row for n_space + 1 =

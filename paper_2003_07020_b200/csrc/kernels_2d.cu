@@ -7,6 +7,7 @@
 // time block (matvec) or one frequency row (tau): each lattice row ix contributes C contiguous
 // values (coalesced), and each column becomes one smem FFT buffer.
 #include <algorithm>
+#include <cstdlib>
 
 #include "dst_block.cuh"
 #include "fft_block.cuh"
@@ -352,9 +353,22 @@ cudaError_t launch_dst_cols_2d(double2* Z, int n, int n_planes, const double2* t
 
 cudaError_t launch_tau_solve_2d(double2* Z, int n, int n_rows, const double2* lambda,
                                 const double* sigma, double dt, const double2* tw_base,
-                                cudaStream_t st, bool forward) {
+                                cudaStream_t st, bool forward, double2* scratch) {
   // rows (iy) DST, columns (ix) DST-divide-DST, rows DST again (tau.hpp:79-96, 98-119)
-  cudaError_t err = launch_dst_rows(Z, n, n_rows * n, tw_base, st);
+  cudaError_t err = cudaSuccess;
+  static const bool transposed = [] {  // FPC_TAU_T=0: the strided column pass (A/B)
+    const char* e = std::getenv("FPC_TAU_T");
+    return !(e && e[0] == '0');
+  }();
+  if (n == 255 && scratch && transposed && warp_kernels_enabled()) {
+    if ((err = launch_dst_rows_T(Z, scratch, n, n_rows, nullptr, nullptr, 0.0, tw_base, st, 0)) != cudaSuccess)
+      return err;
+    if ((err = launch_dst_rows_T(scratch, Z, n, n_rows, lambda, sigma, dt, tw_base, st, forward ? 2 : 1)) !=
+        cudaSuccess)
+      return err;
+    return launch_dst_rows(Z, n, n_rows * n, tw_base, st);
+  }
+  err = launch_dst_rows(Z, n, n_rows * n, tw_base, st);
   if (err != cudaSuccess) return err;
   const int lm = ilog2i(n + 1);
   if (n == 255 && warp_kernels_enabled()) {

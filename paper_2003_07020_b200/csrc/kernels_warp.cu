@@ -662,6 +662,78 @@ __global__ void __launch_bounds__(32 * kTauStWarps, kTauColOcc / kTauStWarps)
   }
 }
 
+// Row transforms with a transposed store, for the 2D tau solve without strided loads (tau.hpp:79-119):
+// plane p of `in` holds 255 contiguous rows; each 16-lane group transforms one row (MODE 0: DST;
+// MODE 1 / 2: DST, divide / multiply by lambda_p - dt sigma, DST), and the CTA's 8 rows r0..r0+7 are
+// written to out[p][c][r0..r0+7] -- 128-byte segments -- from the groups' tiles.  Two such passes
+// and an in-place row pass make the solve: Z -> (DST_y, transpose) -> ZT -> (DST_x, shift, DST_x,
+// transpose back) -> Z -> DST_y.  sigT = the transposed sigma table [iy][ix].
+template <int MODE>
+__global__ void __launch_bounds__(32 * 4, 3)
+    k_dst_rows_T(const double2* __restrict__ in, double2* __restrict__ out, const double2* __restrict__ lam,
+                 const double* __restrict__ sigT, double dt, const double2* __restrict__ twb) {
+  constexpr int R = 16, G = 2, NSR = 255, NG = 4 * G, TPP = (NSR + NG - 1) / NG;
+  extern __shared__ double2 wsm[];
+  const int p = int(blockIdx.x) / TPP;
+  const int r0 = (int(blockIdx.x) - p * TPP) * NG;
+  const int lane = int(threadIdx.x) & 31;
+  const int t = lane & (R - 1);
+  const int grp = (int(threadIdx.x) >> 5) * G + lane / R;
+  const int rr = min(r0 + grp, NSR - 1);  // a group past the plane's last row repeats it, stores nothing
+  const double2* zr = in + (size_t(p) * NSR + rr) * NSR;
+  double2* xs = wsm + grp * kDstTileStage + (grp & 7);
+  const double scale = 0.088388347648318440550;  // sqrt(2/256)
+  warp_dst256([&](int j) { return zr[j - 1]; }, xs, t, twb, scale);
+  if constexpr (MODE != 0) {
+    const double2 l = __ldg(lam + p);
+    const double* sg = sigT + size_t(rr) * NSR;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int i = t + R * r;
+      if (i < NSR) xs[dst_slot(i)] = shift_apply<MODE>(xs[dst_slot(i)], l.x - dt * __ldg(sg + i), l.y);
+    }
+    __syncwarp();
+    warp_dst256([&](int j) { return xs[dst_slot(j - 1)]; }, xs, t, twb, scale);
+  }
+  __syncthreads();
+  const int g = int(threadIdx.x) % NG, c0 = int(threadIdx.x) / NG;
+  if (r0 + g < NSR) {
+    const double2* src = wsm + g * kDstTileStage + (g & 7);
+    double2* oc = out + size_t(p) * NSR * NSR + r0 + g;
+#pragma unroll
+    for (int u = 0; u < (NSR + 15) / 16; ++u) {
+      const int c = c0 + 16 * u;
+      if (c < NSR) oc[size_t(c) * NSR] = src[dst_slot(c)];
+    }
+  }
+}
+
+// mode 0: out = transpose(DST rows of in); 1 / 2: out = transpose(DST, shift (solve / forward), DST)
+cudaError_t launch_dst_rows_T(const double2* in, double2* out, int n, int n_planes, const double2* lambda,
+                              const double* sigma, double dt, const double2* tw_base, cudaStream_t st, int mode) {
+  if (n != 255) return cudaErrorNotSupported;
+  const size_t smem = size_t(8) * kDstTileStage * sizeof(double2);
+  const unsigned grid = unsigned(n_planes) * 32u;
+  const double* sigT = sigma ? sigma + size_t(255) * 255 : nullptr;
+  cudaError_t e = cudaSuccess;
+#define FPC_DSTT(MODE)                                                                                         \
+  {                                                                                                            \
+    if ((e = cudaFuncSetAttribute(k_dst_rows_T<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem))) \
+        != cudaSuccess)                                                                                        \
+      return e;                                                                                                \
+    k_dst_rows_T<MODE><<<grid, 128, smem, st>>>(in, out, lambda, sigT, dt, tw_base);                           \
+    note_launch();                                                                                             \
+  }
+  if (mode == 0)
+    FPC_DSTT(0)
+  else if (mode == 1)
+    FPC_DSTT(1)
+  else
+    FPC_DSTT(2)
+#undef FPC_DSTT
+  return cudaGetLastError();
+}
+
 cudaError_t launch_tau_cols_warp(double2* Z, int n, int n_planes, const double2* lambda, const double* sigma,
                                  double dt, const double2* tw_base, cudaStream_t st, bool forward) {
   if (n != 255) return cudaErrorNotSupported;
