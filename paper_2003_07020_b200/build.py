@@ -15,7 +15,9 @@ CSRC = os.path.join(HERE, "csrc")
 ROOT = os.path.dirname(HERE)
 BUILD = os.path.join(ROOT, "build", "fpc")
 LIB = os.path.join(HERE, "libfracpint_b200.so")
-SOURCES = ["kernels_1d.cu", "kernels_mv.cu", "kernels_large.cu", "kernels_2d.cu", "kernels_full.cu",
+# "file.cu:N" compiles file.cu with -DFPC_1D_PART=N into file_pN.o (kernels_1d.cu is three units: its
+# size instantiations took 3.5 of a cold build's 3.7 minutes in one nvcc process)
+SOURCES = ["kernels_1d.cu:0", "kernels_1d.cu:1", "kernels_1d.cu:2", "kernels_mv.cu", "kernels_large.cu", "kernels_2d.cu", "kernels_full.cu",
            "kernels_krylov.cu", "kernels_commuted.cu", "kernels_tsplit.cu", "kernels_p2p.cu", "kernels_warp.cu", "kernels_warp32.cu", "kernels_generic.cu", "kernels_time_tma.cu", "kernels_time_warp.cu",
            "api.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
@@ -44,11 +46,14 @@ def build(verbose: bool = False, force: bool = False) -> str:
     headers = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cuh", ".h"))]
     headers.append(os.path.join(ROOT, "include", "fracpint_b200.h"))
     jobs = []
-    for src in SOURCES:
+    objs = []
+    for spec in SOURCES:
+        src, _, part = spec.partition(":")
         s = os.path.join(CSRC, src)
-        o = os.path.join(BUILD, src.replace(".cu", ".o"))
+        o = os.path.join(BUILD, src.replace(".cu", f"_p{part}.o" if part else ".o"))
+        objs.append(o)
         if force or _stale(o, [s] + headers):
-            jobs.append([NVCC, *ARCH, *FLAGS, "-c", s, "-o", o])
+            jobs.append([NVCC, *ARCH, *FLAGS, *([f"-DFPC_1D_PART={part}"] if part else []), "-c", s, "-o", o])
 
     def run(cmd):
         r = subprocess.run(cmd, capture_output=True, text=True)
@@ -60,7 +65,6 @@ def build(verbose: bool = False, force: bool = False) -> str:
         for out in ex.map(run, jobs):
             if verbose and out.strip():
                 print(out)
-    objs = [os.path.join(BUILD, s.replace(".cu", ".o")) for s in SOURCES]
     if force or jobs or not os.path.exists(LIB) or _stale(LIB, objs):
         run([NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-Xcompiler", "-fPIC"])
     with open(stamp, "w") as f:

@@ -13,6 +13,18 @@
 
 #include <cstdlib>
 
+// build.py compiles this file as three translation units (-DFPC_1D_PART=0: matvec, 1: time FFTs,
+// 2: tau solves), so a cold build is not bound by one nvcc process working through every size
+// instantiation; without the macro it is one unit (scripts/build_timing.sh, build_variant.sh).
+#ifdef FPC_1D_PART
+#define FPC_1D_HAS(p) (FPC_1D_PART == (p))
+#ifdef FPC_PHASE_TIMING
+#error "FPC_PHASE_TIMING builds compile kernels_1d.cu as one unit (no FPC_1D_PART)"
+#endif
+#else
+#define FPC_1D_HAS(p) 1
+#endif
+
 #ifdef FPC_PHASE_TIMING
 namespace fpc {
 __device__ long long g_phase[1 << 16][16];
@@ -91,6 +103,7 @@ __device__ __forceinline__ double& comp(double2* s, int slot_padded, int c) {
   return reinterpret_cast<double*>(s + slot_padded)[c];
 }
 
+#if FPC_1D_HAS(0)
 // =====================================================================================
 // K1: 1D all-at-once matvec.  One buffer per time block k; real packing of the length-L
 // circulant embedding (L = 2M = next_pow2(2 Ns), toeplitz.hpp:26) into an M-point FFT.
@@ -334,6 +347,9 @@ __global__ void __launch_bounds__(Geo<LOGM, TOT, 16>::NT, minb(Geo<LOGM, TOT, 16
   }
 }
 
+#endif  // part 0 kernels
+
+#if FPC_1D_HAS(1)
 // =====================================================================================
 // K2: time FFT forward over spatial columns (alpha_circulant.hpp:146-156), Hermitian half.
 // CTA = B columns; M = Nt/2.
@@ -481,6 +497,9 @@ __global__ void __launch_bounds__(Geo<LOGM, TOT>::NT, minb(Geo<LOGM, TOT>::NT))
   FPC_PT(1, 3);
 }
 
+#endif  // part 1 kernels
+
+#if FPC_1D_HAS(2)
 // =====================================================================================
 // K3 (1D): tau shifted solves (tau.hpp:98-119): for each retained frequency row n,
 //   Z_n <- DST( DST(Z_n) ./ (lambda_n - dt sigma) ),
@@ -601,6 +620,8 @@ __global__ void __launch_bounds__(TauGeo<LOGM, TOT>::G::NT, minb(TauGeo<LOGM, TO
   FPC_PH(5);
 }
 
+#endif  // part 2 kernels
+
 // =====================================================================================
 // launchers
 // =====================================================================================
@@ -644,6 +665,7 @@ constexpr int small_tot() { return (1 << LM) >= 512 ? (1 << LM) : 512; }
 template <int LM, int TOT>
 constexpr bool is_smaller() { return small_tot<LM>() < TOT; }
 
+#if FPC_1D_HAS(0)
 cudaError_t launch_matvec_rows(const double* v, double* y, int len, int nrows, int rpt,
                                int sstride, int log_m, const double* eig_scaled,
                                const double2* tw_base, cudaStream_t st, int koff) {
@@ -688,12 +710,15 @@ cudaError_t launch_matvec_1d(const double* v, double* y, int n_space, int n_time
   return launch_matvec_rows(v, y, n_space, n_time, 1, n_space, log_m, eig_scaled, tw_base, st, koff);
 }
 
-static int ilog2(int n) {
+#endif  // part 0 launchers
+
+static inline int ilog2(int n) {
   int l = 0;
   while ((1 << l) < n) ++l;
   return l;
 }
 
+#if FPC_1D_HAS(1)
 cudaError_t launch_time_fwd(const double* v, double2* Z, int n_space, int n_time,
                             const double* scale_fwd, double s_in, const double2* tw_base,
                             cudaStream_t st) {
@@ -759,6 +784,9 @@ cudaError_t launch_time_inv(const double2* Z, double* z, int n_space, int n_time
   return cudaGetLastError();
 }
 
+#endif  // part 1 launchers
+
+#if FPC_1D_HAS(2)
 // in-place orthonormal DST-I of n_rows contiguous complex rows of length n (n + 1 = 2^k)
 cudaError_t launch_dst_rows(double2* Z, int n, int n_rows, const double2* tw_base, cudaStream_t st) {
   cudaError_t err = cudaSuccess;
@@ -821,5 +849,7 @@ cudaError_t launch_tau_solve_1d(double2* Z, int n_space, int n_rows, const doubl
 #undef CALL
   return err;
 }
+
+#endif  // part 2 launchers
 
 }  // namespace fpc

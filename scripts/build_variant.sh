@@ -9,10 +9,12 @@ mkdir -p build/var_$name scripts/_timing
 F="-gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC,-O3,-march=x86-64-v3,-ffp-contract=fast --expt-relaxed-constexpr -diag-suppress 39 $*"
 objs=""
 for o in build/fpc/*.o; do
-  s=$(basename $o .o)
+  b=$(basename $o .o)
+  s=${b%_p[0-9]}; part=""   # kernels_1d_pN.o = kernels_1d.cu compiled with -DFPC_1D_PART=N (build.py)
+  [[ $b != $s ]] && part="-DFPC_1D_PART=${b##*_p}"
   if [[ " $srcs " == *" $s "* ]]; then
-    nvcc $F -c paper_2003_07020_b200/csrc/$s.cu -o build/var_$name/$s.o &
-    objs="$objs build/var_$name/$s.o"
+    nvcc $F $part -c paper_2003_07020_b200/csrc/$s.cu -o build/var_$name/$b.o &
+    objs="$objs build/var_$name/$b.o"
   else
     objs="$objs $o"
   fi
