@@ -146,10 +146,30 @@ def run_reference(args, w):
     if rank != 0:
         return
     threads = os.cpu_count() or 1
-    times, iters = [], None
-    for _ in range(args.steps_ref):
+    # K timed full solves behind W untimed ones, like the GPU arm; every step is one complete reference
+    # solve (nothing extrapolated).  A wall-clock budget guards the driver's limit on a slow host: warm-up
+    # solves are dropped first, then timed ones, and the line reports what actually ran.
+    budget = float(os.environ.get("FPC_REF_BUDGET_S", "1300"))
+    t_start = time.perf_counter()
+    want_k, want_w = args.steps_ref, args.warmup_ref
+    times, iters, warm, est = [], None, 0, None
+    reserve = 0.0  # the single-thread / nproc operator timings after the solves (~1.3 solves' worth at config 2)
+    while len(times) < want_k:
+        elapsed = time.perf_counter() - t_start
+        if est is not None:
+            reserve = 1.5 * est
+            left = budget - elapsed - reserve
+            if warm < want_w and left < (want_k + 1) * est:
+                want_w = warm  # no room for another warm-up solve
+            if left < est and times:
+                break
         sec, iters = cpu_reference_solve(w, threads)
-        times.append(sec)
+        est = sec if est is None else max(est, sec)
+        if warm < want_w:
+            warm += 1
+        else:
+            times.append(sec)
+    args.steps_ref, args.warmup_ref = len(times), warm
     t = statistics.mean(times)
     val = 1.0 / t
     # the single-thread figure (set_thread_count(1), parallel.hpp:24) beside nproc: one PC apply and
@@ -157,9 +177,9 @@ def run_reference(args, w):
     pc1, mv1 = cpu_reference_ops(w, 1)
     pcn, mvn = cpu_reference_ops(w, threads)
     sample = (f"reference gmres_right (oracle/_ref, unmodified headers) on {w.name}: {args.steps_ref} full solves of "
-              f"{iters} iterations, {threads} threads, the reference's own report.seconds (krylov.hpp:87-190)")
+              f"{iters} iterations ({args.warmup_ref} untimed ones first), {threads} threads, the reference's own report.seconds (krylov.hpp:87-190)")
     line = {"impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": world,
-            "steps": args.steps_ref, "warmup": 0, "ms_per_step": t * 1e3, "higher_is_better": True,
+            "steps": args.steps_ref, "warmup": args.warmup_ref, "ms_per_step": t * 1e3, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded uniform source)",
             "config": workload_config(w),
             "iterations": iters, "step_seconds": times,
@@ -633,7 +653,8 @@ def main():
     ap.add_argument("--config", type=int, default=2, help="headline BASELINE config (default 2)")
     ap.add_argument("--gamma", type=float, default=1.2, help="config 1 only")
     ap.add_argument("--secondary", default="1,3", help="BASELINE configs measured after the headline ('' = none)")
-    ap.add_argument("--ref-steps", type=int, default=3, help="reference arm: full solves timed (<= --steps)")
+    ap.add_argument("--ref-steps", type=int, default=0,
+                    help="reference arm: cap on the full solves timed (0 = --steps; FPC_REF_BUDGET_S bounds the run)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--transport", default="nccl", choices=["nccl", "p2p"],
                     help="N > 1 sharded solve: NCCL all_to_all exchanges, or peer-store kernels into "
@@ -653,7 +674,8 @@ def main():
     if args.sweep:
         run_sweep(args)
         return
-    args.steps_ref = max(1, min(args.steps, args.ref_steps))
+    args.steps_ref = max(1, min(args.steps, args.ref_steps) if args.ref_steps > 0 else args.steps)
+    args.warmup_ref = max(0, args.warmup)
 
     from paper_2003_07020_b200 import problems
     w = problems.config(args.config, args.gamma if args.config == 1 else None)
